@@ -1,0 +1,6 @@
+"""CPU oracle for the HOBOTAN hot path — TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and --impl reference)
+may import this package.  The product package never does.
+"""
+from .oracle import Oracle, build_oracle_lib, hash4, splitmix64, search_thresholds  # noqa: F401
