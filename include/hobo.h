@@ -1,0 +1,136 @@
+/*
+ * hobo.h — C ABI of the B200-native HOBOTAN hot path (arXiv 2407.19987).
+ *
+ * The library (paper_2407_19987_b200/_lib/libhobo.so) contracts a dense, upper-
+ * triangular order-k HOBO tensor with a batch of binary candidates on sm_100a tensor
+ * cores.  Citations "P:<n>" refer to lines of the paper's LaTeX.
+ *
+ * Conventions (all calls):
+ *   - Every call returns hobo_status; nothing throws across the ABI.  On failure
+ *     hobo_last_error() returns a thread-local message naming the problem.
+ *   - "device" pointers live on the CUDA device that was current when the handle was
+ *     built (the handle's device); they are caller-owned (e.g. torch tensors'
+ *     data_ptr()).  "host" pointers are ordinary CPU memory.
+ *   - Work is ordered on the caller's `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream).  Calls that fill host outputs synchronise that stream.
+ *   - A handle must not be used from two threads at once.  A CUDA error poisons the
+ *     handle (later calls return HOBO_ECUDA).
+ *   - Energies EXCLUDE the compile offset, like the paper's printed "Energy"
+ *     (Energy -30 reported together with offset 30).
+ */
+#ifndef HOBO_H_
+#define HOBO_H_
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HOBO_OK = 0,
+  HOBO_EINVAL = 1,  /* bad order/N/ids/degree, non-finite coefficient, bad pointer/size  */
+  HOBO_ERANGE = 2,  /* a compiled cell exceeds FLT_MAX                                     */
+  HOBO_ENOMEM = 3,  /* host or device allocation failed / size budget exceeded             */
+  HOBO_ECUDA = 4,   /* CUDA error (sticky per handle) or no sm_100 device                  */
+  HOBO_ENCCL = 5,   /* reserved for the multi-GPU combine                                  */
+  HOBO_ESTATE = 6   /* handle poisoned by an earlier error                                 */
+} hobo_status;
+
+typedef struct hobo_tensor hobo_tensor;   /* opaque; owns host cells + one device replica */
+
+/* Term format: coeff * prod_f (c0_f + sum_l w_l * x_{var_l}).  It covers plain monomials,
+ * the binary integer encoding y = sum_k 2^k x_k of P:133-139 (one factor with weights
+ * 2^k, LSB- or MSB-first as in P:283-286 / P:371-373), (1 - q) factors and
+ * powers (repeat a factor).  A term with nfac = 0 is a constant.        */
+typedef struct { int32_t var; double w; } hobo_lin;
+typedef struct { double c0; int32_t nlin, lin0; } hobo_factor;
+typedef struct { double coeff; int32_t nfac, fac0; } hobo_term;
+typedef struct { float e; int64_t idx; } hobo_best;
+
+/* hobo_tensor_build — "Compile(H).get_hobo() -> hobo, offset".
+ * Expands every term with x^n = x (binary variables), sums like monomials, drops
+ * exact zeros, and stores each monomial S = {s1<...<sr} in the order-`order` tensor at
+ * its canonical cell (s1 repeated order-r+1 times, s2..sr): the smallest-subscript
+ * replication of P:111-117 / P:123-127.  Exact in integer arithmetic when all inputs are
+ * integral, otherwise long double; one round-to-nearest-even to fp32 per cell.
+ *   order   tensor order k, 1..6; must be >= the reduced degree (else HOBO_EINVAL)
+ *   N       number of binary variables (axis extent), 1..65535 (N <= 1024 when order>3)
+ *   terms/facs/lins  host arrays in the format above (copied; caller keeps ownership)
+ *   out     receives the new handle (device = current CUDA device)
+ *   offset_out (nullable) receives the constant term.                                  */
+hobo_status hobo_tensor_build(int order, int N, const hobo_term* terms, size_t nterms,
+                              const hobo_factor* facs, const hobo_lin* lins,
+                              hobo_tensor** out, double* offset_out);
+
+/* hobo_tensor_import_cells — explicit tensor cells (host).  Cell c has index tuple
+ * idx[c*order .. c*order+order) (any order, any repetition) and value val[c]; it is added
+ * to the canonical cell of its index SET, so energies on binary x are those of the raw
+ * tensor.  This is how the dense random configs enter (BASELINE configs 2, 4, 5).       */
+hobo_status hobo_tensor_import_cells(int order, int N, int64_t ncells, const int32_t* idx,
+                                     const float* val, hobo_tensor** out);
+
+hobo_status hobo_tensor_free(hobo_tensor* t);
+
+/* info: order, N, #nonzero canonical cells, all cells integral (0/1), sum |cell| (the
+ * parity scale: tolerance = 1e-5 * sum_abs), bf16 limb count L used on the device (1..3,
+ * the least L such that hi+mid+lo represents every fp32 cell exactly), offset.          */
+hobo_status hobo_tensor_info(const hobo_tensor* t, int* order, int* N, int64_t* ncells,
+                             int* is_integer, double* sum_abs, int* limbs, double* offset);
+
+/* host export of the canonical cells (lexicographic by index tuple): idx[ncells*order],
+ * val[ncells]; and of the dense N^order fp32 tensor (row-major, last index fastest;
+ * refuses N^order > 2^28 with HOBO_ENOMEM).  Test/inspection helpers.                 */
+hobo_status hobo_tensor_export_cells(const hobo_tensor* t, int32_t* idx, float* val);
+hobo_status hobo_tensor_export_dense(const hobo_tensor* t, float* host_out);
+
+/* hobo_energy — the tensor batch system: E_b = sum H_{ij..} X_bi X_bj ...
+ *   X_dev   device u8, row-major B x N; any nonzero byte means 1
+ *   B       number of candidates (>= 0)
+ *   row0    global index of row 0 (0 on one GPU; the shard offset on a multi-GPU run)
+ *   E_dev   device float[B] output (nullable if only `best` is wanted)
+ *   best    host output (nullable): argmin over (E, row0+b), ties -> lowest index
+ * Runs the energy-mode tensor-core contraction (strict, last-index-open layout).       */
+hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X_dev, int64_t B, int64_t row0,
+                        float* E_dev, hobo_best* best, void* stream);
+
+/* hobo_local_field — the same contraction with one index left open ("the gradient
+ * is computed based on tensor contraction results"):
+ *   G_dev[b*N+m] = E(x_b | x_m <- 1) - E(x_b | x_m <- 0)
+ * (the discrete local field; flip gain (1 - 2 x_m) G).  E_dev (nullable) receives the
+ * energies, computed from the per-degree fields in the same pass; best (host, nullable)
+ * receives the argmin over (E, row0+b) as in hobo_energy.                               */
+hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X_dev, int64_t B, int64_t row0,
+                             float* G_dev, float* E_dev, hobo_best* best, void* stream);
+
+/* hobo_search — batched heuristic search (P:81-83 simulated annealing is described only
+ * qualitatively and the paper's sampler is undisclosed; the rule implemented is
+ * DESIGN.md "Search rule").  `batch` chains start from counter-hash random x, run
+ * `iters` field evaluations + single-flip moves, and the lexicographically smallest
+ * (E_best, chain) is returned: x_best_host (u8[N]) and *e_best_host.  Deterministic in
+ * (tensor, seed, batch, iters).  iters = 0 returns the best random initial candidate.   */
+hobo_status hobo_search(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t iters,
+                        uint8_t* x_best_host, float* e_best_host, void* stream);
+
+/* hobo_search_shard — the same rule on global chains [chain0, chain0+nchains) (one GPU's
+ * shard); p0/p1 are the exploration-probability endpoints (defaults 0.5 / 0.005).  Also
+ * returns the winning global chain id.  Results per chain do not depend on the shard.   */
+hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains,
+                              int64_t iters, double p0, double p1, uint8_t* x_best_host,
+                              float* e_best_host, int64_t* best_chain, void* stream);
+
+/* Launch statistics of the last call on this handle: number of kernel launches issued,
+ * the executed tensor-core MACs of its contraction kernel(s), the algorithmic MACs
+ * (DESIGN.md "Roofline"), and — when profiling is on — the CUDA-event time in ms of its
+ * contraction kernel(s), recorded on the launch stream (this call synchronises on it).  */
+hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mma_macs,
+                                   double* algo_macs, double* kernel_ms);
+/* profiling on/off: record CUDA events around every contraction-kernel launch.         */
+hobo_status hobo_set_profiling(hobo_tensor* t, int enable);
+
+const char* hobo_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOBO_H_ */

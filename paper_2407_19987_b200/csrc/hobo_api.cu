@@ -1,0 +1,551 @@
+// hobo_api.cu — the C ABI of include/hobo.h: device layouts, launches, search loop.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hobo.h"
+#include "host_compile.h"
+#include "kernels.cuh"
+
+using namespace hobo;
+
+namespace {
+
+thread_local std::string g_err;
+
+hobo_status fail(hobo_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct DevLayout {
+  bool built = false;
+  int NT = 256, NACC = 1, n_ct = 0, Npad = 0;
+  __nv_bfloat16* W = nullptr;
+  int2* d_sched = nullptr;
+  std::vector<int32_t> sched;
+  alignas(64) CUtensorMap tmap;
+  double lcm = 1.0;
+  double wacc[6] = {1, 1, 1, 1, 1, 1};
+  double wp = 1.0;
+};
+
+}  // namespace
+
+struct hobo_tensor {
+  HostTensor host;
+  KLayout kl;
+  int device = -1;         // bound on first device use (the then-current CUDA device)
+  bool dev_init = false;
+  bool poisoned = false;
+  uint4* d_runs = nullptr;
+  uint32_t* d_runoff = nullptr;
+  float* d_p1 = nullptr;   // padded to 256-multiples
+  int W = 0;               // 32-bit words per candidate bit row
+  DevLayout lay[2];        // 0 = energy (strict), 1 = field (open index)
+  // scratch (grown on demand)
+  uint32_t* d_bits = nullptr; size_t bits_cap = 0;
+  double* d_Q = nullptr; size_t Q_cap = 0;
+  unsigned long long* d_key = nullptr;
+  float* d_G = nullptr; size_t G_cap = 0;
+  uint32_t* d_xbest = nullptr; size_t xbest_cap = 0;
+  float* d_ebest = nullptr; size_t ebest_cap = 0;
+  int64_t last_launches = 0;
+  double last_mma_macs = 0, last_algo_macs = 0;
+  bool profile = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // around the contraction kernel(s) of the last call
+  bool ev_valid = false;
+};
+
+namespace {
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      t->poisoned = true;                                                                            \
+      return fail(HOBO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+    }                                                                                                \
+  } while (0)
+
+template <class T>
+hobo_status grow(hobo_tensor* t, T*& p, size_t& cap, size_t n) {
+  if (n <= cap) return HOBO_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  cap = n;
+  return HOBO_OK;
+}
+
+void field_tile(int order, int& NT, int& NACC) {
+  switch (order) {
+    case 1: NT = 256; NACC = 1; break;
+    case 2: NT = 256; NACC = 1; break;
+    case 3: NT = 256; NACC = 2; break;
+    case 4: NT = 128; NACC = 3; break;
+    case 5: NT = 128; NACC = 4; break;
+    default: NT = 64; NACC = 5; break;
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+template <int NT, int NACC>
+cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  auto* k = kr_gemm_kernel<NT, NACC>;
+  const size_t smem = KrCfg<NT, NACC>::smem_bytes(p.W);
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k<<<dim3((unsigned)(p.n_ct * p.n_cb)), dim3(kThreads), smem, s>>>(L.tmap, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  if (L.NT == 256 && L.NACC == 1) return launch_kr<256, 1>(L, p, s);
+  if (L.NT == 256 && L.NACC == 2) return launch_kr<256, 2>(L, p, s);
+  if (L.NT == 128 && L.NACC == 3) return launch_kr<128, 3>(L, p, s);
+  if (L.NT == 128 && L.NACC == 4) return launch_kr<128, 4>(L, p, s);
+  return launch_kr<64, 5>(L, p, s);
+}
+
+hobo_status init_device(hobo_tensor* t);
+
+hobo_status check_device(hobo_tensor* t) {
+  if (t->poisoned) return fail(HOBO_ESTATE, "handle poisoned by an earlier CUDA error");
+  if (!t->dev_init) return init_device(t);
+  int cur = -1;
+  CK(cudaGetDevice(&cur));
+  if (cur != t->device) CK(cudaSetDevice(t->device));
+  return HOBO_OK;
+}
+
+hobo_status init_device(hobo_tensor* t) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) return fail(HOBO_ECUDA, "sm_100 (B200) device required; found sm_" + std::to_string(prop.major) +
+                                                    std::to_string(prop.minor));
+  t->device = dev;
+  const int N = t->host.N;
+  t->W = (N + 31) / 32;
+  std::string msg;
+  if (build_klayout(t->host.order, N, t->kl, msg)) return fail(HOBO_ENOMEM, msg);
+  CK(cudaMalloc(&t->d_runs, std::max<size_t>(t->kl.runs.size() / 4, 1) * sizeof(uint4)));
+  if (!t->kl.runs.empty())
+    CK(cudaMemcpy(t->d_runs, t->kl.runs.data(), t->kl.runs.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_runoff, t->kl.run_off.size() * 4));
+  CK(cudaMemcpy(t->d_runoff, t->kl.run_off.data(), t->kl.run_off.size() * 4, cudaMemcpyHostToDevice));
+  const int Npad = (N + 255) / 256 * 256;
+  std::vector<float> p1(Npad, 0.0f);
+  for (int m = 0; m < N; ++m) p1[m] = t->host.strict[1][m];
+  CK(cudaMalloc(&t->d_p1, Npad * sizeof(float)));
+  CK(cudaMemcpy(t->d_p1, p1.data(), Npad * sizeof(float), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_key, sizeof(unsigned long long)));
+  t->dev_init = true;
+  return HOBO_OK;
+}
+
+// builds W (bf16 limb planes) of one layout on the device, plus its TMA map and schedule
+hobo_status ensure_layout(hobo_tensor* t, int field) {
+  DevLayout& L = t->lay[field];
+  if (L.built) return HOBO_OK;
+  const HostTensor& H = t->host;
+  const int N = H.N, k = H.order;
+  if (field) field_tile(k, L.NT, L.NACC);
+  else { L.NT = 256; L.NACC = 1; }
+  if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
+  L.n_ct = (N + L.NT - 1) / L.NT;
+  L.Npad = L.n_ct * L.NT;
+  const int64_t Tpad = std::max<int64_t>(t->kl.Tpad, kBK);
+  const double bytes = (double)H.limbs * L.Npad * Tpad * 2.0;
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  if (bytes > 0.8 * (double)free_b)
+    return fail(HOBO_ENOMEM, "device layout needs " + std::to_string(bytes / 1e9) + " GB (N=" + std::to_string(N) +
+                                 ", order=" + std::to_string(k) + ", limbs=" + std::to_string(H.limbs) + ")");
+  CK(cudaMalloc(&L.W, (size_t)bytes));
+  if (t->kl.Tpad > 0) {
+    // temporaries: per-degree cells, binomials, tuple list
+    std::vector<float*> dstrict(7, nullptr);
+    for (int r = 2; r <= k; ++r) {
+      CK(cudaMalloc(&dstrict[r], std::max<size_t>(H.strict[r].size(), 1) * sizeof(float)));
+      CK(cudaMemcpy(dstrict[r], H.strict[r].data(), H.strict[r].size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    float** d_strict_ptrs = nullptr;
+    CK(cudaMalloc(&d_strict_ptrs, 7 * sizeof(float*)));
+    CK(cudaMemcpy(d_strict_ptrs, dstrict.data(), 7 * sizeof(float*), cudaMemcpyHostToDevice));
+    std::vector<long long> bt((size_t)(N + 1) * 7);
+    for (int n = 0; n <= N; ++n)
+      for (int i = 0; i < 7; ++i) bt[(size_t)n * 7 + i] = binom(n, i);
+    long long* d_bt = nullptr;
+    CK(cudaMalloc(&d_bt, bt.size() * sizeof(long long)));
+    CK(cudaMemcpy(d_bt, bt.data(), bt.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    uint16_t* d_tup = nullptr;
+    CK(cudaMalloc(&d_tup, t->kl.tuples.size() * sizeof(uint16_t)));
+    CK(cudaMemcpy(d_tup, t->kl.tuples.data(), t->kl.tuples.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    LayoutParams lp;
+    lp.tuples = d_tup;
+    lp.strict = d_strict_ptrs;
+    lp.binomT = d_bt;
+    lp.Wout = L.W;
+    lp.Tpad = t->kl.Tpad;
+    lp.N = N;
+    lp.Npad = L.Npad;
+    lp.L = H.limbs;
+    lp.field_mode = field;
+    layout_kernel<<<148 * 8, 256>>>(lp);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    for (int r = 2; r <= k; ++r) cudaFree(dstrict[r]);
+    cudaFree(d_strict_ptrs);
+    cudaFree(d_bt);
+    cudaFree(d_tup);
+  } else {
+    CK(cudaMemset(L.W, 0, (size_t)bytes));
+  }
+  // TMA map over the 2-D view [L * Npad rows][Tpad tuples], box 64 x NT, 128-byte swizzle
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)Tpad, (cuuint64_t)H.limbs * L.Npad};
+  cuuint64_t strides[1] = {(cuuint64_t)Tpad * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)L.NT};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&L.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, L.W, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+  L.sched = schedule(t->kl, L.NT, L.n_ct, field != 0);
+  CK(cudaMalloc(&L.d_sched, L.sched.size() * sizeof(int32_t)));
+  CK(cudaMemcpy(L.d_sched, L.sched.data(), L.sched.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (field) {
+    double lcm = 1;
+    for (int r = 2; r <= k; ++r) {
+      double a = lcm, b = r;
+      while (b) { double tmp = std::fmod(a, b); a = b; b = tmp; }
+      lcm = lcm * r / a;
+    }
+    L.lcm = lcm;
+    for (int j = 0; j < 6; ++j) L.wacc[j] = (j < k - 1) ? lcm / (double)(k - j) : 0.0;
+    L.wp = lcm;
+  }
+  L.built = true;
+  return HOBO_OK;
+}
+
+KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, long long B, float* G, double* Q) {
+  KrParams p;
+  p.xbits = bits;
+  p.runs = t->d_runs;
+  p.run_off = t->d_runoff;
+  p.sched = L.d_sched;
+  p.p1 = t->d_p1;
+  p.G = G;
+  p.Q = Q;
+  p.B = B;
+  p.N = t->host.N;
+  p.W = t->W;
+  p.Npad = L.Npad;
+  p.n_ct = L.n_ct;
+  p.n_cb = (int)((B + kBM - 1) / kBM);
+  p.nseg = t->kl.nseg;
+  p.L = t->host.limbs;
+  p.field_mode = (&L == &t->lay[1]) ? 1 : 0;
+  for (int j = 0; j < 6; ++j) p.wacc[j] = L.wacc[j];
+  p.wp = L.wp;
+  return p;
+}
+
+double exec_macs(hobo_tensor* t, const DevLayout& L, long long B) {
+  double kb = 0;
+  for (int ct = 0; ct < L.n_ct; ++ct)
+    for (int j = 0; j < t->kl.nseg; ++j) kb += L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1];
+  return kb * kBK * (double)L.NT * kBM * (double)((B + kBM - 1) / kBM) * t->host.limbs;
+}
+
+double algo_macs(hobo_tensor* t, bool field, long long B) {
+  double s = 0;
+  for (int r = 1; r <= t->host.order; ++r) s += (field ? r : 1) * (double)binom(t->host.N, r);
+  return s * (double)B;
+}
+
+float key_energy(unsigned long long key) {
+  uint32_t u = (uint32_t)(key >> 32) ^ 0x80000000u;
+  int32_t i = (int32_t)u;
+  if (i < 0) i ^= 0x7FFFFFFF;
+  float f;
+  std::memcpy(&f, &i, 4);
+  return f;
+}
+
+hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s) {
+  if (hobo_status st = ensure_layout(t, field)) return st;
+  const DevLayout& L = t->lay[field];
+  if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * t->W)) return st;
+  if (hobo_status st = grow(t, t->d_Q, t->Q_cap, (size_t)B * L.n_ct)) return st;
+  const long long nw = B * t->W;
+  pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, t->host.N, t->W, t->d_bits);
+  CK(cudaGetLastError());
+  KrParams p = make_params(t, L, t->d_bits, B, G, t->d_Q);
+  if (t->profile) CK(cudaEventRecord(t->ev0, s));
+  CK(launch_kr_any(L, p, s));
+  if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+  t->last_launches = 2;
+  t->last_mma_macs = exec_macs(t, L, B);
+  t->last_algo_macs = algo_macs(t, field != 0, B);
+  return HOBO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hobo_last_error(void) { return g_err.c_str(); }
+
+hobo_status hobo_tensor_build(int order, int N, const hobo_term* terms, size_t nterms, const hobo_factor* facs,
+                              const hobo_lin* lins, hobo_tensor** out, double* offset_out) {
+  if (!out) return fail(HOBO_EINVAL, "null output handle");
+  std::unique_ptr<hobo_tensor> t(new hobo_tensor());
+  std::string msg;
+  TermView tv{terms, nterms, facs, lins};
+  int st = compile_terms(order, N, tv, t->host, msg);
+  if (st) return fail(st == 3 ? HOBO_ENOMEM : (hobo_status)st, msg);
+  if (offset_out) *offset_out = t->host.offset;
+  *out = t.release();
+  return HOBO_OK;
+}
+
+hobo_status hobo_tensor_import_cells(int order, int N, int64_t ncells, const int32_t* idx, const float* val,
+                                     hobo_tensor** out) {
+  if (!out) return fail(HOBO_EINVAL, "null output handle");
+  std::unique_ptr<hobo_tensor> t(new hobo_tensor());
+  std::string msg;
+  int st = compile_cells(order, N, ncells, idx, val, t->host, msg);
+  if (st) return fail(st == 3 ? HOBO_ENOMEM : (hobo_status)st, msg);
+  *out = t.release();
+  return HOBO_OK;
+}
+
+hobo_status hobo_tensor_free(hobo_tensor* t) {
+  if (!t) return HOBO_OK;
+  if (t->dev_init) cudaSetDevice(t->device);
+  for (auto& L : t->lay) {
+    if (L.W) cudaFree(L.W);
+    if (L.d_sched) cudaFree(L.d_sched);
+  }
+  if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
+  void* ptrs[] = {t->d_runs, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete t;
+  return HOBO_OK;
+}
+
+hobo_status hobo_tensor_info(const hobo_tensor* t, int* order, int* N, int64_t* ncells, int* is_integer,
+                             double* sum_abs, int* limbs, double* offset) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (order) *order = t->host.order;
+  if (N) *N = t->host.N;
+  if (ncells) *ncells = t->host.nnz;
+  if (is_integer) *is_integer = t->host.is_integer ? 1 : 0;
+  if (sum_abs) *sum_abs = t->host.sum_abs;
+  if (limbs) *limbs = t->host.limbs;
+  if (offset) *offset = t->host.offset;
+  return HOBO_OK;
+}
+
+hobo_status hobo_tensor_export_cells(const hobo_tensor* t, int32_t* idx, float* val) {
+  if (!t || !idx || !val) return fail(HOBO_EINVAL, "null argument");
+  export_cells(t->host, idx, val);
+  return HOBO_OK;
+}
+
+hobo_status hobo_tensor_export_dense(const hobo_tensor* t, float* host_out) {
+  if (!t || !host_out) return fail(HOBO_EINVAL, "null argument");
+  if (export_dense(t->host, host_out)) return fail(HOBO_ENOMEM, "dense export limited to N^order <= 2^28 cells");
+  return HOBO_OK;
+}
+
+hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row0, float* E, hobo_best* best,
+                        void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (B < 0 || (B > 0 && !X) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF)
+    return fail(HOBO_EINVAL, "bad batch (B >= 0, X non-null, row0 + B < 2^32)");
+  if (hobo_status st = check_device(t)) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (B == 0) {
+    if (best) { best->e = INFINITY; best->idx = -1; }
+    return HOBO_OK;
+  }
+  if (hobo_status st = contract(t, 0, X, B, nullptr, s)) return st;
+  const DevLayout& L = t->lay[0];
+  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
+      t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
+  CK(cudaGetLastError());
+  t->last_launches += 1;
+  if (best) {
+    unsigned long long key = 0;
+    CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    best->idx = (int64_t)(key & 0xFFFFFFFFull);
+    best->e = key_energy(key);
+  }
+  return HOBO_OK;
+}
+
+hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row0, float* G, float* E,
+                             hobo_best* best, void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (B < 0 || (B > 0 && (!X || !G)) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF)
+    return fail(HOBO_EINVAL, "bad batch (B >= 0, X and G non-null, row0 + B < 2^32)");
+  if (hobo_status st = check_device(t)) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (B == 0) {
+    if (best) { best->e = INFINITY; best->idx = -1; }
+    return HOBO_OK;
+  }
+  if (hobo_status st = contract(t, 1, X, B, G, s)) return st;
+  if (E || best) {
+    const DevLayout& L = t->lay[1];
+    if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+    finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
+        t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
+    CK(cudaGetLastError());
+    t->last_launches += 1;
+  }
+  if (best) {
+    unsigned long long key = 0;
+    CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    best->idx = (int64_t)(key & 0xFFFFFFFFull);
+    best->e = key_energy(key);
+  }
+  return HOBO_OK;
+}
+
+hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
+                              double p0, double p1, uint8_t* x_best_host, float* e_best_host, int64_t* best_chain,
+                              void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (nchains < 1 || iters < 0 || chain0 < 0 || chain0 + nchains > (int64_t)0xFFFFFFFF || !(p0 > 0) || !(p1 > 0))
+    return fail(HOBO_EINVAL, "bad search arguments");
+  if (hobo_status st = check_device(t)) return st;
+  if (hobo_status st = ensure_layout(t, 1)) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevLayout& L = t->lay[1];
+  const int N = t->host.N, W = t->W;
+  const long long B = nchains;
+  if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * W)) return st;
+  if (hobo_status st = grow(t, t->d_Q, t->Q_cap, (size_t)B * L.n_ct)) return st;
+  if (hobo_status st = grow(t, t->d_G, t->G_cap, (size_t)B * N)) return st;
+  if (hobo_status st = grow(t, t->d_xbest, t->xbest_cap, (size_t)B * W)) return st;
+  if (hobo_status st = grow(t, t->d_ebest, t->ebest_cap, (size_t)B)) return st;
+  // exploration threshold P_t = floor(2^32 p0 (p1/p0)^(t / max(1, iters-1)))
+  std::vector<uint32_t> P((size_t)std::max<int64_t>(iters, 1));
+  for (int64_t it = 0; it < iters; ++it) {
+    const double v = std::floor(4294967296.0 * p0 * std::pow(p1 / p0, (double)it / (double)std::max<int64_t>(1, iters - 1)));
+    P[(size_t)it] = (uint32_t)std::min(4294967295.0, std::max(0.0, v));
+  }
+  int64_t launches = 0;
+  const unsigned g1 = (unsigned)std::min<long long>((B * W + 255) / 256, 148 * 16);
+  search_init_kernel<<<g1, 256, 0, s>>>(seed, chain0, B, N, W, t->d_bits, t->d_ebest);
+  CK(cudaGetLastError());
+  ++launches;
+  KrParams p = make_params(t, L, t->d_bits, B, t->d_G, t->d_Q);
+  const unsigned gs = (unsigned)((B * 32 + 255) / 256);
+  if (t->profile) CK(cudaEventRecord(t->ev0, s));
+  for (int64_t it = 0; it <= iters; ++it) {
+    CK(launch_kr_any(L, p, s));
+    const int move = it < iters;
+    search_step_kernel<<<gs, 256, 0, s>>>(t->d_Q, L.n_ct, L.lcm, t->d_G, t->d_bits, t->d_xbest, t->d_ebest, chain0, B,
+                                          N, W, seed, it, move ? P[(size_t)it] : 0u, move);
+    CK(cudaGetLastError());
+    launches += 2;
+  }
+  if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  search_best_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_ebest, B, chain0,
+                                                                                             t->d_key);
+  CK(cudaGetLastError());
+  ++launches;
+  unsigned long long key = 0;
+  CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t c = (int64_t)(key & 0xFFFFFFFFull);
+  std::vector<uint32_t> xb(W);
+  CK(cudaMemcpyAsync(xb.data(), t->d_xbest + (size_t)(c - chain0) * W, W * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (x_best_host)
+    for (int m = 0; m < N; ++m) x_best_host[m] = (uint8_t)((xb[m >> 5] >> (m & 31)) & 1u);
+  if (e_best_host) *e_best_host = key_energy(key);
+  if (best_chain) *best_chain = c;
+  t->last_launches = launches;
+  t->last_mma_macs = exec_macs(t, L, B) * (double)(iters + 1);
+  t->last_algo_macs = algo_macs(t, true, B) * (double)(iters + 1);
+  return HOBO_OK;
+}
+
+hobo_status hobo_search(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t iters, uint8_t* x_best_host,
+                        float* e_best_host, void* stream) {
+  return hobo_search_shard(t, seed, 0, batch, iters, 0.5, 0.005, x_best_host, e_best_host, nullptr, stream);
+}
+
+hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mma_macs, double* algo,
+                                   double* kernel_ms) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (launches) *launches = t->last_launches;
+  if (mma_macs) *mma_macs = t->last_mma_macs;
+  if (algo) *algo = t->last_algo_macs;
+  if (kernel_ms) {
+    *kernel_ms = -1.0;
+    if (t->profile && t->ev_valid) {
+      CK(cudaEventSynchronize(t->ev1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, t->ev0, t->ev1));
+      *kernel_ms = ms;
+    }
+  }
+  return HOBO_OK;
+}
+
+hobo_status hobo_set_profiling(hobo_tensor* t, int enable) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (hobo_status st = check_device(t)) return st;
+  if (enable && !t->ev0) {
+    CK(cudaEventCreate(&t->ev0));
+    CK(cudaEventCreate(&t->ev1));
+  }
+  t->profile = enable != 0;
+  t->ev_valid = false;
+  return HOBO_OK;
+}
+
+}  // extern "C"

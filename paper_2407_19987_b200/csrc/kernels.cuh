@@ -1,0 +1,468 @@
+// kernels.cuh — sm_100a kernels of the HOBOTAN hot path.
+//
+// The contraction (batched as in PAPER.md:141-149) is evaluated as ONE
+// tensor-core GEMM per (candidate block, column tile) with one tensor index left open:
+//
+//     F[b, m] = sum_t  A[b, t] * W[m, t]          (tcgen05.mma, fp32 accumulate in TMEM)
+//
+// t runs over the "tuples" = (r-1)-subsets T of the variables, grouped in segments by
+// degree r = k..2, each segment in colex order.  A[b, t] = prod_{u in T} x_bu is the
+// Khatri-Rao product of the candidate's bits — generated on chip from the bit-packed
+// candidates, never stored in HBM.  W is the bf16 limb plane of one of two layouts:
+//   field  mode: W[m, T] = c(T u {m}) for m not in T   -> F = per-degree local fields
+//   energy mode: W[m, T] = c(T u {m}) for max T < m    -> F = last-index-open partials
+// c(S) is the fp32 canonical cell of monomial S (PAPER.md:111-117 puts c(S) at the
+// smallest-subscript-replicated cell; for binary x only the set S matters).
+// The epilogue reduces F over m against x_bm (energy) and writes the fields.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+
+#include "ptx.cuh"
+
+namespace hobo {
+
+constexpr int kBM = 128;        // candidates per CTA (UMMA M, TMEM lanes)
+constexpr int kBK = 64;         // tuples per K-block (one 128-byte SW128 row of bf16)
+constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA, warps 2-5 A-generator + epilogue
+
+struct KrParams {
+  const uint32_t* xbits;    // [B][W] bit-packed candidates (bit m of word m/32)
+  const uint4* runs;        // A-generator runs (host_compile.cpp build_klayout)
+  const uint32_t* run_off;  // [n_kb + 1]
+  const int2* sched;        // [n_ct][nseg] (first K-block, #K-blocks)
+  const float* p1;          // [Npad] degree-1 cells (the field of an order-1 term), 0 past N
+  float* G;                 // field mode: [B][N] local fields; else nullptr
+  double* Q;                // [n_ct][B] weighted partial energies (fixed-order, no atomics)
+  long long B;
+  int N, W, Npad, n_ct, n_cb, nseg, L, field_mode;
+  double wacc[6];           // weight of accumulator j in the partial energy
+  double wp;                // weight of the degree-1 term
+};
+
+template <int NT, int NACC>
+struct KrCfg {
+  static constexpr int B_STAGE = NT * 128;   // NT rows x 64 bf16
+  static constexpr int A_STAGE = kBM * 128;  // 128 rows x 64 bf16
+  static constexpr int NB = NT >= 256 ? 5 : 8;
+  static constexpr int NA = NT >= 256 ? 3 : 4;
+  static constexpr int COLS = NACC * NT;
+  static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
+  static_assert(COLS <= 512, "TMEM holds 512 fp32 columns");
+  static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
+  static constexpr int BAR_BYTES = 8 * (2 * NB + 2 * NA + 1) + 16;
+  static size_t smem_bytes(int W) {
+    return 1024 + (size_t)NB * B_STAGE + (size_t)NA * A_STAGE + BAR_BYTES + 128 + (size_t)(W + 2) * kBM * 4;
+  }
+};
+
+// one thread builds its candidate's 64-bit row of A for one K-block from the block's runs
+__device__ __forceinline__ uint64_t kr_row_bits(const uint32_t* xs, int row, const uint4* __restrict__ runs, uint32_t r0,
+                                                uint32_t r1) {
+  uint64_t bits = 0;
+  for (uint32_t i = r0; i < r1; ++i) {
+    const uint4 rr = __ldg(runs + i);
+    const uint32_t start = rr.x & 0xFFu, cnt = (rr.x >> 8) & 0xFFu, lo = rr.x >> 16;
+    uint32_t on = 1;
+    const uint32_t f[4] = {rr.y & 0xFFFFu, rr.y >> 16, rr.z & 0xFFFFu, rr.z >> 16};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (f[q] != 0xFFFFu) on &= xs[(f[q] >> 5) * kBM + row] >> (f[q] & 31);
+    const uint32_t w = lo >> 5, sh = lo & 31;
+    uint64_t v = ((uint64_t)xs[(w + 1) * kBM + row] << 32) | xs[w * kBM + row];
+    v >>= sh;
+    if (sh) v |= (uint64_t)xs[(w + 2) * kBM + row] << (64 - sh);
+    const uint64_t mask = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1ull);
+    if (on & 1u) bits |= (v & mask) << start;
+  }
+  return bits;
+}
+
+template <int NT, int NACC>
+__global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
+  using C = KrCfg<NT, NACC>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 atoms need 1024-byte alignment
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sB = base;
+  const uint32_t sA = sB + C::NB * C::B_STAGE;
+  const uint32_t sBar = sA + C::NA * C::A_STAGE;
+  const uint32_t acc_full = sBar + 8 * (2 * C::NB + 2 * C::NA);
+  const uint32_t tslot = acc_full + 8;
+  const uint32_t sX = (tslot + 16 + 127u) & ~127u;
+  uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
+  volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
+#define FULL_B(s) (sBar + 8u * (s))
+#define EMPTY_B(s) (sBar + 8u * (C::NB + (s)))
+#define FULL_A(s) (sBar + 8u * (2 * C::NB + (s)))
+#define EMPTY_A(s) (sBar + 8u * (2 * C::NB + C::NA + (s)))
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ct = blockIdx.x / p.n_cb, cb = blockIdx.x % p.n_cb;  // column-tile-major: concurrent CTAs share W tiles in L2
+  const long long b0 = (long long)cb * kBM;
+  const int2* sched = p.sched + (size_t)ct * p.nseg;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NB; ++s) { mbar_init(FULL_B(s), 1); mbar_init(EMPTY_B(s), 1); }
+    for (int s = 0; s < C::NA; ++s) { mbar_init(FULL_A(s), 4); mbar_init(EMPTY_A(s), 1); }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
+  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  // this CTA's candidate bits, column-major xs[w][row] (+2 zero words for window reads)
+  {
+    const int Wp = p.W + 2;
+    for (int i = threadIdx.x; i < Wp * kBM; i += kThreads) {
+      const int r = i / Wp, w = i % Wp;
+      uint32_t v = 0;
+      if (w < p.W && b0 + r < p.B) v = __ldg(p.xbits + (size_t)(b0 + r) * p.W + w);
+      xs[w * kBM + r] = v;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot_g;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: W limb tiles (NT rows x 64 tuples, SW128) -------------
+    if (lane == 0) {
+      int sb = 0;
+      uint32_t ph = 0;
+      for (int j = 0; j < p.nseg; ++j) {
+        const int2 s = sched[j];
+        for (int kb = s.x; kb < s.x + s.y; ++kb)
+          for (int l = 0; l < p.L; ++l) {
+            mbar_wait(EMPTY_B(sb), ph ^ 1u);
+            mbar_arrive_expect_tx(FULL_B(sb), C::B_STAGE);
+            tma_load_2d(sB + sb * C::B_STAGE, &tmap, FULL_B(sb), kb * kBK, l * p.Npad + ct * NT);
+            if (++sb == C::NB) { sb = 0; ph ^= 1u; }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread) ----------------------------------------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
+      int sb = 0, sa = 0;
+      uint32_t phb = 0, pha = 0, used = 0;
+      for (int j = 0; j < p.nseg; ++j) {
+        const int2 s = sched[j];
+        const int acc = p.field_mode ? j : 0;
+        const uint32_t d = tmem + (uint32_t)(acc * NT);
+        for (int kb = s.x; kb < s.x + s.y; ++kb) {
+          mbar_wait(FULL_A(sa), pha);
+          tc_fence_after();
+          const uint64_t adesc = sw128_kmajor_desc(sA + sa * C::A_STAGE);
+          for (int l = 0; l < p.L; ++l) {
+            mbar_wait(FULL_B(sb), phb);
+            tc_fence_after();
+            const uint64_t bdesc = sw128_kmajor_desc(sB + sb * C::B_STAGE);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint32_t accumulate = ((used >> acc) & 1u) | (uint32_t)(l | k);
+              umma_bf16_ss(d, adesc + 2u * k, bdesc + 2u * k, idesc, accumulate);
+            }
+            umma_commit(EMPTY_B(sb));
+            if (++sb == C::NB) { sb = 0; phb ^= 1u; }
+          }
+          umma_commit(EMPTY_A(sa));
+          if (++sa == C::NA) { sa = 0; pha ^= 1u; }
+          used |= 1u << acc;
+        }
+      }
+      if (used) umma_commit(acc_full);
+      else mbar_arrive(acc_full);
+    }
+  } else {
+    // ---------------- A generator, then epilogue (warps 2..5) ---------------------------------
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;   // candidate row within the block == TMEM lane
+    int sa = 0;
+    uint32_t pha = 0;
+    for (int j = 0; j < p.nseg; ++j) {
+      const int2 s = sched[j];
+      for (int kb = s.x; kb < s.x + s.y; ++kb) {
+        mbar_wait(EMPTY_A(sa), pha ^ 1u);
+        const uint64_t bits = kr_row_bits(xs, row, p.runs, __ldg(p.run_off + kb), __ldg(p.run_off + kb + 1));
+        const uint32_t rowaddr = sA + sa * C::A_STAGE + row * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t byte = (uint32_t)(bits >> (8 * c)) & 0xFFu;
+          uint32_t w4[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t t = byte >> (2 * i);
+            w4[i] = (t & 1u) * 0x3F80u + (t & 2u) * 0x1FC00000u;  // two bf16 {0, 1.0}
+          }
+          st_shared_v4(rowaddr + ((uint32_t)(c ^ (row & 7)) << 4), w4[0], w4[1], w4[2], w4[3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(FULL_A(sa));
+        if (++sa == C::NA) { sa = 0; pha ^= 1u; }
+      }
+    }
+
+    // ---------------- epilogue -----------------------------------------------------------------
+    uint32_t used = 0;
+    for (int j = 0; j < p.nseg; ++j)
+      if (sched[j].y > 0) used |= 1u << (p.field_mode ? j : 0);
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const long long b = b0 + row;
+    const bool live = b < p.B;
+    double qsum = 0.0;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    for (int c0 = 0; c0 < NT; c0 += 32) {
+      const int mbase = ct * NT + c0;
+      const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
+      float g[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) g[c] = 0.0f;
+#pragma unroll
+      for (int a = 0; a < NACC; ++a) {
+        if (!((used >> a) & 1u)) continue;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld32(lane_base + (uint32_t)(a * NT + c0), r);
+        tmem_ld_wait();
+        const double wa = p.wacc[a];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float v = __uint_as_float(r[c]);
+          g[c] += v;
+          if ((xw >> c) & 1u) qsum += wa * (double)v;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float pm = __ldg(p.p1 + mbase + c);
+        g[c] += pm;
+        if ((xw >> c) & 1u) qsum += p.wp * (double)pm;
+      }
+      if (p.field_mode && live) {
+        float* gout = p.G + (size_t)b * p.N + mbase;
+        const int nvalid = min(32, p.N - mbase);
+        if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(gout) & 15) == 0)) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) *reinterpret_cast<float4*>(gout + c) = make_float4(g[c], g[c + 1], g[c + 2], g[c + 3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c < nvalid) gout[c] = g[c];
+        }
+      }
+    }
+    if (live) p.Q[(size_t)ct * p.B + b] = qsum;
+  }
+#undef FULL_B
+#undef EMPTY_B
+#undef FULL_A
+#undef EMPTY_A
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ------------------------------------------------------------------------------------------
+// u8 candidates (row-major B x N, nonzero = 1) -> bit rows [B][W]
+__global__ void pack_x_kernel(const uint8_t* __restrict__ X, long long B, int N, int W, uint32_t* __restrict__ bits) {
+  const long long total = B * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / W;
+    const int w = (int)(i % W);
+    const uint8_t* src = X + b * N + (long long)w * 32;
+    const int n = min(32, N - w * 32);
+    uint32_t v = 0;
+    for (int j = 0; j < n; ++j) v |= (uint32_t)(src[j] != 0) << j;
+    bits[i] = v;
+  }
+}
+
+// signed-orderable key of (E, global index): lexicographic min == min of the u64
+__device__ __forceinline__ unsigned long long argmin_key(float e, unsigned long long idx) {
+  if (e == 0.0f) e = 0.0f;  // -0 -> +0
+  int i = __float_as_int(e);
+  i ^= (i >> 31) & 0x7FFFFFFF;
+  const uint32_t u = (uint32_t)i ^ 0x80000000u;
+  return ((unsigned long long)u << 32) | (idx & 0xFFFFFFFFull);
+}
+
+// E_b = (sum_ct Q[ct][b]) / lcm in double (exact for integer instances), one rounding to fp32
+__device__ __forceinline__ float combine_q(const double* __restrict__ Q, int n_ct, long long B, long long b, double lcm) {
+  double s = 0.0;
+  for (int c = 0; c < n_ct; ++c) s += Q[(size_t)c * B + b];
+  return (float)(s / lcm);
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// E_b = (sum_ct Q[ct][b]) / lcm; argmin via warp shuffles -> smem block min -> one atomicMin
+__global__ void finalize_kernel(const double* __restrict__ Q, int n_ct, long long B, double lcm, long long row0,
+                                float* __restrict__ E, unsigned long long* __restrict__ best_key) {
+  __shared__ unsigned long long red[32];
+  unsigned long long key = ~0ull;
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B; b += (long long)gridDim.x * blockDim.x) {
+    const float e = combine_q(Q, n_ct, B, b, lcm);
+    if (E) E[b] = e;
+    const unsigned long long k = argmin_key(e, (unsigned long long)(row0 + b));
+    key = k < key ? k : key;
+  }
+  key = warp_min_u64(key);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    key = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : ~0ull;
+    key = warp_min_u64(key);
+    if (threadIdx.x == 0 && best_key) atomicMin(best_key, key);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// device layout: W[l][m][t] bf16 limb planes from the per-degree colex cell arrays
+struct LayoutParams {
+  const uint16_t* tuples;        // [Tpad][6]
+  const float* const* strict;    // strict[r] device pointers (r = 0..order)
+  const long long* binomT;       // [(N+1) * 7]: C(n, i)
+  __nv_bfloat16* Wout;           // [L][Npad][Tpad]
+  long long Tpad;
+  int N, Npad, L, field_mode;
+};
+
+__device__ __forceinline__ long long dbinom(const long long* t, int n, int i) { return (n < i || i < 0) ? 0 : t[n * 7 + i]; }
+
+__global__ void layout_kernel(const LayoutParams lp) {
+  const long long total = (long long)lp.Npad * lp.Tpad;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e / lp.Tpad);
+    const long long t = e % lp.Tpad;
+    const uint16_t* tp = lp.tuples + t * 6;
+    const int r = tp[0];
+    float c = 0.0f;
+    if (r >= 2 && m < lp.N) {
+      int S[6];
+      int n = 0;
+      bool ok = true, placed = false;
+      for (int i = 0; i < r - 1; ++i) {
+        const int v = tp[1 + i];
+        if (v == m) ok = false;
+        if (!placed && m < v) { S[n++] = m; placed = true; }
+        S[n++] = v;
+      }
+      if (!placed) S[n++] = m;
+      if (!lp.field_mode && placed) ok = false;  // strict layout: m must be the largest index
+      if (ok) {
+        long long rank = 0;
+        for (int i = 0; i < r; ++i) rank += dbinom(lp.binomT, S[i], i + 1);
+        c = lp.strict[r][rank];
+      }
+    }
+    // exact split into bf16 limbs: hi + mid + lo
+    const __nv_bfloat16 hi = __float2bfloat16_rn(c);
+    const float r1 = c - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const float r2 = r1 - __bfloat162float(mid);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
+    const size_t plane = (size_t)lp.Npad * lp.Tpad;
+    const size_t off = (size_t)m * lp.Tpad + t;
+    lp.Wout[off] = hi;
+    if (lp.L > 1) lp.Wout[plane + off] = mid;
+    if (lp.L > 2) lp.Wout[2 * plane + off] = lo;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// search: counter-hash RNG, integer decisions on fp32 values
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t d_hash(uint64_t s, uint64_t a, uint64_t b, uint64_t c) {
+  return d_splitmix64(d_splitmix64(d_splitmix64(s ^ a) ^ b) ^ c);
+}
+
+// chain c's initial x: bit m = bit (m & 63) of h(seed, 1, c, m >> 6)
+__global__ void search_init_kernel(uint64_t seed, long long chain0, long long nchains, int N, int W, uint32_t* bits,
+                                   float* ebest) {
+  const long long total = nchains * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long c = i / W;
+    const int w = (int)(i % W);
+    const uint64_t hv = d_hash(seed, 1, (uint64_t)(chain0 + c), (uint64_t)(w >> 1));
+    uint32_t v = (uint32_t)(hv >> ((w & 1) * 32));
+    const int valid = N - w * 32;
+    if (valid < 32) v &= (valid <= 0) ? 0u : ((1u << valid) - 1u);
+    bits[i] = v;
+    if (w == 0) ebest[c] = __int_as_float(0x7f800000);  // +inf
+  }
+}
+
+// one warp per chain: best tracking, flip gain, move rule, flip
+__global__ void search_step_kernel(const double* __restrict__ Q, int n_ct, double lcm, const float* __restrict__ G,
+                                   uint32_t* bits, uint32_t* xbest, float* ebest, long long chain0, long long nchains,
+                                   int N, int W, uint64_t seed, long long t, uint32_t P_t, int do_move) {
+  const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nchains) return;
+  const float e = combine_q(Q, n_ct, nchains, c, lcm);
+  uint32_t* xb = bits + c * W;
+  if (e < ebest[c]) {  // strict: on equal E the earliest iteration is kept
+    for (int w = lane; w < W; w += 32) xbest[c * W + w] = xb[w];
+    __syncwarp();
+    if (lane == 0) ebest[c] = e;
+  }
+  if (!do_move) return;
+  // argmin over m of (1 - 2 x_m) g_m, lowest m on ties
+  float dmin = __int_as_float(0x7f800000);
+  int mmin = 0x7fffffff;
+  for (int m = lane; m < N; m += 32) {
+    const float g = G[(size_t)c * N + m];
+    const float d = ((xb[m >> 5] >> (m & 31)) & 1u) ? -g : g;
+    if (d < dmin) { dmin = d; mmin = m; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float od = __shfl_xor_sync(0xffffffffu, dmin, o);
+    const int om = __shfl_xor_sync(0xffffffffu, mmin, o);
+    if (od < dmin || (od == dmin && om < mmin)) { dmin = od; mmin = om; }
+  }
+  if (lane == 0) {
+    const uint64_t r = d_hash(seed, 2, (uint64_t)(chain0 + c), (uint64_t)t);
+    const int mrand = (int)(((r & 0xffffffffull) * (uint64_t)N) >> 32);
+    int ms;
+    if ((uint32_t)(r >> 32) < P_t) ms = mrand;
+    else ms = (dmin < 0.0f) ? mmin : mrand;
+    xb[ms >> 5] ^= 1u << (ms & 31);
+  }
+}
+
+__global__ void search_best_kernel(const float* __restrict__ ebest, long long nchains, long long chain0,
+                                   unsigned long long* best_key) {
+  __shared__ unsigned long long red[32];
+  unsigned long long key = ~0ull;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nchains; c += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = argmin_key(ebest[c], (unsigned long long)(chain0 + c));
+    key = k < key ? k : key;
+  }
+  key = warp_min_u64(key);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    key = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : ~0ull;
+    key = warp_min_u64(key);
+    if (threadIdx.x == 0) atomicMin(best_key, key);
+  }
+}
+
+}  // namespace hobo

@@ -1,0 +1,202 @@
+"""Thin ctypes binding of include/hobo.h (libhobo.so).  Argument marshalling only: every
+step of the hot path runs in the library's CUDA kernels.  PyTorch provides device memory
+and streams.  There is no CPU fallback: if the library is missing, importing raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libhobo.so")
+
+HOBO_OK, HOBO_EINVAL, HOBO_ERANGE, HOBO_ENOMEM, HOBO_ECUDA, HOBO_ENCCL, HOBO_ESTATE = range(7)
+_STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
+
+EXPORTED = [
+    "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_free", "hobo_tensor_info",
+    "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field",
+    "hobo_search", "hobo_search_shard", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
+]
+
+
+class HoboError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class HoboBest(C.Structure):
+    _fields_ = [("e", C.c_float), ("idx", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhobo.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2407_19987_b200.build` "
+                              "(the HOBO hot path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P, I, I64, U64, D, SZ = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_size_t
+        L.hobo_tensor_build.argtypes = [I, I, P, SZ, P, P, C.POINTER(P), C.POINTER(D)]
+        L.hobo_tensor_import_cells.argtypes = [I, I, I64, P, P, C.POINTER(P)]
+        L.hobo_tensor_free.argtypes = [P]
+        L.hobo_tensor_info.argtypes = [P, C.POINTER(I), C.POINTER(I), C.POINTER(I64), C.POINTER(I),
+                                       C.POINTER(D), C.POINTER(I), C.POINTER(D)]
+        L.hobo_tensor_export_cells.argtypes = [P, P, P]
+        L.hobo_tensor_export_dense.argtypes = [P, P]
+        L.hobo_energy.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
+        L.hobo_local_field.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
+        L.hobo_search.argtypes = [P, U64, I64, I64, P, C.POINTER(C.c_float), P]
+        L.hobo_search_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, C.POINTER(C.c_float),
+                                        C.POINTER(I64), P]
+        L.hobo_last_launch_stats.argtypes = [P, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]
+        L.hobo_set_profiling.argtypes = [P, I]
+        L.hobo_last_error.restype = C.c_char_p
+        for name in EXPORTED:
+            if name != "hobo_last_error":
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != HOBO_OK:
+        raise HoboError(st, lib().hobo_last_error().decode())
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _dev_ptr(t, dtype, shape=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA torch tensor")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"expected a contiguous {dtype} tensor, got {t.dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
+    return C.c_void_p(t.data_ptr())
+
+
+class HoboTensor:
+    """Owner of one compiled problem (hobo_tensor*)."""
+
+    def __init__(self, handle, offset=0.0):
+        self._h = handle
+        o, n, nc, ii, sa, lb, off = (C.c_int(), C.c_int(), C.c_int64(), C.c_int(), C.c_double(), C.c_int(),
+                                     C.c_double())
+        _check(lib().hobo_tensor_info(self._h, C.byref(o), C.byref(n), C.byref(nc), C.byref(ii), C.byref(sa),
+                                      C.byref(lb), C.byref(off)))
+        self.order, self.N, self.ncells = o.value, n.value, nc.value
+        self.is_integer, self.sum_abs, self.limbs, self.offset = bool(ii.value), sa.value, lb.value, off.value
+
+    # -- construction ---------------------------------------------------------------------
+    @classmethod
+    def build(cls, order, N, terms, facs, lins):
+        """hobo_tensor_build from numpy structured arrays (workloads.TERM/FAC/LIN layout)."""
+        h, off = C.c_void_p(), C.c_double()
+        _check(lib().hobo_tensor_build(order, N, _np_ptr(terms), len(terms), _np_ptr(facs), _np_ptr(lins),
+                                       C.byref(h), C.byref(off)))
+        return cls(h, off.value)
+
+    @classmethod
+    def from_problem(cls, p):
+        return cls.build(p.order, p.N, p.terms, p.facs, p.lins)
+
+    @classmethod
+    def import_cells(cls, order, N, idx, val):
+        idx = np.ascontiguousarray(idx, np.int32)
+        val = np.ascontiguousarray(val, np.float32)
+        h = C.c_void_p()
+        _check(lib().hobo_tensor_import_cells(order, N, len(val), _np_ptr(idx), _np_ptr(val), C.byref(h)))
+        return cls(h, 0.0)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hobo_tensor_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def tau(self):
+        return 1e-5 * self.sum_abs
+
+    # -- host exports -----------------------------------------------------------------------
+    def cells(self):
+        idx = np.zeros((self.ncells, self.order), np.int32)
+        val = np.zeros(self.ncells, np.float32)
+        _check(lib().hobo_tensor_export_cells(self._h, _np_ptr(idx), _np_ptr(val)))
+        return idx, val
+
+    def dense(self):
+        out = np.zeros((self.N,) * self.order, np.float32)
+        _check(lib().hobo_tensor_export_dense(self._h, _np_ptr(out)))
+        return out
+
+    # -- the hot path -------------------------------------------------------------------------
+    def energy(self, X, E=None, row0=0, want_best=True, stream=None):
+        """E_b for a CUDA u8 tensor X (B x N).  Returns (E, best) with best = (e, global idx)."""
+        import torch
+        B = X.shape[0]
+        xp = _dev_ptr(X, torch.uint8, (B, self.N))
+        if E is None:
+            E = torch.empty(B, dtype=torch.float32, device=X.device)
+        best = HoboBest()
+        _check(lib().hobo_energy(self._h, xp, B, row0, _dev_ptr(E, torch.float32, (B,)),
+                                 C.byref(best) if want_best else None, _stream_handle(stream)))
+        return E, ((best.e, best.idx) if want_best else None)
+
+    def local_field(self, X, G=None, E=None, row0=0, want_energy=True, want_best=False, stream=None):
+        """G[b, m] = E(x_b | x_m=1) - E(x_b | x_m=0) (and E, and the argmin) for a CUDA u8 X.
+        Returns (G, E) or, with want_best, (G, E, (e_best, global idx))."""
+        import torch
+        B = X.shape[0]
+        xp = _dev_ptr(X, torch.uint8, (B, self.N))
+        if G is None:
+            G = torch.empty(B, self.N, dtype=torch.float32, device=X.device)
+        if E is None and want_energy:
+            E = torch.empty(B, dtype=torch.float32, device=X.device)
+        best = HoboBest()
+        _check(lib().hobo_local_field(self._h, xp, B, row0, _dev_ptr(G, torch.float32, (B, self.N)),
+                                      _dev_ptr(E, torch.float32, (B,)) if E is not None else None,
+                                      C.byref(best) if want_best else None, _stream_handle(stream)))
+        return (G, E, (best.e, best.idx)) if want_best else (G, E)
+
+    def search(self, seed, batch, iters, chain0=None, nchains=None, p0=0.5, p1=0.005, stream=None):
+        """hobo_search (or the shard [chain0, chain0+nchains)).  Returns (x_best u8[N], e_best, chain)."""
+        x = np.zeros(self.N, np.uint8)
+        e = C.c_float()
+        c = C.c_int64()
+        if chain0 is None:
+            chain0, nchains = 0, batch
+        _check(lib().hobo_search_shard(self._h, seed, chain0, nchains, iters, p0, p1, _np_ptr(x), C.byref(e),
+                                       C.byref(c), _stream_handle(stream)))
+        return x, e.value, c.value
+
+    def set_profiling(self, enable=True):
+        _check(lib().hobo_set_profiling(self._h, 1 if enable else 0))
+
+    def launch_stats(self):
+        """Launches, executed MMA MACs, algorithmic MACs and (profiling on) kernel ms of the last call."""
+        n, mm, am, ms = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        _check(lib().hobo_last_launch_stats(self._h, C.byref(n), C.byref(mm), C.byref(am), C.byref(ms)))
+        return dict(launches=n.value, mma_macs=mm.value, algo_macs=am.value, kernel_ms=ms.value)

@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Bars (BASELINE.json north_star): bit-exact on integer-coefficient instances;
+|dE|, |dG| <= tau = 1e-5 * sum|H| for fp32 coefficients; argmin exact when the energy gap
+exceeds 2 tau (reading 11), else the returned candidate is within 2 tau."""
+import numpy as np
+import pytest
+
+from oracle import Oracle
+from workloads import (cfg3_problem, exhaustive_X, int_twin_cells, paper_grids, pythagoras,
+                       random_integer_problem, seating, tsp, uniform_cells, x_bits)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+    assert _t.cuda.is_available(), "GPU tests need a CUDA device"
+    return _t
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2407_19987_b200 import build
+    build.build()
+    from paper_2407_19987_b200 import hobo
+    return hobo
+
+
+def dev(torch, X):
+    return torch.from_numpy(np.ascontiguousarray(X, np.uint8)).cuda()
+
+
+def energies(H, torch, t, X, row0=0):
+    E, best = t.energy(dev(torch, X), row0=row0)
+    torch.cuda.synchronize()
+    return E.cpu().numpy().astype(np.float64), best
+
+
+def fields(H, torch, t, X):
+    G, E = t.local_field(dev(torch, X))
+    torch.cuda.synchronize()
+    return G.cpu().numpy().astype(np.float64), E.cpu().numpy().astype(np.float64)
+
+
+def check_argmin(best, E_or, tau, row0=0):
+    order = np.argsort(E_or, kind="stable")
+    e1 = E_or[order[0]]
+    nxt = E_or[E_or > e1]
+    gap = (nxt.min() - e1) if nxt.size else np.inf
+    if gap > 2 * tau:
+        assert best[1] == row0 + int(np.flatnonzero(E_or == e1)[0])
+    else:
+        assert E_or[best[1] - row0] <= e1 + 2 * tau
+
+
+# ---- energies on integer instances: bit-exact ---------------------------------------------
+def test_energy_seating4_exhaustive(H, torch):
+    p = seating(4)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = exhaustive_X(16)
+    E, best = energies(H, torch, t, X)
+    assert np.array_equal(E, o.energy(X))
+    assert best == (-11.0, 46811)
+
+
+def test_energy_cfg1(H, torch):
+    p = seating(4)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = x_bits(1, 1024, 16)
+    E, best = energies(H, torch, t, X)
+    assert np.array_equal(E, o.energy(X)) and best == (-10.0, 551)
+
+
+def test_energy_paper_problems(H, torch):
+    t = H.HoboTensor.from_problem(seating(5))
+    E, _ = energies(H, torch, t, paper_grids())
+    assert np.all(E == -17.0)
+    for p, emin, arg in ((pythagoras(), -30.0, 1332), (tsp(), -360.0, 27)):
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        X = exhaustive_X(p.N)
+        E, best = energies(H, torch, t, X)
+        assert np.array_equal(E, o.energy(X)), p.name
+        assert best == (emin, arg), p.name
+
+
+def test_energy_seating5_full_space(H, torch):
+    """2^25 candidates in one batch: min -17 at the lowest ground-state index."""
+    t = H.HoboTensor.from_problem(seating(5))
+    b = torch.arange(1 << 25, device="cuda", dtype=torch.int64)[:, None]
+    X = ((b >> torch.arange(25, device="cuda")[None, :]) & 1).to(torch.uint8).contiguous()
+    E, best = t.energy(X)
+    torch.cuda.synchronize()
+    assert best == (-17.0, 14539195)
+    assert int((E == -17.0).sum()) == 5
+
+
+@pytest.mark.parametrize("order,N,B,seed", [(1, 37, 129, 1), (2, 100, 1000, 2), (3, 33, 127, 3), (3, 100, 300, 4),
+                                            (3, 257, 130, 5), (4, 40, 200, 6), (5, 14, 256, 7), (6, 9, 100, 8),
+                                            (2, 1, 5, 9), (3, 3, 1, 10)])
+def test_energy_integer_dense(H, torch, order, N, B, seed):
+    if order <= 4 and N >= 20:
+        idx, val = int_twin_cells(order, N, seed)
+        t, o = H.HoboTensor.import_cells(order, N, idx, val), Oracle.from_cells(order, N, idx, val)
+    else:
+        p = random_integer_problem(order, N, seed, nterms=300)
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = x_bits(seed, B, N)
+    E, best = energies(H, torch, t, X, row0=7)
+    Eo = o.energy(X)
+    assert np.array_equal(E, Eo)
+    check_argmin(best, Eo, 0.0, row0=7)
+
+
+# ---- fp32 coefficients: tolerance -----------------------------------------------------------
+@pytest.mark.parametrize("order,N,B,seed", [(2, 300, 700, 11), (3, 130, 500, 12), (3, 256, 256, 13), (4, 30, 300, 14)])
+def test_energy_fp32(H, torch, order, N, B, seed):
+    idx, val = uniform_cells(order, N, seed)
+    t, o = H.HoboTensor.import_cells(order, N, idx, val), Oracle.from_cells(order, N, idx, val)
+    assert t.limbs == 3
+    X = x_bits(seed, B, N)
+    E, best = energies(H, torch, t, X)
+    Eo = o.energy(X)
+    assert np.max(np.abs(E - Eo)) <= o.tau
+    check_argmin(best, Eo, o.tau)
+
+
+# ---- local fields ---------------------------------------------------------------------------
+@pytest.mark.parametrize("order,N,B,seed", [(1, 40, 64, 1), (2, 70, 300, 2), (3, 50, 200, 3), (3, 300, 129, 4),
+                                            (4, 24, 150, 5), (5, 12, 100, 6), (6, 8, 64, 7)])
+def test_field_integer(H, torch, order, N, B, seed):
+    p = random_integer_problem(order, N, seed, nterms=400)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = x_bits(seed, B, N)
+    G, E = fields(H, torch, t, X)
+    assert np.array_equal(G, o.field(X))
+    assert np.array_equal(E, o.energy(X))
+
+
+def test_field_paper_problems(H, torch):
+    for p in (seating(4), pythagoras(), tsp()):
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        X = exhaustive_X(p.N)
+        G, E = fields(H, torch, t, X)
+        assert np.array_equal(G, o.field(X)), p.name
+        assert np.array_equal(E, o.energy(X)), p.name
+
+
+@pytest.mark.parametrize("order,N,B,seed", [(2, 260, 300, 21), (3, 100, 257, 22), (4, 20, 130, 23)])
+def test_field_fp32(H, torch, order, N, B, seed):
+    idx, val = uniform_cells(order, N, seed)
+    t, o = H.HoboTensor.import_cells(order, N, idx, val), Oracle.from_cells(order, N, idx, val)
+    X = x_bits(seed, B, N)
+    G, E = fields(H, torch, t, X)
+    assert np.max(np.abs(G - o.field(X))) <= o.tau
+    assert np.max(np.abs(E - o.energy(X))) <= o.tau
+
+
+# ---- full-size configs, sampled -------------------------------------------------------------
+def test_cfg3_full_batch_sampled(H, torch):
+    """BASELINE config 3 at its full size (B=65536) in the bench's launch configuration;
+    every 2048th candidate is checked against the oracle, bit-exact."""
+    p = cfg3_problem()
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = x_bits(3, 65536, 512)
+    G, E = fields(H, torch, t, X)
+    rows = np.arange(0, 65536, 2048)
+    assert np.array_equal(G[rows], o.field(X[rows]))
+    assert np.array_equal(E[rows], o.energy(X[rows]))
+    Ee, best = energies(H, torch, t, X)
+    assert np.array_equal(Ee, E)                       # energy mode == field-mode energies
+    assert Ee[best[1]] == best[0] == Ee.min() and best[1] == int(np.argmin(Ee))
+
+
+def test_cfg2_full_batch(H, torch):
+    """BASELINE config 2: QUBO N=1024 U(-1,1), B=65536.  Closed form x^T Q x (float64 numpy)
+    on a sample, oracle on fewer rows, and the argmin."""
+    idx, val = uniform_cells(2, 1024, 2)
+    t, o = H.HoboTensor.import_cells(2, 1024, idx, val), Oracle.from_cells(2, 1024, idx, val)
+    X = x_bits(2, 65536, 1024)
+    E, best = energies(H, torch, t, X)
+    rows = np.arange(0, 65536, 4096)
+    assert np.max(np.abs(E[rows] - o.energy(X[rows]))) <= o.tau
+    assert np.allclose(E[:4], [225.87784564495087, 211.0458381175995, 31.37024474143982, 149.2058583498001],
+                       rtol=0, atol=o.tau)
+    assert E[best[1]] == best[0] == E.min()
+
+
+# ---- search ---------------------------------------------------------------------------------
+def test_search_finds_brute_force_optimum(H, torch):
+    for p, emin, nch, it in ((seating(4), -11.0, 1024, 64), (pythagoras(), -30.0, 2048, 64), (tsp(), -360.0, 256, 32)):
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        x, e, c = t.search(1, nch, it)
+        assert e == emin, p.name
+        assert o.energy(x[None])[0] == e, p.name          # energy honesty
+
+
+def test_search_replays_oracle_exactly(H, torch):
+    """Integer instance: the device search and the oracle replay agree chain for chain."""
+    p = random_integer_problem(3, 40, 77, nterms=500)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    for chain0, n, iters in ((0, 300, 20), (1000, 129, 7), (5, 1, 0)):
+        x, e, c = t.search(9, None, iters, chain0=chain0, nchains=n)
+        r = o.search(9, chain0, n, iters)
+        assert (e, c) == (r["e_best"], r["best_chain"])
+        assert np.array_equal(x, r["chain_xbest"][c - chain0])
+
+
+def test_search_shard_invariance(H, torch):
+    p = seating(4)
+    t = H.HoboTensor.from_problem(p)
+    full = t.search(3, 512, 16)
+    a = t.search(3, None, 16, chain0=0, nchains=256)
+    b = t.search(3, None, 16, chain0=256, nchains=256)
+    win = min((a[1], a[2], 0), (b[1], b[2], 1))
+    assert (full[1], full[2]) == win[:2]

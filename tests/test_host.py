@@ -1,0 +1,131 @@
+"""CPU tests of the product's host side: the C-ABI library loads and exports every symbol
+of include/hobo.h, and its compiler (hobo_tensor_build / import_cells) produces exactly the
+oracle's canonical cells.  No GPU compute is called here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import Oracle
+from workloads import (TermBuilder, cfg3_problem, int_twin_cells, pythagoras, random_integer_problem,
+                       seating, tsp, uniform_cells)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2407_19987_b200 import build
+    build.build()
+    from paper_2407_19987_b200 import hobo
+    return hobo
+
+
+def test_library_exports_every_header_symbol(H):
+    import ctypes
+    hdr = open(os.path.join(ROOT, "include", "hobo.h")).read()
+    names = set(re.findall(r"^\s*(?:hobo_status|const char\*)\s+(hobo_\w+)\s*\(", hdr, re.M))
+    assert len(names) >= 12
+    L = H.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(H.EXPORTED) == names
+    # the library must link no oracle code
+    so = open(H.LIB_PATH, "rb").read()
+    assert b"or_energy" not in so and b"hobo_oracle" not in so
+    assert isinstance(ctypes.CDLL(H.LIB_PATH), ctypes.CDLL)
+
+
+def _same_cells(t, o):
+    i1, v1 = t.cells()
+    i2, v2 = o.cells()
+    assert np.array_equal(i1, i2)
+    assert np.array_equal(v1.view(np.uint32), v2.view(np.uint32))   # bit-exact fp32 cells
+
+
+@pytest.mark.parametrize("maker", [lambda: seating(5), pythagoras, tsp, cfg3_problem,
+                                   lambda: random_integer_problem(3, 20, 5, 200),
+                                   lambda: random_integer_problem(4, 9, 6, 300),
+                                   lambda: random_integer_problem(2, 30, 7, 400)])
+def test_build_matches_oracle_cells(H, maker):
+    p = maker()
+    t = H.HoboTensor.from_problem(p)
+    o = Oracle.from_problem(p)
+    _same_cells(t, o)
+    assert t.offset == o.offset and t.ncells == o.ncells
+    assert t.is_integer == o.is_integer and t.sum_abs == o.sum_abs
+
+
+def test_build_non_integer_terms_matches_oracle(H):
+    rng = np.random.default_rng(3)
+    tb = TermBuilder()
+    for _ in range(300):
+        k = int(rng.integers(0, 4))
+        facs = []
+        for _ in range(k):
+            if rng.random() < 0.5:
+                facs.append((float(rng.normal()), [(int(rng.integers(0, 12)), float(rng.normal()))]))
+            else:
+                facs.append((0.0, [(int(rng.integers(0, 12)), 1.0)]))
+        tb.add(float(rng.normal()), facs)
+    p = tb.problem(3, 12)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    i1, v1 = t.cells()
+    i2, v2 = o.cells()
+    assert np.array_equal(i1, i2)
+    # both expand in long double and round once; allow 1 ulp where the summation order differs
+    assert np.all(np.abs(v1.view(np.int32) - v2.view(np.int32)) <= 1)
+    assert abs(t.offset - o.offset) <= 1e-12 * max(1, abs(o.offset))
+
+
+@pytest.mark.parametrize("order,N,seed,kind", [(2, 64, 2, "u"), (3, 24, 5, "u"), (4, 10, 4, "u"), (3, 30, 9, "int")])
+def test_import_cells_matches_oracle(H, order, N, seed, kind):
+    idx, val = (uniform_cells if kind == "u" else int_twin_cells)(order, N, seed)
+    # scramble index order inside each cell: import must canonicalise by index set
+    rng = np.random.default_rng(seed)
+    idx = np.take_along_axis(idx, rng.permuted(np.tile(np.arange(order), (len(idx), 1)), axis=1), axis=1)
+    t = H.HoboTensor.import_cells(order, N, idx, val)
+    o = Oracle.from_cells(order, N, idx, val)
+    _same_cells(t, o)
+
+
+def test_dense_export_matches_oracle(H):
+    p = tsp()
+    assert np.array_equal(H.HoboTensor.from_problem(p).dense(), Oracle.from_problem(p).dense())
+
+
+def test_limb_counts(H):
+    assert H.HoboTensor.from_problem(seating(4)).limbs == 1
+    assert H.HoboTensor.from_problem(tsp()).limbs == 1
+    assert H.HoboTensor.from_problem(cfg3_problem()).limbs == 1
+    assert H.HoboTensor.from_problem(pythagoras()).limbs == 2     # 14-bit coefficients
+    assert H.HoboTensor.import_cells(3, 20, *uniform_cells(3, 20, 1)).limbs == 3
+
+
+def test_errors(H):
+    tb = TermBuilder()
+    tb.add(1.0, [(0.0, [(0, 1.0)]), (0.0, [(1, 1.0)]), (0.0, [(2, 1.0)])])
+    p = tb.problem(2, 3)                    # degree 3 > order 2
+    with pytest.raises(H.HoboError) as e:
+        H.HoboTensor.from_problem(p)
+    assert e.value.status == H.HOBO_EINVAL
+    tb = TermBuilder()
+    tb.add(1.0, [(0.0, [(5, 1.0)])])        # id outside [0, N)
+    with pytest.raises(H.HoboError):
+        H.HoboTensor.from_problem(tb.problem(2, 3))
+    tb = TermBuilder()
+    tb.add(float("nan"), [(0.0, [(0, 1.0)])])
+    with pytest.raises(H.HoboError):
+        H.HoboTensor.from_problem(tb.problem(2, 3))
+    tb = TermBuilder()
+    tb.add(1e300, [(0.0, [(0, 1.0)])])
+    with pytest.raises(H.HoboError) as e:
+        H.HoboTensor.from_problem(tb.problem(2, 3))
+    assert e.value.status == H.HOBO_ERANGE
+    # cancellation to zero is fine even above the order
+    tb = TermBuilder()
+    tb.add(1.0, [(0.0, [(i, 1.0)]) for i in range(4)])
+    tb.add(-1.0, [(0.0, [(i, 1.0)]) for i in range(4)])
+    tb.add(2.0, [(0.0, [(0, 1.0)])])
+    assert H.HoboTensor.from_problem(tb.problem(2, 4)).ncells == 1

@@ -254,7 +254,7 @@ def random_integer_problem(order: int, N: int, seed: int, nterms: int, maxc: int
         facs = []
         for _ in range(deg):
             if with_affine and rng.random() < 0.3:
-                k = int(rng.integers(1, 3))
+                k = min(int(rng.integers(1, 3)), N)
                 vs = rng.choice(N, size=k, replace=False)
                 facs.append((float(rng.integers(-1, 2)), [(int(v), float(rng.integers(-2, 3) or 1)) for v in vs]))
             else:
