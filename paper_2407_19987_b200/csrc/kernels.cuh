@@ -24,7 +24,7 @@ namespace hobo {
 
 constexpr int kBM = 128;        // candidates per CTA (UMMA M, TMEM lanes)
 constexpr int kBK = 64;         // tuples per K-block (one 128-byte SW128 row of bf16)
-constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA, warps 2-5 A-generator + epilogue
+constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2-9 A-generator + epilogue (2 per lane quarter)
 
 struct KrParams {
   const uint32_t* xbits;    // [B][W] bit-packed candidates (bit m of word m/32)
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NB; ++s) { mbar_init(FULL_B(s), 1); mbar_init(EMPTY_B(s), 1); }
-    for (int s = 0; s < C::NA; ++s) { mbar_init(FULL_A(s), 4); mbar_init(EMPTY_A(s), 1); }
+    for (int s = 0; s < C::NA; ++s) { mbar_init(FULL_A(s), 8); mbar_init(EMPTY_A(s), 1); }
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
@@ -177,8 +177,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       else mbar_arrive(acc_full);
     }
   } else {
-    // ---------------- A generator, then epilogue (warps 2..5) ---------------------------------
-    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    // ---------------- A generator, then epilogue (warps 2..9) ---------------------------------
+    // warp w serves TMEM lane quarter q = w % 4 (rows 32q..32q+31) and half h of each K-block
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
     const int row = q * 32 + lane;   // candidate row within the block == TMEM lane
     int sa = 0;
     uint32_t pha = 0;
@@ -187,17 +189,24 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       for (int kb = s.x; kb < s.x + s.y; ++kb) {
         mbar_wait(EMPTY_A(sa), pha ^ 1u);
         const uint64_t bits = kr_row_bits(xs, row, p.runs, __ldg(p.run_off + kb), __ldg(p.run_off + kb + 1));
+        const uint32_t half = (uint32_t)(bits >> (32 * h));
+        // 32 bits -> 16 words of two bf16 {0, 1.0}: PRMT replicates the msb of a byte into
+        // a 0x00/0xFF byte; bit 2i+s sits at a byte msb after shifting by 7-2s (or 6-2s).
+        uint32_t w[16];
+#pragma unroll
+        for (int sh = 0; sh < 4; ++sh) {
+          const uint32_t ev = half << (7 - 2 * sh), od = half << (6 - 2 * sh);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t sel = (0x8u | k) | ((0x8u | k) << 4) | ((0xCu | k) << 8) | ((0xCu | k) << 12);
+            w[4 * k + sh] = prmt_b32(ev, od, sel) & 0x3F803F80u;
+          }
+        }
         const uint32_t rowaddr = sA + sa * C::A_STAGE + row * 128;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t byte = (uint32_t)(bits >> (8 * c)) & 0xFFu;
-          uint32_t w4[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t t = byte >> (2 * i);
-            w4[i] = (t & 1u) * 0x3F80u + (t & 2u) * 0x1FC00000u;  // two bf16 {0, 1.0}
-          }
-          st_shared_v4(rowaddr + ((uint32_t)(c ^ (row & 7)) << 4), w4[0], w4[1], w4[2], w4[3]);
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t chunk = (uint32_t)(4 * h + c);
+          st_shared_v4(rowaddr + ((chunk ^ (uint32_t)(row & 7)) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
         }
         fence_async_smem();
         __syncwarp();
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       }
     }
 
-    // ---------------- epilogue -----------------------------------------------------------------
+    // ---------------- epilogue: warp half h takes column chunks [h*NT/2, (h+1)*NT/2) ------------
     uint32_t used = 0;
     for (int j = 0; j < p.nseg; ++j)
       if (sched[j].y > 0) used |= 1u << (p.field_mode ? j : 0);
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     const bool live = b < p.B;
     double qsum = 0.0;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    for (int c0 = 0; c0 < NT; c0 += 32) {
+    for (int c0 = h * (NT / 2); c0 < (h + 1) * (NT / 2); c0 += 32) {
       const int mbase = ct * NT + c0;
       const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
       float g[32];
@@ -255,7 +264,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
       }
     }
-    if (live) p.Q[(size_t)ct * p.B + b] = qsum;
+    // combine the two column halves in a fixed order (deterministic, no atomics)
+    double* qpart = reinterpret_cast<double*>(gbase + (sA - base));  // A stage 0 is free now
+    if (h == 1) qpart[row] = qsum;
+    named_bar_sync(1, 256);
+    if (h == 0 && live) p.Q[(size_t)ct * p.B + b] = qsum + qpart[row];
   }
 #undef FULL_B
 #undef EMPTY_B
