@@ -46,6 +46,7 @@ struct hobo_tensor {
   bool dev_init = false;
   bool poisoned = false;
   uint4* d_runs = nullptr;
+  uint4* d_kdesc = nullptr;
   uint32_t* d_runoff = nullptr;
   float* d_p1 = nullptr;   // padded to 256-multiples
   int W = 0;               // 32-bit words per candidate bit row
@@ -161,6 +162,9 @@ hobo_status init_device(hobo_tensor* t) {
   CK(cudaMalloc(&t->d_runs, std::max<size_t>(t->kl.runs.size() / 4, 1) * sizeof(uint4)));
   if (!t->kl.runs.empty())
     CK(cudaMemcpy(t->d_runs, t->kl.runs.data(), t->kl.runs.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_kdesc, std::max<size_t>(t->kl.kdesc.size() / 4, 2) * sizeof(uint4)));
+  if (!t->kl.kdesc.empty())
+    CK(cudaMemcpy(t->d_kdesc, t->kl.kdesc.data(), t->kl.kdesc.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&t->d_runoff, t->kl.run_off.size() * 4));
   CK(cudaMemcpy(t->d_runoff, t->kl.run_off.data(), t->kl.run_off.size() * 4, cudaMemcpyHostToDevice));
   const int Npad = (N + 255) / 256 * 256;
@@ -264,7 +268,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   KrParams p;
   p.xbits = bits;
   p.runs = t->d_runs;
-  p.run_off = t->d_runoff;
+  p.kdesc = t->d_kdesc;
   p.sched = L.d_sched;
   p.p1 = t->d_p1;
   p.G = G;
@@ -361,7 +365,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
     if (L.d_sched) cudaFree(L.d_sched);
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
-  void* ptrs[] = {t->d_runs, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
+  void* ptrs[] = {t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;

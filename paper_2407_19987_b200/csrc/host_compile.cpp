@@ -344,6 +344,18 @@ int build_klayout(int order, int N, KLayout& k, std::string& msg) {
     while (ri < run_t.size() && run_t[ri] < kb * KBLK) ++ri;
     k.run_off[(size_t)kb] = (uint32_t)ri;
   }
+  k.kdesc.assign((size_t)nkb * 8, 0);
+  if (k.runs.size() / 4 + 2 >= (1u << 22)) { msg = "too many generator runs"; return 3; }
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    int seg = 0;
+    while (seg + 1 < k.nseg && k.seg_t0[seg + 1] <= kb * KBLK) ++seg;
+    const uint32_t nfix = (uint32_t)std::max(0, order - seg - 2);
+    const uint32_t r0 = k.run_off[(size_t)kb], n = k.run_off[(size_t)kb + 1] - r0;
+    uint32_t* d = &k.kdesc[(size_t)kb * 8];
+    for (uint32_t q = 0; q < std::min(n, 2u); ++q)
+      for (int f = 0; f < 4; ++f) d[4 * q + f] = k.runs[(size_t)(r0 + q) * 4 + f];
+    d[3] = nfix | (n << 3) | ((r0 + 2) << 10);
+  }
   return 0;
 }
 

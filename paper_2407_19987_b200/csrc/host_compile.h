@@ -47,6 +47,9 @@ struct KLayout {
   std::vector<uint16_t> tuples;       // [Tpad][6]: r (0 = padding), then the r-1 elements
   std::vector<uint32_t> runs;         // [nruns][4] generator runs (see kernels.cuh)
   std::vector<uint32_t> run_off;      // [Tpad/KBLK + 1]
+  // per K-block descriptor, directly indexed (no dependent loads): two inline runs
+  // rec0, rec1; rec0.w = nfix | nruns << 3 | (index of the 3rd run in `runs`) << 10
+  std::vector<uint32_t> kdesc;        // [Tpad/KBLK][8]
 };
 int build_klayout(int order, int N, KLayout& k, std::string& msg);
 

@@ -29,7 +29,7 @@ constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2-9 A-generator
 struct KrParams {
   const uint32_t* xbits;    // [B][W] bit-packed candidates (bit m of word m/32)
   const uint4* runs;        // A-generator runs (host_compile.cpp build_klayout)
-  const uint32_t* run_off;  // [n_kb + 1]
+  const uint4* kdesc;       // [n_kb][2] per-K-block descriptor (two inline runs)
   const int2* sched;        // [n_ct][nseg] (first K-block, #K-blocks)
   const float* p1;          // [Npad] degree-1 cells (the field of an order-1 term), 0 past N
   float* G;                 // field mode: [B][N] local fields; else nullptr
@@ -56,26 +56,70 @@ struct KrCfg {
   }
 };
 
-// one thread builds its candidate's 64-bit row of A for one K-block from the block's runs
-__device__ __forceinline__ uint64_t kr_row_bits(const uint32_t* xs, int row, const uint4* __restrict__ runs, uint32_t r0,
-                                                uint32_t r1) {
-  uint64_t bits = 0;
-  for (uint32_t i = r0; i < r1; ++i) {
-    const uint4 rr = __ldg(runs + i);
-    const uint32_t start = rr.x & 0xFFu, cnt = (rr.x >> 8) & 0xFFu, lo = rr.x >> 16;
-    uint32_t on = 1;
-    const uint32_t f[4] = {rr.y & 0xFFFFu, rr.y >> 16, rr.z & 0xFFFFu, rr.z >> 16};
+// A bits of one run for one candidate row: x[lo .. lo+cnt) AND the fixed elements' bits,
+// placed at tuple offset `start` of the K-block (see host_compile.cpp build_klayout)
+__device__ __forceinline__ uint64_t run_bits(const uint32_t* xs, int row, const uint4 rr, uint32_t nfix) {
+  const uint32_t start = rr.x & 0xFFu, cnt = (rr.x >> 8) & 0xFFu, lo = rr.x >> 16;
+  uint32_t on = 1;
+  const uint32_t f[4] = {rr.y & 0xFFFFu, rr.y >> 16, rr.z & 0xFFFFu, rr.z >> 16};
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (f[q] != 0xFFFFu) on &= xs[(f[q] >> 5) * kBM + row] >> (f[q] & 31);
-    const uint32_t w = lo >> 5, sh = lo & 31;
-    uint64_t v = ((uint64_t)xs[(w + 1) * kBM + row] << 32) | xs[w * kBM + row];
-    v >>= sh;
-    if (sh) v |= (uint64_t)xs[(w + 2) * kBM + row] << (64 - sh);
-    const uint64_t mask = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1ull);
-    if (on & 1u) bits |= (v & mask) << start;
-  }
+  for (int q = 0; q < 4; ++q)
+    if ((uint32_t)q < nfix) on &= xs[(f[q] >> 5) * kBM + row] >> (f[q] & 31);
+  const uint32_t w = lo >> 5, sh = lo & 31;
+  uint64_t v = ((uint64_t)xs[(w + 1) * kBM + row] << 32) | xs[w * kBM + row];
+  v >>= sh;
+  if (sh) v |= (uint64_t)xs[(w + 2) * kBM + row] << (64 - sh);
+  const uint64_t mask = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1ull);
+  return (on & 1u) ? (v & mask) << start : 0ull;
+}
+
+// the candidate row's 64 A bits of one K-block from its descriptor (d0, d1)
+__device__ __forceinline__ uint64_t block_bits(const uint32_t* xs, int row, const uint4 d0, const uint4 d1,
+                                               const uint4* __restrict__ runs) {
+  const uint32_t nfix = d0.w & 7u, nruns = (d0.w >> 3) & 127u;
+  uint64_t bits = 0;
+  if (nruns > 0) bits |= run_bits(xs, row, d0, nfix);
+  if (nruns > 1) bits |= run_bits(xs, row, d1, nfix);
+  for (uint32_t i = 2; i < nruns; ++i) bits |= run_bits(xs, row, __ldg(runs + (d0.w >> 10) + (i - 2)), nfix);
   return bits;
+}
+
+// 32 bits -> 16 words of two bf16 {0, 1.0}.  prmt with a selector-nibble msb replicates the
+// picked byte's sign bit: after shifting by 7-2s (6-2s) bit 8k+2s (+1) is byte k's msb.
+__device__ __forceinline__ void expand32(uint32_t half, uint32_t (&w)[16]) {
+#pragma unroll
+  for (int sh = 0; sh < 4; ++sh) {
+    const uint32_t ev = half << (7 - 2 * sh), od = half << (6 - 2 * sh);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t sel = (0x8u | k) | ((0x8u | k) << 4) | ((0xCu | k) << 8) | ((0xCu | k) << 12);
+      w[4 * k + sh] = prmt_b32(ev, od, sel) & 0x3F803F80u;
+    }
+  }
+}
+
+// position in the CTA's K schedule (segment j, K-block kb)
+struct KPos {
+  int j, kb, end;
+};
+__device__ __forceinline__ void kpos_next(KPos& p, const int2* sched, int nseg) {
+  if (++p.kb < p.end) return;
+  while (++p.j < nseg) {
+    const int2 s = sched[p.j];
+    p.kb = s.x;
+    p.end = s.x + s.y;
+    if (s.y > 0) return;
+  }
+}
+__device__ __forceinline__ KPos kpos_first(const int2* sched, int nseg) {
+  KPos p{-1, 0, 0};
+  while (++p.j < nseg) {
+    const int2 s = sched[p.j];
+    p.kb = s.x;
+    p.end = s.x + s.y;
+    if (s.y > 0) return p;
+  }
+  return p;
 }
 
 template <int NT, int NACC>
@@ -105,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NB; ++s) { mbar_init(FULL_B(s), 1); mbar_init(EMPTY_B(s), 1); }
-    for (int s = 0; s < C::NA; ++s) { mbar_init(FULL_A(s), 8); mbar_init(EMPTY_A(s), 1); }
+    for (int s = 0; s < C::NA; ++s) { mbar_init(FULL_A(s), 4); mbar_init(EMPTY_A(s), 1); }
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
@@ -178,41 +222,45 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     }
   } else {
     // ---------------- A generator, then epilogue (warps 2..9) ---------------------------------
-    // warp w serves TMEM lane quarter q = w % 4 (rows 32q..32q+31) and half h of each K-block
+    // team h = (w-2)/4 builds every other K-block (h = 0: even, 1: odd positions of the
+    // schedule); warp w of a team serves TMEM lane quarter q = w % 4 (rows 32q..32q+31).
+    // The next descriptor of the team is prefetched one iteration ahead.
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
     const int row = q * 32 + lane;   // candidate row within the block == TMEM lane
-    int sa = 0;
+    KPos pos = kpos_first(sched, p.nseg);
+    if (h == 1 && pos.j < p.nseg) kpos_next(pos, sched, p.nseg);
+    uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
+    if (pos.j < p.nseg) { d0 = __ldg(p.kdesc + 2 * pos.kb); d1 = __ldg(p.kdesc + 2 * pos.kb + 1); }
+    int sa = h;
     uint32_t pha = 0;
-    for (int j = 0; j < p.nseg; ++j) {
-      const int2 s = sched[j];
-      for (int kb = s.x; kb < s.x + s.y; ++kb) {
-        mbar_wait(EMPTY_A(sa), pha ^ 1u);
-        const uint64_t bits = kr_row_bits(xs, row, p.runs, __ldg(p.run_off + kb), __ldg(p.run_off + kb + 1));
-        const uint32_t half = (uint32_t)(bits >> (32 * h));
-        // 32 bits -> 16 words of two bf16 {0, 1.0}: PRMT replicates the msb of a byte into
-        // a 0x00/0xFF byte; bit 2i+s sits at a byte msb after shifting by 7-2s (or 6-2s).
+    while (pos.j < p.nseg) {
+      KPos nx = pos;
+      kpos_next(nx, sched, p.nseg);
+      if (nx.j < p.nseg) kpos_next(nx, sched, p.nseg);
+      uint4 n0 = d0, n1 = d1;
+      if (nx.j < p.nseg) { n0 = __ldg(p.kdesc + 2 * nx.kb); n1 = __ldg(p.kdesc + 2 * nx.kb + 1); }
+      mbar_wait(EMPTY_A(sa), pha ^ 1u);
+      const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
+      const uint32_t rowaddr = sA + sa * C::A_STAGE + row * 128;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
         uint32_t w[16];
-#pragma unroll
-        for (int sh = 0; sh < 4; ++sh) {
-          const uint32_t ev = half << (7 - 2 * sh), od = half << (6 - 2 * sh);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t sel = (0x8u | k) | ((0x8u | k) << 4) | ((0xCu | k) << 8) | ((0xCu | k) << 12);
-            w[4 * k + sh] = prmt_b32(ev, od, sel) & 0x3F803F80u;
-          }
-        }
-        const uint32_t rowaddr = sA + sa * C::A_STAGE + row * 128;
+        expand32((uint32_t)(bits >> (32 * half)), w);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const uint32_t chunk = (uint32_t)(4 * h + c);
+          const uint32_t chunk = (uint32_t)(4 * half + c);
           st_shared_v4(rowaddr + ((chunk ^ (uint32_t)(row & 7)) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
         }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(FULL_A(sa));
-        if (++sa == C::NA) { sa = 0; pha ^= 1u; }
       }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(FULL_A(sa));
+      sa += 2;                                   // this team's next stage in the ring
+      if (sa >= C::NA) { sa -= C::NA; pha ^= 1u; }
+      pos = nx;
+      d0 = n0;
+      d1 = n1;
     }
 
     // ---------------- epilogue: warp half h takes column chunks [h*NT/2, (h+1)*NT/2) ------------
