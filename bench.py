@@ -242,14 +242,16 @@ def main():
     exec_flops = 2.0 * st["mma_macs"]
     kms = statistics.mean(kern_ms)
     burst, sustained, src = measured_peaks()
-    peak = sustained   # the kernel runs back to back inside a seconds-long timed region
+    # the timed region is ~0.3 s of back-to-back ~7 ms steps with clocks at max (see "clocks"):
+    # judged against the BURST figure; the sustained (power-capped) ratio is reported beside it
+    peak = burst
     achieved = algo_flops / (kms / 1e3) / 1e12
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": None, "kernel": "kr_gemm_kernel<256,2> (open-index contraction, field mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms,
             "algorithmic_flops_per_launch": algo_flops, "executed_mma_flops_per_launch": exec_flops,
-            "executed_tflops": exec_flops / (kms / 1e3) / 1e12, "frac_of_burst": achieved / burst,
-            "peak_source": f"{src} bf16 dense, sustained {sustained} / burst {burst} TFLOP/s"}
+            "executed_tflops": exec_flops / (kms / 1e3) / 1e12, "frac_of_sustained": achieved / sustained,
+            "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s"}
 
     extras = {}
     if not a.no_extras:

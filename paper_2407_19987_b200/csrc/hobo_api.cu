@@ -27,13 +27,13 @@ hobo_status fail(hobo_status s, const std::string& msg) {
 
 struct DevLayout {
   bool built = false;
-  int NT = 256, NACC = 1, n_ct = 0, Npad = 0;
+  int NT = 256, n_ct = 0, Npad = 0;
   __nv_bfloat16* W = nullptr;
   int2* d_sched = nullptr;
   std::vector<int32_t> sched;
   alignas(64) CUtensorMap tmap;
   double lcm = 1.0;
-  double wacc[6] = {1, 1, 1, 1, 1, 1};
+  double wdeg[8] = {1, 1, 1, 1, 1, 1, 1, 1};
   double wp = 1.0;
 };
 
@@ -87,17 +87,6 @@ hobo_status grow(hobo_tensor* t, T*& p, size_t& cap, size_t n) {
   return HOBO_OK;
 }
 
-void field_tile(int order, int& NT, int& NACC) {
-  switch (order) {
-    case 1: NT = 256; NACC = 1; break;
-    case 2: NT = 256; NACC = 1; break;
-    case 3: NT = 256; NACC = 2; break;
-    case 4: NT = 128; NACC = 3; break;
-    case 5: NT = 128; NACC = 4; break;
-    default: NT = 64; NACC = 5; break;
-  }
-}
-
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -114,10 +103,10 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int NT, int NACC>
+template <int NT>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  auto* k = kr_gemm_kernel<NT, NACC>;
-  const size_t smem = KrCfg<NT, NACC>::smem_bytes(p.W);
+  auto* k = kr_gemm_kernel<NT>;
+  const size_t smem = KrCfg<NT>::smem_bytes(p.W);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -128,13 +117,7 @@ cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  if (L.NT == 256 && L.NACC == 1) return launch_kr<256, 1>(L, p, s);
-  if (L.NT == 256 && L.NACC == 2) return launch_kr<256, 2>(L, p, s);
-  if (L.NT == 128 && L.NACC == 3) return launch_kr<128, 3>(L, p, s);
-  if (L.NT == 128 && L.NACC == 4) return launch_kr<128, 4>(L, p, s);
-  return launch_kr<64, 5>(L, p, s);
-}
+cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) { return launch_kr<256>(L, p, s); }
 
 hobo_status init_device(hobo_tensor* t);
 
@@ -183,8 +166,7 @@ hobo_status ensure_layout(hobo_tensor* t, int field) {
   if (L.built) return HOBO_OK;
   const HostTensor& H = t->host;
   const int N = H.N, k = H.order;
-  if (field) field_tile(k, L.NT, L.NACC);
-  else { L.NT = 256; L.NACC = 1; }
+  L.NT = 256;
   if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
   L.n_ct = (N + L.NT - 1) / L.NT;
   L.Npad = L.n_ct * L.NT;
@@ -257,7 +239,7 @@ hobo_status ensure_layout(hobo_tensor* t, int field) {
       lcm = lcm * r / a;
     }
     L.lcm = lcm;
-    for (int j = 0; j < 6; ++j) L.wacc[j] = (j < k - 1) ? lcm / (double)(k - j) : 0.0;
+    for (int r = 0; r < 8; ++r) L.wdeg[r] = (r >= 1 && r <= k) ? lcm / (double)r : 0.0;
     L.wp = lcm;
   }
   L.built = true;
@@ -282,7 +264,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.nseg = t->kl.nseg;
   p.L = t->host.limbs;
   p.field_mode = (&L == &t->lay[1]) ? 1 : 0;
-  for (int j = 0; j < 6; ++j) p.wacc[j] = L.wacc[j];
+  for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
   return p;
 }

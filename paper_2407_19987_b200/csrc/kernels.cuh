@@ -36,23 +36,21 @@ struct KrParams {
   double* Q;                // [n_ct][B] weighted partial energies (fixed-order, no atomics)
   long long B;
   int N, W, Npad, n_ct, n_cb, nseg, L, field_mode;
-  double wacc[6];           // weight of accumulator j in the partial energy
+  double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
   double wp;                // weight of the degree-1 term
 };
 
-template <int NT, int NACC>
+template <int NT>
 struct KrCfg {
-  static constexpr int B_STAGE = NT * 128;   // NT rows x 64 bf16
-  static constexpr int A_STAGE = kBM * 128;  // 128 rows x 64 bf16
-  static constexpr int NB = NT >= 256 ? 5 : 8;
-  static constexpr int NA = NT >= 256 ? 3 : 4;
-  static constexpr int COLS = NACC * NT;
-  static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
-  static_assert(COLS <= 512, "TMEM holds 512 fp32 columns");
+  static constexpr int B_STAGE = NT * 128;               // NT rows x 64 bf16 (one SW128 atom row each)
+  static constexpr int NB = NT >= 256 ? 6 : 10;          // shared-memory B ring
+  static constexpr int A_COLS = kBK / 2;                 // TMEM columns per A stage (64 bf16 per lane)
+  static constexpr int NA = (512 - NT) / A_COLS < 8 ? (512 - NT) / A_COLS : 8;  // TMEM A ring
+  static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator, [NT, NT+NA*32): A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
-  static constexpr int BAR_BYTES = 8 * (2 * NB + 2 * NA + 1) + 16;
+  static constexpr int NBAR = 2 * NB + 2 * NA + 3;
   static size_t smem_bytes(int W) {
-    return 1024 + (size_t)NB * B_STAGE + (size_t)NA * A_STAGE + BAR_BYTES + 128 + (size_t)(W + 2) * kBM * 4;
+    return 1024 + (size_t)NB * B_STAGE + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)(W + 2) * kBM * 4 + 128;
   }
 };
 
@@ -98,44 +96,22 @@ __device__ __forceinline__ void expand32(uint32_t half, uint32_t (&w)[16]) {
   }
 }
 
-// position in the CTA's K schedule (segment j, K-block kb)
-struct KPos {
-  int j, kb, end;
-};
-__device__ __forceinline__ void kpos_next(KPos& p, const int2* sched, int nseg) {
-  if (++p.kb < p.end) return;
-  while (++p.j < nseg) {
-    const int2 s = sched[p.j];
-    p.kb = s.x;
-    p.end = s.x + s.y;
-    if (s.y > 0) return;
-  }
-}
-__device__ __forceinline__ KPos kpos_first(const int2* sched, int nseg) {
-  KPos p{-1, 0, 0};
-  while (++p.j < nseg) {
-    const int2 s = sched[p.j];
-    p.kb = s.x;
-    p.end = s.x + s.y;
-    if (s.y > 0) return p;
-  }
-  return p;
-}
-
-template <int NT, int NACC>
+template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
-  using C = KrCfg<NT, NACC>;
+  using C = KrCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 atoms need 1024-byte alignment
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sB = base;
-  const uint32_t sA = sB + C::NB * C::B_STAGE;
-  const uint32_t sBar = sA + C::NA * C::A_STAGE;
+  const uint32_t sBar = sB + C::NB * C::B_STAGE;
   const uint32_t acc_full = sBar + 8 * (2 * C::NB + 2 * C::NA);
-  const uint32_t tslot = acc_full + 8;
-  const uint32_t sX = (tslot + 16 + 127u) & ~127u;
+  const uint32_t snap_full = acc_full + 8, snap_empty = acc_full + 16;
+  const uint32_t tslot = acc_full + 24;
+  const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
+  const uint32_t sX = sQ + kBM * 8;
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
+  double* qpart = reinterpret_cast<double*>(gbase + (sQ - base));
   volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
 #define FULL_B(s) (sBar + 8u * (s))
 #define EMPTY_B(s) (sBar + 8u * (C::NB + (s)))
@@ -146,11 +122,16 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const int ct = blockIdx.x / p.n_cb, cb = blockIdx.x % p.n_cb;  // column-tile-major: concurrent CTAs share W tiles in L2
   const long long b0 = (long long)cb * kBM;
   const int2* sched = p.sched + (size_t)ct * p.nseg;
+  // segments run in ascending degree order (j = nseg-1 .. 0); in field mode the single
+  // accumulator is snapshot after each degree so the energy can weight degree r by 1/r
+  const bool snaps = p.field_mode != 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NB; ++s) { mbar_init(FULL_B(s), 1); mbar_init(EMPTY_B(s), 1); }
     for (int s = 0; s < C::NA; ++s) { mbar_init(FULL_A(s), 4); mbar_init(EMPTY_A(s), 1); }
     mbar_init(acc_full, 1);
+    mbar_init(snap_full, 1);
+    mbar_init(snap_empty, 8);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
@@ -175,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     if (lane == 0) {
       int sb = 0;
       uint32_t ph = 0;
-      for (int j = 0; j < p.nseg; ++j) {
+      for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
         for (int kb = s.x; kb < s.x + s.y; ++kb)
           for (int l = 0; l < p.L; ++l) {
@@ -187,117 +168,130 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread) ----------------------------------------------
+    // ---------------- MMA issuer (one thread): D[tmem] += A[tmem] * B[smem] ------------------
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
-      int sb = 0, sa = 0;
-      uint32_t phb = 0, pha = 0, used = 0;
-      for (int j = 0; j < p.nseg; ++j) {
+      int sb = 0, sa = 0, snap = 0;
+      uint32_t phb = 0, pha = 0, issued = 0;
+      for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
-        const int acc = p.field_mode ? j : 0;
-        const uint32_t d = tmem + (uint32_t)(acc * NT);
         for (int kb = s.x; kb < s.x + s.y; ++kb) {
           mbar_wait(FULL_A(sa), pha);
           tc_fence_after();
-          const uint64_t adesc = sw128_kmajor_desc(sA + sa * C::A_STAGE);
+          const uint32_t a_t = tmem + (uint32_t)(NT + sa * C::A_COLS);
           for (int l = 0; l < p.L; ++l) {
             mbar_wait(FULL_B(sb), phb);
             tc_fence_after();
             const uint64_t bdesc = sw128_kmajor_desc(sB + sb * C::B_STAGE);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              const uint32_t accumulate = ((used >> acc) & 1u) | (uint32_t)(l | k);
-              umma_bf16_ss(d, adesc + 2u * k, bdesc + 2u * k, idesc, accumulate);
-            }
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(l | k));
             umma_commit(EMPTY_B(sb));
             if (++sb == C::NB) { sb = 0; phb ^= 1u; }
           }
           umma_commit(EMPTY_A(sa));
           if (++sa == C::NA) { sa = 0; pha ^= 1u; }
-          used |= 1u << acc;
+          issued = 1;
+        }
+        if (snaps && j > 0) {  // hand the degree-(k-j) partial sum to the epilogue warps
+          if (issued) umma_commit(snap_full);
+          else mbar_arrive(snap_full);
+          mbar_wait(snap_empty, (uint32_t)(snap & 1));
+          tc_fence_after();
+          ++snap;
         }
       }
-      if (used) umma_commit(acc_full);
+      if (issued) umma_commit(acc_full);
       else mbar_arrive(acc_full);
     }
   } else {
-    // ---------------- A generator, then epilogue (warps 2..9) ---------------------------------
-    // team h = (w-2)/4 builds every other K-block (h = 0: even, 1: odd positions of the
-    // schedule); warp w of a team serves TMEM lane quarter q = w % 4 (rows 32q..32q+31).
-    // The next descriptor of the team is prefetched one iteration ahead.
+    // ---------------- A generator (warps 2..9), then epilogue --------------------------------
+    // team h = (w-2)/4 builds every other K-block of the schedule; warp w of a team serves
+    // TMEM lane quarter q = w % 4 (rows 32q..32q+31) and writes its rows of A with tcgen05.st.
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
     const int row = q * 32 + lane;   // candidate row within the block == TMEM lane
-    KPos pos = kpos_first(sched, p.nseg);
-    if (h == 1 && pos.j < p.nseg) kpos_next(pos, sched, p.nseg);
-    uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
-    if (pos.j < p.nseg) { d0 = __ldg(p.kdesc + 2 * pos.kb); d1 = __ldg(p.kdesc + 2 * pos.kb + 1); }
-    int sa = h;
-    uint32_t pha = 0;
-    while (pos.j < p.nseg) {
-      KPos nx = pos;
-      kpos_next(nx, sched, p.nseg);
-      if (nx.j < p.nseg) kpos_next(nx, sched, p.nseg);
-      uint4 n0 = d0, n1 = d1;
-      if (nx.j < p.nseg) { n0 = __ldg(p.kdesc + 2 * nx.kb); n1 = __ldg(p.kdesc + 2 * nx.kb + 1); }
-      mbar_wait(EMPTY_A(sa), pha ^ 1u);
-      const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
-      const uint32_t rowaddr = sA + sa * C::A_STAGE + row * 128;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const int c_lo = h * (NT / 2), c_hi = (h + 1) * (NT / 2);   // this warp's epilogue columns
+    double S[8];                     // S[r]: sum_m x_m F_m over this warp's columns after degree r
+    int nsnap = 0;
+    int n = 0;                       // position in the CTA's K-block sequence
+    bool any = false;                // has any MMA been issued yet (else F = 0)
+    auto xsum = [&](void) -> double {  // sum over this warp's columns of x_m * F_m
+      double acc = 0.0;
+      for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+        const int mbase = ct * NT + c0;
+        const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
+        uint32_t r[32];
+        tmem_ld32(lane_base + (uint32_t)c0, r);
+        tmem_ld_wait();
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t w[16];
-        expand32((uint32_t)(bits >> (32 * half)), w);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint32_t chunk = (uint32_t)(4 * half + c);
-          st_shared_v4(rowaddr + ((chunk ^ (uint32_t)(row & 7)) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-        }
+        for (int c = 0; c < 32; ++c)
+          if ((xw >> c) & 1u) acc += (double)__uint_as_float(r[c]);
       }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(FULL_A(sa));
-      sa += 2;                                   // this team's next stage in the ring
-      if (sa >= C::NA) { sa -= C::NA; pha ^= 1u; }
-      pos = nx;
-      d0 = n0;
-      d1 = n1;
+      return acc;
+    };
+    for (int j = p.nseg - 1; j >= 0; --j) {
+      const int2 s = sched[j];
+      int i = (h ^ (n & 1)) & 1;     // first position of this team in the segment
+      uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
+      if (i < s.y) { d0 = __ldg(p.kdesc + 2 * (s.x + i)); d1 = __ldg(p.kdesc + 2 * (s.x + i) + 1); }
+      for (; i < s.y; i += 2) {
+        uint4 n0 = d0, n1 = d1;
+        if (i + 2 < s.y) { n0 = __ldg(p.kdesc + 2 * (s.x + i + 2)); n1 = __ldg(p.kdesc + 2 * (s.x + i + 2) + 1); }
+        const int pos = n + i;
+        const int sa = pos % C::NA;
+        mbar_wait(EMPTY_A(sa), (uint32_t)(((pos / C::NA) & 1) ^ 1));
+        tc_fence_after();
+        const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
+        uint32_t w[32];
+        expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+        expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
+        tmem_st32(lane_base + (uint32_t)(NT + sa * C::A_COLS), w);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(FULL_A(sa));
+        d0 = n0;
+        d1 = n1;
+      }
+      n += s.y;
+      any = any || s.y > 0;
+      if (snaps && j > 0) {
+        mbar_wait(snap_full, (uint32_t)(nsnap & 1));
+        tc_fence_after();
+        S[nsnap] = any ? xsum() : 0.0;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(snap_empty);
+        ++nsnap;
+      }
     }
 
-    // ---------------- epilogue: warp half h takes column chunks [h*NT/2, (h+1)*NT/2) ------------
-    uint32_t used = 0;
-    for (int j = 0; j < p.nseg; ++j)
-      if (sched[j].y > 0) used |= 1u << (p.field_mode ? j : 0);
+    // ---------------- epilogue: fields, energy partial (this warp's column half) ---------------
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const long long b = b0 + row;
     const bool live = b < p.B;
-    double qsum = 0.0;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    for (int c0 = h * (NT / 2); c0 < (h + 1) * (NT / 2); c0 += 32) {
+    double sfin = 0.0, sp = 0.0;
+    for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
       const int mbase = ct * NT + c0;
       const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
+      uint32_t r[32];
+      if (any) {
+        tmem_ld32(lane_base + (uint32_t)c0, r);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = 0u;
+      }
       float g[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) g[c] = 0.0f;
-#pragma unroll
-      for (int a = 0; a < NACC; ++a) {
-        if (!((used >> a) & 1u)) continue;  // warp-uniform
-        uint32_t r[32];
-        tmem_ld32(lane_base + (uint32_t)(a * NT + c0), r);
-        tmem_ld_wait();
-        const double wa = p.wacc[a];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float v = __uint_as_float(r[c]);
-          g[c] += v;
-          if ((xw >> c) & 1u) qsum += wa * (double)v;
-        }
-      }
-#pragma unroll
       for (int c = 0; c < 32; ++c) {
+        const float v = __uint_as_float(r[c]);
         const float pm = __ldg(p.p1 + mbase + c);
-        g[c] += pm;
-        if ((xw >> c) & 1u) qsum += p.wp * (double)pm;
+        g[c] = v + pm;
+        if ((xw >> c) & 1u) { sfin += (double)v; sp += (double)pm; }
       }
       if (p.field_mode && live) {
         float* gout = p.G + (size_t)b * p.N + mbase;
@@ -312,8 +306,20 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
       }
     }
+    double qsum;
+    if (snaps) {
+      // S[0] = after degree 2, S[1] = after degree 3, ..., sfin = after degree k
+      qsum = p.wp * sp;
+      double prev = 0.0;
+      for (int t = 0; t <= nsnap; ++t) {
+        const double cur = t < nsnap ? S[t] : sfin;
+        qsum += p.wdeg[t + 2] * (cur - prev);
+        prev = cur;
+      }
+    } else {
+      qsum = sfin + sp;
+    }
     // combine the two column halves in a fixed order (deterministic, no atomics)
-    double* qpart = reinterpret_cast<double*>(gbase + (sA - base));  // A stage 0 is free now
     if (h == 1) qpart[row] = qsum;
     named_bar_sync(1, 256);
     if (h == 0 && live) p.Q[(size_t)ct * p.B + b] = qsum + qpart[row];
