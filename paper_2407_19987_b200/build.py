@@ -29,19 +29,22 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, debug_stats: bool = False) -> str:
+    """debug_stats=True builds _lib/libhobo_dbg.so with per-CTA pipeline counters (tools only)."""
+    lib = LIB.replace("libhobo.so", "libhobo_dbg.so") if debug_stats else LIB
+    if not force and not debug_stats and not stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", LIB, *SOURCES]
+    cmd = [NVCC, *FLAGS, *(["-DHOBO_PIPE_STATS"] if debug_stats else []), *(["-Xptxas", "-v"] if verbose else []),
+           "-o", lib, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libhobo.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug_stats="--debug-stats" in sys.argv))

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -266,6 +267,10 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.field_mode = (&L == &t->lay[1]) ? 1 : 0;
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
+  p.dbg = 0;
+#ifdef HOBO_PIPE_STATS
+  if (const char* e = getenv("HOBO_DBG")) p.dbg = atoi(e);
+#endif
   return p;
 }
 
@@ -521,6 +526,16 @@ hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mm
   }
   return HOBO_OK;
 }
+
+#ifdef HOBO_PIPE_STATS
+// debug builds only: copy (and reset) the per-CTA pipeline counters
+hobo_status hobo_debug_pipe_stats(unsigned long long* out /* 8192 x 8 */) {
+  if (cudaMemcpyFromSymbol(out, g_pipe_stats, sizeof(g_pipe_stats)) != cudaSuccess) return HOBO_ECUDA;
+  static unsigned long long zeros[8192][8];
+  cudaMemcpyToSymbol(g_pipe_stats, zeros, sizeof(zeros));
+  return HOBO_OK;
+}
+#endif
 
 hobo_status hobo_set_profiling(hobo_tensor* t, int enable) {
   if (!t) return fail(HOBO_EINVAL, "null handle");

@@ -38,20 +38,24 @@ struct KrParams {
   int N, W, Npad, n_ct, n_cb, nseg, L, field_mode;
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
   double wp;                // weight of the degree-1 term
+  int dbg;                  // debug builds only (HOBO_PIPE_STATS): pipeline bisection switches
 };
 
 template <int NT>
 struct KrCfg {
-  static constexpr int B_STAGE = NT * 128;               // NT rows x 64 bf16 (one SW128 atom row each)
-  static constexpr int NB = NT >= 256 ? 6 : 10;          // shared-memory B ring
-  static constexpr int A_COLS = kBK / 2;                 // TMEM columns per A stage (64 bf16 per lane)
-  static constexpr int NA = (512 - NT) / A_COLS < 8 ? (512 - NT) / A_COLS : 8;  // TMEM A ring
-  static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator, [NT, NT+NA*32): A stages
+  static constexpr int BOX = NT * 128;                   // one TMA box: NT rows x 64 bf16 (SW128)
+  static constexpr int RING_BOXES = 6;                   // shared-memory budget for W, in boxes
+  static constexpr int MAXST = 3;                        // max pipeline stages
+  static constexpr int A_COLS = kBK / 2;                 // TMEM columns of one K-block of A (64 bf16 / lane)
+  static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator, then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
-  static constexpr int NBAR = 2 * NB + 2 * NA + 3;
+  static constexpr int NBAR = 2 * MAXST + 3;
   static size_t smem_bytes(int W) {
-    return 1024 + (size_t)NB * B_STAGE + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)(W + 2) * kBM * 4 + 128;
+    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)(W + 2) * kBM * 4 + 128;
   }
+  // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages
+  __host__ __device__ static constexpr int kps(int L) { return L == 1 ? 2 : 1; }
+  __host__ __device__ static constexpr int nst(int L) { return RING_BOXES / (kps(L) * L) < MAXST ? RING_BOXES / (kps(L) * L) : MAXST; }
 };
 
 // A bits of one run for one candidate row: x[lo .. lo+cnt) AND the fixed elements' bits,
@@ -96,6 +100,22 @@ __device__ __forceinline__ void expand32(uint32_t half, uint32_t (&w)[16]) {
   }
 }
 
+#ifdef HOBO_PIPE_STATS
+// debug builds only: per-CTA pipeline accounting (clock64 cycles), accumulated in registers
+//  [0] MMA loop  [1] MMA waiting FULL  [2] stages  [3] K-blocks  [4] issuing MMAs  [5] commits
+//  [6] TMA waiting EMPTY  [7] gen warp waiting EMPTY
+__device__ unsigned long long g_pipe_stats[8192][8];
+#define PSTAT_FLUSH(i, v) atomicAdd(&g_pipe_stats[blockIdx.x & 8191][i], (unsigned long long)(v))
+#define PT(...) __VA_ARGS__
+#else
+#define PSTAT_FLUSH(i, v)
+#define PT(...)
+#endif
+
+// One pipeline stage = KPS consecutive K-blocks of one segment (x L limb boxes of W).
+// Ring slot s holds the stage's W boxes in shared memory and its A K-blocks in TMEM;
+// FULL(s) completes when the 8 generator warps arrived and the TMA bytes landed, EMPTY(s)
+// when the MMAs reading the slot completed (one tcgen05.commit).
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
   using C = KrCfg<NT>;
@@ -104,8 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 atoms need 1024-byte alignment
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sB = base;
-  const uint32_t sBar = sB + C::NB * C::B_STAGE;
-  const uint32_t acc_full = sBar + 8 * (2 * C::NB + 2 * C::NA);
+  const uint32_t sBar = sB + C::RING_BOXES * C::BOX;
+  const uint32_t acc_full = sBar + 8 * (2 * C::MAXST);
   const uint32_t snap_full = acc_full + 8, snap_empty = acc_full + 16;
   const uint32_t tslot = acc_full + 24;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
@@ -113,22 +133,21 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
   double* qpart = reinterpret_cast<double*>(gbase + (sQ - base));
   volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
-#define FULL_B(s) (sBar + 8u * (s))
-#define EMPTY_B(s) (sBar + 8u * (C::NB + (s)))
-#define FULL_A(s) (sBar + 8u * (2 * C::NB + (s)))
-#define EMPTY_A(s) (sBar + 8u * (2 * C::NB + C::NA + (s)))
+#define FULL(s) (sBar + 8u * (s))
+#define EMPTY(s) (sBar + 8u * (C::MAXST + (s)))
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ct = blockIdx.x / p.n_cb, cb = blockIdx.x % p.n_cb;  // column-tile-major: concurrent CTAs share W tiles in L2
   const long long b0 = (long long)cb * kBM;
   const int2* sched = p.sched + (size_t)ct * p.nseg;
+  const int KPS = C::kps(p.L), NST = C::nst(p.L);
+  const uint32_t stage_bytes = (uint32_t)(KPS * p.L) * C::BOX;
   // segments run in ascending degree order (j = nseg-1 .. 0); in field mode the single
   // accumulator is snapshot after each degree so the energy can weight degree r by 1/r
   const bool snaps = p.field_mode != 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::NB; ++s) { mbar_init(FULL_B(s), 1); mbar_init(EMPTY_B(s), 1); }
-    for (int s = 0; s < C::NA; ++s) { mbar_init(FULL_A(s), 4); mbar_init(EMPTY_A(s), 1); }
+    for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), 9); mbar_init(EMPTY(s), 1); }
     mbar_init(acc_full, 1);
     mbar_init(snap_full, 1);
     mbar_init(snap_empty, 8);
@@ -152,45 +171,55 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t tmem = *tslot_g;
 
   if (warp == 0) {
-    // ---------------- TMA producer: W limb tiles (NT rows x 64 tuples, SW128) -------------
+    // ---------------- TMA producer: W limb boxes (NT rows x 64 tuples, SW128) ---------------
     if (lane == 0) {
-      int sb = 0;
-      uint32_t ph = 0;
+      int n = 0;
+      PT(unsigned long long w_tma = 0;)
       for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
-        for (int kb = s.x; kb < s.x + s.y; ++kb)
-          for (int l = 0; l < p.L; ++l) {
-            mbar_wait(EMPTY_B(sb), ph ^ 1u);
-            mbar_arrive_expect_tx(FULL_B(sb), C::B_STAGE);
-            tma_load_2d(sB + sb * C::B_STAGE, &tmap, FULL_B(sb), kb * kBK, l * p.Npad + ct * NT);
-            if (++sb == C::NB) { sb = 0; ph ^= 1u; }
-          }
+        for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS, ++n) {
+          const int nkb = min(KPS, s.x + s.y - kb0);
+          const int st = n % NST;
+          PT(const long long t0 = clock64();)
+          mbar_wait(EMPTY(st), (uint32_t)(((n / NST) & 1) ^ 1));
+          PT(w_tma += clock64() - t0;)
+          mbar_arrive_expect_tx(FULL(st), (uint32_t)(nkb * p.L) * C::BOX);
+          for (int q = 0; q < nkb; ++q)
+            for (int l = 0; l < p.L; ++l)
+              tma_load_2d(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX, &tmap, FULL(st), (kb0 + q) * kBK,
+                          l * p.Npad + ct * NT);
+        }
       }
+      PSTAT_FLUSH(6, w_tma);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread): D[tmem] += A[tmem] * B[smem] ------------------
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
-      int sb = 0, sa = 0, snap = 0;
-      uint32_t phb = 0, pha = 0, issued = 0;
+      int n = 0, snap = 0;
+      uint32_t issued = 0;
+      PT(unsigned long long stt[6] = {0, 0, 0, 0, 0, 0}; const long long t_start = clock64(); long long t0;)
       for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
-        for (int kb = s.x; kb < s.x + s.y; ++kb) {
-          mbar_wait(FULL_A(sa), pha);
+        for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS, ++n) {
+          const int nkb = min(KPS, s.x + s.y - kb0);
+          const int st = n % NST;
+          PT(t0 = clock64();)
+          mbar_wait(FULL(st), (uint32_t)((n / NST) & 1));
+          PT(stt[1] += clock64() - t0; stt[2] += 1; stt[3] += nkb; t0 = clock64();)
           tc_fence_after();
-          const uint32_t a_t = tmem + (uint32_t)(NT + sa * C::A_COLS);
-          for (int l = 0; l < p.L; ++l) {
-            mbar_wait(FULL_B(sb), phb);
-            tc_fence_after();
-            const uint64_t bdesc = sw128_kmajor_desc(sB + sb * C::B_STAGE);
+          for (int q = 0; q < nkb; ++q) {
+            const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
+            for (int l = 0; l < p.L; ++l) {
+              const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(l | k));
-            umma_commit(EMPTY_B(sb));
-            if (++sb == C::NB) { sb = 0; phb ^= 1u; }
+              for (int k = 0; k < kBK / 16; ++k)
+                umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
+            }
           }
-          umma_commit(EMPTY_A(sa));
-          if (++sa == C::NA) { sa = 0; pha ^= 1u; }
+          PT(stt[4] += clock64() - t0; t0 = clock64();)
+          umma_commit(EMPTY(st));
+          PT(stt[5] += clock64() - t0;)
           issued = 1;
         }
         if (snaps && j > 0) {  // hand the degree-(k-j) partial sum to the epilogue warps
@@ -203,11 +232,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       }
       if (issued) umma_commit(acc_full);
       else mbar_arrive(acc_full);
+      PT(stt[0] = clock64() - t_start; for (int i = 0; i < 6; ++i) PSTAT_FLUSH(i, stt[i]);)
     }
   } else {
     // ---------------- A generator (warps 2..9), then epilogue --------------------------------
-    // team h = (w-2)/4 builds every other K-block of the schedule; warp w of a team serves
-    // TMEM lane quarter q = w % 4 (rows 32q..32q+31) and writes its rows of A with tcgen05.st.
+    // team h = (w-2)/4 builds K-block h of every stage; warp w of a team serves TMEM lane
+    // quarter q = w % 4 (rows 32q..32q+31) and writes its rows of A with tcgen05.st.
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
     const int row = q * 32 + lane;   // candidate row within the block == TMEM lane
@@ -215,8 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     const int c_lo = h * (NT / 2), c_hi = (h + 1) * (NT / 2);   // this warp's epilogue columns
     double S[8];                     // S[r]: sum_m x_m F_m over this warp's columns after degree r
     int nsnap = 0;
-    int n = 0;                       // position in the CTA's K-block sequence
+    int n = 0;                       // stage counter (same sequence as the MMA issuer)
     bool any = false;                // has any MMA been issued yet (else F = 0)
+    PT(unsigned long long w_gen = 0;)
     auto xsum = [&](void) -> double {  // sum over this warp's columns of x_m * F_m
       double acc = 0.0;
       for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
@@ -233,29 +264,32 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     };
     for (int j = p.nseg - 1; j >= 0; --j) {
       const int2 s = sched[j];
-      int i = (h ^ (n & 1)) & 1;     // first position of this team in the segment
       uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
-      if (i < s.y) { d0 = __ldg(p.kdesc + 2 * (s.x + i)); d1 = __ldg(p.kdesc + 2 * (s.x + i) + 1); }
-      for (; i < s.y; i += 2) {
-        uint4 n0 = d0, n1 = d1;
-        if (i + 2 < s.y) { n0 = __ldg(p.kdesc + 2 * (s.x + i + 2)); n1 = __ldg(p.kdesc + 2 * (s.x + i + 2) + 1); }
-        const int pos = n + i;
-        const int sa = pos % C::NA;
-        mbar_wait(EMPTY_A(sa), (uint32_t)(((pos / C::NA) & 1) ^ 1));
-        tc_fence_after();
-        const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
-        uint32_t w[32];
-        expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
-        expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
-        tmem_st32(lane_base + (uint32_t)(NT + sa * C::A_COLS), w);
-        tmem_st_wait();
-        tc_fence_before();
+      if (h < s.y) { d0 = __ldg(p.kdesc + 2 * (s.x + h)); d1 = __ldg(p.kdesc + 2 * (s.x + h) + 1); }
+      for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS, ++n) {
+        const int kb = kb0 + h;                       // this team's K-block of the stage
+        const bool mine = h < KPS && kb < s.x + s.y;
+        uint4 n0 = d0, n1 = d1;                       // prefetch the next stage's descriptor
+        if (kb + KPS < s.x + s.y) { n0 = __ldg(p.kdesc + 2 * (kb + KPS)); n1 = __ldg(p.kdesc + 2 * (kb + KPS) + 1); }
+        const int st = n % NST;
+        PT(const long long tg = clock64();)
+        mbar_wait(EMPTY(st), (uint32_t)(((n / NST) & 1) ^ 1));
+        PT(w_gen += clock64() - tg;)
+        if (mine) {
+          tc_fence_after();
+          const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
+          uint32_t w[32];
+          expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+          expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
+          tmem_st32(lane_base + (uint32_t)(NT + (st * KPS + h) * C::A_COLS), w);
+          tmem_st_wait();
+          tc_fence_before();
+        }
         __syncwarp();
-        if (lane == 0) mbar_arrive(FULL_A(sa));
+        if (lane == 0) mbar_arrive(FULL(st));
         d0 = n0;
         d1 = n1;
       }
-      n += s.y;
       any = any || s.y > 0;
       if (snaps && j > 0) {
         mbar_wait(snap_full, (uint32_t)(nsnap & 1));
@@ -269,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     }
 
     // ---------------- epilogue: fields, energy partial (this warp's column half) ---------------
+    PT(if (warp == 2 && lane == 0) PSTAT_FLUSH(7, w_gen);)
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const long long b = b0 + row;
@@ -324,10 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     named_bar_sync(1, 256);
     if (h == 0 && live) p.Q[(size_t)ct * p.B + b] = qsum + qpart[row];
   }
-#undef FULL_B
-#undef EMPTY_B
-#undef FULL_A
-#undef EMPTY_A
+#undef FULL
+#undef EMPTY
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
