@@ -246,8 +246,17 @@ def main():
     # judged against the BURST figure; the sustained (power-capped) ratio is reported beside it
     peak = burst
     achieved = algo_flops / (kms / 1e3) / 1e12
+    traffic, traffic_src = None, None
+    try:   # dram read+write bytes per launch of this kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01_cfg3_ncu.json")) as f:
+            traffic = json.load(f)["traffic_bytes_per_launch"]
+            traffic_src = "profiles/r01_cfg3_ncu.json (ncu --set full, dram__bytes_read+write)"
+    except Exception:
+        pass
+    Npad, Tpad = 512, 130816 + 512
+    algo_bytes = t.limbs * Npad * Tpad * 2 + B * 16 * 4 + B * 512 * 4 + 2 * B * 8   # W once, X bits, G, Q
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "kr_gemm_kernel<256,2> (open-index contraction, field mode)",
+            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": "kr_gemm_kernel<256,2> (open-index contraction, field mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms,
             "algorithmic_flops_per_launch": algo_flops, "executed_mma_flops_per_launch": exec_flops,
             "executed_tflops": exec_flops / (kms / 1e3) / 1e12, "frac_of_sustained": achieved / sustained,
