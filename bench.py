@@ -34,13 +34,44 @@ UNIT = "candidate evals/s"
 WORKLOAD = "cfg3: order-3 HOBO, N=512 (128 x 4-bit integer vars), B=65536 per GPU, energy + local field + argmin"
 
 
+def _cfg3():
+    from workloads import cfg3_problem
+    from paper_2407_19987_b200 import HoboTensor
+    return HoboTensor.from_problem(cfg3_problem())
+
+
+def _colex(order, N, seed):
+    def make():
+        from workloads import uniform_colex
+        from paper_2407_19987_b200 import HoboTensor
+        return HoboTensor.import_colex(order, N, uniform_colex(order, N, seed))
+    return make
+
+
+# name: (workload text, tensor factory, N, seed for X, batch per GPU (None = total / world), mode, scaling)
+CONFIGS = {
+    "cfg3": (WORKLOAD, _cfg3, 512, 3, 65536, "field", "weak"),
+    "cfg3f": ("cfg3-fp32: order-3 HOBO, N=512, all 22,370,048 canonical cells U(-1,1) (L=3), B=65536 per GPU, "
+              "energy + local field + argmin", _colex(3, 512, 3), 512, 3, 65536, "field", "weak"),
+    "cfg2": ("cfg2: QUBO N=1024, all canonical cells U(-1,1) (L=3), B=65536 per GPU, energies + argmin",
+             _colex(2, 1024, 2), 1024, 2, 65536, "energy", "weak"),
+    "cfg4": ("cfg4: order-4 HOBO, N=128, all canonical cells U(-1,1) (L=3), B=262144 per GPU, "
+             "energy + local field + argmin (one search iteration's contraction)", _colex(4, 128, 4), 128, 4, 262144,
+             "field", "weak"),
+    "cfg5": ("cfg5: order-3 HOBO, N=1024, all 178,957,824 canonical cells U(-1,1) (L=3), B=2^20 sharded over the "
+             "GPUs, energies + global argmin", _colex(3, 1024, 5), 1024, 5, None, "energy", "strong"),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=65536, help="candidates per GPU")
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (cfg3 = the headline metric; the others for context)")
+    ap.add_argument("--batch", type=int, default=0, help="override candidates per GPU")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / search / cpu baseline (profiling runs)")
     return ap.parse_args()
 
@@ -179,21 +210,34 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2407_19987_b200 import HoboTensor, build
     from paper_2407_19987_b200.dist import combine_best
-    from workloads import cfg3_problem, x_bits
+    from workloads import x_bits
     build.build()
 
-    B = a.batch
-    t = HoboTensor.from_problem(cfg3_problem())
-    row0 = rank * B
-    Xh = torch.from_numpy(x_bits(3, B, 512, row0=row0)).pin_memory()
+    from paper_2407_19987_b200.dist import shard
+    wl_text, factory, N, xseed, per_gpu, mode, scaling = CONFIGS[a.config]
+    if per_gpu is None:                       # strong scaling: a fixed total batch
+        total = a.batch * world if a.batch else (1 << 20)
+        row0, hi = shard(total, rank, world)
+        B = hi - row0
+    else:
+        B = a.batch or per_gpu
+        row0 = rank * B
+    t = factory()
+    Xh = torch.empty(B, N, dtype=torch.uint8).pin_memory()
+    for lo in range(0, B, 1 << 17):
+        n = min(1 << 17, B - lo)
+        Xh[lo:lo + n] = torch.from_numpy(x_bits(xseed, n, N, row0=row0 + lo))
     Xd = Xh.to(dev)
-    G = torch.empty(B, 512, dtype=torch.float32, device=dev)
+    G = torch.empty(B, N, dtype=torch.float32, device=dev) if mode == "field" else None
     E = torch.empty(B, dtype=torch.float32, device=dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step():
-        _, _, best = t.local_field(Xd, G, E, row0=row0, want_best=True)
+        if mode == "field":
+            _, _, best = t.local_field(Xd, G, E, row0=row0, want_best=True)
+        else:
+            _, best = t.energy(Xd, E, row0=row0)
         if world > 1:
             best = combine_best(best[0], best[1], device=dev)
         return best
@@ -234,7 +278,8 @@ def main():
         m = torch.tensor([my_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         ms = float(m.item())
-    value = world * B / (ms / 1e3)
+    units = world * B if per_gpu is not None else (a.batch * world if a.batch else (1 << 20))
+    value = units / (ms / 1e3)
 
     # roofline of the dominant kernel (the open-index contraction), live CUDA events
     st = t.launch_stats()
@@ -248,13 +293,18 @@ def main():
     achieved = algo_flops / (kms / 1e3) / 1e12
     traffic, traffic_src = None, None
     try:   # dram read+write bytes per launch of this kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r01_cfg3_ncu.json")) as f:
-            traffic = json.load(f)["traffic_bytes_per_launch"]
-            traffic_src = "profiles/r01_cfg3_ncu.json (ncu --set full, dram__bytes_read+write)"
+        if a.config == "cfg3" and B == 65536:
+            with open(os.path.join(ROOT, "profiles", "r01_cfg3_ncu.json")) as f:
+                traffic = json.load(f)["traffic_bytes_per_launch"]
+                traffic_src = "profiles/r01_cfg3_ncu.json (ncu --set full, dram__bytes_read+write)"
     except Exception:
         pass
-    Npad, Tpad = 512, 130816 + 512
-    algo_bytes = t.limbs * Npad * Tpad * 2 + B * 16 * 4 + B * 512 * 4 + 2 * B * 8   # W once, X bits, G, Q
+    import math
+    Npad = (N + 255) // 256 * 256
+    Tpad = sum((math.comb(N, r - 1) + 63) // 64 * 64 for r in range(2, t.order + 1))
+    nct = Npad // 256
+    algo_bytes = (t.limbs * Npad * Tpad * 2 + B * ((N + 31) // 32) * 4 + (B * N * 4 if mode == "field" else B * 4)
+                  + nct * B * 8)                                    # W once, X bits, G (or E), Q
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": "kr_gemm_kernel<256,2> (open-index contraction, field mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms,
@@ -283,30 +333,33 @@ def main():
             mm = torch.tensor([m2], dtype=torch.float64, device=dev)
             dist.all_reduce(mm, op=dist.ReduceOp.MAX)
             m2 = float(mm.item())
-        extras["e2e"] = {"value": world * B / (m2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * 512,
+        extras["e2e"] = {"value": units / (m2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * N,
                          "d2h_bytes_per_step": B * 4 + 8, "ms_per_step": m2}
-        # the config-3 search loop (16 iterations of field + move over B chains), context only
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        xs, es, cs = t.search(3, B, 16)
-        e.record(stream)
-        e.synchronize()
-        sm = s.elapsed_time(e)
-        extras["search_loop"] = {"chains_per_gpu": B, "iters": 16, "ms": sm,
-                                 "chain_evals_per_s": B * 17 / (sm / 1e3), "e_best": es}
-        if rank == 0:
+        if mode == "field":
+            # the search loop (16 iterations of field + move over B chains), context only
+            t.search(3, B, 1)                     # warm the search scratch buffers
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            xs, es, cs = t.search(3, B, 16)
+            e.record(stream)
+            e.synchronize()
+            sm = s.elapsed_time(e)
+            extras["search_loop"] = {"chains_per_gpu": B, "iters": 16, "ms": sm,
+                                     "chain_evals_per_s": B * 17 / (sm / 1e3), "e_best": es}
+        if rank == 0 and a.config == "cfg3":
             extras["cpu_baseline"] = cpu_baseline()
     if world > 1:
         dist.barrier()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "order": 3, "N": 512, "batch_per_gpu": B, "limbs": t.limbs,
-                           "global_batch": world * B, "parallelism": f"dp{world} (H replicated, batch sharded)",
+                "config": {"workload": wl_text, "name": a.config, "order": t.order, "N": N, "batch_per_gpu": B,
+                           "limbs": t.limbs, "global_batch": units,
+                           "parallelism": f"dp{world} (H replicated, batch sharded)",
                            "l2": "flushed before every timed step (256 MiB write)",
-                           "inputs": "x_bits(seed=3), cfg3_problem() (workloads/gen.py)",
+                           "inputs": f"x_bits(seed={xseed}) and the {a.config} instance (workloads/gen.py)",
                            "best": list(best)},
                 "roofline": roof, "gpu_launches": launches, "clocks": clocks}
         line.update(extras)

@@ -70,6 +70,14 @@ hobo_status hobo_tensor_build(int order, int N, const hobo_term* terms, size_t n
 hobo_status hobo_tensor_import_cells(int order, int N, int64_t ncells, const int32_t* idx,
                                      const float* val, hobo_tensor** out);
 
+/* hobo_tensor_import_colex — the canonical cells themselves (the upper-triangular tensor
+ * without its replicated copies): cells_by_degree[r-1] is a host float array of
+ * C(N, r) entries, entry colex_rank(S) = sum_i C(s_i, i) holding c(S) for the r-subset
+ * S = {s1<...<sr}, r = 1..order.  Copied.  The efficient path for large dense instances
+ * (BASELINE config 5: 178,957,824 cells).                                                 */
+hobo_status hobo_tensor_import_colex(int order, int N, const float* const* cells_by_degree,
+                                     hobo_tensor** out);
+
 hobo_status hobo_tensor_free(hobo_tensor* t);
 
 /* info: order, N, #nonzero canonical cells, all cells integral (0/1), sum |cell| (the

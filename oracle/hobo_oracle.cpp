@@ -386,6 +386,82 @@ int or_brute(void* h, double* emin, int64_t* argmin, int64_t* n_ground, double* 
   return 0;
 }
 
+}  // extern "C"
+
+// C(n, i) for the colex ranks (n <= 65536, i <= 6)
+static long double binom_ld(int64_t n, int i) {
+  if (i < 0 || n < i) return 0;
+  long double c = 1;
+  for (int t = 1; t <= i; ++t) c = c * (long double)(n - i + t) / t;
+  return c;
+}
+
+// sum over all k-subsets of `v` (sorted) of f(subset)
+template <class F>
+static void for_subsets(const std::vector<int32_t>& v, int k, F f) {
+  const int n = (int)v.size();
+  if (k > n) return;
+  std::vector<int> c(k);
+  for (int i = 0; i < k; ++i) c[i] = i;
+  std::vector<int32_t> s(k);
+  while (true) {
+    for (int i = 0; i < k; ++i) s[i] = v[c[i]];
+    f(s);
+    int i = k - 1;
+    while (i >= 0 && c[i] == n - k + i) --i;
+    if (i < 0) return;
+    ++c[i];
+    for (int j = i + 1; j < k; ++j) c[j] = c[j - 1] + 1;
+  }
+}
+
+static int64_t colex_rank_of(const std::vector<int32_t>& s) {
+  long double r = 0;
+  for (size_t i = 0; i < s.size(); ++i) r += binom_ld(s[i], (int)i + 1);
+  return (int64_t)r;
+}
+
+extern "C" {
+
+int or_colex_energy(int order, int N, const float* const* by_degree, const uint8_t* X, int64_t B, double* E,
+                    int nthreads) {
+  if (order < 1 || N < 1 || !by_degree) return 1;
+  parallel_for(B, nthreads, [&](int64_t b) {
+    std::vector<int32_t> ones;
+    for (int m = 0; m < N; ++m)
+      if (X[b * N + m]) ones.push_back(m);
+    long double e = 0;
+    for (int r = 1; r <= order; ++r)
+      for_subsets(ones, r, [&](const std::vector<int32_t>& s) { e += by_degree[r - 1][colex_rank_of(s)]; });
+    E[b] = (double)e;
+  });
+  return 0;
+}
+
+int or_colex_field(int order, int N, const float* const* by_degree, const uint8_t* X, int64_t B, double* G,
+                   int nthreads) {
+  if (order < 1 || N < 1 || !by_degree) return 1;
+  parallel_for(B, nthreads, [&](int64_t b) {
+    std::vector<int32_t> ones;
+    for (int m = 0; m < N; ++m)
+      if (X[b * N + m]) ones.push_back(m);
+    for (int m = 0; m < N; ++m) {
+      std::vector<int32_t> rest;
+      for (int32_t u : ones)
+        if (u != m) rest.push_back(u);
+      long double g = by_degree[0][m];  // T = {} : the degree-1 cell of {m}
+      for (int r = 2; r <= order; ++r)
+        for_subsets(rest, r - 1, [&](const std::vector<int32_t>& t) {
+          std::vector<int32_t> s(t);
+          s.insert(std::lower_bound(s.begin(), s.end(), m), m);
+          g += by_degree[r - 1][colex_rank_of(s)];
+        });
+      G[b * N + m] = (double)g;
+    }
+  });
+  return 0;
+}
+
 int or_search_thresholds(int64_t iters, double p0, double p1, uint32_t* out) {
   for (int64_t t = 0; t < iters; ++t) {
     double frac = (double)t / (double)std::max<int64_t>(1, iters - 1);

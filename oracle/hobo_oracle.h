@@ -65,6 +65,16 @@ int or_brute(void* handle, double* emin, int64_t* argmin, int64_t* n_ground, dou
 int or_search(void* handle, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
               double p0, double p1, double* chain_ebest, uint8_t* chain_xbest,
               double* e_best, int64_t* best_chain, int nthreads);
+/* Large instances given as canonical cells per degree in colex order
+ * (by_degree[r-1][colex_rank(S)] = c(S), colex_rank({a1<..<ar}) = sum_i C(a_i, i)):
+ * E(x) = sum over subsets S of the candidate's ones, |S| <= order, of c(S)
+ * g_m(x) = sum over subsets T of ones minus {m}, |T| <= order-1, of c(T u {m})
+ * evaluated one candidate at a time by plain subset enumeration (long double).       */
+int or_colex_energy(int order, int N, const float* const* by_degree, const uint8_t* X, int64_t B, double* E,
+                    int nthreads);
+int or_colex_field(int order, int N, const float* const* by_degree, const uint8_t* X, int64_t B, double* G,
+                   int nthreads);
+
 /* the counter-based hash of SURVEY 8(d): h(s,a,b,c) = sm(sm(sm(s^a)^b)^c) */
 uint64_t or_hash(uint64_t s, uint64_t a, uint64_t b, uint64_t c);
 uint64_t or_splitmix64(uint64_t z);

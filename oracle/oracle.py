@@ -48,6 +48,8 @@ def _L():
         _lib.or_splitmix64.argtypes = [U64]
         _lib.or_splitmix64.restype = U64
         _lib.or_search_thresholds.argtypes = [I64, D, D, P]
+        _lib.or_colex_energy.argtypes = [I, I, P, P, I64, P, I]
+        _lib.or_colex_field.argtypes = [I, I, P, P, I64, P, I]
     return _lib
 
 
@@ -170,3 +172,25 @@ class Oracle:
         if st:
             raise ValueError(f"or_search status {st}")
         return dict(e_best=e.value, best_chain=c.value, chain_ebest=eb, chain_xbest=xb)
+
+
+def _colex_ptrs(by_degree):
+    arrs = [np.ascontiguousarray(a, np.float32) for a in by_degree]
+    return arrs, (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+
+
+def colex_energy(order, N, by_degree, X, nthreads=0):
+    """Energies of candidates X from per-degree colex canonical cells (large instances)."""
+    arrs, ptrs = _colex_ptrs(by_degree)
+    X = np.ascontiguousarray(X, np.uint8)
+    E = np.zeros(X.shape[0], np.float64)
+    _L().or_colex_energy(order, N, C.cast(ptrs, C.c_void_p), _ptr(X), X.shape[0], _ptr(E), _nthreads(nthreads))
+    return E
+
+
+def colex_field(order, N, by_degree, X, nthreads=0):
+    arrs, ptrs = _colex_ptrs(by_degree)
+    X = np.ascontiguousarray(X, np.uint8)
+    G = np.zeros((X.shape[0], N), np.float64)
+    _L().or_colex_field(order, N, C.cast(ptrs, C.c_void_p), _ptr(X), X.shape[0], _ptr(G), _nthreads(nthreads))
+    return G

@@ -344,6 +344,16 @@ hobo_status hobo_tensor_import_cells(int order, int N, int64_t ncells, const int
   return HOBO_OK;
 }
 
+hobo_status hobo_tensor_import_colex(int order, int N, const float* const* cells_by_degree, hobo_tensor** out) {
+  if (!out) return fail(HOBO_EINVAL, "null output handle");
+  std::unique_ptr<hobo_tensor> t(new hobo_tensor());
+  std::string msg;
+  int st = compile_colex(order, N, cells_by_degree, t->host, msg);
+  if (st) return fail(st == 3 ? HOBO_ENOMEM : (hobo_status)st, msg);
+  *out = t.release();
+  return HOBO_OK;
+}
+
 hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (!t) return HOBO_OK;
   if (t->dev_init) cudaSetDevice(t->device);

@@ -90,6 +90,21 @@ int limbs_needed(float c) {
   return 3;
 }
 
+void cell_stats(HostTensor& out) {
+  out.nnz = 0;
+  out.sum_abs = 0.0;
+  out.is_integer = true;
+  out.limbs = 1;
+  for (int r = 1; r <= out.order; ++r)
+    for (float f : out.strict[r]) {
+      if (f == 0.0f) continue;
+      ++out.nnz;
+      out.sum_abs += std::fabs((double)f);
+      if (f != std::nearbyint(f)) out.is_integer = false;
+      out.limbs = std::max(out.limbs, limbs_needed(f));
+    }
+}
+
 template <class Num>
 int finish(int order, int N, const std::unordered_map<Mono, Num, MonoHash>& poly, HostTensor& out, std::string& msg) {
   out = HostTensor();
@@ -128,14 +143,7 @@ int finish(int order, int N, const std::unordered_map<Mono, Num, MonoHash>& poly
     if (f == 0.0f) continue;
     out.strict[kv.first.n][(size_t)colex_rank(kv.first)] = f;
   }
-  for (int r = 1; r <= order; ++r)
-    for (float f : out.strict[r]) {
-      if (f == 0.0f) continue;
-      ++out.nnz;
-      out.sum_abs += std::fabs((double)f);
-      if (f != std::nearbyint(f)) out.is_integer = false;
-      out.limbs = std::max(out.limbs, limbs_needed(f));
-    }
+  cell_stats(out);
   return 0;
 }
 
@@ -225,6 +233,33 @@ int compile_cells(int order, int N, int64_t ncells, const int32_t* idx, const fl
     poly[m] += (long double)val[c];
   }
   return finish<long double>(order, N, poly, out, msg);
+}
+
+int compile_colex(int order, int N, const float* const* by_degree, HostTensor& out, std::string& msg) {
+  if (order < 1 || order > 6) { msg = "order must be in 1..6"; return 1; }
+  if (N < 1 || N > 65535 || (order > 3 && N > 1024)) { msg = "N out of range"; return 1; }
+  if (!by_degree) { msg = "null cell arrays"; return 1; }
+  double total = 0;
+  for (int r = 1; r <= order; ++r) total += (double)binom(N, r);
+  if (total > 1.6e9) { msg = "canonical cell space exceeds the 1.6e9-cell host budget"; return 3; }
+  out = HostTensor();
+  out.order = order;
+  out.N = N;
+  out.strict.resize(order + 1);
+  for (int r = 1; r <= order; ++r) {
+    const size_t n = (size_t)binom(N, r);
+    if (n && !by_degree[r - 1]) { msg = "null cell array for degree " + std::to_string(r); return 1; }
+    try {
+      out.strict[r].assign(by_degree[r - 1], by_degree[r - 1] + n);
+    } catch (...) {
+      msg = "host allocation of the canonical cells failed";
+      return 3;
+    }
+    for (float f : out.strict[r])
+      if (!std::isfinite(f)) { msg = "non-finite cell value"; return 1; }
+  }
+  cell_stats(out);
+  return 0;
 }
 
 namespace {

@@ -33,6 +33,8 @@ struct TermView {  // mirrors hobo_term / hobo_factor / hobo_lin
 int compile_terms(int order, int N, const TermView& tv, HostTensor& out, std::string& msg);
 int compile_cells(int order, int N, int64_t ncells, const int32_t* idx, const float* val, HostTensor& out,
                   std::string& msg);
+// canonical cells given directly: by_degree[r-1][colex_rank(S)] = c(S), r = 1..order
+int compile_colex(int order, int N, const float* const* by_degree, HostTensor& out, std::string& msg);
 void export_cells(const HostTensor& t, int32_t* idx, float* val);   // lexicographic by tuple
 int export_dense(const HostTensor& t, float* out);                   // 0 ok, 3 too large
 

@@ -15,7 +15,7 @@ HOBO_OK, HOBO_EINVAL, HOBO_ERANGE, HOBO_ENOMEM, HOBO_ECUDA, HOBO_ENCCL, HOBO_EST
 _STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
 
 EXPORTED = [
-    "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_free", "hobo_tensor_info",
+    "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_free", "hobo_tensor_info",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field",
     "hobo_search", "hobo_search_shard", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
 ]
@@ -45,6 +45,7 @@ def lib():
         P, I, I64, U64, D, SZ = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_size_t
         L.hobo_tensor_build.argtypes = [I, I, P, SZ, P, P, C.POINTER(P), C.POINTER(D)]
         L.hobo_tensor_import_cells.argtypes = [I, I, I64, P, P, C.POINTER(P)]
+        L.hobo_tensor_import_colex.argtypes = [I, I, P, C.POINTER(P)]
         L.hobo_tensor_free.argtypes = [P]
         L.hobo_tensor_info.argtypes = [P, C.POINTER(I), C.POINTER(I), C.POINTER(I64), C.POINTER(I),
                                        C.POINTER(D), C.POINTER(I), C.POINTER(D)]
@@ -123,6 +124,17 @@ class HoboTensor:
         val = np.ascontiguousarray(val, np.float32)
         h = C.c_void_p()
         _check(lib().hobo_tensor_import_cells(order, N, len(val), _np_ptr(idx), _np_ptr(val), C.byref(h)))
+        return cls(h, 0.0)
+
+    @classmethod
+    def import_colex(cls, order, N, by_degree):
+        """Canonical cells per degree r = 1..order, each a float32 array of C(N, r) in colex order."""
+        arrs = [np.ascontiguousarray(a, np.float32) for a in by_degree]
+        if len(arrs) != order:
+            raise ValueError("need one array per degree 1..order")
+        ptrs = (C.c_void_p * order)(*[a.ctypes.data for a in arrs])
+        h = C.c_void_p()
+        _check(lib().hobo_tensor_import_colex(order, N, C.cast(ptrs, C.c_void_p), C.byref(h)))
         return cls(h, 0.0)
 
     def close(self):

@@ -214,3 +214,59 @@ def test_search_shard_invariance(H, torch):
     b = t.search(3, None, 16, chain0=256, nchains=256)
     win = min((a[1], a[2], 0), (b[1], b[2], 1))
     assert (full[1], full[2]) == win[:2]
+
+
+# ---- remaining BASELINE configs at full size, sampled ----------------------------------------
+def test_cfg5_full_batch_sampled(H, torch):
+    """BASELINE config 5 at one GPU's full size: order 3, N=1024, all 178,957,824 canonical
+    cells U(-1,1) (L=3), B = 2^20 candidates, energies + argmin in the energy-mode layout.
+    Sampled rows against the oracle (subset enumeration per candidate), tolerance tau."""
+    from oracle import colex_energy
+    from workloads import uniform_colex
+    N, B = 1024, 1 << 20
+    v = uniform_colex(3, N, 5)
+    t = H.HoboTensor.import_colex(3, N, v)
+    # 178,957,824 canonical cells; the U(-1,1) draw hits exactly 0 for ~2^-24 of them
+    assert t.limbs == 3 and t.ncells == sum(int(np.count_nonzero(a)) for a in v)
+    assert sum(a.size for a in v) == 178957824
+    Xd = torch.empty(B, N, dtype=torch.uint8, device="cuda")
+    for lo in range(0, B, 1 << 17):
+        Xd[lo:lo + (1 << 17)] = torch.from_numpy(x_bits(5, 1 << 17, N, row0=lo)).cuda()
+    E, best = t.energy(Xd)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 77777, 524288, B - 1])
+    Xs = Xd[torch.from_numpy(rows).cuda()].cpu().numpy()
+    ref = colex_energy(3, N, v, Xs)
+    tau = t.tau
+    assert np.max(np.abs(E.cpu().numpy()[rows].astype(np.float64) - ref)) <= tau
+    Eh = E.cpu().numpy()
+    assert best[0] == Eh.min() and best[1] == int(np.argmin(Eh))
+
+
+def test_cfg4_full_batch_sampled(H, torch):
+    """BASELINE config 4: order 4, N=128, all canonical cells U(-1,1) (L=3), B=262,144:
+    local fields + energies at full size, sampled rows against the oracle."""
+    from oracle import colex_energy, colex_field
+    from workloads import uniform_colex
+    N, B = 128, 262144
+    v = uniform_colex(4, N, 4)
+    t = H.HoboTensor.import_colex(4, N, v)
+    X = x_bits(4, B, N)
+    G, E = fields(H, torch, t, X)
+    rows = np.array([0, 3, 131072, B - 1])
+    assert np.max(np.abs(E[rows] - colex_energy(4, N, v, X[rows]))) <= t.tau
+    assert np.max(np.abs(G[rows] - colex_field(4, N, v, X[rows]))) <= t.tau
+
+
+def test_cfg3_fp32_companion_sampled(H, torch):
+    """cfg3-fp32: order 3, N=512, all 22,370,048 canonical cells U(-1,1) (L=3), B=65,536."""
+    from oracle import colex_energy, colex_field
+    from workloads import uniform_colex
+    N, B = 512, 65536
+    v = uniform_colex(3, N, 3)
+    t = H.HoboTensor.import_colex(3, N, v)
+    X = x_bits(3, B, N)
+    G, E = fields(H, torch, t, X)
+    rows = np.array([0, 4097, B - 1])
+    assert np.max(np.abs(E[rows] - colex_energy(3, N, v, X[rows]))) <= t.tau
+    assert np.max(np.abs(G[rows] - colex_field(3, N, v, X[rows]))) <= t.tau

@@ -293,3 +293,44 @@ def test_search_oracle_finds_brute_optimum_and_is_honest():
     X0 = np.stack([[(hash4(1, 1, c, m >> 6) >> (m & 63)) & 1 for m in range(16)] for c in range(1024)]).astype(np.uint8)
     E0 = o.energy(X0)
     assert r0["e_best"] == E0.min() and r0["best_chain"] == int(np.argmin(E0))
+
+
+# ---- the colex-array oracle entry points used at full size ----------------------------------
+def test_colex_energy_qubo_closed_form():
+    """E = x^T Q x with Q_ii = c({i}), Q_ij = c({i,j}) (i<j): numpy float64 matmul."""
+    from oracle import colex_energy
+    from workloads import colex_rank, uniform_colex
+    N = 48
+    v = uniform_colex(2, N, 31)
+    Q = np.zeros((N, N))
+    for i in range(N):
+        Q[i, i] = v[0][i]
+        for j in range(i + 1, N):
+            Q[i, j] = v[1][colex_rank([i, j])]
+    X = x_bits(5, 200, N)
+    ref = np.einsum("bi,ij,bj->b", X.astype(np.float64), Q, X.astype(np.float64))
+    assert np.allclose(colex_energy(2, N, v, X), ref, rtol=0, atol=1e-9 * np.abs(Q).sum())
+
+
+@pytest.mark.parametrize("order", [3, 4])
+def test_colex_field_flip_identity(order):
+    from oracle import colex_energy, colex_field
+    from workloads import int_twin_colex
+    N = 9
+    v = int_twin_colex(order, N, 17)
+    X = exhaustive_X(N)
+    E = colex_energy(order, N, v, X)
+    G = colex_field(order, N, v, X)
+    t = np.arange(1 << N)
+    for m in range(N):
+        assert np.array_equal(E[t ^ (1 << m)] - E, (1 - 2 * X[:, m].astype(np.float64)) * G[:, m])
+
+
+def test_colex_matches_cell_list():
+    from oracle import colex_energy, colex_field
+    from workloads import uniform_colex
+    v = uniform_colex(3, 26, 4)
+    o = Oracle.from_cells(3, 26, *uniform_cells(3, 26, 4))
+    X = x_bits(2, 64, 26)
+    assert np.array_equal(colex_energy(3, 26, v, X), o.energy(X))
+    assert np.array_equal(colex_field(3, 26, v, X), o.field(X))

@@ -17,7 +17,8 @@ __all__ = [
     "LIN", "FAC", "TERM", "Problem", "TermBuilder", "splitmix64", "h", "x_bits",
     "seating", "pythagoras", "tsp", "cfg3_problem", "uniform_cells", "int_twin_cells",
     "canonical_cells_all", "subsets", "random_integer_problem", "exhaustive_X",
-    "paper_grids", "pyth_bits", "tsp_bits",
+    "paper_grids", "pyth_bits", "tsp_bits", "colex_subsets", "uniform_colex", "int_twin_colex",
+    "colex_rank",
 ]
 
 # memory layout of hobo_lin / hobo_factor / hobo_term (16 bytes each, natural alignment)
@@ -261,3 +262,63 @@ def random_integer_problem(order: int, N: int, seed: int, nterms: int, maxc: int
                 facs.append(_var(int(rng.integers(0, N))))
         tb.add(float(rng.integers(-maxc, maxc + 1)), facs)
     return tb.problem(order, N, f"randint{order}_{N}")
+
+
+def colex_subsets(n: int, r: int) -> np.ndarray:
+    """All r-subsets of range(n) in colex order (sorted rows; max element slowest), int32."""
+    if r == 0:
+        return np.zeros((1, 0), np.int32)
+    if n < r:
+        return np.zeros((0, r), np.int32)
+    parts = []
+    for m in range(r - 1, n):
+        head = colex_subsets(m, r - 1) if r > 1 else np.zeros((1, 0), np.int32)
+        parts.append(np.concatenate([head, np.full((head.shape[0], 1), m, np.int32)], axis=1))
+    return np.concatenate(parts, axis=0)
+
+
+def colex_rank(s) -> int:
+    """colex_rank({a1<...<ar}) = sum_i C(a_i, i) (the index used by import_colex)."""
+    return sum(math.comb(int(a), i + 1) for i, a in enumerate(sorted(s)))
+
+
+def _colex_values(order, N, seed, fn, chunk_rows=1 << 22):
+    """Per-degree arrays over colex r-subsets (r = 1..order): value of the canonical cell
+    (s1 repeated order-r+1 times, s2..sr) with cell id sum_p t_p N^p, from fn(cid)."""
+    out = []
+    pw = np.array([N ** p for p in range(order)], dtype=np.uint64)
+    for r in range(1, order + 1):
+        vals = np.empty(math.comb(N, r), np.float32)
+        pos = 0
+        # colex order = for each max element m: the colex (r-1)-subsets of [0, m), then m
+        prev = colex_subsets(N, r - 1) if r > 1 else np.zeros((1, 0), np.int32)
+        for m in range(r - 1, N):
+            cnt = math.comb(m, r - 1)
+            head = prev[:cnt].astype(np.uint64)          # colex prefix = subsets of [0, m)
+            if r == 1:
+                tup_first = np.full(1, m, np.uint64)
+                cid = tup_first * pw.sum()
+            else:
+                s1 = head[:, 0]
+                cid = s1 * pw[: order - r + 1].sum()
+                for i in range(1, r - 1):
+                    cid = cid + head[:, i] * pw[order - r + i]
+                cid = cid + np.uint64(m) * pw[order - 1]
+            vals[pos:pos + cnt] = fn(cid)
+            pos += cnt
+        out.append(vals)
+    return out
+
+
+def uniform_colex(order: int, N: int, seed: int):
+    """The U(-1,1) canonical cells of uniform_cells(), as per-degree colex arrays."""
+    def fn(cid):
+        q = (h(seed, 0, cid, 0) >> np.uint64(40)).astype(np.int64)
+        return ((q - (1 << 23)).astype(np.float64) * 2.0 ** -23).astype(np.float32)
+    return _colex_values(order, N, seed, fn)
+
+
+def int_twin_colex(order: int, N: int, seed: int, mod: int = 17, shift: int = 8):
+    def fn(cid):
+        return ((h(seed, 0, cid, 0) % np.uint64(mod)).astype(np.int64) - shift).astype(np.float32)
+    return _colex_values(order, N, seed, fn)
