@@ -130,7 +130,8 @@ class ClockSampler:
             time.sleep(0.02)
 
     def summary(self, lo=0, hi=None):
-        rows = self.rows[lo:hi] or self.rows[-1:]
+        ok = lambda r: len(r) >= 7 and r[0].replace(".", "").isdigit()  # noqa: E731
+        rows = [r for r in self.rows[lo:hi] if ok(r)] or [r for r in self.rows if ok(r)][-1:]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
@@ -204,10 +205,14 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; HOBO_BENCH_BACKEND=gloo (+ ranks sharing a GPU) only for host-path tests
+    backend = os.environ.get("HOBO_BENCH_BACKEND", "nccl")
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    cdev = dev if backend == "nccl" else None     # where the combine's key tensor lives
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     from paper_2407_19987_b200 import HoboTensor, build
     from paper_2407_19987_b200.dist import combine_best
     from workloads import x_bits
@@ -239,7 +244,7 @@ def main():
         else:
             _, best = t.energy(Xd, E, row0=row0)
         if world > 1:
-            best = combine_best(best[0], best[1], device=dev)
+            best = combine_best(best[0], best[1], device=cdev)
         return best
 
     clk = ClockSampler(local).__enter__()
@@ -275,7 +280,7 @@ def main():
     my_ms = statistics.mean(step_ms)
     ms = my_ms
     if world > 1:
-        m = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+        m = torch.tensor([my_ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         ms = float(m.item())
     units = world * B if per_gpu is not None else (a.batch * world if a.batch else (1 << 20))
@@ -330,7 +335,7 @@ def main():
                 e2e_ms.append(s.elapsed_time(e))
         m2 = statistics.mean(e2e_ms)
         if world > 1:
-            mm = torch.tensor([m2], dtype=torch.float64, device=dev)
+            mm = torch.tensor([m2], dtype=torch.float64, device=cdev)
             dist.all_reduce(mm, op=dist.ReduceOp.MAX)
             m2 = float(mm.item())
         extras["e2e"] = {"value": units / (m2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * N,
