@@ -83,6 +83,14 @@ def dist_env():
     return world, rank, local
 
 
+def measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["hbm_gbs"]
+    except Exception:
+        return 6650.0
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -296,6 +304,7 @@ def main():
     # judged against the BURST figure; the sustained (power-capped) ratio is reported beside it
     peak = burst
     achieved = algo_flops / (kms / 1e3) / 1e12
+    hbm_peak = measured_hbm()
     traffic, traffic_src = None, None
     try:   # dram read+write bytes per launch of this kernel from the committed ncu --set full capture
         if a.config == "cfg3" and B == 65536:
@@ -310,9 +319,17 @@ def main():
     nct = Npad // 256
     algo_bytes = (t.limbs * Npad * Tpad * 2 + B * ((N + 31) // 32) * 4 + (B * N * 4 if mode == "field" else B * 4)
                   + nct * B * 8)                                    # W once, X bits, G (or E), Q
-    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+    # below the ridge (few candidates per W byte) the W stream from HBM binds instead
+    ridge = burst * 1e12 / (hbm_peak * 1e9)
+    hbm_bound = exec_flops / algo_bytes < ridge
+    if hbm_bound:
+        achieved_b = algo_bytes / (kms / 1e3) / 1e9
+    roof = {"bound": "hbm" if hbm_bound else "tensor",
+            "achieved": achieved_b if hbm_bound else achieved, "peak": hbm_peak if hbm_bound else peak,
+            "unit": "GB/s" if hbm_bound else "TFLOP/s",
+            "frac": (achieved_b / hbm_peak) if hbm_bound else achieved / peak, "tflops_algorithmic": achieved,
             "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": "kr_gemm_kernel<256,2> (open-index contraction, field mode)",
-            "kernel_ms": kms, "kernel_share_of_step": kms / my_ms,
+            "kernel_ms": kms, "kernel_share_of_step": kms / my_ms, "launches_per_step": launches / max(1, a.steps),
             "algorithmic_flops_per_launch": algo_flops, "executed_mma_flops_per_launch": exec_flops,
             "executed_tflops": exec_flops / (kms / 1e3) / 1e12, "frac_of_sustained": achieved / sustained,
             "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s"}

@@ -59,6 +59,8 @@ struct hobo_tensor {
   float* d_G = nullptr; size_t G_cap = 0;
   uint32_t* d_xbest = nullptr; size_t xbest_cap = 0;
   float* d_ebest = nullptr; size_t ebest_cap = 0;
+  float* d_Gpart = nullptr; size_t Gpart_cap = 0;      // split-K partials
+  double* d_Qpart = nullptr; size_t Qpart_cap = 0;
   int64_t last_launches = 0;
   double last_mma_macs = 0, last_algo_macs = 0;
   bool profile = false;
@@ -114,7 +116,7 @@ cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  k<<<dim3((unsigned)(p.n_ct * p.n_cb)), dim3(kThreads), smem, s>>>(L.tmap, p);
+  k<<<dim3((unsigned)(p.n_split * p.n_ct * p.n_cb)), dim3(kThreads), smem, s>>>(L.tmap, p);
   return cudaGetLastError();
 }
 
@@ -208,6 +210,7 @@ hobo_status ensure_layout(hobo_tensor* t, int field) {
     lp.Npad = L.Npad;
     lp.L = H.limbs;
     lp.field_mode = field;
+    lp.NT = L.NT;
     layout_kernel<<<148 * 8, 256>>>(lp);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
@@ -221,11 +224,13 @@ hobo_status ensure_layout(hobo_tensor* t, int field) {
   // TMA map over the 2-D view [L * Npad rows][Tpad tuples], box 64 x NT, 128-byte swizzle
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {(cuuint64_t)Tpad, (cuuint64_t)H.limbs * L.Npad};
-  cuuint64_t strides[1] = {(cuuint64_t)Tpad * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)L.NT};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&L.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, L.W, dims, strides, box, estr,
+  // 3-D view of the tile-blocked planes: (64 tuples, NT rows, box index), box = one block
+  const int64_t n_kb = Tpad / kBK;
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)L.NT, (cuuint64_t)H.limbs * L.n_ct * n_kb};
+  cuuint64_t strides[2] = {(cuuint64_t)kBK * 2, (cuuint64_t)kBK * 2 * L.NT};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)L.NT, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&L.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.W, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
@@ -262,6 +267,8 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.Npad = L.Npad;
   p.n_ct = L.n_ct;
   p.n_cb = (int)((B + kBM - 1) / kBM);
+  p.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, kBK) / kBK);
+  p.n_split = 1;
   p.nseg = t->kl.nseg;
   p.L = t->host.limbs;
   p.field_mode = (&L == &t->lay[1]) ? 1 : 0;
@@ -272,6 +279,22 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   if (const char* e = getenv("HOBO_DBG")) p.dbg = atoi(e);
 #endif
   return p;
+}
+
+// split-K factor: only when the (candidate block x column tile) grid cannot fill the GPU;
+// then about one wave of long-running CTAs (each streams its K chunk of W once)
+int choose_split(hobo_tensor* t, const DevLayout& L, long long B) {
+  const long long tiles = ((B + kBM - 1) / kBM) * L.n_ct;
+  if (tiles >= 148) return 1;
+  const int KPS = KrCfg<256>::kps(t->host.limbs);
+  int stages = 0;
+  for (int ct = 0; ct < L.n_ct; ++ct) {
+    int s = 0;
+    for (int j = 0; j < t->kl.nseg; ++j) s += (L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1] + KPS - 1) / KPS;
+    stages = std::max(stages, s);
+  }
+  const long long want = 148 / tiles;
+  return (int)std::max<long long>(1, std::min<long long>({want, stages / 4, 148}));
 }
 
 double exec_macs(hobo_tensor* t, const DevLayout& L, long long B) {
@@ -305,10 +328,26 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, t->host.N, t->W, t->d_bits);
   CK(cudaGetLastError());
   KrParams p = make_params(t, L, t->d_bits, B, G, t->d_Q);
+  p.n_split = choose_split(t, L, B);
+  if (p.n_split > 1) {
+    if (field) {
+      if (hobo_status st = grow(t, t->d_Gpart, t->Gpart_cap, (size_t)p.n_split * B * t->host.N)) return st;
+      p.G = t->d_Gpart;
+    }
+    if (hobo_status st = grow(t, t->d_Qpart, t->Qpart_cap, (size_t)p.n_split * L.n_ct * B)) return st;
+    p.Q = t->d_Qpart;
+  }
   if (t->profile) CK(cudaEventRecord(t->ev0, s));
   CK(launch_kr_any(L, p, s));
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
   t->last_launches = 2;
+  if (p.n_split > 1) {
+    const long long nG = field ? B * t->host.N : 0, nQ = (long long)L.n_ct * B;
+    splitk_reduce_kernel<<<(unsigned)std::min<long long>((std::max(nG, nQ) + 255) / 256, 148 * 8), 256, 0, s>>>(
+        t->d_Gpart, G, nG, t->d_Qpart, t->d_Q, nQ, p.n_split);
+    CK(cudaGetLastError());
+    t->last_launches += 1;
+  }
   t->last_mma_macs = exec_macs(t, L, B);
   t->last_algo_macs = algo_macs(t, field != 0, B);
   return HOBO_OK;
@@ -362,7 +401,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
     if (L.d_sched) cudaFree(L.d_sched);
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
-  void* ptrs[] = {t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
+  void* ptrs[] = {t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;

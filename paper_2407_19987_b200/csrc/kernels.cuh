@@ -36,6 +36,9 @@ struct KrParams {
   double* Q;                // [n_ct][B] weighted partial energies (fixed-order, no atomics)
   long long B;
   int N, W, Npad, n_ct, n_cb, nseg, L, field_mode;
+  int n_kb;                 // K-blocks per (limb, column tile): Tpad / 64
+  int n_split;              // split-K: CTAs of one (candidate block, column tile) split the K
+                            // schedule; split s writes partials G + s*B*N, Q[(s*n_ct + ct)*B + b]
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
   double wp;                // weight of the degree-1 term
   int dbg;                  // debug builds only (HOBO_PIPE_STATS): pipeline bisection switches
@@ -137,10 +140,30 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #define EMPTY(s) (sBar + 8u * (C::MAXST + (s)))
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ct = blockIdx.x / p.n_cb, cb = blockIdx.x % p.n_cb;  // column-tile-major: concurrent CTAs share W tiles in L2
+  // block order: candidate block fastest, then column tile, then K split (concurrent CTAs
+  // share W tiles in L2)
+  const int cb = blockIdx.x % p.n_cb;
+  const int ct = (blockIdx.x / p.n_cb) % p.n_ct;
+  const int split = blockIdx.x / (p.n_cb * p.n_ct);
   const long long b0 = (long long)cb * kBM;
-  const int2* sched = p.sched + (size_t)ct * p.nseg;
   const int KPS = C::kps(p.L), NST = C::nst(p.L);
+  __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
+  if (threadIdx.x == 0) {
+    // stage range of this split over the tile's whole schedule (segments j = nseg-1 .. 0)
+    const int2* gs = p.sched + (size_t)ct * p.nseg;
+    int total = 0;
+    for (int j = 0; j < p.nseg; ++j) total += (gs[j].y + KPS - 1) / KPS;
+    const int per = (total + p.n_split - 1) / p.n_split;
+    const int c0 = split * per, c1 = min(total, c0 + per);
+    int s0 = 0;
+    for (int j = p.nseg - 1; j >= 0; --j) {
+      const int ns = (gs[j].y + KPS - 1) / KPS;
+      const int a = max(s0, c0) - s0, bb = min(s0 + ns, c1) - s0;
+      if (bb > a) sched[j] = make_int2(gs[j].x + a * KPS, min(gs[j].y, bb * KPS) - a * KPS);
+      else sched[j] = make_int2(gs[j].x, 0);
+      s0 += ns;
+    }
+  }
   const uint32_t stage_bytes = (uint32_t)(KPS * p.L) * C::BOX;
   // segments run in ascending degree order (j = nseg-1 .. 0); in field mode the single
   // accumulator is snapshot after each degree so the energy can weight degree r by 1/r
@@ -186,8 +209,9 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           mbar_arrive_expect_tx(FULL(st), (uint32_t)(nkb * p.L) * C::BOX);
           for (int q = 0; q < nkb; ++q)
             for (int l = 0; l < p.L; ++l)
-              tma_load_2d(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX, &tmap, FULL(st), (kb0 + q) * kBK,
-                          l * p.Npad + ct * NT);
+              // W is tile-blocked: box (l, ct, kb) is one contiguous NT x 64 block
+              tma_load_3d(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX, &tmap, FULL(st), 0, 0,
+                          (l * p.n_ct + ct) * p.n_kb + kb0 + q);
         }
       }
       PSTAT_FLUSH(6, w_tma);
@@ -324,12 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         const float v = __uint_as_float(r[c]);
-        const float pm = __ldg(p.p1 + mbase + c);
+        const float pm = split == 0 ? __ldg(p.p1 + mbase + c) : 0.0f;   // degree 1 counted once
         g[c] = v + pm;
         if ((xw >> c) & 1u) { sfin += (double)v; sp += (double)pm; }
       }
       if (p.field_mode && live) {
-        float* gout = p.G + (size_t)b * p.N + mbase;
+        float* gout = p.G + ((size_t)split * p.B + b) * p.N + mbase;
         const int nvalid = min(32, p.N - mbase);
         if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(gout) & 15) == 0)) {
 #pragma unroll
@@ -357,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     // combine the two column halves in a fixed order (deterministic, no atomics)
     if (h == 1) qpart[row] = qsum;
     named_bar_sync(1, 256);
-    if (h == 0 && live) p.Q[(size_t)ct * p.B + b] = qsum + qpart[row];
+    if (h == 0 && live) p.Q[((size_t)split * p.n_ct + ct) * p.B + b] = qsum + qpart[row];
   }
 #undef FULL
 #undef EMPTY
@@ -378,6 +402,22 @@ __global__ void pack_x_kernel(const uint8_t* __restrict__ X, long long B, int N,
     uint32_t v = 0;
     for (int j = 0; j < n; ++j) v |= (uint32_t)(src[j] != 0) << j;
     bits[i] = v;
+  }
+}
+
+// split-K: sum the per-split partials in a fixed order (deterministic)
+__global__ void splitk_reduce_kernel(const float* __restrict__ Gp, float* __restrict__ G, long long nG,
+                                     const double* __restrict__ Qp, double* __restrict__ Q, long long nQ, int n_split) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nG; i += stride) {
+    float g = 0.0f;
+    for (int s = 0; s < n_split; ++s) g += Gp[(size_t)s * nG + i];
+    G[i] = g;
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nQ; i += stride) {
+    double q = 0.0;
+    for (int s = 0; s < n_split; ++s) q += Qp[(size_t)s * nQ + i];
+    Q[i] = q;
   }
 }
 
@@ -428,14 +468,15 @@ __global__ void finalize_kernel(const double* __restrict__ Q, int n_ct, long lon
 }
 
 // ------------------------------------------------------------------------------------------
-// device layout: W[l][m][t] bf16 limb planes from the per-degree colex cell arrays
+// device layout: bf16 limb planes of W, tile-blocked so that every TMA box is one
+// contiguous NT x 64 block: W[l][ct][kb][m % NT][t % 64]
 struct LayoutParams {
   const uint16_t* tuples;        // [Tpad][6]
   const float* const* strict;    // strict[r] device pointers (r = 0..order)
   const long long* binomT;       // [(N+1) * 7]: C(n, i)
   __nv_bfloat16* Wout;           // [L][Npad][Tpad]
   long long Tpad;
-  int N, Npad, L, field_mode;
+  int N, Npad, L, field_mode, NT;
 };
 
 __device__ __forceinline__ long long dbinom(const long long* t, int n, int i) { return (n < i || i < 0) ? 0 : t[n * 7 + i]; }
@@ -473,7 +514,8 @@ __global__ void layout_kernel(const LayoutParams lp) {
     const float r2 = r1 - __bfloat162float(mid);
     const __nv_bfloat16 lo = __float2bfloat16_rn(r2);
     const size_t plane = (size_t)lp.Npad * lp.Tpad;
-    const size_t off = (size_t)m * lp.Tpad + t;
+    const long long n_kb = lp.Tpad / 64;
+    const size_t off = ((size_t)((m / lp.NT) * n_kb + t / 64) * lp.NT + (m % lp.NT)) * 64 + (t % 64);
     lp.Wout[off] = hi;
     if (lp.L > 1) lp.Wout[plane + off] = mid;
     if (lp.L > 2) lp.Wout[2 * plane + off] = lo;

@@ -270,3 +270,28 @@ def test_cfg3_fp32_companion_sampled(H, torch):
     rows = np.array([0, 4097, B - 1])
     assert np.max(np.abs(E[rows] - colex_energy(3, N, v, X[rows]))) <= t.tau
     assert np.max(np.abs(G[rows] - colex_field(3, N, v, X[rows]))) <= t.tau
+
+
+# ---- split-K (small batches) -----------------------------------------------------------------
+@pytest.mark.parametrize("B", [1, 16, 200])
+def test_small_batch_split_k_matches(H, torch, B):
+    """Small batches split the K schedule across CTAs (HBM-bound regime); on an integer
+    instance the fields and energies are bit-identical to the unsplit full-batch run and to
+    the oracle."""
+    p = cfg3_problem()
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = x_bits(3, B, 512)
+    G, E = fields(H, torch, t, X)
+    assert np.array_equal(G, o.field(X)) and np.array_equal(E, o.energy(X))
+    Ee, best = energies(H, torch, t, X)
+    assert np.array_equal(Ee, E) and best == (E.min(), int(np.argmin(E)))
+
+
+def test_small_batch_split_k_fp32(H, torch):
+    idx, val = uniform_cells(3, 300, 41)
+    t, o = H.HoboTensor.import_cells(3, 300, idx, val), Oracle.from_cells(3, 300, idx, val)
+    X = x_bits(41, 37, 300)
+    G, E = fields(H, torch, t, X)
+    assert np.max(np.abs(G - o.field(X))) <= o.tau and np.max(np.abs(E - o.energy(X))) <= o.tau
+    Ee, _ = energies(H, torch, t, X)
+    assert np.max(np.abs(Ee - o.energy(X))) <= o.tau
