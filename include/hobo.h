@@ -127,6 +127,17 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
                               int64_t iters, double p0, double p1, uint8_t* x_best_host,
                               float* e_best_host, int64_t* best_chain, void* stream);
 
+/* hobo_search_samples — the paper's result list ("Energy e, Occurrence n", P:202-206,
+ * P:226-243): the same search as hobo_search over `batch` chains, then the chains' best
+ * states are aggregated on the device (sorted by (E, assignment hash), duplicates grouped
+ * and counted) and the first `topk` distinct assignments are returned in the order
+ * energy ascending, occurrence descending, assignment lexicographic (x_0 first):
+ *   x_host [topk*N] u8, e_host [topk] (offset excluded), count_host [topk], *n_out =
+ *   min(topk, #distinct).  Host outputs; synchronises the stream.                        */
+hobo_status hobo_search_samples(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t iters,
+                                int64_t topk, uint8_t* x_host, float* e_host, int64_t* count_host,
+                                int64_t* n_out, void* stream);
+
 /* Launch statistics of the last call on this handle: number of kernel launches issued,
  * the executed tensor-core MACs of its contraction kernel(s), the algorithmic MACs
  * (DESIGN.md "Roofline"), and — when profiling is on — the CUDA-event time in ms of its

@@ -194,3 +194,19 @@ def colex_field(order, N, by_degree, X, nthreads=0):
     G = np.zeros((X.shape[0], N), np.float64)
     _L().or_colex_field(order, N, C.cast(ptrs, C.c_void_p), _ptr(X), X.shape[0], _ptr(G), _nthreads(nthreads))
     return G
+
+
+def aggregate(xs, es, topk=None):
+    """The sampler's result list ("Energy e, Occurrence n"):
+    distinct assignments with occurrence counts, ordered by energy ascending, occurrence
+    descending, assignment lexicographic (x_0 first).  xs: (n, N) u8, es: (n,) energies."""
+    groups = {}
+    for x, e in zip(np.asarray(xs, np.uint8), es):
+        k = bytes(x)
+        if k in groups:
+            groups[k][1] += 1
+        else:
+            groups[k] = [float(e), 1]
+    out = sorted(((e, -c, k) for k, (e, c) in groups.items()))
+    res = [(np.frombuffer(k, np.uint8).copy(), e, -c) for e, c, k in out]
+    return res if topk is None else res[:topk]

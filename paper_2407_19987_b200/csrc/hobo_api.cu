@@ -60,6 +60,10 @@ struct hobo_tensor {
   uint32_t* d_xbest = nullptr; size_t xbest_cap = 0;
   float* d_ebest = nullptr; size_t ebest_cap = 0;
   float* d_Gpart = nullptr; size_t Gpart_cap = 0;      // split-K partials
+  unsigned long long* d_k1 = nullptr; size_t k_cap = 0; // aggregation sort keys
+  unsigned long long* d_k2 = nullptr; size_t k2_cap = 0;
+  uint32_t* d_flag = nullptr; size_t flag_cap = 0;
+  uint32_t* d_starts = nullptr; size_t starts_cap = 0;
   double* d_Qpart = nullptr; size_t Qpart_cap = 0;
   int64_t last_launches = 0;
   double last_mma_macs = 0, last_algo_macs = 0;
@@ -401,7 +405,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
     if (L.d_sched) cudaFree(L.d_sched);
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
-  void* ptrs[] = {t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
+  void* ptrs[] = {t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -491,15 +495,16 @@ hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_
   return HOBO_OK;
 }
 
-hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
-                              double p0, double p1, uint8_t* x_best_host, float* e_best_host, int64_t* best_chain,
-                              void* stream) {
-  if (!t) return fail(HOBO_EINVAL, "null handle");
+}  // extern "C"
+
+namespace {
+// the search loop (reading 14): leaves each chain's best state in d_xbest / d_ebest
+hobo_status run_search(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters, double p0,
+                       double p1, cudaStream_t s, int64_t& launches) {
   if (nchains < 1 || iters < 0 || chain0 < 0 || chain0 + nchains > (int64_t)0xFFFFFFFF || !(p0 > 0) || !(p1 > 0))
     return fail(HOBO_EINVAL, "bad search arguments");
   if (hobo_status st = check_device(t)) return st;
   if (hobo_status st = ensure_layout(t, 1)) return st;
-  cudaStream_t s = (cudaStream_t)stream;
   const DevLayout& L = t->lay[1];
   const int N = t->host.N, W = t->W;
   const long long B = nchains;
@@ -514,13 +519,13 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
     const double v = std::floor(4294967296.0 * p0 * std::pow(p1 / p0, (double)it / (double)std::max<int64_t>(1, iters - 1)));
     P[(size_t)it] = (uint32_t)std::min(4294967295.0, std::max(0.0, v));
   }
-  int64_t launches = 0;
+  launches = 0;
   const unsigned g1 = (unsigned)std::min<long long>((B * W + 255) / 256, 148 * 16);
   search_init_kernel<<<g1, 256, 0, s>>>(seed, chain0, B, N, W, t->d_bits, t->d_ebest);
   CK(cudaGetLastError());
   ++launches;
-  KrParams p = make_params(t, L, t->d_bits, B, t->d_G, t->d_Q);
-  const unsigned gs = (unsigned)((B * 32 + 255) / 256);
+  KrParams p = make_params(t, L, t->d_bits, B, t->d_G, t->d_Q);   // n_split = 1: per-chain results never
+  const unsigned gs = (unsigned)((B * 32 + 255) / 256);             // depend on the shard size
   if (t->profile) CK(cudaEventRecord(t->ev0, s));
   for (int64_t it = 0; it <= iters; ++it) {
     CK(launch_kr_any(L, p, s));
@@ -531,6 +536,23 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
     launches += 2;
   }
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+  t->last_mma_macs = exec_macs(t, L, B) * (double)(iters + 1);
+  t->last_algo_macs = algo_macs(t, true, B) * (double)(iters + 1);
+  return HOBO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
+                              double p0, double p1, uint8_t* x_best_host, float* e_best_host, int64_t* best_chain,
+                              void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t launches = 0;
+  if (hobo_status st = run_search(t, seed, chain0, nchains, iters, p0, p1, s, launches)) return st;
+  const int N = t->host.N, W = t->W;
+  const long long B = nchains;
   CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
   search_best_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_ebest, B, chain0,
                                                                                              t->d_key);
@@ -548,8 +570,94 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
   if (e_best_host) *e_best_host = key_energy(key);
   if (best_chain) *best_chain = c;
   t->last_launches = launches;
-  t->last_mma_macs = exec_macs(t, L, B) * (double)(iters + 1);
-  t->last_algo_macs = algo_macs(t, true, B) * (double)(iters + 1);
+  return HOBO_OK;
+}
+
+hobo_status hobo_search_samples(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t iters, int64_t topk,
+                                uint8_t* x_host, float* e_host, int64_t* count_host, int64_t* n_out, void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (topk < 1 || !x_host || !e_host || !count_host || !n_out) return fail(HOBO_EINVAL, "bad output arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t launches = 0;
+  if (hobo_status st = run_search(t, seed, 0, batch, iters, 0.5, 0.005, s, launches)) return st;
+  const int N = t->host.N, W = t->W;
+  const long long B = batch;
+  long long n = 2048;
+  while (n < B) n <<= 1;
+  if (hobo_status st = grow(t, t->d_k1, t->k_cap, (size_t)n)) return st;
+  if (hobo_status st = grow(t, t->d_k2, t->k2_cap, (size_t)n)) return st;
+  if (hobo_status st = grow(t, t->d_flag, t->flag_cap, (size_t)B + 1)) return st;
+  if (hobo_status st = grow(t, t->d_starts, t->starts_cap, (size_t)B + 1)) return st;
+  const unsigned gb = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
+  agg_key_kernel<<<gb, 256, 0, s>>>(t->d_ebest, t->d_xbest, B, W, n, t->d_k1, t->d_k2);
+  CK(cudaGetLastError());
+  ++launches;
+  for (long long k = 2; k <= n; k <<= 1) {   // bitonic sort of (k1, k2), ascending
+    for (long long j = k >> 1; j >= 2048; j >>= 1) {
+      bitonic_global_kernel<<<gb, 256, 0, s>>>(t->d_k1, t->d_k2, n, j, k);
+      ++launches;
+    }
+    bitonic_shared_kernel<<<(unsigned)(n / 2048), 1024, 0, s>>>(t->d_k1, t->d_k2, k);
+    ++launches;
+  }
+  CK(cudaGetLastError());
+  agg_flag_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 16), 256, 0, s>>>(t->d_k1, t->d_k2, t->d_xbest,
+                                                                                          B, W, t->d_flag);
+  agg_scan_kernel<<<1, 1024, 0, s>>>(t->d_flag, B, t->d_starts, t->d_flag + B);
+  CK(cudaGetLastError());
+  launches += 2;
+  uint32_t ng = 0;
+  CK(cudaMemcpyAsync(&ng, t->d_flag + B, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // host: take leading groups (E ascending) until every group tied with the k-th is included
+  struct Grp { float e; int64_t count; uint32_t chain; std::vector<uint8_t> x; };
+  std::vector<Grp> gs;
+  std::vector<uint32_t> starts;
+  int64_t G = std::min<int64_t>(ng, std::max<int64_t>(4 * topk, 64));
+  for (;;) {
+    starts.resize((size_t)G + 1);
+    CK(cudaMemcpyAsync(starts.data(), t->d_starts, (size_t)G * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    starts[(size_t)G] = G < (int64_t)ng ? 0u : (uint32_t)B;
+    if (G < (int64_t)ng) CK(cudaMemcpy(&starts[(size_t)G], t->d_starts + G, 4, cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> k1(G), k2(G);
+    for (int64_t g = 0; g < G; ++g) {
+      CK(cudaMemcpyAsync(&k1[g], t->d_k1 + starts[g], 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&k2[g], t->d_k2 + starts[g], 8, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    const int64_t kth = std::min<int64_t>(topk, G) - 1;
+    const bool need_more = G < (int64_t)ng && (k1[G - 1] >> 32) == (k1[kth] >> 32);
+    if (need_more) { G = std::min<int64_t>(ng, 2 * G); continue; }
+    gs.clear();
+    for (int64_t g = 0; g < G; ++g) {
+      if ((k1[g] >> 32) > (k1[kth] >> 32)) break;
+      Grp r;
+      r.e = key_energy(k1[g]);
+      r.count = (int64_t)starts[g + 1] - starts[g];
+      r.chain = (uint32_t)(k2[g] & 0xFFFFFFFFull);
+      std::vector<uint32_t> row(W);
+      CK(cudaMemcpy(row.data(), t->d_xbest + (size_t)r.chain * W, W * 4, cudaMemcpyDeviceToHost));
+      r.x.resize(N);
+      for (int m = 0; m < N; ++m) r.x[m] = (uint8_t)((row[m >> 5] >> (m & 31)) & 1u);
+      gs.push_back(std::move(r));
+    }
+    break;
+  }
+  // the paper's listing order: energy ascending, occurrence descending, assignment lexicographic
+  std::sort(gs.begin(), gs.end(), [](const Grp& a, const Grp& b) {
+    if (a.e != b.e) return a.e < b.e;
+    if (a.count != b.count) return a.count > b.count;
+    return a.x < b.x;
+  });
+  const int64_t nk = std::min<int64_t>(topk, (int64_t)gs.size());
+  for (int64_t i = 0; i < nk; ++i) {
+    std::memcpy(x_host + i * N, gs[i].x.data(), N);
+    e_host[i] = gs[i].e;
+    count_host[i] = gs[i].count;
+  }
+  *n_out = nk;
+  t->last_launches = launches;
   return HOBO_OK;
 }
 

@@ -608,3 +608,104 @@ __global__ void search_best_kernel(const float* __restrict__ ebest, long long nc
 }
 
 }  // namespace hobo
+
+namespace hobo {
+
+// ------------------------------------------------------------------------------------------
+// sample aggregation (the paper's result list): dedupe the chains' best states,
+// count occurrences.  Sort key (k1, k2) = (ord(E) << 32 | hash_hi, hash_lo << 32 | chain):
+// equal assignments are contiguous, the order is total and deterministic.
+__device__ __forceinline__ uint64_t row_hash(const uint32_t* row, int W) {
+  uint64_t h = 0x243F6A8885A308D3ull;
+  for (int w = 0; w < W; ++w) h = d_splitmix64(h ^ row[w]);
+  return h;
+}
+
+__global__ void agg_key_kernel(const float* __restrict__ ebest, const uint32_t* __restrict__ xbest, long long B, int W,
+                               long long n, unsigned long long* k1, unsigned long long* k2) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if (i < B) {
+      const uint64_t h = row_hash(xbest + i * W, W);
+      k1[i] = (argmin_key(ebest[i], 0) & 0xFFFFFFFF00000000ull) | (h >> 32);
+      k2[i] = (h << 32) | (unsigned long long)i;
+    } else {
+      k1[i] = ~0ull;
+      k2[i] = ~0ull;
+    }
+  }
+}
+
+__device__ __forceinline__ bool key_gt(unsigned long long a1, unsigned long long a2, unsigned long long b1,
+                                       unsigned long long b2) {
+  return a1 > b1 || (a1 == b1 && a2 > b2);
+}
+
+// one bitonic pass with partner distance j >= 1024 (global memory)
+__global__ void bitonic_global_kernel(unsigned long long* k1, unsigned long long* k2, long long n, long long j, long long k) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long l = i ^ j;
+    if (l <= i) continue;
+    const bool up = (i & k) == 0;
+    const unsigned long long a1 = k1[i], a2 = k2[i], b1 = k1[l], b2 = k2[l];
+    if (key_gt(a1, a2, b1, b2) == up) { k1[i] = b1; k2[i] = b2; k1[l] = a1; k2[l] = a2; }
+  }
+}
+
+// all passes with j < 1024 of stage k, on 2048-element chunks in shared memory
+__global__ void __launch_bounds__(1024) bitonic_shared_kernel(unsigned long long* k1, unsigned long long* k2, long long k) {
+  __shared__ unsigned long long s1[2048], s2[2048];
+  const long long base = (long long)blockIdx.x * 2048;
+  for (int t = threadIdx.x; t < 2048; t += 1024) { s1[t] = k1[base + t]; s2[t] = k2[base + t]; }
+  __syncthreads();
+  for (long long j = (k >> 1) < 1024 ? (k >> 1) : 1024; j >= 1; j >>= 1) {
+    for (int t = threadIdx.x; t < 2048; t += 1024) {
+      const int l = t ^ (int)j;
+      if (l > t) {
+        const bool up = ((base + t) & k) == 0;
+        const unsigned long long a1 = s1[t], a2 = s2[t], b1 = s1[l], b2 = s2[l];
+        if (key_gt(a1, a2, b1, b2) == up) { s1[t] = b1; s2[t] = b2; s1[l] = a1; s2[l] = a2; }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < 2048; t += 1024) { k1[base + t] = s1[t]; k2[base + t] = s2[t]; }
+}
+
+// group starts: element i opens a group unless it repeats the previous assignment
+__global__ void agg_flag_kernel(const unsigned long long* __restrict__ k1, const unsigned long long* __restrict__ k2,
+                                const uint32_t* __restrict__ xbest, long long B, int W, uint32_t* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < B; i += (long long)gridDim.x * blockDim.x) {
+    uint32_t f = 1;
+    if (i > 0 && k1[i] == k1[i - 1] && (k2[i] >> 32) == (k2[i - 1] >> 32)) {
+      const uint32_t* a = xbest + (k2[i] & 0xFFFFFFFFull) * W;
+      const uint32_t* b = xbest + (k2[i - 1] & 0xFFFFFFFFull) * W;
+      f = 0;
+      for (int w = 0; w < W; ++w) f |= (a[w] != b[w]);   // a 64-bit hash collision stays a new group
+    }
+    flag[i] = f;
+  }
+}
+
+// one block: exclusive scan of the flags -> starts[g] = sorted position of group g
+__global__ void __launch_bounds__(1024) agg_scan_kernel(const uint32_t* __restrict__ flag, long long B, uint32_t* starts,
+                                                        uint32_t* n_groups) {
+  __shared__ uint32_t sums[1024];
+  const long long per = (B + 1023) / 1024;
+  const long long lo = threadIdx.x * per, hi = lo + per < B ? lo + per : B;
+  uint32_t c = 0;
+  for (long long i = lo; i < hi; ++i) c += flag[i];
+  sums[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {   // inclusive Hillis-Steele scan
+    const uint32_t v = threadIdx.x >= o ? sums[threadIdx.x - o] : 0u;
+    __syncthreads();
+    sums[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t g = sums[threadIdx.x] - c;
+  for (long long i = lo; i < hi; ++i)
+    if (flag[i]) starts[g++] = (uint32_t)i;
+  if (threadIdx.x == 1023) *n_groups = sums[1023];
+}
+
+}  // namespace hobo

@@ -17,7 +17,7 @@ _STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ES
 EXPORTED = [
     "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_free", "hobo_tensor_info",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field",
-    "hobo_search", "hobo_search_shard", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
+    "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
 ]
 
 
@@ -56,6 +56,7 @@ def lib():
         L.hobo_search.argtypes = [P, U64, I64, I64, P, C.POINTER(C.c_float), P]
         L.hobo_search_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, C.POINTER(C.c_float),
                                         C.POINTER(I64), P]
+        L.hobo_search_samples.argtypes = [P, U64, I64, I64, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_last_launch_stats.argtypes = [P, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]
         L.hobo_set_profiling.argtypes = [P, I]
         L.hobo_last_error.restype = C.c_char_p
@@ -203,6 +204,16 @@ class HoboTensor:
         _check(lib().hobo_search_shard(self._h, seed, chain0, nchains, iters, p0, p1, _np_ptr(x), C.byref(e),
                                        C.byref(c), _stream_handle(stream)))
         return x, e.value, c.value
+
+    def search_samples(self, seed, batch, iters, topk=10, stream=None):
+        """hobo_search_samples: list of (x u8[N], energy, occurrence), the paper's result format."""
+        x = np.zeros((topk, self.N), np.uint8)
+        e = np.zeros(topk, np.float32)
+        cnt = np.zeros(topk, np.int64)
+        n = C.c_int64()
+        _check(lib().hobo_search_samples(self._h, seed, batch, iters, topk, _np_ptr(x), _np_ptr(e), _np_ptr(cnt),
+                                         C.byref(n), _stream_handle(stream)))
+        return [(x[i], float(e[i]), int(cnt[i])) for i in range(n.value)]
 
     def set_profiling(self, enable=True):
         _check(lib().hobo_set_profiling(self._h, 1 if enable else 0))

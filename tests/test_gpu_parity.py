@@ -295,3 +295,19 @@ def test_small_batch_split_k_fp32(H, torch):
     assert np.max(np.abs(G - o.field(X))) <= o.tau and np.max(np.abs(E - o.energy(X))) <= o.tau
     Ee, _ = energies(H, torch, t, X)
     assert np.max(np.abs(Ee - o.energy(X))) <= o.tau
+
+
+# ---- result aggregation (the paper's Energy / Occurrence listing) ---------------------------
+@pytest.mark.parametrize("name,batch,iters,topk", [("seating4", 1024, 16, 8), ("pythagoras", 3000, 24, 10),
+                                                   ("tsp", 2000, 6, 6), ("rand", 5000, 9, 50)])
+def test_search_samples_match_oracle(H, torch, name, batch, iters, topk):
+    from oracle import aggregate
+    p = {"seating4": seating(4), "pythagoras": pythagoras(), "tsp": tsp(),
+         "rand": random_integer_problem(3, 18, 4, nterms=200)}[name]
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    got = t.search_samples(7, batch, iters, topk)
+    r = o.search(7, 0, batch, iters)
+    want = aggregate(r["chain_xbest"], r["chain_ebest"], topk)
+    assert len(got) == len(want)
+    for (gx, ge, gc), (wx, we, wc) in zip(got, want):
+        assert np.array_equal(gx, wx) and ge == we and gc == wc

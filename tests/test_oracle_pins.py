@@ -334,3 +334,25 @@ def test_colex_matches_cell_list():
     X = x_bits(2, 64, 26)
     assert np.array_equal(colex_energy(3, 26, v, X), o.energy(X))
     assert np.array_equal(colex_field(3, 26, v, X), o.field(X))
+
+
+# ---- result aggregation (SPEC S:472-480 examples) ---------------------------------------------
+def test_aggregate_examples():
+    from oracle import aggregate
+    r = aggregate(np.array([[0, 1], [0, 1], [1, 0]], np.uint8), [-1.0, -1.0, 0.0])
+    assert [(x.tolist(), e, c) for x, e, c in r] == [([0, 1], -1.0, 2), ([1, 0], 0.0, 1)]
+    assert aggregate(np.zeros((0, 3), np.uint8), []) == []
+    # ties in energy: occurrence descending, then assignment lexicographic
+    r = aggregate(np.array([[1, 0], [0, 1], [0, 1], [1, 1]], np.uint8), [0.0, 0.0, 0.0, 0.0])
+    assert [(x.tolist(), c) for x, _, c in r] == [([0, 1], 2), ([1, 0], 1), ([1, 1], 1)]
+
+
+def test_aggregate_occurrences_sum_to_shots():
+    from oracle import aggregate
+    o = Oracle.from_problem(tsp())
+    r = o.search(3, 0, 500, 8)
+    agg = aggregate(r["chain_xbest"], r["chain_ebest"])
+    assert sum(c for _, _, c in agg) == 500
+    assert agg[0][1] == r["e_best"] == -360.0
+    for x, e, _ in agg:
+        assert o.energy(x[None])[0] == e          # energy honesty
