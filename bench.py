@@ -376,6 +376,31 @@ def main():
             sa_ms = (time.perf_counter() - t0) * 1e3
             extras["search_samples"] = {"ms_wall": sa_ms, "aggregation_ms_wall": sa_ms - sm,
                                         "top": [[e, c] for _, e, c in samples[:3]]}
+        if mode == "field" and N <= 512 and t.limbs == 1:
+            # gradient descent's hot path: the same contraction at real p (bf16, A in 2 limbs)
+            from workloads import h as _h
+            u = ((_h(3, 3, np.arange(B, dtype=np.uint64)[:, None], np.arange(N, dtype=np.uint64)[None, :])
+                  >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -24))
+            Pd = torch.from_numpy(u).to(dev).to(torch.bfloat16).contiguous()
+            for _ in range(2):
+                t.multilinear_field(Pd, G, E)
+            t.set_profiling(True)
+            km = []
+            for _ in range(5):
+                flush.zero_()
+                t.multilinear_field(Pd, G, E)
+                km.append(t.launch_stats()["kernel_ms"])
+            st2 = t.launch_stats()
+            t.set_profiling(False)
+            kmm = statistics.mean(km)
+            extras["multilinear_field"] = {"kernel_ms": kmm, "cand_per_s": B / (kmm / 1e3),
+                                           "algo_tflops": 2 * st2["algo_macs"] / (kmm / 1e3) / 1e12,
+                                           "exec_tflops": 2 * st2["mma_macs"] / (kmm / 1e3) / 1e12}
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = t.gd_run(3, B, 20, 0.05, greedy_iters=32, topk=3)
+            extras["gd_run"] = {"shots": B, "steps": 20, "greedy_iters": 32, "ms_wall": (time.perf_counter() - t0) * 1e3,
+                                "top": [[e, c] for _, e, c in res]}
         if rank == 0 and a.config == "cfg3":
             extras["cpu_baseline"] = cpu_baseline()
     if world > 1:

@@ -111,6 +111,28 @@ hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X_dev, int64_t B, int64_t
 hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X_dev, int64_t B, int64_t row0,
                              float* G_dev, float* E_dev, hobo_best* best, void* stream);
 
+/* hobo_multilinear_field — the same contraction on REAL candidates p in [0,1]^N, the
+ * multilinear relaxation used by gradient descent ("the gradient is computed based
+ * on tensor contraction results"):
+ *   G_dev[b*N+m] = dE/dp_m = sum_{S contains m} c(S) prod_{u in S, u != m} p_bu,
+ *   E_dev[b]     = E(p_b) = sum_S c(S) prod_{u in S} p_bu        (nullable)
+ *   P_dev        device bf16 (raw 16-bit patterns), row-major B x N.  The products of up to
+ *                three bf16 values are exact in fp32 and are split exactly into bf16 limbs,
+ *                so the result is the gradient AT the bf16 p (fp32 accumulation).
+ * Requires N <= 512 (p rows are staged in shared memory) at L = 1.                       */
+hobo_status hobo_multilinear_field(hobo_tensor* t, const uint16_t* P_dev, int64_t B, float* G_dev,
+                                   float* E_dev, void* stream);
+
+/* hobo_gd_run — gradient descent on the multilinear relaxation:
+ * `shots` independent restarts; each starts from p = U(0,1) (counter hash), takes `steps`
+ * logit-parameterised steps theta <- theta - step_size * dE/dp * p(1-p) with p = sigmoid(theta)
+ * carried in bf16 (gradient from hobo_multilinear_field's contraction), rounds at 0.5 and
+ * runs `greedy_iters` steepest single-flip descent steps on the binary problem.  The final
+ * states are aggregated like hobo_search_samples (top-k, energy / occurrence).           */
+hobo_status hobo_gd_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t steps, double step_size,
+                        int64_t greedy_iters, int64_t topk, uint8_t* x_host, float* e_host,
+                        int64_t* count_host, int64_t* n_out, void* stream);
+
 /* hobo_search — batched heuristic search (P:81-83 simulated annealing is described only
  * qualitatively and the paper's sampler is undisclosed; the rule implemented is
  * DESIGN.md "Search rule").  `batch` chains start from counter-hash random x, run

@@ -332,6 +332,40 @@ int or_field(void* h, const uint8_t* X, int64_t B, double* G, int nthreads) {
 }
 
 // O7: idx t in [0, 2^N), x_m = (t >> m) & 1 (SURVEY 8(c) reading 12)
+int or_menergy(void* h, const double* P, int64_t B, double* E, int nthreads) {
+  Oracle* o = (Oracle*)h;
+  parallel_for(B, nthreads, [&](int64_t b) {
+    const double* p = P + b * o->N;
+    long double e = 0;
+    for (size_t c = 0; c < o->val.size(); ++c) {
+      long double t = o->val[c];
+      for (int32_t u : o->sets[c]) t *= p[u];
+      e += t;
+    }
+    E[b] = (double)e;
+  });
+  return 0;
+}
+
+int or_mfield(void* h, const double* P, int64_t B, double* G, int nthreads) {
+  Oracle* o = (Oracle*)h;
+  parallel_for(B, nthreads, [&](int64_t b) {
+    const double* p = P + b * o->N;
+    std::vector<long double> acc(o->N, 0.0L);
+    for (size_t c = 0; c < o->val.size(); ++c) {
+      const Mono& s = o->sets[c];
+      for (int32_t m : s) {
+        long double t = o->val[c];
+        for (int32_t u : s)
+          if (u != m) t *= p[u];
+        acc[m] += t;
+      }
+    }
+    for (int m = 0; m < o->N; ++m) G[b * o->N + m] = (double)acc[m];
+  });
+  return 0;
+}
+
 int or_brute(void* h, double* emin, int64_t* argmin, int64_t* n_ground, double* next_level,
              int64_t* ground, int64_t max_ground, int nthreads) {
   Oracle* o = (Oracle*)h;

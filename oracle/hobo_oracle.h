@@ -53,6 +53,10 @@ int or_monomials(void* handle, int32_t* degree, int32_t* vars, float* val);
 int or_energy(void* handle, const uint8_t* X, int64_t B, double* E, int nthreads);
 /* O4': the literal N^k contraction of the dense canonical tensor (small N only) */
 int or_energy_tensor(void* handle, const uint8_t* X, int64_t B, double* E);
+/* multilinear relaxation at real p in [0,1]^N:
+ *   E(p) = sum_cells val * prod_{u in S} p_u,  dE/dp_m = sum_{S contains m} val * prod_{S\m} p_u */
+int or_menergy(void* handle, const double* P, int64_t B, double* E, int nthreads);
+int or_mfield(void* handle, const double* P, int64_t B, double* G, int nthreads);
 /* O5: G[b*N + m] */
 int or_field(void* handle, const uint8_t* X, int64_t B, double* G, int nthreads);
 /* O7: brute force over 2^N (N <= 26).  Returns min, lowest argmin, #ground states,

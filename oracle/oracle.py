@@ -49,6 +49,8 @@ def _L():
         _lib.or_splitmix64.restype = U64
         _lib.or_search_thresholds.argtypes = [I64, D, D, P]
         _lib.or_colex_energy.argtypes = [I, I, P, P, I64, P, I]
+        _lib.or_menergy.argtypes = [P, P, I64, P, I]
+        _lib.or_mfield.argtypes = [P, P, I64, P, I]
         _lib.or_colex_field.argtypes = [I, I, P, P, I64, P, I]
     return _lib
 
@@ -151,6 +153,20 @@ class Oracle:
         X = np.ascontiguousarray(X, np.uint8)
         G = np.zeros((X.shape[0], self.N), np.float64)
         _L().or_field(self._h, _ptr(X), X.shape[0], _ptr(G), _nthreads(nthreads))
+        return G
+
+    def menergy(self, P, nthreads=0):
+        """E(p) of the multilinear relaxation at real p (rows of P)."""
+        P = np.ascontiguousarray(P, np.float64)
+        E = np.zeros(P.shape[0], np.float64)
+        _L().or_menergy(self._h, _ptr(P), P.shape[0], _ptr(E), _nthreads(nthreads))
+        return E
+
+    def mfield(self, P, nthreads=0):
+        """dE/dp of the multilinear relaxation at real p."""
+        P = np.ascontiguousarray(P, np.float64)
+        G = np.zeros((P.shape[0], self.N), np.float64)
+        _L().or_mfield(self._h, _ptr(P), P.shape[0], _ptr(G), _nthreads(nthreads))
         return G
 
     def brute(self, max_ground=64, nthreads=0):

@@ -63,6 +63,8 @@ struct hobo_tensor {
   unsigned long long* d_k1 = nullptr; size_t k_cap = 0; // aggregation sort keys
   unsigned long long* d_k2 = nullptr; size_t k2_cap = 0;
   uint32_t* d_flag = nullptr; size_t flag_cap = 0;
+  float* d_theta = nullptr; size_t theta_cap = 0;       // gradient descent state
+  uint16_t* d_P = nullptr; size_t P_cap = 0;
   uint32_t* d_starts = nullptr; size_t starts_cap = 0;
   double* d_Qpart = nullptr; size_t Qpart_cap = 0;
   int64_t last_launches = 0;
@@ -110,10 +112,10 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int NT>
+template <int NT, bool REAL>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  auto* k = kr_gemm_kernel<NT>;
-  const size_t smem = KrCfg<NT>::smem_bytes(p.W);
+  auto* k = kr_gemm_kernel<NT, REAL>;
+  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT>::smem_bytes(p.W);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -124,7 +126,22 @@ cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) { return launch_kr<256>(L, p, s); }
+cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  return p.preal ? launch_kr<256, true>(L, p, s) : launch_kr<256, false>(L, p, s);
+}
+
+constexpr size_t kMaxSmem = 232448 - 1024;   // 227 KB opt-in per block, minus static smem + margin
+
+// real-valued path geometry: p rows in shared memory next to the W ring
+bool real_geometry(hobo_tensor* t, int& pstride, int& ring, int& LA) {
+  int words = (t->host.N + 1) / 2;
+  if ((words & 1) == 0) ++words;            // odd word stride: conflict-free per-row reads
+  pstride = 2 * words;
+  ring = 0;
+  while (ring < KrCfg<256>::RING_BOXES && KrCfg<256>::smem_bytes_real(ring + 1, pstride) <= kMaxSmem) ++ring;
+  LA = std::min(3, std::max(1, t->host.order - 1));
+  return ring >= t->host.limbs;
+}
 
 hobo_status init_device(hobo_tensor* t);
 
@@ -273,6 +290,10 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.n_cb = (int)((B + kBM - 1) / kBM);
   p.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, kBK) / kBK);
   p.n_split = 1;
+  p.preal = nullptr;
+  p.LA = 1;
+  p.ring_boxes = KrCfg<256>::RING_BOXES;
+  p.pstride = 0;
   p.nseg = t->kl.nseg;
   p.L = t->host.limbs;
   p.field_mode = (&L == &t->lay[1]) ? 1 : 0;
@@ -323,15 +344,25 @@ float key_energy(unsigned long long key) {
   return f;
 }
 
-hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s) {
+hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
+                     const uint16_t* P = nullptr) {
   if (hobo_status st = ensure_layout(t, field)) return st;
   const DevLayout& L = t->lay[field];
-  if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * t->W)) return st;
   if (hobo_status st = grow(t, t->d_Q, t->Q_cap, (size_t)B * L.n_ct)) return st;
-  const long long nw = B * t->W;
-  pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, t->host.N, t->W, t->d_bits);
-  CK(cudaGetLastError());
+  if (!P) {
+    if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * t->W)) return st;
+    const long long nw = B * t->W;
+    pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, t->host.N, t->W,
+                                                                                             t->d_bits);
+    CK(cudaGetLastError());
+  }
   KrParams p = make_params(t, L, t->d_bits, B, G, t->d_Q);
+  if (P) {
+    if (!real_geometry(t, p.pstride, p.ring_boxes, p.LA))
+      return fail(HOBO_EINVAL, "real-valued path: N=" + std::to_string(t->host.N) + " with " +
+                                   std::to_string(t->host.limbs) + " limbs does not fit shared memory (N <= 512 at L=1)");
+    p.preal = P;
+  }
   p.n_split = choose_split(t, L, B);
   if (p.n_split > 1) {
     if (field) {
@@ -344,7 +375,7 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   if (t->profile) CK(cudaEventRecord(t->ev0, s));
   CK(launch_kr_any(L, p, s));
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
-  t->last_launches = 2;
+  t->last_launches = P ? 1 : 2;
   if (p.n_split > 1) {
     const long long nG = field ? B * t->host.N : 0, nQ = (long long)L.n_ct * B;
     splitk_reduce_kernel<<<(unsigned)std::min<long long>((std::max(nG, nQ) + 255) / 256, 148 * 8), 256, 0, s>>>(
@@ -352,7 +383,7 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     CK(cudaGetLastError());
     t->last_launches += 1;
   }
-  t->last_mma_macs = exec_macs(t, L, B);
+  t->last_mma_macs = exec_macs(t, L, B) * p.LA;
   t->last_algo_macs = algo_macs(t, field != 0, B);
   return HOBO_OK;
 }
@@ -405,7 +436,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
     if (L.d_sched) cudaFree(L.d_sched);
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
-  void* ptrs[] = {t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
+  void* ptrs[] = {t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -544,6 +575,23 @@ hobo_status run_search(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nc
 
 extern "C" {
 
+hobo_status hobo_multilinear_field(hobo_tensor* t, const uint16_t* P, int64_t B, float* G, float* E, void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (B < 0 || (B > 0 && (!P || !G))) return fail(HOBO_EINVAL, "bad batch or null P/G");
+  if (hobo_status st = check_device(t)) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (B == 0) return HOBO_OK;
+  if (hobo_status st = contract(t, 1, nullptr, B, G, s, P)) return st;
+  if (E) {
+    const DevLayout& L = t->lay[1];
+    finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_Q, L.n_ct, B, L.lcm, 0,
+                                                                                          E, nullptr);
+    CK(cudaGetLastError());
+    t->last_launches += 1;
+  }
+  return HOBO_OK;
+}
+
 hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
                               double p0, double p1, uint8_t* x_best_host, float* e_best_host, int64_t* best_chain,
                               void* stream) {
@@ -573,13 +621,13 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
   return HOBO_OK;
 }
 
-hobo_status hobo_search_samples(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t iters, int64_t topk,
-                                uint8_t* x_host, float* e_host, int64_t* count_host, int64_t* n_out, void* stream) {
-  if (!t) return fail(HOBO_EINVAL, "null handle");
-  if (topk < 1 || !x_host || !e_host || !count_host || !n_out) return fail(HOBO_EINVAL, "bad output arguments");
-  cudaStream_t s = (cudaStream_t)stream;
-  int64_t launches = 0;
-  if (hobo_status st = run_search(t, seed, 0, batch, iters, 0.5, 0.005, s, launches)) return st;
+}  // extern "C"
+
+namespace {
+// dedupe the chains' best states (d_xbest / d_ebest), count occurrences, return the top-k in
+// the paper's listing order (energy ascending, occurrence descending, assignment lexicographic)
+hobo_status aggregate_best(hobo_tensor* t, int64_t batch, int64_t topk, uint8_t* x_host, float* e_host,
+                           int64_t* count_host, int64_t* n_out, cudaStream_t s, int64_t& launches) {
   const int N = t->host.N, W = t->W;
   const long long B = batch;
   long long n = 2048;
@@ -657,6 +705,74 @@ hobo_status hobo_search_samples(hobo_tensor* t, uint64_t seed, int64_t batch, in
     count_host[i] = gs[i].count;
   }
   *n_out = nk;
+  return HOBO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+hobo_status hobo_search_samples(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t iters, int64_t topk,
+                                uint8_t* x_host, float* e_host, int64_t* count_host, int64_t* n_out, void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (topk < 1 || !x_host || !e_host || !count_host || !n_out) return fail(HOBO_EINVAL, "bad output arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t launches = 0;
+  if (hobo_status st = run_search(t, seed, 0, batch, iters, 0.5, 0.005, s, launches)) return st;
+  if (hobo_status st = aggregate_best(t, batch, topk, x_host, e_host, count_host, n_out, s, launches)) return st;
+  t->last_launches = launches;
+  return HOBO_OK;
+}
+
+hobo_status hobo_gd_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t steps, double step_size,
+                        int64_t greedy_iters, int64_t topk, uint8_t* x_host, float* e_host, int64_t* count_host,
+                        int64_t* n_out, void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (shots < 1 || steps < 0 || greedy_iters < 0 || !(step_size > 0) || topk < 1 || !x_host || !e_host ||
+      !count_host || !n_out || shots > (int64_t)0xFFFFFFFF)
+    return fail(HOBO_EINVAL, "bad gradient-descent arguments");
+  if (hobo_status st = check_device(t)) return st;
+  if (hobo_status st = ensure_layout(t, 1)) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevLayout& L = t->lay[1];
+  const int N = t->host.N, W = t->W;
+  const long long B = shots;
+  if (hobo_status st = grow(t, t->d_theta, t->theta_cap, (size_t)B * N)) return st;
+  if (hobo_status st = grow(t, t->d_P, t->P_cap, (size_t)B * N)) return st;
+  if (hobo_status st = grow(t, t->d_G, t->G_cap, (size_t)B * N)) return st;
+  if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * W)) return st;
+  if (hobo_status st = grow(t, t->d_Q, t->Q_cap, (size_t)B * L.n_ct)) return st;
+  if (hobo_status st = grow(t, t->d_xbest, t->xbest_cap, (size_t)B * W)) return st;
+  if (hobo_status st = grow(t, t->d_ebest, t->ebest_cap, (size_t)B)) return st;
+  int64_t launches = 0;
+  const unsigned ge = (unsigned)std::min<long long>((B * N + 255) / 256, 148 * 16);
+  gd_init_kernel<<<ge, 256, 0, s>>>(seed, B, N, t->d_theta, reinterpret_cast<__nv_bfloat16*>(t->d_P));
+  CK(cudaGetLastError());
+  ++launches;
+  if (t->profile) CK(cudaEventRecord(t->ev0, s));
+  for (int64_t it = 0; it < steps; ++it) {   // descent on the relaxation
+    if (hobo_status st = contract(t, 1, nullptr, B, t->d_G, s, t->d_P)) return st;
+    launches += t->last_launches;
+    gd_update_kernel<<<ge, 256, 0, s>>>(B * N, (float)step_size, t->d_G, t->d_theta,
+                                          reinterpret_cast<__nv_bfloat16*>(t->d_P));
+    CK(cudaGetLastError());
+    ++launches;
+  }
+  if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+  // round at 0.5, then steepest single-flip descent on the binary problem
+  gd_round_kernel<<<(unsigned)std::min<long long>((B * W + 255) / 256, 148 * 16), 256, 0, s>>>(B, N, W, reinterpret_cast<const __nv_bfloat16*>(t->d_P), t->d_bits,
+                                                                                             t->d_ebest);
+  CK(cudaGetLastError());
+  ++launches;
+  KrParams p = make_params(t, L, t->d_bits, B, t->d_G, t->d_Q);
+  const unsigned gs = (unsigned)((B * 32 + 255) / 256);
+  for (int64_t it = 0; it <= greedy_iters; ++it) {
+    CK(launch_kr_any(L, p, s));
+    search_step_kernel<<<gs, 256, 0, s>>>(t->d_Q, L.n_ct, L.lcm, t->d_G, t->d_bits, t->d_xbest, t->d_ebest, 0, B, N, W,
+                                          seed, it, 0u, it < greedy_iters ? 1 : 0, 1);
+    CK(cudaGetLastError());
+    launches += 2;
+  }
+  if (hobo_status st = aggregate_best(t, B, topk, x_host, e_host, count_host, n_out, s, launches)) return st;
   t->last_launches = launches;
   return HOBO_OK;
 }

@@ -37,6 +37,11 @@ struct KrParams {
   long long B;
   int N, W, Npad, n_ct, n_cb, nseg, L, field_mode;
   int n_kb;                 // K-blocks per (limb, column tile): Tpad / 64
+  // real-valued candidates (multilinear relaxation): p in bf16, B x N
+  const uint16_t* preal;
+  int LA;                   // bf16 limbs of the Khatri-Rao products of p (exact for <= 3 factors)
+  int ring_boxes;           // W boxes that fit next to the p rows in shared memory
+  int pstride;              // p row stride in shared memory (elements, odd word count)
   int n_split;              // split-K: CTAs of one (candidate block, column tile) split the K
                             // schedule; split s writes partials G + s*B*N, Q[(s*n_ct + ct)*B + b]
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
@@ -59,6 +64,16 @@ struct KrCfg {
   // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages
   __host__ __device__ static constexpr int kps(int L) { return L == 1 ? 2 : 1; }
   __host__ __device__ static constexpr int nst(int L) { return RING_BOXES / (kps(L) * L) < MAXST ? RING_BOXES / (kps(L) * L) : MAXST; }
+  // real-valued A: one K-block per stage, LA limb tiles of A in TMEM, ring sized at run time
+  __host__ __device__ static int nst_real(int L, int LA, int ring) {
+    int n = ring / L;
+    if (n > MAXST) n = MAXST;
+    const int t = (TMEM_COLS - NT) / (LA * A_COLS);
+    return n < t ? n : t;
+  }
+  static size_t smem_bytes_real(int ring, int pstride) {
+    return 1024 + (size_t)ring * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)kBM * pstride * 2 + 256;
+  }
 };
 
 // A bits of one run for one candidate row: x[lo .. lo+cnt) AND the fixed elements' bits,
@@ -103,6 +118,33 @@ __device__ __forceinline__ void expand32(uint32_t half, uint32_t (&w)[16]) {
   }
 }
 
+__device__ __forceinline__ float bf16_bits_to_float(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+
+// real-valued candidates: this thread's 32 Khatri-Rao entries (K-block half h) of one
+// K-block, a[c] = prod_{u in T} p_u for the tuple T at position 32h + c (0 for padding)
+__device__ __forceinline__ void real_block(const uint16_t* pr, const uint4 d0, const uint4 d1,
+                                           const uint4* __restrict__ runs, int h, float (&a)[32]) {
+  const uint32_t nfix = d0.w & 7u, nruns = (d0.w >> 3) & 127u;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = 0.0f;
+  auto apply = [&](const uint4 rr) {
+    const uint32_t start = rr.x & 0xFFu, cnt = (rr.x >> 8) & 0xFFu, lo = rr.x >> 16;
+    const uint32_t f[4] = {rr.y & 0xFFFFu, rr.y >> 16, rr.z & 0xFFFFu, rr.z >> 16};
+    float pf = 1.0f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if ((uint32_t)q < nfix) pf *= bf16_bits_to_float(pr[f[q]]);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t off = (uint32_t)(32 * h + c) - start;
+      if (off < cnt) a[c] = pf * bf16_bits_to_float(pr[lo + off]);
+    }
+  };
+  if (nruns > 0) apply(d0);
+  if (nruns > 1) apply(d1);
+  for (uint32_t i = 2; i < nruns; ++i) apply(__ldg(runs + (d0.w >> 10) + (i - 2)));
+}
+
 #ifdef HOBO_PIPE_STATS
 // debug builds only: per-CTA pipeline accounting (clock64 cycles), accumulated in registers
 //  [0] MMA loop  [1] MMA waiting FULL  [2] stages  [3] K-blocks  [4] issuing MMAs  [5] commits
@@ -119,7 +161,7 @@ __device__ unsigned long long g_pipe_stats[8192][8];
 // Ring slot s holds the stage's W boxes in shared memory and its A K-blocks in TMEM;
 // FULL(s) completes when the 8 generator warps arrived and the TMA bytes landed, EMPTY(s)
 // when the MMAs reading the slot completed (one tcgen05.commit).
-template <int NT>
+template <int NT, bool REAL>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
   using C = KrCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
@@ -127,13 +169,15 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 atoms need 1024-byte alignment
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sB = base;
-  const uint32_t sBar = sB + C::RING_BOXES * C::BOX;
+  const int ring = REAL ? p.ring_boxes : C::RING_BOXES;
+  const uint32_t sBar = sB + ring * C::BOX;
   const uint32_t acc_full = sBar + 8 * (2 * C::MAXST);
   const uint32_t snap_full = acc_full + 8, snap_empty = acc_full + 16;
   const uint32_t tslot = acc_full + 24;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
   const uint32_t sX = sQ + kBM * 8;
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
+  uint16_t* prow = reinterpret_cast<uint16_t*>(gbase + (sX - base));   // REAL: p rows [128][pstride]
   double* qpart = reinterpret_cast<double*>(gbase + (sQ - base));
   volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
 #define FULL(s) (sBar + 8u * (s))
@@ -146,7 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const int ct = (blockIdx.x / p.n_cb) % p.n_ct;
   const int split = blockIdx.x / (p.n_cb * p.n_ct);
   const long long b0 = (long long)cb * kBM;
-  const int KPS = C::kps(p.L), NST = C::nst(p.L);
+  const int KPS = REAL ? 1 : C::kps(p.L);
+  const int NST = REAL ? C::nst_real(p.L, p.LA, ring) : C::nst(p.L);
+  const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
   if (threadIdx.x == 0) {
     // stage range of this split over the tile's whole schedule (segments j = nseg-1 .. 0)
@@ -178,8 +224,16 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
   if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
-  // this CTA's candidate bits, column-major xs[w][row] (+2 zero words for window reads)
-  {
+  if constexpr (REAL) {
+    // this CTA's p rows (bf16), zero past N and past B; +64 slack for window over-reads
+    for (int i = threadIdx.x; i < kBM * p.pstride + 64; i += kThreads) {
+      const int r = i / p.pstride, c = i % p.pstride;
+      uint16_t v = 0;
+      if (r < kBM && c < p.N && b0 + r < p.B) v = __ldg(p.preal + (size_t)(b0 + r) * p.N + c);
+      prow[i] = v;
+    }
+  } else {
+    // this CTA's candidate bits, column-major xs[w][row] (+2 zero words for window reads)
     const int Wp = p.W + 2;
     for (int i = threadIdx.x; i < Wp * kBM; i += kThreads) {
       const int r = i / Wp, w = i % Wp;
@@ -232,13 +286,25 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           mbar_wait(FULL(st), (uint32_t)((n / NST) & 1));
           PT(stt[1] += clock64() - t0; stt[2] += 1; stt[3] += nkb; t0 = clock64();)
           tc_fence_after();
-          for (int q = 0; q < nkb; ++q) {
-            const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
-            for (int l = 0; l < p.L; ++l) {
-              const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX);
+          if constexpr (REAL) {   // one K-block: LA limb tiles of A x L limb boxes of W
+            for (int la = 0; la < p.LA; ++la) {
+              const uint32_t a_t = tmem + (uint32_t)(NT + st * ACOLS + la * C::A_COLS);
+              for (int l = 0; l < p.L; ++l) {
+                const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)l * C::BOX);
 #pragma unroll
-              for (int k = 0; k < kBK / 16; ++k)
-                umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
+                for (int k = 0; k < kBK / 16; ++k)
+                  umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(la | l | k));
+              }
+            }
+          } else {
+            for (int q = 0; q < nkb; ++q) {
+              const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
+              for (int l = 0; l < p.L; ++l) {
+                const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX);
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                  umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
+              }
             }
           }
           PT(stt[4] += clock64() - t0; t0 = clock64();)
@@ -272,22 +338,60 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     int n = 0;                       // stage counter (same sequence as the MMA issuer)
     bool any = false;                // has any MMA been issued yet (else F = 0)
     PT(unsigned long long w_gen = 0;)
-    auto xsum = [&](void) -> double {  // sum over this warp's columns of x_m * F_m
+    const uint16_t* prow_r = prow + (size_t)row * (REAL ? p.pstride : 0);
+    auto xsum = [&](void) -> double {  // sum over this warp's columns of x_m * F_m (p_m * F_m)
       double acc = 0.0;
       for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
         const int mbase = ct * NT + c0;
-        const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
         uint32_t r[32];
         tmem_ld32(lane_base + (uint32_t)c0, r);
         tmem_ld_wait();
+        if constexpr (REAL) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if ((xw >> c) & 1u) acc += (double)__uint_as_float(r[c]);
+          for (int c = 0; c < 32; ++c)
+            if (mbase + c < p.N) acc += (double)bf16_bits_to_float(prow_r[mbase + c]) * (double)__uint_as_float(r[c]);
+        } else {
+          const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if ((xw >> c) & 1u) acc += (double)__uint_as_float(r[c]);
+        }
       }
       return acc;
     };
     for (int j = p.nseg - 1; j >= 0; --j) {
       const int2 s = sched[j];
+      if constexpr (REAL) {
+        // one K-block per stage; both teams build it (team h: tuple positions 32h..32h+31)
+        uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
+        if (s.y > 0) { d0 = __ldg(p.kdesc + 2 * s.x); d1 = __ldg(p.kdesc + 2 * s.x + 1); }
+        for (int kb = s.x; kb < s.x + s.y; ++kb, ++n) {
+          uint4 n0 = d0, n1 = d1;
+          if (kb + 1 < s.x + s.y) { n0 = __ldg(p.kdesc + 2 * (kb + 1)); n1 = __ldg(p.kdesc + 2 * (kb + 1) + 1); }
+          const int st = n % NST;
+          mbar_wait(EMPTY(st), (uint32_t)(((n / NST) & 1) ^ 1));
+          tc_fence_after();
+          float a[32];
+          real_block(prow_r, d0, d1, p.runs, h, a);
+          for (int la = 0; la < p.LA; ++la) {   // exact bf16 limb split of the fp32 products
+            uint32_t w[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const __nv_bfloat16 h0 = __float2bfloat16_rn(a[2 * c]), h1 = __float2bfloat16_rn(a[2 * c + 1]);
+              w[c] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+              a[2 * c] -= __bfloat162float(h0);
+              a[2 * c + 1] -= __bfloat162float(h1);
+            }
+            tmem_st16(lane_base + (uint32_t)(NT + st * ACOLS + la * C::A_COLS + 16 * h), w);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(FULL(st));
+          d0 = n0;
+          d1 = n1;
+        }
+      } else {
       uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
       if (h < s.y) { d0 = __ldg(p.kdesc + 2 * (s.x + h)); d1 = __ldg(p.kdesc + 2 * (s.x + h) + 1); }
       for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS, ++n) {
@@ -314,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         d0 = n0;
         d1 = n1;
       }
+      }
       any = any || s.y > 0;
       if (snaps && j > 0) {
         mbar_wait(snap_full, (uint32_t)(nsnap & 1));
@@ -335,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     double sfin = 0.0, sp = 0.0;
     for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
       const int mbase = ct * NT + c0;
-      const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
+      const uint32_t xw = REAL ? 0u : ((mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u);
       uint32_t r[32];
       if (any) {
         tmem_ld32(lane_base + (uint32_t)c0, r);
@@ -350,7 +455,14 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const float v = __uint_as_float(r[c]);
         const float pm = split == 0 ? __ldg(p.p1 + mbase + c) : 0.0f;   // degree 1 counted once
         g[c] = v + pm;
-        if ((xw >> c) & 1u) { sfin += (double)v; sp += (double)pm; }
+        if constexpr (REAL) {
+          const double pw = mbase + c < p.N ? (double)bf16_bits_to_float(prow_r[mbase + c]) : 0.0;
+          sfin += pw * (double)v;
+          sp += pw * (double)pm;
+        } else if ((xw >> c) & 1u) {
+          sfin += (double)v;
+          sp += (double)pm;
+        }
       }
       if (p.field_mode && live) {
         float* gout = p.G + ((size_t)split * p.B + b) * p.N + mbase;
@@ -553,7 +665,7 @@ __global__ void search_init_kernel(uint64_t seed, long long chain0, long long nc
 // one warp per chain: best tracking, flip gain, move rule, flip
 __global__ void search_step_kernel(const double* __restrict__ Q, int n_ct, double lcm, const float* __restrict__ G,
                                    uint32_t* bits, uint32_t* xbest, float* ebest, long long chain0, long long nchains,
-                                   int N, int W, uint64_t seed, long long t, uint32_t P_t, int do_move) {
+                                   int N, int W, uint64_t seed, long long t, uint32_t P_t, int do_move, int greedy = 0) {
   const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (c >= nchains) return;
@@ -580,12 +692,16 @@ __global__ void search_step_kernel(const double* __restrict__ Q, int n_ct, doubl
     if (od < dmin || (od == dmin && om < mmin)) { dmin = od; mmin = om; }
   }
   if (lane == 0) {
-    const uint64_t r = d_hash(seed, 2, (uint64_t)(chain0 + c), (uint64_t)t);
-    const int mrand = (int)(((r & 0xffffffffull) * (uint64_t)N) >> 32);
-    int ms;
-    if ((uint32_t)(r >> 32) < P_t) ms = mrand;
-    else ms = (dmin < 0.0f) ? mmin : mrand;
-    xb[ms >> 5] ^= 1u << (ms & 31);
+    if (greedy) {            // steepest single-flip descent: flip only an improving site
+      if (dmin < 0.0f) xb[mmin >> 5] ^= 1u << (mmin & 31);
+    } else {
+      const uint64_t r = d_hash(seed, 2, (uint64_t)(chain0 + c), (uint64_t)t);
+      const int mrand = (int)(((r & 0xffffffffull) * (uint64_t)N) >> 32);
+      int ms;
+      if ((uint32_t)(r >> 32) < P_t) ms = mrand;
+      else ms = (dmin < 0.0f) ? mmin : mrand;
+      xb[ms >> 5] ^= 1u << (ms & 31);
+    }
   }
 }
 
@@ -708,4 +824,45 @@ __global__ void __launch_bounds__(1024) agg_scan_kernel(const uint32_t* __restri
   if (threadIdx.x == 1023) *n_groups = sums[1023];
 }
 
+}  // namespace hobo
+
+namespace hobo {
+// ------------------------------------------------------------------------------------------
+// gradient descent on the multilinear relaxation:
+// p = sigmoid(theta), theta <- theta - eta * dE/dp * p(1-p); p is carried in bf16.
+__global__ void gd_init_kernel(uint64_t seed, long long B, int N, float* theta, __nv_bfloat16* P) {
+  const long long total = B * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / N;
+    const int m = (int)(i % N);
+    const double u = ((double)(d_hash(seed, 3, (uint64_t)b, (uint64_t)m) >> 40) + 0.5) * 0x1p-24;   // U(0,1)
+    theta[i] = (float)log(u / (1.0 - u));
+    P[i] = __float2bfloat16_rn((float)u);
+  }
+}
+
+__global__ void gd_update_kernel(long long total, float eta, const float* __restrict__ G, float* theta,
+                                 __nv_bfloat16* P) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const float p = 1.0f / (1.0f + __expf(-theta[i]));
+    const float th = theta[i] - eta * G[i] * p * (1.0f - p);
+    theta[i] = th;
+    P[i] = __float2bfloat16_rn(1.0f / (1.0f + __expf(-th)));
+  }
+}
+
+// round at 0.5 into candidate bit rows (and reset the per-chain best)
+__global__ void gd_round_kernel(long long B, int N, int W, const __nv_bfloat16* __restrict__ P, uint32_t* bits,
+                                float* ebest) {
+  const long long total = B * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / W;
+    const int w = (int)(i % W);
+    uint32_t v = 0;
+    for (int j = 0; j < 32 && w * 32 + j < N; ++j)
+      v |= (uint32_t)(__bfloat162float(P[b * N + w * 32 + j]) >= 0.5f) << j;
+    bits[i] = v;
+    if (w == 0) ebest[b] = __int_as_float(0x7f800000);
+  }
+}
 }  // namespace hobo

@@ -17,7 +17,8 @@ _STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ES
 EXPORTED = [
     "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_free", "hobo_tensor_info",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field",
-    "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
+    "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
+    "hobo_gd_run", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
 ]
 
 
@@ -56,6 +57,8 @@ def lib():
         L.hobo_search.argtypes = [P, U64, I64, I64, P, C.POINTER(C.c_float), P]
         L.hobo_search_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, C.POINTER(C.c_float),
                                         C.POINTER(I64), P]
+        L.hobo_multilinear_field.argtypes = [P, P, I64, P, P, P]
+        L.hobo_gd_run.argtypes = [P, U64, I64, I64, D, I64, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_search_samples.argtypes = [P, U64, I64, I64, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_last_launch_stats.argtypes = [P, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]
         L.hobo_set_profiling.argtypes = [P, I]
@@ -194,6 +197,19 @@ class HoboTensor:
                                       C.byref(best) if want_best else None, _stream_handle(stream)))
         return (G, E, (best.e, best.idx)) if want_best else (G, E)
 
+    def multilinear_field(self, P, G=None, E=None, stream=None):
+        """Gradient and value of the multilinear relaxation at real p (CUDA bf16 tensor B x N)."""
+        import torch
+        B = P.shape[0]
+        pp = _dev_ptr(P, torch.bfloat16, (B, self.N))
+        if G is None:
+            G = torch.empty(B, self.N, dtype=torch.float32, device=P.device)
+        if E is None:
+            E = torch.empty(B, dtype=torch.float32, device=P.device)
+        _check(lib().hobo_multilinear_field(self._h, pp, B, _dev_ptr(G, torch.float32, (B, self.N)),
+                                            _dev_ptr(E, torch.float32, (B,)), _stream_handle(stream)))
+        return G, E
+
     def search(self, seed, batch, iters, chain0=None, nchains=None, p0=0.5, p1=0.005, stream=None):
         """hobo_search (or the shard [chain0, chain0+nchains)).  Returns (x_best u8[N], e_best, chain)."""
         x = np.zeros(self.N, np.uint8)
@@ -213,6 +229,18 @@ class HoboTensor:
         n = C.c_int64()
         _check(lib().hobo_search_samples(self._h, seed, batch, iters, topk, _np_ptr(x), _np_ptr(e), _np_ptr(cnt),
                                          C.byref(n), _stream_handle(stream)))
+        return [(x[i], float(e[i]), int(cnt[i])) for i in range(n.value)]
+
+    def gd_run(self, seed, shots, steps, step_size, greedy_iters=None, topk=10, stream=None):
+        """hobo_gd_run: gradient descent on the relaxation + rounding + greedy descent, aggregated."""
+        if greedy_iters is None:
+            greedy_iters = self.N
+        x = np.zeros((topk, self.N), np.uint8)
+        e = np.zeros(topk, np.float32)
+        cnt = np.zeros(topk, np.int64)
+        n = C.c_int64()
+        _check(lib().hobo_gd_run(self._h, seed, shots, steps, step_size, greedy_iters, topk, _np_ptr(x), _np_ptr(e),
+                                 _np_ptr(cnt), C.byref(n), _stream_handle(stream)))
         return [(x[i], float(e[i]), int(cnt[i])) for i in range(n.value)]
 
     def set_profiling(self, enable=True):

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import Oracle
-from workloads import (cfg3_problem, exhaustive_X, int_twin_cells, paper_grids, pythagoras,
+from workloads import (cfg3_problem, exhaustive_X, h, int_twin_cells, paper_grids, pythagoras,
                        random_integer_problem, seating, tsp, uniform_cells, x_bits)
 
 pytestmark = pytest.mark.gpu
@@ -311,3 +311,64 @@ def test_search_samples_match_oracle(H, torch, name, batch, iters, topk):
     assert len(got) == len(want)
     for (gx, ge, gc), (wx, we, wc) in zip(got, want):
         assert np.array_equal(gx, wx) and ge == we and gc == wc
+
+
+# ---- multilinear relaxation at real p (gradient descent's hot path) --------------------------
+def _p_bf16(torch, seed, B, N):
+    u = ((h(seed, 3, np.arange(B, dtype=np.uint64)[:, None], np.arange(N, dtype=np.uint64)[None, :]) >> np.uint64(40))
+         .astype(np.float64) * 2.0 ** -24)
+    Pd = torch.from_numpy(u.astype(np.float32)).cuda().to(torch.bfloat16).contiguous()
+    return Pd, Pd.float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("kind,order,N,B,seed", [("int", 3, 40, 300, 1), ("int", 2, 100, 129, 2), ("int", 4, 20, 200, 3),
+                                                 ("u", 3, 130, 257, 4), ("u", 3, 512, 64, 5), ("u", 2, 300, 500, 6),
+                                                 ("cfg3", 3, 512, 1000, 7)])
+def test_multilinear_field(H, torch, kind, order, N, B, seed):
+    from workloads import h  # noqa: F401
+    if kind == "int":
+        p = random_integer_problem(order, N, seed, nterms=300)
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    elif kind == "cfg3":
+        p = cfg3_problem()
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    else:
+        idx, val = uniform_cells(order, N, seed)
+        t, o = H.HoboTensor.import_cells(order, N, idx, val), Oracle.from_cells(order, N, idx, val)
+    if t.limbs > 1 and N > 300:
+        pytest.skip("real-valued path stages p rows in shared memory")
+    Pd, P = _p_bf16(torch, seed, B, N)
+    G, E = t.multilinear_field(Pd)
+    torch.cuda.synchronize()
+    Gr, Er = o.mfield(P), o.menergy(P)
+    assert np.max(np.abs(G.cpu().numpy() - Gr)) <= o.tau
+    assert np.max(np.abs(E.cpu().numpy() - Er)) <= o.tau
+
+
+def test_multilinear_field_binary_points_exact(H, torch):
+    """At p in {0,1} the relaxation is the binary field: bit-exact on an integer instance."""
+    p = random_integer_problem(3, 60, 9, nterms=400)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = x_bits(9, 200, 60)
+    G, E = t.multilinear_field(torch.from_numpy(X).cuda().to(torch.bfloat16))
+    torch.cuda.synchronize()
+    assert np.array_equal(G.cpu().numpy().astype(np.float64), o.field(X))
+    assert np.array_equal(E.cpu().numpy().astype(np.float64), o.energy(X))
+
+
+# ---- gradient descent (PAPER.md:85-87): quality and honesty of the returned states -------------
+@pytest.mark.parametrize("name,shots,steps,eta", [("tsp", 2000, 30, 0.05), ("seating4", 2000, 30, 0.2),
+                                                  ("pythagoras", 4000, 40, 1e-4), ("rand", 1000, 20, 0.05)])
+def test_gd_run(H, torch, name, shots, steps, eta):
+    p = {"seating4": seating(4), "pythagoras": pythagoras(), "tsp": tsp(),
+         "rand": random_integer_problem(3, 18, 4, nterms=200)}[name]
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    res = t.gd_run(11, shots, steps, eta, topk=20)
+    assert 1 <= len(res) <= 20 and sum(c for _, _, c in res) <= shots
+    X = np.stack([x for x, _, _ in res])
+    E = o.energy(X)
+    assert np.array_equal(E, np.array([e for _, e, _ in res], np.float64))       # honest energies
+    G = o.field(X)
+    assert np.all((1 - 2 * X.astype(np.float64)) * G >= 0)                          # greedy local minima
+    assert list(E) == sorted(E)
+    assert E[0] == o.brute()["emin"]                                                # finds the optimum

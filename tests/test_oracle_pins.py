@@ -356,3 +356,46 @@ def test_aggregate_occurrences_sum_to_shots():
     assert agg[0][1] == r["e_best"] == -360.0
     for x, e, _ in agg:
         assert o.energy(x[None])[0] == e          # energy honesty
+
+
+# ---- multilinear relaxation (gradient descent) ----------------
+def test_menergy_is_the_multilinear_extension():
+    """E(p) = sum over all binary x of E(x) prod p^x (1-p)^(1-x): the expectation of the
+    (pinned) binary energy under independent Bernoulli(p) bits, exhaustively for N = 9."""
+    p_ = random_integer_problem(3, 9, 12, nterms=80)
+    o = Oracle.from_problem(p_)
+    X = exhaustive_X(9).astype(np.float64)
+    Ex = o.energy(X.astype(np.uint8))
+    rng = np.random.default_rng(1)
+    P = rng.random((20, 9))
+    w = np.prod(np.where(X[None, :, :] == 1, P[:, None, :], 1 - P[:, None, :]), axis=2)   # 20 x 512
+    assert np.allclose(o.menergy(P), w @ Ex, rtol=0, atol=1e-9 * o.sum_abs)
+
+
+def test_mfield_central_differences():
+    """the gradient matches central finite differences of E(p)."""
+    idx, val = uniform_cells(4, 10, 3)
+    o = Oracle.from_cells(4, 10, idx, val)
+    rng = np.random.default_rng(2)
+    P = rng.random((6, 10))
+    G = o.mfield(P)
+    h_ = 1e-5
+    for m in range(10):
+        Pp, Pm = P.copy(), P.copy()
+        Pp[:, m] += h_
+        Pm[:, m] -= h_
+        fd = (o.menergy(Pp) - o.menergy(Pm)) / (2 * h_)
+        assert np.allclose(G[:, m], fd, rtol=1e-6, atol=1e-7 * o.sum_abs)
+
+
+def test_mfield_qubo_closed_form_and_binary_points():
+    idx, val = uniform_cells(2, 30, 8)
+    o = Oracle.from_cells(2, 30, idx, val)
+    Q = o.dense().astype(np.float64)
+    S = Q + Q.T
+    np.fill_diagonal(S, 0)
+    P = np.random.default_rng(3).random((7, 30))
+    assert np.allclose(o.mfield(P), np.diag(Q)[None, :] + P @ S, rtol=0, atol=1e-9 * o.sum_abs)
+    X = x_bits(4, 50, 30)
+    assert np.array_equal(o.mfield(X.astype(np.float64)), o.field(X))
+    assert np.array_equal(o.menergy(X.astype(np.float64)), o.energy(X))
