@@ -125,15 +125,39 @@ __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) { return __uint_
 __device__ __forceinline__ void real_block(const uint16_t* pr, const uint4 d0, const uint4 d1,
                                            const uint4* __restrict__ runs, int h, float (&a)[32]) {
   const uint32_t nfix = d0.w & 7u, nruns = (d0.w >> 3) & 127u;
-#pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = 0.0f;
-  auto apply = [&](const uint4 rr) {
-    const uint32_t start = rr.x & 0xFFu, cnt = (rr.x >> 8) & 0xFFu, lo = rr.x >> 16;
+  auto fixed_product = [&](const uint4 rr) {
     const uint32_t f[4] = {rr.y & 0xFFFFu, rr.y >> 16, rr.z & 0xFFFFu, rr.z >> 16};
     float pf = 1.0f;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if ((uint32_t)q < nfix) pf *= bf16_bits_to_float(pr[f[q]]);
+    return pf;
+  };
+  {
+    // fast path: run 0 covers this whole half -> 32 consecutive p values
+    const uint32_t start = d0.x & 0xFFu, cnt = (d0.x >> 8) & 0xFFu, lo = d0.x >> 16;
+    if (nruns >= 1 && start <= (uint32_t)(32 * h) && start + cnt >= (uint32_t)(32 * h + 32)) {
+      const float pf = fixed_product(d0);
+      const uint32_t base = lo + 32 * h - start;
+      const uint32_t* pw = reinterpret_cast<const uint32_t*>(pr) + (base >> 1);
+      const bool odd = base & 1u;
+      uint32_t wv[17];
+#pragma unroll
+      for (int i = 0; i < 17; ++i) wv[i] = pw[i];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint32_t pair = odd ? __funnelshift_r(wv[c], wv[c + 1], 16) : wv[c];
+        a[2 * c] = pf * __uint_as_float(pair << 16);
+        a[2 * c + 1] = pf * __uint_as_float(pair & 0xFFFF0000u);
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = 0.0f;
+  auto apply = [&](const uint4 rr) {
+    const uint32_t start = rr.x & 0xFFu, cnt = (rr.x >> 8) & 0xFFu, lo = rr.x >> 16;
+    const float pf = fixed_product(rr);
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       const uint32_t off = (uint32_t)(32 * h + c) - start;
@@ -377,10 +401,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             uint32_t w[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
-              const __nv_bfloat16 h0 = __float2bfloat16_rn(a[2 * c]), h1 = __float2bfloat16_rn(a[2 * c + 1]);
-              w[c] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-              a[2 * c] -= __bfloat162float(h0);
-              a[2 * c + 1] -= __bfloat162float(h1);
+              const __nv_bfloat162 hv = __floats2bfloat162_rn(a[2 * c], a[2 * c + 1]);   // one packed cvt
+              const uint32_t u = *reinterpret_cast<const uint32_t*>(&hv);
+              w[c] = u;
+              a[2 * c] -= __uint_as_float(u << 16);
+              a[2 * c + 1] -= __uint_as_float(u & 0xFFFF0000u);
             }
             tmem_st16(lane_base + (uint32_t)(NT + st * ACOLS + la * C::A_COLS + 16 * h), w);
           }
