@@ -127,18 +127,28 @@ cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  if (L.NT == 128) return p.preal ? launch_kr<128, true>(L, p, s) : launch_kr<128, false>(L, p, s);
   return p.preal ? launch_kr<256, true>(L, p, s) : launch_kr<256, false>(L, p, s);
 }
+
+template <int NT>
+int ring_boxes_for() { return KrCfg<NT>::RING_BOXES; }
 
 constexpr size_t kMaxSmem = 232448 - 1024;   // 227 KB opt-in per block, minus static smem + margin
 
 // real-valued path geometry: p rows in shared memory next to the W ring
-bool real_geometry(hobo_tensor* t, int& pstride, int& ring, int& LA) {
+template <int NT>
+int real_ring(int pstride) {
+  int ring = 0;
+  while (ring < KrCfg<NT>::RING_BOXES && KrCfg<NT>::smem_bytes_real(ring + 1, pstride) <= kMaxSmem) ++ring;
+  return ring;
+}
+
+bool real_geometry(hobo_tensor* t, int NT, int& pstride, int& ring, int& LA) {
   int words = (t->host.N + 1) / 2;
   if ((words & 1) == 0) ++words;            // odd word stride: conflict-free per-row reads
   pstride = 2 * words;
-  ring = 0;
-  while (ring < KrCfg<256>::RING_BOXES && KrCfg<256>::smem_bytes_real(ring + 1, pstride) <= kMaxSmem) ++ring;
+  ring = NT == 128 ? real_ring<128>(pstride) : real_ring<256>(pstride);
   LA = std::min(3, std::max(1, t->host.order - 1));
   return ring >= t->host.limbs;
 }
@@ -190,7 +200,7 @@ hobo_status ensure_layout(hobo_tensor* t, int field) {
   if (L.built) return HOBO_OK;
   const HostTensor& H = t->host;
   const int N = H.N, k = H.order;
-  L.NT = 256;
+  L.NT = N <= 128 ? 128 : 256;     // a 128-column tile when N fits (no padded columns)
   if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
   L.n_ct = (N + L.NT - 1) / L.NT;
   L.Npad = L.n_ct * L.NT;
@@ -292,7 +302,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.n_split = 1;
   p.preal = nullptr;
   p.LA = 1;
-  p.ring_boxes = KrCfg<256>::RING_BOXES;
+  p.ring_boxes = L.NT == 128 ? ring_boxes_for<128>() : ring_boxes_for<256>();
   p.pstride = 0;
   p.nseg = t->kl.nseg;
   p.L = t->host.limbs;
@@ -358,7 +368,7 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   }
   KrParams p = make_params(t, L, t->d_bits, B, G, t->d_Q);
   if (P) {
-    if (!real_geometry(t, p.pstride, p.ring_boxes, p.LA))
+    if (!real_geometry(t, L.NT, p.pstride, p.ring_boxes, p.LA))
       return fail(HOBO_EINVAL, "real-valued path: N=" + std::to_string(t->host.N) + " with " +
                                    std::to_string(t->host.limbs) + " limbs does not fit shared memory (N <= 512 at L=1)");
     p.preal = P;

@@ -52,8 +52,8 @@ struct KrParams {
 template <int NT>
 struct KrCfg {
   static constexpr int BOX = NT * 128;                   // one TMA box: NT rows x 64 bf16 (SW128)
-  static constexpr int RING_BOXES = 6;                   // shared-memory budget for W, in boxes
-  static constexpr int MAXST = 3;                        // max pipeline stages
+  static constexpr int RING_BOXES = 6 * 256 / NT;        // shared-memory budget for W (192 KB), in boxes
+  static constexpr int MAXST = NT >= 256 ? 3 : 6;        // max pipeline stages
   static constexpr int A_COLS = kBK / 2;                 // TMEM columns of one K-block of A (64 bf16 / lane)
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator, then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
