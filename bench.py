@@ -150,6 +150,46 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def tt_form_extra(dev, stream, flush, B=1 << 22):
+    """Section 8(f) row 4: energies from the Tensor-Train form of the paper's TSP
+    tensor (order 6, N=36, cores (6,2)...(2,6)) against the dense contraction, same candidates."""
+    import torch
+    from paper_2407_19987_b200.hobo import HoboTensor
+    from workloads import tsp, x_bits
+    t = HoboTensor.from_problem(tsp())
+    ranks = t.tt_build(0.0)
+    X = torch.from_numpy(x_bits(11, B, t.N)).to(dev)
+    E1 = torch.empty(B, dtype=torch.float32, device=dev)
+    E2 = torch.empty_like(E1)
+
+    def timed(fn):
+        fn()
+        ms = []
+        for _ in range(5):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            fn()
+            e.record(stream)
+            e.synchronize()
+            ms.append(s.elapsed_time(e))
+        return statistics.mean(ms)
+    tt_ms = timed(lambda: t.tt_energy(X, E1, want_best=False, stream=stream))
+    de_ms = timed(lambda: t.energy(X, E2, want_best=False, stream=stream))
+    diff = float((E1 - E2).abs().max().item())
+    rr = sum(ranks[p] * ranks[p + 1] for p in range(len(ranks) - 1))
+    flops = 2.0 * rr * (t.N / 2)            # useful: x has about N/2 ones
+    exec_flops = 2.0 * rr * t.N             # executed: a warp walks every i some lane needs
+    peak = 148 * 64 * 2 * 1.965e9 / 1e12    # FP64 FMA pipe, 64 DFMA/clk/SM at the measured 1965 MHz
+    return {"instance": "tsp (order 6, N=36)", "ranks": ranks, "batch": B, "tt_ms": tt_ms,
+            "tt_cand_per_s": B / (tt_ms / 1e3), "dense_ms": de_ms, "dense_cand_per_s": B / (de_ms / 1e3),
+            "max_abs_diff_tt_vs_dense": diff, "tt_fp64_gflops": flops * B / (tt_ms / 1e3) / 1e9,
+            "tt_input_gbps": B * (t.N + 4) / (tt_ms / 1e3) / 1e9,
+            "roofline": {"bound": "alu", "unit": "TFLOP/s", "achieved": exec_flops * B / (tt_ms / 1e3) / 1e12,
+                         "peak": peak, "frac": exec_flops * B / (tt_ms / 1e3) / 1e12 / peak,
+                         "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 1.965 GHz (guide: ~45 TF nominal)"}}
+
+
 def cpu_baseline(seconds=12.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
     import numpy as np
@@ -402,6 +442,7 @@ def main():
             extras["gd_run"] = {"shots": B, "steps": 20, "greedy_iters": 32, "ms_wall": (time.perf_counter() - t0) * 1e3,
                                 "top": [[e, c] for _, e, c in res]}
         if rank == 0 and a.config == "cfg3":
+            extras["tt_form"] = tt_form_extra(dev, stream, flush)
             extras["cpu_baseline"] = cpu_baseline()
     if world > 1:
         dist.barrier()

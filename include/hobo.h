@@ -133,6 +133,20 @@ hobo_status hobo_gd_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t st
                         int64_t greedy_iters, int64_t topk, uint8_t* x_host, float* e_host,
                         int64_t* count_host, int64_t* n_out, void* stream);
 
+/* hobo_tt_build — Tensor-Train decomposition of the canonical HOBO tensor by sequential SVD
+ * (host, double precision, one-sided Jacobi).  Singular values <= rel_tol *
+ * sigma_max of each unfolding are dropped; rel_tol < 1e-12 is raised to 1e-12, the
+ * round-off floor of the double SVD ("without approximation").
+ * ranks_out (nullable, order+1 ints) receives r_0..r_k (P:560 prints the TSP cores).
+ * Needs the dense tensor: N^order <= 2^24 cells, else HOBO_ENOMEM.                       */
+hobo_status hobo_tt_build(hobo_tensor* t, double rel_tol, int32_t* ranks_out);
+
+/* hobo_tt_energy — energies from the TT cores: E_b = prod_p (sum_i x_bi G_p[:, i, :])
+ * (the TT contraction of P:560-575, batched), fp64 arithmetic, ranks <= 32.  Same
+ * X / E / best conventions as hobo_energy.                                                 */
+hobo_status hobo_tt_energy(hobo_tensor* t, const uint8_t* X_dev, int64_t B, int64_t row0,
+                           float* E_dev, hobo_best* best, void* stream);
+
 /* hobo_search — batched heuristic search (P:81-83 simulated annealing is described only
  * qualitatively and the paper's sampler is undisclosed; the rule implemented is
  * DESIGN.md "Search rule").  `batch` chains start from counter-hash random x, run

@@ -10,8 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libhobo.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("hobo_api.cu", "host_compile.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "ptx.cuh", "host_compile.h")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("hobo_api.cu", "host_compile.cpp", "tt.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "ptx.cuh", "host_compile.h", "tt.h")] + [
     os.path.join(ROOT, "include", "hobo.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -13,6 +13,7 @@
 
 #include "../../include/hobo.h"
 #include "host_compile.h"
+#include "tt.h"
 #include "kernels.cuh"
 
 using namespace hobo;
@@ -64,6 +65,9 @@ struct hobo_tensor {
   unsigned long long* d_k2 = nullptr; size_t k2_cap = 0;
   uint32_t* d_flag = nullptr; size_t flag_cap = 0;
   float* d_theta = nullptr; size_t theta_cap = 0;       // gradient descent state
+  TTCores tt;                                           // Tensor-Train form (hobo_tt_build)
+  double* d_tt = nullptr;
+  int* d_tt_meta = nullptr;                             // [k] core offsets, [k+1] ranks
   uint16_t* d_P = nullptr; size_t P_cap = 0;
   uint32_t* d_starts = nullptr; size_t starts_cap = 0;
   double* d_Qpart = nullptr; size_t Qpart_cap = 0;
@@ -446,7 +450,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
     if (L.d_sched) cudaFree(L.d_sched);
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
-  void* ptrs[] = {t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
+  void* ptrs[] = {t->d_tt, t->d_tt_meta, t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -784,6 +788,77 @@ hobo_status hobo_gd_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t st
   }
   if (hobo_status st = aggregate_best(t, B, topk, x_host, e_host, count_host, n_out, s, launches)) return st;
   t->last_launches = launches;
+  return HOBO_OK;
+}
+
+hobo_status hobo_tt_build(hobo_tensor* t, double rel_tol, int32_t* ranks_out) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (!(rel_tol >= 0.0) || rel_tol >= 1.0) return fail(HOBO_EINVAL, "rel_tol must be in [0, 1)");
+  const double cells = std::pow((double)t->host.N, t->host.order);
+  if (cells > (double)(1 << 24)) return fail(HOBO_ENOMEM, "TT build needs the dense tensor: N^order <= 2^24 cells");
+  std::vector<float> dense((size_t)cells);
+  if (export_dense(t->host, dense.data())) return fail(HOBO_ENOMEM, "dense export failed");
+  std::vector<double> dd(dense.begin(), dense.end());
+  std::string msg;
+  // rel_tol below 1e-12 means "without approximation": the double SVD's round-off floor
+  if (int st = tt_decompose(t->host.order, t->host.N, dd, std::max(rel_tol, 1e-12), t->tt, msg))
+    return fail(st == 3 ? HOBO_ENOMEM : HOBO_EINVAL, msg);
+  if (ranks_out)
+    for (int p = 0; p <= t->host.order; ++p) ranks_out[p] = t->tt.ranks[p];
+  if (t->d_tt) { cudaFree(t->d_tt); t->d_tt = nullptr; }   // device copy rebuilt lazily
+  return HOBO_OK;
+}
+
+hobo_status hobo_tt_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row0, float* E, hobo_best* best,
+                           void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (t->tt.cores.empty()) return fail(HOBO_ESTATE, "call hobo_tt_build first");
+  if (B < 0 || (B > 0 && (!X || !E)) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF) return fail(HOBO_EINVAL, "bad batch");
+  if (hobo_status st = check_device(t)) return st;
+  const int k = t->host.order, N = t->host.N, W = t->W;
+  int rmax = 1;
+  for (int r : t->tt.ranks) rmax = std::max(rmax, r);
+  if (rmax > 32) return fail(HOBO_EINVAL, "TT rank " + std::to_string(rmax) + " > 32: use the dense contraction");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!t->d_tt) {
+    std::vector<double> flat;
+    std::vector<int> meta;
+    for (int p = 0; p < k; ++p) {
+      meta.push_back((int)flat.size());
+      flat.insert(flat.end(), t->tt.cores[p].begin(), t->tt.cores[p].end());
+    }
+    for (int r : t->tt.ranks) meta.push_back(r);
+    CK(cudaMalloc(&t->d_tt, flat.size() * sizeof(double)));
+    CK(cudaMemcpy(t->d_tt, flat.data(), flat.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (!t->d_tt_meta) CK(cudaMalloc(&t->d_tt_meta, 16 * sizeof(int)));
+    CK(cudaMemcpy(t->d_tt_meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  if (B == 0) {
+    if (best) { best->e = INFINITY; best->idx = -1; }
+    return HOBO_OK;
+  }
+  if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * W)) return st;
+  const long long nw = B * W;
+  pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, N, W, t->d_bits);
+  const unsigned g = (unsigned)std::min<long long>((B + 127) / 128, 148 * 32);
+  if (t->profile) CK(cudaEventRecord(t->ev0, s));
+  if (rmax <= 4) tt_energy_kernel<4><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+  else if (rmax <= 16) tt_energy_kernel<16><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+  else tt_energy_kernel<32><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+  if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+  CK(cudaGetLastError());
+  t->last_launches = 2;
+  if (best) {
+    CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+    search_best_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(E, B, row0, t->d_key);
+    CK(cudaGetLastError());
+    t->last_launches += 1;
+    unsigned long long key = 0;
+    CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    best->idx = (int64_t)(key & 0xFFFFFFFFull);
+    best->e = key_energy(key);
+  }
   return HOBO_OK;
 }
 

@@ -891,3 +891,41 @@ __global__ void gd_round_kernel(long long B, int N, int W, const __nv_bfloat16* 
   }
 }
 }  // namespace hobo
+
+namespace hobo {
+// ------------------------------------------------------------------------------------------
+// Tensor-Train form: E_b = prod_p ( sum_{i: x_bi = 1} G_p[:, i, :] ), a
+// chain of r x r matrices selected by the bits; fp64 (TT cores carry cancellations).
+template <int RM>
+__global__ void tt_energy_kernel(const double* __restrict__ cores, const int* __restrict__ off,
+                                 const int* __restrict__ ranks, int k, int N, int W, const uint32_t* __restrict__ bits,
+                                 long long B, float* __restrict__ E) {
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B; b += (long long)gridDim.x * blockDim.x) {
+    double v[RM];
+#pragma unroll
+    for (int a = 0; a < RM; ++a) v[a] = a == 0 ? 1.0 : 0.0;
+    int rp = 1;
+    for (int p = 0; p < k; ++p) {
+      const int rn = __ldg(ranks + p + 1);
+      const double* G = cores + __ldg(off + p);
+      double nv[RM];
+#pragma unroll
+      for (int c = 0; c < RM; ++c) nv[c] = 0.0;
+      for (int i = 0; i < N; ++i) {
+        if (!((__ldg(bits + b * W + (i >> 5)) >> (i & 31)) & 1u)) continue;
+#pragma unroll
+        for (int a = 0; a < RM; ++a) {
+          if (a >= rp) break;
+#pragma unroll
+          for (int c = 0; c < RM; ++c)
+            if (c < rn) nv[c] = fma(v[a], __ldg(G + ((size_t)a * N + i) * rn + c), nv[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < RM; ++c) v[c] = nv[c];
+      rp = rn;
+    }
+    E[b] = (float)v[0];
+  }
+}
+}  // namespace hobo

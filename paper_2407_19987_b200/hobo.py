@@ -18,7 +18,7 @@ EXPORTED = [
     "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_free", "hobo_tensor_info",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
-    "hobo_gd_run", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
+    "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
 ]
 
 
@@ -58,6 +58,8 @@ def lib():
         L.hobo_search_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, C.POINTER(C.c_float),
                                         C.POINTER(I64), P]
         L.hobo_multilinear_field.argtypes = [P, P, I64, P, P, P]
+        L.hobo_tt_build.argtypes = [P, D, P]
+        L.hobo_tt_energy.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_gd_run.argtypes = [P, U64, I64, I64, D, I64, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_search_samples.argtypes = [P, U64, I64, I64, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_last_launch_stats.argtypes = [P, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]
@@ -242,6 +244,24 @@ class HoboTensor:
         _check(lib().hobo_gd_run(self._h, seed, shots, steps, step_size, greedy_iters, topk, _np_ptr(x), _np_ptr(e),
                                  _np_ptr(cnt), C.byref(n), _stream_handle(stream)))
         return [(x[i], float(e[i]), int(cnt[i])) for i in range(n.value)]
+
+    def tt_build(self, rel_tol=0.0):
+        """Tensor-Train cores by sequential SVD; returns the bond ranks r_0..r_k."""
+        ranks = np.zeros(self.order + 1, np.int32)
+        _check(lib().hobo_tt_build(self._h, rel_tol, _np_ptr(ranks)))
+        return ranks.tolist()
+
+    def tt_energy(self, X, E=None, row0=0, want_best=True, stream=None):
+        """Energies from the TT form (after tt_build)."""
+        import torch
+        B = X.shape[0]
+        xp = _dev_ptr(X, torch.uint8, (B, self.N))
+        if E is None:
+            E = torch.empty(B, dtype=torch.float32, device=X.device)
+        best = HoboBest()
+        _check(lib().hobo_tt_energy(self._h, xp, B, row0, _dev_ptr(E, torch.float32, (B,)),
+                                    C.byref(best) if want_best else None, _stream_handle(stream)))
+        return E, ((best.e, best.idx) if want_best else None)
 
     def set_profiling(self, enable=True):
         _check(lib().hobo_set_profiling(self._h, 1 if enable else 0))

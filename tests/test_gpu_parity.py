@@ -372,3 +372,18 @@ def test_gd_run(H, torch, name, shots, steps, eta):
     assert np.all((1 - 2 * X.astype(np.float64)) * G >= 0)                          # greedy local minima
     assert list(E) == sorted(E)
     assert E[0] == o.brute()["emin"]                                                # finds the optimum
+
+
+# ---- Tensor-Train form ---------------------------------------------------
+@pytest.mark.parametrize("name", ["tsp", "seating4", "pythagoras", "rand"])
+def test_tt_energy(H, torch, name):
+    p = {"tsp": tsp(), "seating4": seating(4), "pythagoras": pythagoras(),
+         "rand": random_integer_problem(3, 10, 3, nterms=60)}[name]
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    t.tt_build(0.0)
+    X = exhaustive_X(p.N)
+    E, best = t.tt_energy(dev(torch, X))
+    torch.cuda.synchronize()
+    Eo = o.energy(X)
+    assert np.max(np.abs(E.cpu().numpy().astype(np.float64) - Eo)) <= o.tau
+    check_argmin(best, Eo, o.tau)

@@ -129,3 +129,12 @@ def test_errors(H):
     tb.add(-1.0, [(0.0, [(i, 1.0)]) for i in range(4)])
     tb.add(2.0, [(0.0, [(0, 1.0)])])
     assert H.HoboTensor.from_problem(tb.problem(2, 4)).ncells == 1
+
+
+def test_tt_build_reproduces_paper_core_shapes(H, pins):
+    """the TSP tensor (6,)*6 decomposes without approximation into cores
+    [(6,2),(2,6,3),(3,6,4),(4,6,4),(4,6,2),(2,6)] — the product's own Jacobi TT-SVD."""
+    t = H.HoboTensor.from_problem(tsp())
+    r = t.tt_build(0.0)
+    shapes = [[6, r[1]]] + [[r[p], 6, r[p + 1]] for p in range(1, 5)] + [[r[5], 6]]
+    assert shapes == pins["tt_core_shapes_tsp"]["value"] and r[0] == r[6] == 1
