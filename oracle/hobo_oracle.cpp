@@ -561,4 +561,57 @@ int or_search(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t i
   return 0;
 }
 
+
+// SPEC sa_run's geometric schedule: T_s = t_start (t_end/t_start)^(s/max(1,sweeps-1))
+int or_sa_temps(int64_t sweeps, double t_start, double t_end, double* out) {
+  if (sweeps < 1 || !(t_start > 0) || !(t_end > 0) || t_end > t_start) return 1;
+  for (int64_t s = 0; s < sweeps; ++s)
+    out[s] = t_start * std::pow(t_end / t_start, (double)s / (double)std::max<int64_t>(1, sweeps - 1));
+  return 0;
+}
+
+// SPEC sa_run: Metropolis single-bit flips in index order, one chain at a time
+int or_sa(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweeps, double t_start, double t_end,
+          uint8_t* x_out, double* e_out, int nthreads) {
+  Oracle* o = (Oracle*)h;
+  if (!o || nchains < 1) return 1;
+  std::vector<double> T((size_t)std::max<int64_t>(sweeps, 1));
+  if (or_sa_temps(std::max<int64_t>(sweeps, 1), t_start, t_end, T.data())) return 1;
+  const int N = o->N;
+  // the cells whose monomial contains m (g_m sums exactly these, O5)
+  std::vector<std::vector<size_t>> touching(N);
+  for (size_t c = 0; c < o->val.size(); ++c)
+    for (int32_t m : o->sets[c]) touching[m].push_back(c);
+  parallel_for(nchains, nthreads, [&](int64_t i) {
+    const uint64_t c = (uint64_t)(chain0 + i);
+    std::vector<uint8_t> x(N);
+    for (int m = 0; m < N; ++m) x[m] = (or_hash(seed, 1, c, (uint64_t)(m >> 6)) >> (m & 63)) & 1;
+    double e = energy_one(o, x.data());
+    for (int64_t s = 0; s < sweeps; ++s) {
+      for (int m = 0; m < N; ++m) {
+        long double g = 0;                            // g_m(x) = E(x|x_m=1) - E(x|x_m=0)
+        for (size_t cc : touching[m]) {
+          bool on = true;
+          for (int32_t u : o->sets[cc])
+            if (u != m && !x[u]) { on = false; break; }
+          if (on) g += (long double)o->val[cc];
+        }
+        const double d = x[m] ? -(double)g : (double)g;   // energy change of flipping x_m
+        bool accept = d <= 0.0;
+        if (!accept) {
+          const double u = (double)(or_hash(seed, 4, c, (uint64_t)(s * N + m)) >> 11) * 0x1.0p-53;
+          accept = u < std::exp(-d / T[(size_t)s]);
+        }
+        if (accept) {
+          x[m] ^= 1;
+          e += d;
+        }
+      }
+    }
+    for (int m = 0; m < N; ++m) x_out[i * N + m] = x[m];
+    e_out[i] = e;
+  });
+  return 0;
+}
+
 }  // extern "C"

@@ -52,6 +52,8 @@ def _L():
         _lib.or_menergy.argtypes = [P, P, I64, P, I]
         _lib.or_mfield.argtypes = [P, P, I64, P, I]
         _lib.or_colex_field.argtypes = [I, I, P, P, I64, P, I]
+        _lib.or_sa.argtypes = [P, U64, I64, I64, I64, D, D, P, P, I]
+        _lib.or_sa_temps.argtypes = [I64, D, D, P]
     return _lib
 
 
@@ -188,6 +190,23 @@ class Oracle:
         if st:
             raise ValueError(f"or_search status {st}")
         return dict(e_best=e.value, best_chain=c.value, chain_ebest=eb, chain_xbest=xb)
+
+    def sa(self, seed, chain0, nchains, sweeps, t_start, t_end, nthreads=0):
+        """SPEC sa_run replayed per chain: (final states nchains x N, tracked energies)."""
+        xs = np.zeros((nchains, self.N), np.uint8)
+        es = np.zeros(nchains, np.float64)
+        st = _L().or_sa(self._h, C.c_uint64(seed), chain0, nchains, sweeps, C.c_double(t_start), C.c_double(t_end),
+                        _ptr(xs), _ptr(es), _nthreads(nthreads))
+        if st:
+            raise ValueError(f"or_sa status {st}")
+        return xs, es
+
+
+def sa_temps(sweeps, t_start, t_end):
+    out = np.zeros(max(1, sweeps), np.float64)
+    if _L().or_sa_temps(sweeps, C.c_double(t_start), C.c_double(t_end), _ptr(out)):
+        raise ValueError("bad schedule")
+    return out
 
 
 def _colex_ptrs(by_degree):

@@ -399,3 +399,80 @@ def test_mfield_qubo_closed_form_and_binary_points():
     X = x_bits(4, 50, 30)
     assert np.array_equal(o.mfield(X.astype(np.float64)), o.field(X))
     assert np.array_equal(o.menergy(X.astype(np.float64)), o.energy(X))
+
+
+# ---- simulated annealing (SPEC sa_run) -------------------------
+def test_sa_temps_geometric_endpoints():
+    from oracle import sa_temps
+    T = sa_temps(5, 100.0, 0.01)
+    assert T[0] == 100.0 and abs(T[-1] - 0.01) < 1e-15 and np.allclose(T[1:] / T[:-1], 0.1)
+    assert sa_temps(1, 3.0, 1.0)[0] == 3.0
+
+
+@pytest.mark.parametrize("maker", [lambda: seating(4), pythagoras, lambda: random_integer_problem(3, 14, 8, 60)])
+def test_sa_infinite_temperature_flips_every_bit(maker):
+    """T -> inf: min(1, exp(-d/T)) = 1, every proposal is accepted, so one sweep maps x to 1-x
+    and the tracked energy must equal the fresh energy of 1-x."""
+    o = Oracle.from_problem(maker())
+    xs, es = o.sa(5, 0, 16, 1, 1e300, 1e300)
+    x0 = np.array([[(h(5, 1, c, m >> 6) >> np.uint64(m & 63)) & np.uint64(1) for m in range(o.N)]
+                   for c in range(16)], dtype=np.uint8)
+    assert np.array_equal(xs, 1 - x0)
+    assert np.array_equal(es, o.energy(1 - x0))
+
+
+@pytest.mark.parametrize("maker", [lambda: seating(4), pythagoras, lambda: random_integer_problem(4, 12, 3, 80)])
+def test_sa_zero_temperature_is_monotone_and_honest(maker):
+    """T -> 0: only d <= 0 moves are accepted, so energies never rise from one sweep to the next
+    (a run of s+1 sweeps extends the run of s sweeps: same counters, same T)."""
+    o = Oracle.from_problem(maker())
+    prev = None
+    for s in range(0, 5):
+        xs, es = o.sa(9, 0, 32, s, 1e-300, 1e-300)
+        assert np.array_equal(es, o.energy(xs))
+        if prev is not None:
+            assert np.all(es <= prev)
+        prev = es
+    # converged chains sit in single-flip local minima
+    G = o.field(xs)
+    assert np.all((1 - 2 * xs.astype(np.float64)) * G >= 0)
+
+
+def test_sa_replay_by_energy_differences():
+    """The sweep rule replayed with d = E(x with x_m flipped) - E(x) from exhaustive energy
+    evaluation (no local field), on a small integer instance."""
+    import math
+    p = random_integer_problem(3, 8, 21, 40)
+    o = Oracle.from_problem(p)
+    Eall = o.energy(exhaustive_X(o.N))
+    idx = lambda x: int(sum(int(v) << m for m, v in enumerate(x)))  # noqa: E731
+    T = [4.0 * (0.05 / 4.0) ** (s / 2) for s in range(3)]
+    xs, es = o.sa(13, 3, 6, 3, 4.0, 0.05)
+    for i, c in enumerate(range(3, 9)):
+        x = [int((h(13, 1, c, 0) >> np.uint64(m)) & np.uint64(1)) for m in range(o.N)]
+        for s in range(3):
+            for m in range(o.N):
+                y = list(x)
+                y[m] ^= 1
+                d = Eall[idx(y)] - Eall[idx(x)]
+                u = int(h(13, 4, c, s * o.N + m) >> np.uint64(11)) * 2.0 ** -53
+                if d <= 0 or u < math.exp(-d / T[s]):
+                    x = y
+        assert list(xs[i]) == x and es[i] == Eall[idx(x)]
+
+
+def test_sa_spec_examples():
+    """SPEC sa_run examples: H = q0 -> q0 = 0 at energy 0; the three paper problems reach
+    their brute-force ground energies (-11 seating 4x4, -30 Pythagoras P:322, -360 TSP P:402)."""
+    from workloads import TermBuilder
+    tb = TermBuilder()
+    tb.add(1.0, [(0.0, [(0, 1.0)])])
+    o = Oracle.from_problem(tb.problem(1, 1))
+    xs, es = o.sa(1, 0, 100, 1000, 10.0, 0.01)
+    assert np.all(xs == 0) and np.all(es == 0)
+    for p, emin in [(seating(4), -11.0), (pythagoras(), -30.0), (tsp(), -360.0)]:
+        o = Oracle.from_problem(p)
+        _, v = o.cells()
+        xs, es = o.sa(7, 0, 1000, 200, 10 * float(np.abs(v).max()), 0.01)
+        assert es.min() == emin == o.brute()["emin"]
+        assert np.array_equal(o.energy(xs), es)
