@@ -174,6 +174,29 @@ hobo_status hobo_search_samples(hobo_tensor* t, uint64_t seed, int64_t batch, in
                                 int64_t topk, uint8_t* x_host, float* e_host, int64_t* count_host,
                                 int64_t* n_out, void* stream);
 
+/* hobo_sa_shard — simulated annealing, SPEC sa_run after PAPER.md:81-83 ("starts
+ * at a high temperature and gradually cools down"), on global chains [chain0, chain0+nchains):
+ * chain c starts at x_m = bit (m & 63) of h(seed,1,c,m>>6); sweep s = 0..sweeps-1 at
+ * T_s = t_start (t_end/t_start)^(s / max(1, sweeps-1)) visits m = 0..N-1 in index order and
+ * accepts the flip of x_m iff d = (1-2x_m) g_m <= 0 or u < exp(-d/T_s), u = (h(seed,4,c,
+ * s*N+m) >> 11) 2^-53.  Requires 0 < t_end <= t_start.  Outputs
+ * (device, caller-owned, nullable): X_out [nchains*N] u8 final states, E_out [nchains]
+ * their freshly evaluated energies (offset excluded), E_tracked [nchains] the energies
+ * the sweep tracked incrementally (double).  Per-chain results do not depend on the shard;
+ * on integer instances (sum|H| < 2^24) they equal the oracle's replay bit for bit.
+ * Device memory: one order-(k-1) derivative tensor layout per site, built on first use. */
+hobo_status hobo_sa_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains,
+                          int64_t sweeps, double t_start, double t_end, uint8_t* X_out_dev,
+                          float* E_out_dev, double* E_tracked_dev, void* stream);
+
+/* hobo_sa_run — SPEC sa_run's SampleSet: `shots` chains annealed as above, their final
+ * states aggregated like hobo_search_samples (energy ascending, occurrence descending,
+ * assignment lexicographic; occurrences sum to shots over all distinct states).  Host
+ * outputs as in hobo_search_samples; synchronises the stream.                           */
+hobo_status hobo_sa_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t sweeps,
+                        double t_start, double t_end, int64_t topk, uint8_t* x_host,
+                        float* e_host, int64_t* count_host, int64_t* n_out, void* stream);
+
 /* Launch statistics of the last call on this handle: number of kernel launches issued,
  * the executed tensor-core MACs of its contraction kernel(s), the algorithmic MACs
  * (DESIGN.md "Roofline"), and — when profiling is on — the CUDA-event time in ms of its

@@ -71,6 +71,9 @@ struct hobo_tensor {
   uint16_t* d_P = nullptr; size_t P_cap = 0;
   uint32_t* d_starts = nullptr; size_t starts_cap = 0;
   double* d_Qpart = nullptr; size_t Qpart_cap = 0;
+  std::vector<hobo_tensor*> sa_child;                   // annealing: P_m = dE/dx_m per site m
+  int8_t* d_sa_s = nullptr; size_t sa_s_cap = 0;        // decisions of the last two sites
+  double* d_sa_E = nullptr; size_t sa_E_cap = 0;        // tracked energies
   int64_t last_launches = 0;
   double last_mma_macs = 0, last_algo_macs = 0;
   bool profile = false;
@@ -127,6 +130,20 @@ cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
     configured = smem;
   }
   k<<<dim3((unsigned)(p.n_split * p.n_ct * p.n_cb)), dim3(kThreads), smem, s>>>(L.tmap, p);
+  return cudaGetLastError();
+}
+
+template <int NT>
+cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  auto* k = kr_gemm_kernel<NT, false, true>;
+  const size_t smem = KrCfg<NT>::smem_bytes(p.W);
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k<<<dim3((unsigned)(p.n_ct * p.n_cb)), dim3(kThreads), smem, s>>>(L.tmap, p);
   return cudaGetLastError();
 }
 
@@ -450,6 +467,9 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
     if (L.d_sched) cudaFree(L.d_sched);
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
+  for (hobo_tensor* c : t->sa_child) hobo_tensor_free(c);
+  if (t->d_sa_s) cudaFree(t->d_sa_s);
+  if (t->d_sa_E) cudaFree(t->d_sa_E);
   void* ptrs[] = {t->d_tt, t->d_tt_meta, t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -638,6 +658,116 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
 }  // extern "C"
 
 namespace {
+// ---- simulated annealing (SPEC sa_run S:447-453) ---------
+// The chains' local fields G (B x N) are computed once and then kept current: flipping x_m
+// changes g_j by (x_m' - x_m) d^2E/dx_m dx_j, the field of the derivative tensor P_m at j.
+// One launch per visited site runs the KR-GEMM of P_m with the decision of site m fused in
+// front and the G update fused behind (kr_gemm_kernel<NT, false, true>).
+hobo_status ensure_sa(hobo_tensor* t) {
+  if (!t->sa_child.empty()) return HOBO_OK;
+  const int N = t->host.N, k = t->host.order;
+  std::vector<hobo_tensor*> kids;
+  auto drop = [&](hobo_status st) {
+    for (hobo_tensor* c : kids) hobo_tensor_free(c);
+    return st;
+  };
+  std::vector<float> zeros((size_t)N, 0.0f);
+  const float* zp = zeros.data();
+  for (int m = 0; m < N; ++m) {
+    hobo_tensor* c = new hobo_tensor();
+    kids.push_back(c);
+    std::string msg;
+    // order 1: the field never changes (P_m is a constant); an all-zero order-1 tensor
+    const int st = k >= 2 ? derive(t->host, m, c->host, msg) : compile_colex(1, N, &zp, c->host, msg);
+    if (st) return drop(fail(st == 3 ? HOBO_ENOMEM : HOBO_EINVAL, "annealing site tensor: " + msg));
+    if (hobo_status s2 = check_device(c)) return drop(s2);
+    if (hobo_status s2 = ensure_layout(c, 1)) return drop(s2);
+    for (size_t r = 2; r < c->host.strict.size(); ++r) std::vector<float>().swap(c->host.strict[r]);
+  }
+  t->sa_child = kids;
+  return HOBO_OK;
+}
+
+hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweeps, double t_start,
+                   double t_end, cudaStream_t s, int64_t& launches) {
+  if (nchains < 1 || sweeps < 0 || chain0 < 0 || chain0 + nchains > (int64_t)0xFFFFFFFF)
+    return fail(HOBO_EINVAL, "bad annealing batch (nchains >= 1, sweeps >= 0, chain0 + nchains < 2^32)");
+  if (!(t_start > 0) || !(t_end > 0) || !(t_end <= t_start) || !std::isfinite(t_start))
+    return fail(HOBO_EINVAL, "annealing schedule needs 0 < t_end <= t_start < inf");
+  if (hobo_status st = check_device(t)) return st;
+  if (hobo_status st = ensure_layout(t, 1)) return st;
+  if (hobo_status st = ensure_sa(t)) return st;
+  const DevLayout& L = t->lay[1];
+  const int N = t->host.N, W = t->W;
+  const long long B = nchains;
+  if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * W)) return st;
+  if (hobo_status st = grow(t, t->d_Q, t->Q_cap, (size_t)B * L.n_ct)) return st;
+  if (hobo_status st = grow(t, t->d_G, t->G_cap, (size_t)B * N)) return st;
+  if (hobo_status st = grow(t, t->d_ebest, t->ebest_cap, (size_t)B)) return st;
+  if (hobo_status st = grow(t, t->d_sa_s, t->sa_s_cap, (size_t)2 * B)) return st;
+  if (hobo_status st = grow(t, t->d_sa_E, t->sa_E_cap, (size_t)B)) return st;
+  launches = 0;
+  const unsigned g1 = (unsigned)std::min<long long>((B * W + 255) / 256, 148 * 16);
+  search_init_kernel<<<g1, 256, 0, s>>>(seed, chain0, B, N, W, t->d_bits, t->d_ebest);
+  CK(cudaGetLastError());
+  KrParams p0 = make_params(t, L, t->d_bits, B, t->d_G, t->d_Q);   // the initial fields and energies
+  CK(launch_kr_any(L, p0, s));
+  const unsigned gb = (unsigned)std::min<long long>((B + 255) / 256, 148 * 8);
+  sa_e_init_kernel<<<gb, 256, 0, s>>>(t->d_Q, L.n_ct, B, L.lcm, t->d_sa_E);
+  CK(cudaGetLastError());
+  launches += 3;
+  // geometric schedule T_s = t_start (t_end / t_start)^(s / max(1, sweeps - 1))
+  std::vector<double> T((size_t)std::max<int64_t>(sweeps, 1));
+  for (int64_t sw = 0; sw < sweeps; ++sw)
+    T[(size_t)sw] = t_start * std::pow(t_end / t_start, (double)sw / (double)std::max<int64_t>(1, sweeps - 1));
+  double macs = 0;
+  if (t->profile) CK(cudaEventRecord(t->ev0, s));
+  int64_t step = 0;
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    for (int m = 0; m < N; ++m, ++step) {
+      hobo_tensor* c = t->sa_child[m];
+      const DevLayout& Lc = c->lay[1];
+      KrParams p = make_params(c, Lc, t->d_bits, B, t->d_G, nullptr);
+      p.sa_bits = t->d_bits;
+      p.sa_sprev = step > 0 ? t->d_sa_s + (size_t)((step - 1) & 1) * B : nullptr;
+      p.sa_scur = t->d_sa_s + (size_t)(step & 1) * B;
+      p.sa_E = t->d_sa_E;
+      p.sa_T = T[(size_t)sw];
+      p.sa_seed = seed;
+      p.sa_chain0 = chain0;
+      p.sa_step = step;
+      p.sa_m = m;
+      p.sa_prev = step > 0 ? (m + N - 1) % N : -1;
+      CK(Lc.NT == 128 ? launch_kr_sa<128>(Lc, p, s) : launch_kr_sa<256>(Lc, p, s));
+      if (sw == 0) macs += exec_macs(c, Lc, B);
+    }
+  }
+  if (step > 0) {
+    sa_flush_kernel<<<gb, 256, 0, s>>>(t->d_bits, t->d_sa_s + (size_t)((step - 1) & 1) * B, N - 1, B, W);
+    CK(cudaGetLastError());
+    ++launches;
+  }
+  if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+  launches += step;
+  t->last_mma_macs = macs * (double)sweeps;   // upper bound: blocks whose chains all reject skip the MMA
+  t->last_algo_macs = 0;
+  for (int m = 0; m < N; ++m) t->last_algo_macs += algo_macs(t->sa_child[m], true, B);
+  t->last_algo_macs *= (double)sweeps;
+  return HOBO_OK;
+}
+
+// fresh energies of the chains' current bits (field layout + finalize) into E (float)
+hobo_status sa_energies(hobo_tensor* t, long long B, float* E, cudaStream_t s, int64_t& launches) {
+  const DevLayout& L = t->lay[1];
+  KrParams p = make_params(t, L, t->d_bits, B, t->d_G, t->d_Q);
+  CK(launch_kr_any(L, p, s));
+  finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_Q, L.n_ct, B, L.lcm, 0,
+                                                                                        E, nullptr);
+  CK(cudaGetLastError());
+  launches += 2;
+  return HOBO_OK;
+}
+
 // dedupe the chains' best states (d_xbest / d_ebest), count occurrences, return the top-k in
 // the paper's listing order (energy ascending, occurrence descending, assignment lexicographic)
 hobo_status aggregate_best(hobo_tensor* t, int64_t batch, int64_t topk, uint8_t* x_host, float* e_host,
@@ -786,6 +916,44 @@ hobo_status hobo_gd_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t st
     CK(cudaGetLastError());
     launches += 2;
   }
+  if (hobo_status st = aggregate_best(t, B, topk, x_host, e_host, count_host, n_out, s, launches)) return st;
+  t->last_launches = launches;
+  return HOBO_OK;
+}
+
+hobo_status hobo_sa_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweeps,
+                          double t_start, double t_end, uint8_t* X_out, float* E_out, double* E_tracked, void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t launches = 0;
+  if (hobo_status st = run_sa(t, seed, chain0, nchains, sweeps, t_start, t_end, s, launches)) return st;
+  const long long B = nchains;
+  if (E_tracked) CK(cudaMemcpyAsync(E_tracked, t->d_sa_E, (size_t)B * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (X_out) {
+    unpack_bits_kernel<<<(unsigned)std::min<long long>((B * t->host.N + 255) / 256, 148 * 16), 256, 0, s>>>(
+        t->d_bits, B, t->host.N, t->W, X_out);
+    CK(cudaGetLastError());
+    ++launches;
+  }
+  if (E_out)
+    if (hobo_status st = sa_energies(t, B, E_out, s, launches)) return st;
+  t->last_launches = launches;
+  return HOBO_OK;
+}
+
+hobo_status hobo_sa_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t sweeps, double t_start, double t_end,
+                        int64_t topk, uint8_t* x_host, float* e_host, int64_t* count_host, int64_t* n_out,
+                        void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (topk < 1 || !x_host || !e_host || !count_host || !n_out) return fail(HOBO_EINVAL, "bad output arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t launches = 0;
+  if (hobo_status st = run_sa(t, seed, 0, shots, sweeps, t_start, t_end, s, launches)) return st;
+  const long long B = shots;
+  // the sample set holds the chains' final states with freshly evaluated energies
+  if (hobo_status st = grow(t, t->d_xbest, t->xbest_cap, (size_t)B * t->W)) return st;
+  CK(cudaMemcpyAsync(t->d_xbest, t->d_bits, (size_t)B * t->W * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  if (hobo_status st = sa_energies(t, B, t->d_ebest, s, launches)) return st;
   if (hobo_status st = aggregate_best(t, B, topk, x_host, e_host, count_host, n_out, s, launches)) return st;
   t->last_launches = launches;
   return HOBO_OK;

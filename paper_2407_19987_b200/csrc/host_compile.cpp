@@ -278,6 +278,46 @@ bool colex_next(std::vector<int32_t>& a, int N) {
 }
 }  // namespace
 
+// P_m = dE/dx_m as an order-(k-1) tensor: c_Pm(T) = c(T u {m}) for m not in T.  Its local
+// field at j is the second difference d^2E / dx_m dx_j, the change of g_j when x_m flips
+// (the incremental field update of the annealing sweep).
+int derive(const HostTensor& H, int m, HostTensor& out, std::string& msg) {
+  const int k = H.order, N = H.N;
+  if (k < 2 || m < 0 || m >= N) { msg = "derive: order >= 2 and 0 <= m < N required"; return 1; }
+  std::vector<std::vector<int64_t>> bt((size_t)N + 1, std::vector<int64_t>(8, 0));
+  for (int n = 0; n <= N; ++n)
+    for (int i = 0; i < 8; ++i) bt[n][i] = binom(n, i);
+  std::vector<std::vector<float>> by(k - 1);
+  for (int rp = 1; rp <= k - 1; ++rp) {
+    std::vector<float>& a = by[rp - 1];
+    a.assign((size_t)binom(N, rp), 0.0f);
+    if (rp + 1 > N) continue;
+    const std::vector<float>& src = H.strict[rp + 1];
+    std::vector<int32_t> T(rp);
+    for (int i = 0; i < rp; ++i) T[i] = i;
+    int64_t rank = 0;
+    do {
+      // colex rank of T u {m} among (rp+1)-subsets: sum_i C(c_i, i), c sorted, i from 1
+      bool has = false, placed = false;
+      int pos = 1;
+      int64_t r2 = 0;
+      for (int i = 0; i < rp; ++i) {
+        if (T[i] == m) { has = true; break; }
+        if (!placed && m < T[i]) { r2 += bt[m][pos++]; placed = true; }
+        r2 += bt[T[i]][pos++];
+      }
+      if (!has) {
+        if (!placed) r2 += bt[m][pos];
+        a[(size_t)rank] = src[(size_t)r2];
+      }
+      ++rank;
+    } while (colex_next(T, N));
+  }
+  std::vector<const float*> ptrs(k - 1);
+  for (int r = 0; r < k - 1; ++r) ptrs[r] = by[r].data();
+  return compile_colex(k - 1, N, ptrs.data(), out, msg);
+}
+
 void export_cells(const HostTensor& t, int32_t* idx, float* val) {
   std::vector<std::pair<std::vector<int32_t>, float>> cells;
   for (int r = 1; r <= t.order; ++r) {

@@ -35,6 +35,8 @@ int compile_cells(int order, int N, int64_t ncells, const int32_t* idx, const fl
                   std::string& msg);
 // canonical cells given directly: by_degree[r-1][colex_rank(S)] = c(S), r = 1..order
 int compile_colex(int order, int N, const float* const* by_degree, HostTensor& out, std::string& msg);
+// derivative tensor P_m = dE/dx_m (order k-1): c_Pm(T) = c(T u {m}) for m not in T
+int derive(const HostTensor& H, int m, HostTensor& out, std::string& msg);
 void export_cells(const HostTensor& t, int32_t* idx, float* val);   // lexicographic by tuple
 int export_dense(const HostTensor& t, float* out);                   // 0 ok, 3 too large
 

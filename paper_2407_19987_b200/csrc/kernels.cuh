@@ -47,6 +47,18 @@ struct KrParams {
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
   double wp;                // weight of the degree-1 term
   int dbg;                  // debug builds only (HOBO_PIPE_STATS): pipeline bisection switches
+  // simulated annealing (kr_gemm_kernel<NT, false, true>): one launch per visited site m with
+  // the layout of P_m = dE/dx_m; every CTA decides site m for its chains, column tile 0
+  // commits the decisions, and the epilogue adds s_b * (field of P_m) to G
+  uint32_t* sa_bits;        // the chains' state bits (== xbits); the flip of sa_prev lands here
+  const int8_t* sa_sprev;   // decisions of the previous site (+1 set, -1 clear, 0 rejected)
+  int8_t* sa_scur;          // decisions of this site
+  double* sa_E;             // tracked energies
+  double sa_T;              // temperature of the sweep
+  unsigned long long sa_seed;
+  long long sa_chain0;      // global id of chain 0 of this shard
+  long long sa_step;        // s * N + m: counter of the acceptance uniform
+  int sa_m, sa_prev;        // visited site, previous site (-1: none)
 };
 
 template <int NT>
@@ -118,6 +130,17 @@ __device__ __forceinline__ void expand32(uint32_t half, uint32_t (&w)[16]) {
   }
 }
 
+// counter-based RNG of SURVEY 8(d): h(s,a,b,c) = sm(sm(sm(s^a)^b)^c)
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t d_hash(uint64_t s, uint64_t a, uint64_t b, uint64_t c) {
+  return d_splitmix64(d_splitmix64(d_splitmix64(s ^ a) ^ b) ^ c);
+}
+
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
 
 // real-valued candidates: this thread's 32 Khatri-Rao entries (K-block half h) of one
@@ -185,7 +208,7 @@ __device__ unsigned long long g_pipe_stats[8192][8];
 // Ring slot s holds the stage's W boxes in shared memory and its A K-blocks in TMEM;
 // FULL(s) completes when the 8 generator warps arrived and the TMA bytes landed, EMPTY(s)
 // when the MMAs reading the slot completed (one tcgen05.commit).
-template <int NT, bool REAL>
+template <int NT, bool REAL, bool SA = false>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
   using C = KrCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
@@ -218,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const int NST = REAL ? C::nst_real(p.L, p.LA, ring) : C::nst(p.L);
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
+  __shared__ int ssa[SA ? kBM : 1];   // annealing: this CTA's decisions for site sa_m
   if (threadIdx.x == 0) {
     // stage range of this split over the tile's whole schedule (segments j = nseg-1 .. 0)
     const int2* gs = p.sched + (size_t)ct * p.nseg;
@@ -237,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t stage_bytes = (uint32_t)(KPS * p.L) * C::BOX;
   // segments run in ascending degree order (j = nseg-1 .. 0); in field mode the single
   // accumulator is snapshot after each degree so the energy can weight degree r by 1/r
-  const bool snaps = p.field_mode != 0;
+  const bool snaps = p.field_mode != 0 && !SA;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), 9); mbar_init(EMPTY(s), 1); }
@@ -270,8 +294,50 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot_g;
+  bool sa_any = true;
+  if constexpr (SA) {
+    // the Metropolis step of site m for this CTA's chains (SPEC sa_run): apply the
+    // previous site's decision to the staged bits, then d = (1 - 2 x_m) g_m, accept iff d <= 0
+    // or u < exp(-d / T).  Every column tile decides identically; tile 0 commits.
+    int sv = 0;
+    if (threadIdx.x < kBM) {
+      const int r = threadIdx.x;
+      const long long b = b0 + r;
+      if (b < p.B) {
+        if (p.sa_prev >= 0) {
+          const int sp = p.sa_sprev[b];
+          if (sp != 0) {
+            const int wi = p.sa_prev >> 5;
+            const uint32_t bit = 1u << (p.sa_prev & 31);
+            xs[wi * kBM + r] = sp > 0 ? (xs[wi * kBM + r] | bit) : (xs[wi * kBM + r] & ~bit);
+            if (ct == 0) {
+              if (sp > 0) atomicOr(p.sa_bits + b * p.W + wi, bit);
+              else atomicAnd(p.sa_bits + b * p.W + wi, ~bit);
+            }
+          }
+        }
+        const int m = p.sa_m;
+        const uint32_t xm = (xs[(m >> 5) * kBM + r] >> (m & 31)) & 1u;
+        const float g = __ldcg(p.G + b * p.N + m);
+        const float d = xm ? -g : g;
+        bool acc = d <= 0.0f;
+        if (!acc) {
+          const double u = (double)(d_hash(p.sa_seed, 4, (uint64_t)(p.sa_chain0 + b), (uint64_t)p.sa_step) >> 11) * 0x1.0p-53;
+          acc = u < exp(-(double)d / p.sa_T);
+        }
+        sv = acc ? (xm ? -1 : 1) : 0;
+        if (ct == 0) {
+          p.sa_scur[b] = (int8_t)sv;
+          if (acc) p.sa_E[b] += (double)d;
+        }
+      }
+      ssa[r] = sv;
+    }
+    sa_any = __syncthreads_or(sv != 0) != 0;   // no chain of this block moved: G is unchanged
+  }
 
-  if (warp == 0) {
+  if (SA && !sa_any) {
+  } else if (warp == 0) {
     // ---------------- TMA producer: W limb boxes (NT rows x 64 tuples, SW128) ---------------
     if (lane == 0) {
       int n = 0;
@@ -489,7 +555,29 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           sp += (double)pm;
         }
       }
-      if (p.field_mode && live) {
+      if constexpr (SA) {   // G[b, j] += s_b * (field of P_m)[j]; column m is unchanged
+        const int sv = ssa[row];
+        if (live && sv != 0) {
+          const float sf = (float)sv;
+          float* gout = p.G + (size_t)b * p.N + mbase;
+          const int nvalid = min(32, p.N - mbase);
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (mbase + c == p.sa_m) g[c] = 0.0f;
+          if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(gout) & 15) == 0)) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 4) {
+              float4 o = *reinterpret_cast<float4*>(gout + c);
+              o.x += sf * g[c]; o.y += sf * g[c + 1]; o.z += sf * g[c + 2]; o.w += sf * g[c + 3];
+              *reinterpret_cast<float4*>(gout + c) = o;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (c < nvalid) gout[c] += sf * g[c];
+          }
+        }
+      } else if (p.field_mode && live) {
         float* gout = p.G + ((size_t)split * p.B + b) * p.N + mbase;
         const int nvalid = min(32, p.N - mbase);
         if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(gout) & 15) == 0)) {
@@ -502,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
       }
     }
+    if constexpr (!SA) {
     double qsum;
     if (snaps) {
       // S[0] = after degree 2, S[1] = after degree 3, ..., sfin = after degree k
@@ -519,6 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     if (h == 1) qpart[row] = qsum;
     named_bar_sync(1, 256);
     if (h == 0 && live) p.Q[((size_t)split * p.n_ct + ct) * p.B + b] = qsum + qpart[row];
+    }
   }
 #undef FULL
 #undef EMPTY
@@ -661,14 +751,36 @@ __global__ void layout_kernel(const LayoutParams lp) {
 
 // ------------------------------------------------------------------------------------------
 // search: counter-hash RNG, integer decisions on fp32 values
-__device__ __forceinline__ uint64_t d_splitmix64(uint64_t z) {
-  z += 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
+
+// ---- simulated annealing helpers ---------------------------------------------------------
+// E_b = sum_ct Q[ct][b] / lcm (double; the annealer tracks E in double)
+__global__ void sa_e_init_kernel(const double* __restrict__ Q, int n_ct, long long B, double lcm, double* __restrict__ E) {
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B; b += (long long)gridDim.x * blockDim.x) {
+    double q = 0.0;
+    for (int c = 0; c < n_ct; ++c) q += Q[(size_t)c * B + b];
+    E[b] = q / lcm;
+  }
 }
-__device__ __forceinline__ uint64_t d_hash(uint64_t s, uint64_t a, uint64_t b, uint64_t c) {
-  return d_splitmix64(d_splitmix64(d_splitmix64(s ^ a) ^ b) ^ c);
+
+// the last visited site's decisions, applied to the state bits after the final launch
+__global__ void sa_flush_kernel(uint32_t* __restrict__ bits, const int8_t* __restrict__ s, int site, long long B, int W) {
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B; b += (long long)gridDim.x * blockDim.x) {
+    const int sv = s[b];
+    const uint32_t bit = 1u << (site & 31);
+    uint32_t& w = bits[b * W + (site >> 5)];
+    if (sv > 0) w |= bit;
+    else if (sv < 0) w &= ~bit;
+  }
+}
+
+// bit rows [B][W] -> u8 rows [B][N]
+__global__ void unpack_bits_kernel(const uint32_t* __restrict__ bits, long long B, int N, int W, uint8_t* __restrict__ X) {
+  const long long total = B * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / N;
+    const int m = (int)(i % N);
+    X[i] = (uint8_t)((bits[b * W + (m >> 5)] >> (m & 31)) & 1u);
+  }
 }
 
 // chain c's initial x: bit m = bit (m & 63) of h(seed, 1, c, m >> 6)

@@ -18,7 +18,8 @@ EXPORTED = [
     "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_free", "hobo_tensor_info",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
-    "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_last_launch_stats", "hobo_set_profiling", "hobo_last_error",
+    "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats",
+    "hobo_set_profiling", "hobo_last_error",
 ]
 
 
@@ -62,6 +63,8 @@ def lib():
         L.hobo_tt_energy.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_gd_run.argtypes = [P, U64, I64, I64, D, I64, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_search_samples.argtypes = [P, U64, I64, I64, I64, P, P, P, C.POINTER(I64), P]
+        L.hobo_sa_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, P, P, P]
+        L.hobo_sa_run.argtypes = [P, U64, I64, I64, D, D, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_last_launch_stats.argtypes = [P, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]
         L.hobo_set_profiling.argtypes = [P, I]
         L.hobo_last_error.restype = C.c_char_p
@@ -242,6 +245,37 @@ class HoboTensor:
         cnt = np.zeros(topk, np.int64)
         n = C.c_int64()
         _check(lib().hobo_gd_run(self._h, seed, shots, steps, step_size, greedy_iters, topk, _np_ptr(x), _np_ptr(e),
+                                 _np_ptr(cnt), C.byref(n), _stream_handle(stream)))
+        return [(x[i], float(e[i]), int(cnt[i])) for i in range(n.value)]
+
+    def default_t_start(self):
+        """SPEC's default schedule start: 10 * max |coefficient| (t_end defaults to 0.01)."""
+        if getattr(self, "_tmax", None) is None:
+            _, v = self.cells()
+            self._tmax = 10.0 * float(np.abs(v).max()) if len(v) else 1.0
+        return self._tmax
+
+    def sa_shard(self, seed, chain0, nchains, sweeps, t_start=None, t_end=0.01, device=None, stream=None):
+        """hobo_sa_shard: annealed final states (u8, nchains x N), fresh energies (f32) and the
+        incrementally tracked energies (f64), as CUDA tensors."""
+        import torch
+        t0 = self.default_t_start() if t_start is None else float(t_start)
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        X = torch.empty(nchains, self.N, dtype=torch.uint8, device=dev)
+        E = torch.empty(nchains, dtype=torch.float32, device=dev)
+        Et = torch.empty(nchains, dtype=torch.float64, device=dev)
+        _check(lib().hobo_sa_shard(self._h, seed, chain0, nchains, sweeps, t0, float(t_end), X.data_ptr(),
+                                   E.data_ptr(), Et.data_ptr(), _stream_handle(stream)))
+        return X, E, Et
+
+    def sa_run(self, seed, shots, sweeps, t_start=None, t_end=0.01, topk=10, stream=None):
+        """hobo_sa_run: SPEC sa_run's SampleSet — list of (x u8[N], energy, occurrence)."""
+        t0 = self.default_t_start() if t_start is None else float(t_start)
+        x = np.zeros((topk, self.N), np.uint8)
+        e = np.zeros(topk, np.float32)
+        cnt = np.zeros(topk, np.int64)
+        n = C.c_int64()
+        _check(lib().hobo_sa_run(self._h, seed, shots, sweeps, t0, float(t_end), topk, _np_ptr(x), _np_ptr(e),
                                  _np_ptr(cnt), C.byref(n), _stream_handle(stream)))
         return [(x[i], float(e[i]), int(cnt[i])) for i in range(n.value)]
 

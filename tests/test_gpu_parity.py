@@ -387,3 +387,98 @@ def test_tt_energy(H, torch, name):
     Eo = o.energy(X)
     assert np.max(np.abs(E.cpu().numpy().astype(np.float64) - Eo)) <= o.tau
     check_argmin(best, Eo, o.tau)
+
+
+# ---- simulated annealing (SPEC sa_run S:447-453) -------------------------
+def _linear_problem():
+    from workloads import TermBuilder
+    tb = TermBuilder()
+    for m, c in enumerate([3, -2, 0, 5, -7, 1, 2, -1, 4]):
+        if c:
+            tb.add(float(c), [(0.0, [(m, 1.0)])])
+    return tb.problem(1, 9)
+
+
+SA_CASES = {
+    "seating4": lambda: seating(4),
+    "pythagoras": pythagoras,                                   # L = 2 limbs
+    "tsp": tsp,                                                 # order 6: site tensors of order 5
+    "o3n40": lambda: random_integer_problem(3, 40, 31, 400),   # two bit words per chain
+    "o4n20": lambda: random_integer_problem(4, 20, 32, 300),
+    "o2n70": lambda: random_integer_problem(2, 70, 33, 500),   # order 2: site tensors of order 1
+    "linear": _linear_problem,                                  # order 1: fields never change
+}
+
+
+@pytest.mark.parametrize("name", list(SA_CASES))
+def test_sa_replays_oracle_exactly(H, torch, name):
+    """Integer instances: final states, tracked and fresh energies equal the oracle's replay."""
+    p = SA_CASES[name]()
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    t0 = t.default_t_start()
+    for chain0, n, sweeps in ((0, 300, 6), (4000, 129, 2), (7, 1, 0)):
+        X, E, Et = t.sa_shard(11, chain0, n, sweeps, t0, 0.05)
+        torch.cuda.synchronize()
+        xs, es = o.sa(11, chain0, n, sweeps, t0, 0.05)
+        assert np.array_equal(X.cpu().numpy(), xs), (name, chain0)
+        assert np.array_equal(Et.cpu().numpy(), es), (name, chain0)
+        assert np.array_equal(E.cpu().numpy().astype(np.float64), es), (name, chain0)
+
+
+def test_sa_shard_invariance(H, torch):
+    p = random_integer_problem(3, 24, 5, 200)
+    t = H.HoboTensor.from_problem(p)
+    Xa, Ea, _ = t.sa_shard(2, 0, 400, 4)
+    Xb, Eb, _ = t.sa_shard(2, 150, 100, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(Xa[150:250], Xb) and torch.equal(Ea[150:250], Eb)
+
+
+def test_sa_cfg3_full_batch_sampled(H, torch):
+    """BASELINE config 3 (order 3, N=512, integer, L=1) at its full 65,536 chains, one sweep
+    (512 site launches): sampled chains against the oracle replay, bit for bit."""
+    p = cfg3_problem()
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    B = 65536
+    t0 = t.default_t_start()
+    X, E, Et = t.sa_shard(3, 0, B, 1, t0, t0 / 10)
+    torch.cuda.synchronize()
+    Xh, Eh, Eth = X.cpu().numpy(), E.cpu().numpy().astype(np.float64), Et.cpu().numpy()
+    assert np.array_equal(Eh, Eth)                               # incremental = fresh (integer)
+    for c0 in (0, 777, B - 16):
+        xs, es = o.sa(3, c0, 16, 1, t0, t0 / 10)
+        assert np.array_equal(Xh[c0:c0 + 16], xs) and np.array_equal(Eth[c0:c0 + 16], es)
+
+
+def test_sa_fp32_instance_is_honest(H, torch):
+    """fp32 coefficients (L = 3): decisions follow the fp32 fields, so states are checked by
+    invariants: fresh energies equal the oracle's energy of the returned states within tau,
+    and the tracked energies stay within tau of them."""
+    idx, val = uniform_cells(3, 30, 8)
+    t, o = H.HoboTensor.import_cells(3, 30, idx, val), Oracle.from_cells(3, 30, idx, val)
+    X, E, Et = t.sa_shard(4, 0, 500, 8, 5.0, 0.01)
+    torch.cuda.synchronize()
+    Eo = o.energy(X.cpu().numpy())
+    assert np.max(np.abs(E.cpu().numpy() - Eo)) <= o.tau
+    assert np.max(np.abs(Et.cpu().numpy() - Eo)) <= o.tau
+    # converged chains (T_end = 0.01) are single-flip local minima up to tau
+    G = o.field(X.cpu().numpy())
+    assert np.all((1 - 2 * X.cpu().numpy().astype(np.float64)) * G >= -2 * o.tau)
+
+
+@pytest.mark.parametrize("name,emin", [("seating4", -11.0), ("pythagoras", -30.0), ("tsp", -360.0)])
+def test_sa_run_sample_set(H, torch, name, emin):
+    """SPEC sa_run on the paper's problems: the SampleSet equals the oracle's aggregation of
+    its replayed final states, occurrences sum to shots, and the ground energy is reached."""
+    from oracle import aggregate
+    p = SA_CASES[name]()
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    shots, sweeps = 1000, 200
+    got = t.sa_run(7, shots, sweeps, topk=5)
+    xs, es = o.sa(7, 0, shots, sweeps, t.default_t_start(), 0.01)
+    want = aggregate(xs, es.astype(np.float32), 5)
+    assert len(got) == len(want)
+    for (gx, ge, gc), (wx, we, wc) in zip(got, want):
+        assert np.array_equal(gx, wx) and ge == we and gc == wc
+    assert got[0][1] == emin
+    assert sum(c for _, _, c in t.sa_run(7, shots, sweeps, topk=1 << 12)) == shots
