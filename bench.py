@@ -150,9 +150,30 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def sa_extra(t, B, N, stream, sweeps=2):
+    """Section 8(f) row 1: annealing sweeps over the same chains (one fused launch per site:
+    decision + KR-GEMM of dE/dx_m + field update).  Unit: site visits (flip attempts) per s."""
+    import torch
+    t0 = t.default_t_start()
+    t.sa_shard(1, 0, B, 1, t0, t0, stream=stream)          # builds the per-site layouts
+    torch.cuda.synchronize()
+    t.set_profiling(True)
+    res = {}
+    for label, (ta, tb) in {"hot": (t0, t0 / 10), "cold": (t0 / 1000, t0 / 10000)}.items():
+        X, E, Et = t.sa_shard(2, 0, B, sweeps, ta, tb, stream=stream)
+        st = t.launch_stats()
+        torch.cuda.synchronize()
+        ms = st["kernel_ms"]
+        res[label] = {"t_start": ta, "t_end": tb, "ms": ms, "ms_per_site": ms / (sweeps * N),
+                      "flip_attempts_per_s": B * N * sweeps / (ms / 1e3), "launches": st["launches"],
+                      "mean_E": float(E.double().mean().item())}
+    t.set_profiling(False)
+    return {"chains": B, "sweeps": sweeps, "sites": N, **res}
+
+
 def tt_form_extra(dev, stream, flush, B=1 << 22):
     """Section 8(f) row 4: energies from the Tensor-Train form of the paper's TSP
-    tensor (order 6, N=36, cores (6,2)...(2,6)) against the dense contraction, same candidates."""
+    tensor (order 6, N=6, cores (6,2)...(2,6)) against the dense contraction, same candidates."""
     import torch
     from paper_2407_19987_b200.hobo import HoboTensor
     from workloads import tsp, x_bits
@@ -181,7 +202,7 @@ def tt_form_extra(dev, stream, flush, B=1 << 22):
     flops = 2.0 * rr * (t.N / 2)            # useful: x has about N/2 ones
     exec_flops = 2.0 * rr * t.N             # executed: a warp walks every i some lane needs
     peak = 148 * 64 * 2 * 1.965e9 / 1e12    # FP64 FMA pipe, 64 DFMA/clk/SM at the measured 1965 MHz
-    return {"instance": "tsp (order 6, N=36)", "ranks": ranks, "batch": B, "tt_ms": tt_ms,
+    return {"instance": "tsp (order 6, N=6)", "ranks": ranks, "batch": B, "tt_ms": tt_ms,
             "tt_cand_per_s": B / (tt_ms / 1e3), "dense_ms": de_ms, "dense_cand_per_s": B / (de_ms / 1e3),
             "max_abs_diff_tt_vs_dense": diff, "tt_fp64_gflops": flops * B / (tt_ms / 1e3) / 1e9,
             "tt_input_gbps": B * (t.N + 4) / (tt_ms / 1e3) / 1e9,
@@ -441,6 +462,8 @@ def main():
             res = t.gd_run(3, B, 20, 0.05, greedy_iters=32, topk=3)
             extras["gd_run"] = {"shots": B, "steps": 20, "greedy_iters": 32, "ms_wall": (time.perf_counter() - t0) * 1e3,
                                 "top": [[e, c] for _, e, c in res]}
+        if mode == "field":
+            extras["sa_sweep"] = sa_extra(t, B, N, stream)
         if rank == 0 and a.config == "cfg3":
             extras["tt_form"] = tt_form_extra(dev, stream, flush)
             extras["cpu_baseline"] = cpu_baseline()

@@ -15,6 +15,7 @@
 #include "host_compile.h"
 #include "tt.h"
 #include "kernels.cuh"
+#include "sa_kernel.cuh"
 
 using namespace hobo;
 
@@ -72,6 +73,21 @@ struct hobo_tensor {
   uint32_t* d_starts = nullptr; size_t starts_cap = 0;
   double* d_Qpart = nullptr; size_t Qpart_cap = 0;
   std::vector<hobo_tensor*> sa_child;                   // annealing: P_m = dE/dx_m per site m
+  bool sa_borrowed = false;                             // a site tensor: its tables belong to the parent
+  uint4* d_sa_runs = nullptr;                           // the site tensors' shared tables (same order, N)
+  uint4* d_sa_kdesc = nullptr;
+  uint32_t* d_sa_runoff = nullptr;
+  int2* d_sa_sched = nullptr;
+  // persistent annealer (Npad <= 512): every site's layout in one buffer, one TMA map
+  bool sa_persistent = false;
+  __nv_bfloat16* d_sa_W = nullptr;
+  int* d_sa_L = nullptr;
+  int* d_sa_base = nullptr;
+  double* d_sa_T = nullptr; size_t sa_T_cap = 0;
+  alignas(64) CUtensorMap sa_tmap;
+  int sa_NT = 256, sa_nct = 1, sa_nkb1 = 1, sa_nseg = 0, sa_nq = 1;
+  int sa_seg_kb0[8] = {0}, sa_seg_cnt[8] = {0};
+  std::vector<int> sa_L;
   int8_t* d_sa_s = nullptr; size_t sa_s_cap = 0;        // decisions of the last two sites
   double* d_sa_E = nullptr; size_t sa_E_cap = 0;        // tracked energies
   int64_t last_launches = 0;
@@ -462,6 +478,16 @@ hobo_status hobo_tensor_import_colex(int order, int N, const float* const* cells
 hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (!t) return HOBO_OK;
   if (t->dev_init) cudaSetDevice(t->device);
+  if (t->sa_borrowed) {   // annealing site tensor: owns only its W planes and degree-1 cells
+    for (auto& L : t->lay)
+      if (L.W) cudaFree(L.W);
+    if (t->d_p1) cudaFree(t->d_p1);
+    delete t;
+    return HOBO_OK;
+  }
+  void* sa_tabs[] = {t->d_sa_runs, t->d_sa_kdesc, t->d_sa_runoff, t->d_sa_sched, t->d_sa_W, t->d_sa_L, t->d_sa_base, t->d_sa_T};
+  for (void* p : sa_tabs)
+    if (p) cudaFree(p);
   for (auto& L : t->lay) {
     if (L.W) cudaFree(L.W);
     if (L.d_sched) cudaFree(L.d_sched);
@@ -663,29 +689,296 @@ namespace {
 // changes g_j by (x_m' - x_m) d^2E/dx_m dx_j, the field of the derivative tensor P_m at j.
 // One launch per visited site runs the KR-GEMM of P_m with the decision of site m fused in
 // front and the G update fused behind (kr_gemm_kernel<NT, false, true>).
-hobo_status ensure_sa(hobo_tensor* t) {
+hobo_status ensure_sa_sites(hobo_tensor* t) {
   if (!t->sa_child.empty()) return HOBO_OK;
-  const int N = t->host.N, k = t->host.order;
+  const int N = t->host.N, k = t->host.order, kc = std::max(1, k - 1);
+  std::string msg;
+  // tables shared by all site tensors (they have the same order k-1 and N)
+  KLayout kl;
+  if (build_klayout(kc, N, kl, msg)) return fail(HOBO_ENOMEM, msg);
+  CK(cudaMalloc(&t->d_sa_runs, std::max<size_t>(kl.runs.size() / 4, 1) * sizeof(uint4)));
+  if (!kl.runs.empty()) CK(cudaMemcpy(t->d_sa_runs, kl.runs.data(), kl.runs.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_sa_kdesc, std::max<size_t>(kl.kdesc.size() / 4, 2) * sizeof(uint4)));
+  if (!kl.kdesc.empty()) CK(cudaMemcpy(t->d_sa_kdesc, kl.kdesc.data(), kl.kdesc.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_sa_runoff, kl.run_off.size() * 4));
+  CK(cudaMemcpy(t->d_sa_runoff, kl.run_off.data(), kl.run_off.size() * 4, cudaMemcpyHostToDevice));
+  const int NT = N <= 128 ? 128 : 256, n_ct = (N + NT - 1) / NT, Npad = n_ct * NT;
+  const std::vector<int32_t> sched = schedule(kl, NT, n_ct, true);
+  CK(cudaMalloc(&t->d_sa_sched, sched.size() * sizeof(int32_t)));
+  CK(cudaMemcpy(t->d_sa_sched, sched.data(), sched.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  const int64_t Tpad = std::max<int64_t>(kl.Tpad, kBK);
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const double need = (double)N * t->host.limbs * Npad * (double)Tpad * 2.0;   // site limbs <= the tensor's
+  if (need > 0.8 * (double)free_b)
+    return fail(HOBO_ENOMEM, "annealing site layouts need " + std::to_string(need / 1e9) + " GB (N=" +
+                                 std::to_string(N) + ", order=" + std::to_string(k) + ")");
+  // layout-kernel inputs shared by every site: binomials, tuple list, per-degree staging
+  std::vector<long long> bt((size_t)(N + 1) * 7);
+  for (int n = 0; n <= N; ++n)
+    for (int i = 0; i < 7; ++i) bt[(size_t)n * 7 + i] = binom(n, i);
+  long long* d_bt = nullptr;
+  uint16_t* d_tup = nullptr;
+  float** d_strict_ptrs = nullptr;
+  std::vector<float*> dstage(7, nullptr);
+  auto release = [&]() {
+    for (float* p : dstage)
+      if (p) cudaFree(p);
+    if (d_bt) cudaFree(d_bt);
+    if (d_tup) cudaFree(d_tup);
+    if (d_strict_ptrs) cudaFree(d_strict_ptrs);
+  };
   std::vector<hobo_tensor*> kids;
   auto drop = [&](hobo_status st) {
+    cudaDeviceSynchronize();
+    release();
     for (hobo_tensor* c : kids) hobo_tensor_free(c);
+    void** tabs[] = {(void**)&t->d_sa_runs, (void**)&t->d_sa_kdesc, (void**)&t->d_sa_runoff, (void**)&t->d_sa_sched};
+    for (void** p : tabs) {
+      if (*p) cudaFree(*p);
+      *p = nullptr;
+    }
     return st;
   };
+#define CKS(call)                                                                                    \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) return drop(fail(HOBO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
+  if (kl.Tpad > 0) {
+    CKS(cudaMalloc(&d_bt, bt.size() * sizeof(long long)));
+    CKS(cudaMemcpy(d_bt, bt.data(), bt.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    CKS(cudaMalloc(&d_tup, kl.tuples.size() * sizeof(uint16_t)));
+    CKS(cudaMemcpy(d_tup, kl.tuples.data(), kl.tuples.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    for (int r = 2; r <= kc; ++r) CKS(cudaMalloc(&dstage[r], std::max<int64_t>(binom(N, r), 1) * sizeof(float)));
+    CKS(cudaMalloc(&d_strict_ptrs, 7 * sizeof(float*)));
+    CKS(cudaMemcpy(d_strict_ptrs, dstage.data(), 7 * sizeof(float*), cudaMemcpyHostToDevice));
+  }
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return drop(fail(HOBO_ECUDA, "cuTensorMapEncodeTiled unavailable"));
   std::vector<float> zeros((size_t)N, 0.0f);
   const float* zp = zeros.data();
   for (int m = 0; m < N; ++m) {
     hobo_tensor* c = new hobo_tensor();
     kids.push_back(c);
-    std::string msg;
-    // order 1: the field never changes (P_m is a constant); an all-zero order-1 tensor
+    c->sa_borrowed = true;
+    // order 1: the fields never change (P_m is a constant): an all-zero order-1 tensor
     const int st = k >= 2 ? derive(t->host, m, c->host, msg) : compile_colex(1, N, &zp, c->host, msg);
     if (st) return drop(fail(st == 3 ? HOBO_ENOMEM : HOBO_EINVAL, "annealing site tensor: " + msg));
-    if (hobo_status s2 = check_device(c)) return drop(s2);
-    if (hobo_status s2 = ensure_layout(c, 1)) return drop(s2);
+    c->device = t->device;
+    c->dev_init = true;
+    c->W = t->W;
+    c->kl.order = kc;
+    c->kl.N = N;
+    c->kl.nseg = kl.nseg;
+    c->kl.Tpad = kl.Tpad;
+    c->d_runs = t->d_sa_runs;
+    c->d_kdesc = t->d_sa_kdesc;
+    c->d_runoff = t->d_sa_runoff;
+    std::vector<float> p1(Npad, 0.0f);
+    for (int j = 0; j < N; ++j) p1[j] = c->host.strict[1][j];
+    CKS(cudaMalloc(&c->d_p1, Npad * sizeof(float)));
+    CKS(cudaMemcpy(c->d_p1, p1.data(), Npad * sizeof(float), cudaMemcpyHostToDevice));
+    DevLayout& L = c->lay[1];
+    L.NT = NT;
+    L.n_ct = n_ct;
+    L.Npad = Npad;
+    const size_t bytes = (size_t)c->host.limbs * Npad * Tpad * 2;
+    CKS(cudaMalloc(&L.W, bytes));
+    if (kl.Tpad > 0) {
+      // the staging buffers are reused: the copies below queue behind the previous site's
+      // layout kernel on the legacy stream
+      for (int r = 2; r <= kc; ++r)
+        CKS(cudaMemcpy(dstage[r], c->host.strict[r].data(), c->host.strict[r].size() * sizeof(float),
+                       cudaMemcpyHostToDevice));
+      LayoutParams lp;
+      lp.tuples = d_tup;
+      lp.strict = d_strict_ptrs;
+      lp.binomT = d_bt;
+      lp.Wout = L.W;
+      lp.Tpad = kl.Tpad;
+      lp.N = N;
+      lp.Npad = Npad;
+      lp.L = c->host.limbs;
+      lp.field_mode = 1;
+      lp.NT = NT;
+      layout_kernel<<<148 * 8, 256>>>(lp);
+      CKS(cudaGetLastError());
+    } else {
+      CKS(cudaMemset(L.W, 0, bytes));
+    }
+    const int64_t n_kb = Tpad / kBK;
+    cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)NT, (cuuint64_t)c->host.limbs * n_ct * n_kb};
+    cuuint64_t strides[2] = {(cuuint64_t)kBK * 2, (cuuint64_t)kBK * 2 * NT};
+    cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)NT, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = enc(&L.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.W, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return drop(fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr)));
+    L.sched = sched;
+    L.d_sched = t->d_sa_sched;
+    L.built = true;
     for (size_t r = 2; r < c->host.strict.size(); ++r) std::vector<float>().swap(c->host.strict[r]);
   }
+  CKS(cudaDeviceSynchronize());
+#undef CKS
+  release();
   t->sa_child = kids;
   return HOBO_OK;
+}
+
+// the persistent annealer's layout: for every site m, the field layout of P_m over the site
+// K-blocks plus one block holding the empty tuple (W[j, {}] = c({m, j})), all sites in one
+// buffer addressed by one 3-D TMA map (box = NT rows x 64 tuples)
+hobo_status ensure_sa_persistent(hobo_tensor* t) {
+  if (t->sa_persistent) return HOBO_OK;
+  const int N = t->host.N, k = t->host.order, kc = std::max(1, k - 1);
+  std::string msg;
+  KLayout kl;
+  if (build_klayout(kc, N, kl, msg)) return fail(HOBO_ENOMEM, msg);
+  const int NT = N <= 128 ? 128 : 256, n_ct = (N + NT - 1) / NT, Npad = n_ct * NT;
+  const int64_t Tp = kl.Tpad + kBK;        // + the degree-1 block
+  const int nkb1 = (int)(Tp / kBK);
+  if (kl.nseg > 8) return fail(HOBO_EINVAL, "annealing: too many degree segments");
+  std::vector<uint16_t> tup(kl.tuples);
+  tup.resize((size_t)Tp * 6, 0);
+  tup[(size_t)kl.Tpad * 6] = 1;            // r = 1: the empty tuple
+  // pass 1: limbs per site
+  std::vector<float> zeros((size_t)N, 0.0f);
+  const float* zp = zeros.data();
+  auto site = [&](int m, HostTensor& c) {
+    return k >= 2 ? derive(t->host, m, c, msg) : compile_colex(1, N, &zp, c, msg);
+  };
+  std::vector<int> Ls(N), bases(N);
+  int64_t boxes = 0;
+  for (int m = 0; m < N; ++m) {
+    HostTensor c;
+    if (int st = site(m, c)) return fail(st == 3 ? HOBO_ENOMEM : HOBO_EINVAL, "annealing site tensor: " + msg);
+    Ls[m] = c.limbs;
+    bases[m] = (int)boxes;
+    boxes += (int64_t)c.limbs * n_ct * nkb1;
+  }
+  if (boxes >= (1ll << 31)) return fail(HOBO_ENOMEM, "annealing layout too large");
+  const double bytes = (double)boxes * NT * kBK * 2.0;
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  if (bytes > 0.8 * (double)free_b)
+    return fail(HOBO_ENOMEM, "annealing site layouts need " + std::to_string(bytes / 1e9) + " GB");
+  CK(cudaMalloc(&t->d_sa_W, (size_t)bytes));
+  CK(cudaMalloc(&t->d_sa_runs, std::max<size_t>(kl.runs.size() / 4, 1) * sizeof(uint4)));
+  if (!kl.runs.empty()) CK(cudaMemcpy(t->d_sa_runs, kl.runs.data(), kl.runs.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_sa_kdesc, std::max<size_t>(kl.kdesc.size() / 4, 2) * sizeof(uint4)));
+  if (!kl.kdesc.empty()) CK(cudaMemcpy(t->d_sa_kdesc, kl.kdesc.data(), kl.kdesc.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_sa_L, N * sizeof(int)));
+  CK(cudaMemcpy(t->d_sa_L, Ls.data(), N * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&t->d_sa_base, N * sizeof(int)));
+  CK(cudaMemcpy(t->d_sa_base, bases.data(), N * sizeof(int), cudaMemcpyHostToDevice));
+  // layout-kernel inputs shared by every site
+  std::vector<long long> bt((size_t)(N + 1) * 7);
+  for (int n = 0; n <= N; ++n)
+    for (int i = 0; i < 7; ++i) bt[(size_t)n * 7 + i] = binom(n, i);
+  long long* d_bt = nullptr;
+  uint16_t* d_tup = nullptr;
+  float** d_ptrs = nullptr;
+  std::vector<float*> dstage(7, nullptr);
+  auto release = [&]() {
+    for (float* p : dstage)
+      if (p) cudaFree(p);
+    if (d_bt) cudaFree(d_bt);
+    if (d_tup) cudaFree(d_tup);
+    if (d_ptrs) cudaFree(d_ptrs);
+  };
+#define CKP(call)                                                                                    \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      cudaDeviceSynchronize();                                                                       \
+      release();                                                                                     \
+      t->poisoned = true;                                                                            \
+      return fail(HOBO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));                   \
+    }                                                                                                \
+  } while (0)
+  CKP(cudaMalloc(&d_bt, bt.size() * sizeof(long long)));
+  CKP(cudaMemcpy(d_bt, bt.data(), bt.size() * sizeof(long long), cudaMemcpyHostToDevice));
+  CKP(cudaMalloc(&d_tup, tup.size() * sizeof(uint16_t)));
+  CKP(cudaMemcpy(d_tup, tup.data(), tup.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  for (int r = 1; r <= kc; ++r) CKP(cudaMalloc(&dstage[r], std::max<int64_t>(binom(N, r), 1) * sizeof(float)));
+  CKP(cudaMalloc(&d_ptrs, 7 * sizeof(float*)));
+  CKP(cudaMemcpy(d_ptrs, dstage.data(), 7 * sizeof(float*), cudaMemcpyHostToDevice));
+  for (int m = 0; m < N; ++m) {   // pass 2: lay out each site (staging reused: legacy-stream order)
+    HostTensor c;
+    if (int st = site(m, c)) {
+      cudaDeviceSynchronize();
+      release();
+      return fail(st == 3 ? HOBO_ENOMEM : HOBO_EINVAL, "annealing site tensor: " + msg);
+    }
+    for (int r = 1; r <= kc; ++r)
+      CKP(cudaMemcpy(dstage[r], c.strict[r].data(), c.strict[r].size() * sizeof(float), cudaMemcpyHostToDevice));
+    LayoutParams lp;
+    lp.tuples = d_tup;
+    lp.strict = d_ptrs;
+    lp.binomT = d_bt;
+    lp.Wout = t->d_sa_W + (size_t)bases[m] * NT * kBK;
+    lp.Tpad = Tp;
+    lp.N = N;
+    lp.Npad = Npad;
+    lp.L = Ls[m];
+    lp.field_mode = 1;
+    lp.NT = NT;
+    layout_kernel<<<148 * 4, 256>>>(lp);
+    CKP(cudaGetLastError());
+  }
+  CKP(cudaDeviceSynchronize());
+#undef CKP
+  release();
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)NT, (cuuint64_t)boxes};
+  cuuint64_t strides[2] = {(cuuint64_t)kBK * 2, (cuuint64_t)kBK * 2 * NT};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)NT, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&t->sa_tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, t->d_sa_W, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+  t->sa_NT = NT;
+  t->sa_nct = n_ct;
+  t->sa_nkb1 = nkb1;
+  t->sa_nseg = kl.nseg;
+  int nq = 1;
+  for (int j = 0; j < kl.nseg; ++j) {
+    t->sa_seg_kb0[j] = (int)(kl.seg_t0[j] / kBK);
+    t->sa_seg_cnt[j] = (int)((kl.seg_len[j] + kBK - 1) / kBK);
+    nq += t->sa_seg_cnt[j];
+  }
+  t->sa_nq = nq;
+  t->sa_L = Ls;
+  t->sa_persistent = true;
+  return HOBO_OK;
+}
+
+bool sa_fits_persistent(int N) {
+  const int NT = N <= 128 ? 128 : 256;
+  return ((N + NT - 1) / NT) * NT <= 512;
+}
+
+hobo_status ensure_sa(hobo_tensor* t) {
+  return sa_fits_persistent(t->host.N) ? ensure_sa_persistent(t) : ensure_sa_sites(t);
+}
+
+template <int NT>
+cudaError_t launch_sa(const CUtensorMap& tmap, const SaParams& p, unsigned grid, cudaStream_t s) {
+  auto* k = sa_kernel<NT>;
+  const size_t smem = SaCfg<NT>::smem_bytes(p.W);
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k<<<grid, kThreads, smem, s>>>(tmap, p);
+  return cudaGetLastError();
 }
 
 hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweeps, double t_start,
@@ -720,6 +1013,43 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
   std::vector<double> T((size_t)std::max<int64_t>(sweeps, 1));
   for (int64_t sw = 0; sw < sweeps; ++sw)
     T[(size_t)sw] = t_start * std::pow(t_end / t_start, (double)sw / (double)std::max<int64_t>(1, sweeps - 1));
+  if (t->sa_persistent) {
+    if (sweeps == 0) return HOBO_OK;
+    if (hobo_status st = grow(t, t->d_sa_T, t->sa_T_cap, (size_t)sweeps)) return st;
+    CK(cudaMemcpyAsync(t->d_sa_T, T.data(), (size_t)sweeps * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));   // T is a pageable host vector
+    SaParams q;
+    q.bits = t->d_bits;
+    q.G0 = t->d_G;
+    q.E = t->d_sa_E;
+    q.runs = t->d_sa_runs;
+    q.kdesc = t->d_sa_kdesc;
+    q.site_L = t->d_sa_L;
+    q.site_base = t->d_sa_base;
+    q.temps = t->d_sa_T;
+    q.seed = seed;
+    q.chain0 = chain0;
+    q.B = B;
+    q.steps = sweeps * (long long)N;
+    q.N = N;
+    q.W = W;
+    q.n_ct = t->sa_nct;
+    q.nkb1 = t->sa_nkb1;
+    q.nseg = t->sa_nseg;
+    q.nq = t->sa_nq;
+    for (int j = 0; j < 8; ++j) { q.seg_kb0[j] = t->sa_seg_kb0[j]; q.seg_cnt[j] = t->sa_seg_cnt[j]; }
+    const long long n_cb = (B + kBM - 1) / kBM;
+    const unsigned grid = (unsigned)std::min<long long>(n_cb, 148);
+    if (t->profile) CK(cudaEventRecord(t->ev0, s));
+    CK(t->sa_NT == 128 ? launch_sa<128>(t->sa_tmap, q, grid, s) : launch_sa<256>(t->sa_tmap, q, grid, s));
+    if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+    launches += 1;
+    double per_sweep = 0;
+    for (int m = 0; m < N; ++m) per_sweep += (double)t->sa_L[m] * t->sa_nq * t->sa_nct * t->sa_NT * kBK * kBM;
+    t->last_mma_macs = per_sweep * (double)n_cb * (double)sweeps;
+    t->last_algo_macs = 0;   // site tensors are not kept on the host in this layout
+    return HOBO_OK;
+  }
   double macs = 0;
   if (t->profile) CK(cudaEventRecord(t->ev0, s));
   int64_t step = 0;

@@ -733,6 +733,8 @@ __global__ void layout_kernel(const LayoutParams lp) {
         for (int i = 0; i < r; ++i) rank += dbinom(lp.binomT, S[i], i + 1);
         c = lp.strict[r][rank];
       }
+    } else if (r == 1 && m < lp.N) {   // the empty tuple (annealing site layouts): W[m, {}] = c({m})
+      c = lp.strict[1][m];
     }
     // exact split into bf16 limbs: hi + mid + lo
     const __nv_bfloat16 hi = __float2bfloat16_rn(c);

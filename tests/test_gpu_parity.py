@@ -407,6 +407,8 @@ SA_CASES = {
     "o4n20": lambda: random_integer_problem(4, 20, 32, 300),
     "o2n70": lambda: random_integer_problem(2, 70, 33, 500),   # order 2: site tensors of order 1
     "linear": _linear_problem,                                  # order 1: fields never change
+    "o2n600": lambda: random_integer_problem(2, 600, 34, 900),  # N > 512: the per-site launch path
+    "o3n520": lambda: random_integer_problem(3, 520, 35, 900),
 }
 
 
