@@ -166,6 +166,8 @@ def sa_extra(t, B, N, stream, sweeps=2):
         ms = st["kernel_ms"]
         res[label] = {"t_start": ta, "t_end": tb, "ms": ms, "ms_per_site": ms / (sweeps * N),
                       "flip_attempts_per_s": B * N * sweeps / (ms / 1e3), "launches": st["launches"],
+                      "executed_tflops": 2 * st["mma_macs"] / (ms / 1e3) / 1e12,
+                      "frac_of_burst": 2 * st["mma_macs"] / (ms / 1e3) / 1e12 / 1671.8,
                       "mean_E": float(E.double().mean().item())}
     t.set_profiling(False)
     return {"chains": B, "sweeps": sweeps, "sites": N, **res}

@@ -178,8 +178,8 @@ hobo_status hobo_search_samples(hobo_tensor* t, uint64_t seed, int64_t batch, in
  * at a high temperature and gradually cools down"), on global chains [chain0, chain0+nchains):
  * chain c starts at x_m = bit (m & 63) of h(seed,1,c,m>>6); sweep s = 0..sweeps-1 at
  * T_s = t_start (t_end/t_start)^(s / max(1, sweeps-1)) visits m = 0..N-1 in index order and
- * accepts the flip of x_m iff d = (1-2x_m) g_m <= 0 or u < exp(-d/T_s), u = (h(seed,4,c,
- * s*N+m) >> 11) 2^-53.  Requires 0 < t_end <= t_start.  Outputs
+ * accepts the flip of x_m iff d = (1-2x_m) g_m <= 0 or d < -T_s ln u (i.e. u < exp(-d/T_s)),
+ * u = (h(seed,4,c,s*N+m) >> 11) 2^-53 (reading 22).  Requires 0 < t_end <= t_start.  Outputs
  * (device, caller-owned, nullable): X_out [nchains*N] u8 final states, E_out [nchains]
  * their freshly evaluated energies (offset excluded), E_tracked [nchains] the energies
  * the sweep tracked incrementally (double).  Per-chain results do not depend on the shard;

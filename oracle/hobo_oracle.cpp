@@ -597,11 +597,10 @@ int or_sa(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweep
           if (on) g += (long double)o->val[cc];
         }
         const double d = x[m] ? -(double)g : (double)g;   // energy change of flipping x_m
-        bool accept = d <= 0.0;
-        if (!accept) {
-          const double u = (double)(or_hash(seed, 4, c, (uint64_t)(s * N + m)) >> 11) * 0x1.0p-53;
-          accept = u < std::exp(-d / T[(size_t)s]);
-        }
+        // Metropolis: accept with probability min(1, exp(-d/T)), i.e. iff d <= 0 or
+        // u < exp(-d/T) <=> d < -T ln u for u in (0,1)  (reading 22)
+        const double u = (double)(or_hash(seed, 4, c, (uint64_t)(s * N + m)) >> 11) * 0x1.0p-53;
+        const bool accept = d <= 0.0 || d < -T[(size_t)s] * std::log(u);
         if (accept) {
           x[m] ^= 1;
           e += d;

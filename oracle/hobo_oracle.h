@@ -73,8 +73,8 @@ int or_search(void* handle, uint64_t seed, int64_t chain0, int64_t nchains, int6
  * temperature and gradually cools down"), replayed on chains [chain0, chain0+nchains):
  * chain c starts at x_m = bit (m & 63) of h(seed,1,c,m>>6); sweep s = 0..sweeps-1 at
  * T_s = t_start (t_end/t_start)^(s / max(1, sweeps-1)) visits m = 0..N-1 in index order,
- * d = (1 - 2 x_m) g_m(x) (O5, exact), accepts iff d <= 0 or u < exp(-d / T_s) with
- * u = (h(seed,4,c,s*N+m) >> 11) 2^-53, and on acceptance flips x_m and adds d to the
+ * d = (1 - 2 x_m) g_m(x) (O5, exact), accepts iff d <= 0 or d < -T_s ln u (that is
+ * u < exp(-d/T_s)) with u = (h(seed,4,c,s*N+m) >> 11) 2^-53, and on acceptance flips x_m and adds d to the
  * chain's energy.  Outputs the final states (nchains x N) and their tracked energies.  */
 int or_sa(void* handle, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweeps, double t_start,
           double t_end, uint8_t* x_out, double* e_out, int nthreads);

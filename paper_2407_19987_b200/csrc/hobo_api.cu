@@ -1039,8 +1039,8 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
     q.nq = t->sa_nq;
     for (int j = 0; j < 8; ++j) { q.seg_kb0[j] = t->sa_seg_kb0[j]; q.seg_cnt[j] = t->sa_seg_cnt[j]; }
     const long long n_cb = (B + kBM - 1) / kBM;
-    const unsigned grid = (unsigned)std::min<long long>(n_cb, 148);
     if (t->profile) CK(cudaEventRecord(t->ev0, s));
+    const unsigned grid = (unsigned)std::min<long long>(n_cb, 148);
     CK(t->sa_NT == 128 ? launch_sa<128>(t->sa_tmap, q, grid, s) : launch_sa<256>(t->sa_tmap, q, grid, s));
     if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
     launches += 1;

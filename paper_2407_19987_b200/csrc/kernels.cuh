@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   if constexpr (SA) {
     // the Metropolis step of site m for this CTA's chains (SPEC sa_run): apply the
     // previous site's decision to the staged bits, then d = (1 - 2 x_m) g_m, accept iff d <= 0
-    // or u < exp(-d / T).  Every column tile decides identically; tile 0 commits.
+    // or d < -T ln u.  Every column tile decides identically; tile 0 commits.
     int sv = 0;
     if (threadIdx.x < kBM) {
       const int r = threadIdx.x;
@@ -321,9 +321,9 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const float g = __ldcg(p.G + b * p.N + m);
         const float d = xm ? -g : g;
         bool acc = d <= 0.0f;
-        if (!acc) {
+        if (!acc) {   // u < exp(-d/T)  <=>  d < -T ln u  (reading 22)
           const double u = (double)(d_hash(p.sa_seed, 4, (uint64_t)(p.sa_chain0 + b), (uint64_t)p.sa_step) >> 11) * 0x1.0p-53;
-          acc = u < exp(-(double)d / p.sa_T);
+          acc = (double)d < -p.sa_T * log(u);
         }
         sv = acc ? (xm ? -1 : 1) : 0;
         if (ct == 0) {

@@ -3,8 +3,9 @@
 //
 // The chains' local fields G (128 rows x Npad fp32) stay in tensor memory for all sweeps.
 // Visiting site m: the decision warps read column m of G (tcgen05.ld), take the Metropolis
-// decision d = (1 - 2 x_m) g_m, accept iff d <= 0 or u < exp(-d/T), and flip x_m in the
-// staged bits.  The change of every other field is then the field of P_m = dE/dx_m:
+// decision d = (1 - 2 x_m) g_m, accept iff d <= 0 or d < -T ln u, and flip x_m in the
+// staged bits (the threshold -T ln u of the uniform is computed before the field is
+// ready, off the critical path).  The change of every other field is then the field of P_m = dE/dx_m:
 //
 //     G[b, j] += s_b * ( sum_T A[b, T] W_m[j, T] + c_m({j}) )        s_b = x_m' - x_m
 //
@@ -14,6 +15,8 @@
 // W_m streams through a TMA ring independent of the decisions; the sites' layouts are
 // concatenated in one buffer (site_base[m] = first box of site m).
 #pragma once
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace hobo {
@@ -39,9 +42,9 @@ struct SaParams {
 template <int NT>
 struct SaCfg {
   static constexpr int BOX = NT * 128;        // one W box: NT rows x 64 bf16 (SW128)
-  static constexpr int RW = NT == 256 ? 4 : 8; // W ring (boxes)
+  static constexpr int RW = NT == 256 ? 5 : 10; // W ring (boxes)
   static constexpr int ABOX = kBM * 128;      // one A tile: 128 rows x 64 bf16 (SW128, K-major)
-  static constexpr int RA = 4;                // A ring (tiles)
+  static constexpr int RA = 2;                // A ring (tiles)
   static constexpr int NBAR = 2 * RW + 2 * RA + 1;
   static size_t smem_bytes(int W) {
     return 1024 + (size_t)RW * BOX + (size_t)RA * ABOX + 8 * NBAR + 16 + (size_t)(W + 2) * kBM * 4 + kBM * 4 + 128;
@@ -104,6 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
     // ---------------- TMA producer: the sites' W boxes, in visiting order, for every block ---------
     if (lane == 0) {
       uint32_t nw = 0;
+      PT(unsigned long long w_tma = 0;)
       for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x)
         for (long long step = 0; step < p.steps; ++step) {
           const int m = (int)(step % p.N);
@@ -113,31 +117,39 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
             for (int l = 0; l < L; ++l)
               for (int h = 0; h < p.n_ct; ++h, ++nw) {
                 const uint32_t s = nw % C::RW;
+                PT(const long long t0 = clock64();)
                 mbar_wait(EMPTYW(s), ((nw / C::RW) & 1u) ^ 1u);
+                PT(w_tma += clock64() - t0;)
                 mbar_arrive_expect_tx(FULLW(s), C::BOX);
                 tma_load_3d(sW + s * C::BOX, &tmap, FULLW(s), 0, 0, sb + (l * p.n_ct + h) * p.nkb1 + kb);
               }
           }
         }
+      PSTAT_FLUSH(6, w_tma);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: G[:, tile h] += A_q * W_m,q (accumulate, never cleared) ---------
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
       uint32_t nw = 0, na = 0;
+      PT(unsigned long long wa = 0, ww = 0; const long long tbeg = clock64(); long long t0;)
       for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x)
         for (long long step = 0; step < p.steps; ++step) {
           const int m = (int)(step % p.N);
           const int L = __ldg(p.site_L + m);
           for (int q = 0; q < p.nq; ++q, ++na) {
             const uint32_t a = na % C::RA;
+            PT(t0 = clock64();)
             mbar_wait(FULLA(a), (na / C::RA) & 1u);
+            PT(wa += clock64() - t0;)
             tc_fence_after();
             const uint64_t adesc = sw128_kmajor_desc(sA + a * C::ABOX);
             for (int l = 0; l < L; ++l)
               for (int h = 0; h < p.n_ct; ++h, ++nw) {
                 const uint32_t s = nw % C::RW;
+                PT(t0 = clock64();)
                 mbar_wait(FULLW(s), (nw / C::RW) & 1u);
+                PT(ww += clock64() - t0;)
                 tc_fence_after();
                 const uint64_t bdesc = sw128_kmajor_desc(sW + s * C::BOX);
 #pragma unroll
@@ -149,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
           }
           umma_commit(SITE);   // this site's G update is complete when this arrives
         }
+      PT(PSTAT_FLUSH(0, clock64() - tbeg); PSTAT_FLUSH(1, wa); PSTAT_FLUSH(2, ww);)
     }
   } else {
     // ---------------- decisions (team 0) + A generator (both teams), one row per thread -----------
@@ -158,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
     const uint32_t lane_base = tmem + ((uint32_t)(qd * 32) << 16);
     const int gtid = threadIdx.x - 64;       // 0..255
     uint32_t na = 0, nsite = 0;
+    PT(unsigned long long g_site = 0, g_dec = 0, g_gen = 0, g_ea = 0; long long tg;)
     for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x) {
       const long long b0 = cb * kBM, b = b0 + row;
       const bool live = b < p.B;
@@ -182,11 +196,19 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
       tc_fence_after();
       for (long long step = 0; step < p.steps; ++step) {
         const int m = (int)(step % p.N);
+        // the acceptance threshold -T ln u needs no field: computed while the site's MMAs run
+        double thr = 0.0;
+        if (h == 0 && live) {
+          const double u = (double)(d_hash(p.seed, 4, (uint64_t)(p.chain0 + b), (uint64_t)step) >> 11) * 0x1.0p-53;
+          thr = -__ldg(p.temps + step / p.N) * log(u);
+        }
+        PT(tg = clock64();)
         if (step > 0) {
           mbar_wait(SITE, nsite & 1u);
           ++nsite;
           tc_fence_after();
         }
+        PT(g_site += clock64() - tg; tg = clock64();)
         if (h == 0) {
           const float g = __uint_as_float(tmem_ld1(lane_base + (uint32_t)m));
           tmem_ld_wait();
@@ -196,13 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
             const uint32_t bit = 1u << (m & 31);
             const bool xm = (xs[wi * kBM + row] & bit) != 0u;
             const float d = xm ? -g : g;
-            bool acc = d <= 0.0f;
-            if (!acc) {
-              const long long sw = step / p.N;
-              const double u = (double)(d_hash(p.seed, 4, (uint64_t)(p.chain0 + b), (uint64_t)step) >> 11) * 0x1.0p-53;
-              acc = u < exp(-(double)d / __ldg(p.temps + sw));
-            }
-            if (acc) {
+            if (d <= 0.0f || (double)d < thr) {
               sv = xm ? -1 : 1;
               xs[wi * kBM + row] ^= bit;
               E += (double)d;
@@ -211,14 +227,18 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
           sS[row] = sv;
           tc_fence_before();
         }
+        PT(g_dec += clock64() - tg; tg = clock64();)
         named_bar_sync(1, 256);
+        PT(tg = clock64();)
         // A rows of site m: s_b * prod_{u in T} x_bu (x_m itself never occurs with W_m != 0)
         const int sv = sS[row];
         const uint32_t sgn = sv < 0 ? 0x80008000u : 0u;
         for (int q = 0; q < p.nq; ++q, ++na) {
           if ((q & 1) != h) continue;
           const uint32_t a = na % C::RA;
+          PT(const long long te = clock64();)
           mbar_wait(EMPTYA(a), ((na / C::RA) & 1u) ^ 1u);
+          PT(g_ea += clock64() - te;)
           const int kb = sa_site_kb(p, q);
           uint64_t bits = 0;
           if (sv != 0) {
@@ -237,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
           __syncwarp();
           if (lane == 0) mbar_arrive(FULLA(a));
         }
+        PT(g_gen += clock64() - tg;)
       }
       if (p.steps > 0) {   // the last site's update: then the block's results are final
         mbar_wait(SITE, nsite & 1u);
@@ -250,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
       tc_fence_before();
       named_bar_sync(1, 256);   // xs and TMEM are reused by the next block
     }
+    PT(if (gtid == 0) { PSTAT_FLUSH(3, g_site); PSTAT_FLUSH(4, g_dec); PSTAT_FLUSH(5, g_gen); PSTAT_FLUSH(7, g_ea); })
   }
 #undef FULLW
 #undef EMPTYW

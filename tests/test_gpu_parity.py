@@ -399,6 +399,20 @@ def _linear_problem():
     return tb.problem(1, 9)
 
 
+def _wide_int_problem(N=200, seed=36):
+    """Integer cells needing 3 bf16 limbs (a 3-box W stream per K-block) at N in (128, 256]."""
+    from workloads import TermBuilder
+    rng = np.random.default_rng(seed)
+    tb = TermBuilder()
+    for i in range(600):
+        r = int(rng.integers(1, 4))
+        vs = rng.choice(N, size=r, replace=False)
+        # 262657 = 2^18 + 2^9 + 1: hi = 2^18, mid = 2^9, lo = 1 -> three bf16 limbs
+        c = float(rng.integers(-9, 10)) if i % 50 else float(rng.choice([-1, 1]) * 262657)
+        tb.add(c, [(0.0, [(int(v), 1.0)]) for v in vs])
+    return tb.problem(3, N)
+
+
 SA_CASES = {
     "seating4": lambda: seating(4),
     "pythagoras": pythagoras,                                   # L = 2 limbs
@@ -409,6 +423,7 @@ SA_CASES = {
     "linear": _linear_problem,                                  # order 1: fields never change
     "o2n600": lambda: random_integer_problem(2, 600, 34, 900),  # N > 512: the per-site launch path
     "o3n520": lambda: random_integer_problem(3, 520, 35, 900),
+    "wide3limb": _wide_int_problem,
 }
 
 

@@ -456,7 +456,7 @@ def test_sa_replay_by_energy_differences():
                 y[m] ^= 1
                 d = Eall[idx(y)] - Eall[idx(x)]
                 u = int(h(13, 4, c, s * o.N + m) >> np.uint64(11)) * 2.0 ** -53
-                if d <= 0 or u < math.exp(-d / T[s]):
+                if d <= 0 or d < -T[s] * math.log(u):      # u < exp(-d/T) for u in (0, 1)
                     x = y
         assert list(xs[i]) == x and es[i] == Eall[idx(x)]
 
