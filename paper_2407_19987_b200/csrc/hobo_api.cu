@@ -981,6 +981,20 @@ cudaError_t launch_sa(const CUtensorMap& tmap, const SaParams& p, unsigned grid,
   return cudaGetLastError();
 }
 
+template <int NT>
+cudaError_t launch_sa_stage(const CUtensorMap& tmap, const SaParams& p, int SB, unsigned grid, cudaStream_t s) {
+  auto* k = sa_stage_kernel<NT>;
+  const size_t smem = SaStCfg<NT>::smem_bytes(SB, p.W);
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k<<<grid, kThreads, smem, s>>>(tmap, p, SB, SaStCfg<NT>::nst(SB));
+  return cudaGetLastError();
+}
+
 hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweeps, double t_start,
                    double t_end, cudaStream_t s, int64_t& launches) {
   if (nchains < 1 || sweeps < 0 || chain0 < 0 || chain0 + nchains > (int64_t)0xFFFFFFFF)
@@ -1041,7 +1055,17 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
     const long long n_cb = (B + kBM - 1) / kBM;
     if (t->profile) CK(cudaEventRecord(t->ev0, s));
     const unsigned grid = (unsigned)std::min<long long>(n_cb, 148);
-    CK(t->sa_NT == 128 ? launch_sa<128>(t->sa_tmap, q, grid, s) : launch_sa<256>(t->sa_tmap, q, grid, s));
+    // 128-column tiles (64-cycle MMAs): the staged kernel, one barrier pair per K-block, when
+    // two stages fit; 256-column tiles: the box ring (measured faster there)
+    int Lmax = 1;
+    for (int l : t->sa_L) Lmax = std::max(Lmax, l);
+    const int SB = Lmax * t->sa_nct;
+    bool staged = t->sa_NT == 128 && SaStCfg<128>::nst(SB) >= 2;
+    if (const char* e = getenv("HOBO_SA_KERNEL")) staged = e[0] == 's';   // A/B measurement switch
+    if (staged)
+      CK(t->sa_NT == 128 ? launch_sa_stage<128>(t->sa_tmap, q, SB, grid, s) : launch_sa_stage<256>(t->sa_tmap, q, SB, grid, s));
+    else
+      CK(t->sa_NT == 128 ? launch_sa<128>(t->sa_tmap, q, grid, s) : launch_sa<256>(t->sa_tmap, q, grid, s));
     if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
     launches += 1;
     double per_sweep = 0;

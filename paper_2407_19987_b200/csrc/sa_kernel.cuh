@@ -282,4 +282,209 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
   if (warp == 1) tmem_dealloc(tmem, (uint32_t)NPAD);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Staged variant: one pipeline stage = one site K-block, i.e. all n_ct x L W boxes of that
+// K-block plus its A tile, behind ONE full barrier (TMA bytes + 4 generator-warp arrivals)
+// and ONE empty barrier (a single tcgen05.commit).  The box-ring kernel above pays a wait,
+// a fence and a commit per W box and per A tile; with 128-column tiles (64-cycle MMAs) that
+// bookkeeping is what the lone MMA-issuing thread cannot hide.
+template <int NT>
+struct SaStCfg {
+  static constexpr int BOX = NT * 128;
+  static constexpr int ABOX = kBM * 128;
+  static constexpr int BUDGET = 232448 - 1024 - 1024 - 16 * 1024;   // ring bytes (bits, barriers after it)
+  static int stage_bytes(int boxes) { return boxes * BOX + ABOX; }
+  static int nst(int boxes) { return std::min(4, BUDGET / stage_bytes(boxes)); }
+  static size_t smem_bytes(int boxes, int W) {
+    return 1024 + (size_t)nst(boxes) * stage_bytes(boxes) + 8 * 9 + 16 + (size_t)(W + 2) * kBM * 4 + kBM * 4 + 128;
+  }
+};
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_constant__ CUtensorMap tmap, const SaParams p,
+                                                               int SB, int NST) {
+  using C = SaStCfg<NT>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t SBYTES = (uint32_t)(SB * C::BOX + C::ABOX);
+  const uint32_t sSt = base;                                  // stage s: SB W boxes, then the A tile
+  const uint32_t sBar = sSt + (uint32_t)NST * SBYTES;
+#define FULL(s) (sBar + 8u * (s))
+#define EMPTY(s) (sBar + 8u * (4 + (s)))
+  const uint32_t SITE = sBar + 8u * 8;
+  const uint32_t tslot = SITE + 8;
+  const uint32_t sX = (tslot + 16 + 127u) & ~127u;
+  uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
+  int* sS = reinterpret_cast<int*>(gbase + (sX - base) + (size_t)(p.W + 2) * kBM * 4);
+  volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NPAD = NT * p.n_ct;
+  const long long n_cb = (p.B + kBM - 1) / kBM;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) { mbar_init(FULL(s), 5); mbar_init(EMPTY(s), 1); }
+    mbar_init(SITE, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
+  if (warp == 1) tmem_alloc(tslot, (uint32_t)NPAD);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot_g;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: each stage gets one K-block's L x n_ct W boxes -------------
+    if (lane == 0) {
+      uint32_t n = 0;
+      for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x)
+        for (long long step = 0; step < p.steps; ++step) {
+          const int m = (int)(step % p.N);
+          const int L = __ldg(p.site_L + m), sb = __ldg(p.site_base + m);
+          for (int q = 0; q < p.nq; ++q, ++n) {
+            const int kb = sa_site_kb(p, q);
+            const uint32_t s = n % NST;
+            mbar_wait(EMPTY(s), ((n / NST) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(FULL(s), (uint32_t)(L * p.n_ct) * C::BOX);
+            for (int l = 0; l < L; ++l)
+              for (int h = 0; h < p.n_ct; ++h)
+                tma_load_3d(sSt + s * SBYTES + (uint32_t)(l * p.n_ct + h) * C::BOX, &tmap, FULL(s), 0, 0,
+                            sb + (l * p.n_ct + h) * p.nkb1 + kb);
+          }
+        }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: one wait + one commit per K-block ----------------------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
+      uint32_t n = 0;
+      for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x)
+        for (long long step = 0; step < p.steps; ++step) {
+          const int m = (int)(step % p.N);
+          const int L = __ldg(p.site_L + m);
+          for (int q = 0; q < p.nq; ++q, ++n) {
+            const uint32_t s = n % NST;
+            mbar_wait(FULL(s), (n / NST) & 1u);
+            tc_fence_after();
+            const uint32_t st = sSt + s * SBYTES;
+            const uint64_t adesc = sw128_kmajor_desc(st + (uint32_t)SB * C::BOX);
+            for (int l = 0; l < L; ++l)
+              for (int h = 0; h < p.n_ct; ++h) {
+                const uint64_t bdesc = sw128_kmajor_desc(st + (uint32_t)(l * p.n_ct + h) * C::BOX);
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                  umma_bf16_ss(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
+              }
+            umma_commit(EMPTY(s));
+          }
+          umma_commit(SITE);
+        }
+    }
+  } else {
+    // ---------------- decisions (team 0) + A generator (both teams), one row per thread -----------
+    const int qd = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int row = qd * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(qd * 32) << 16);
+    const int gtid = threadIdx.x - 64;
+    uint32_t n = 0, nsite = 0;
+    for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x) {
+      const long long b0 = cb * kBM, b = b0 + row;
+      const bool live = b < p.B;
+      const int Wp = p.W + 2;
+      for (int i = gtid; i < Wp * kBM; i += 256) {
+        const int r = i / Wp, w = i % Wp;
+        xs[w * kBM + r] = (w < p.W && b0 + r < p.B) ? p.bits[(size_t)(b0 + r) * p.W + w] : 0u;
+      }
+      for (int c0 = h * (NPAD / 2); c0 < (h + 1) * (NPAD / 2); c0 += 32) {
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          v[c] = (live && c0 + c < p.N) ? __float_as_uint(__ldg(p.G0 + (size_t)b * p.N + c0 + c)) : 0u;
+        tmem_st32(lane_base + (uint32_t)c0, v);
+      }
+      tmem_st_wait();
+      double E = (h == 0 && live) ? p.E[b] : 0.0;
+      tc_fence_before();
+      named_bar_sync(1, 256);
+      tc_fence_after();
+      for (long long step = 0; step < p.steps; ++step) {
+        const int m = (int)(step % p.N);
+        double thr = 0.0;   // -T ln u: no field needed, computed while the previous site's MMAs run
+        if (h == 0 && live) {
+          const double u = (double)(d_hash(p.seed, 4, (uint64_t)(p.chain0 + b), (uint64_t)step) >> 11) * 0x1.0p-53;
+          thr = -__ldg(p.temps + step / p.N) * log(u);
+        }
+        if (step > 0) {
+          mbar_wait(SITE, nsite & 1u);
+          ++nsite;
+          tc_fence_after();
+        }
+        if (h == 0) {
+          const float g = __uint_as_float(tmem_ld1(lane_base + (uint32_t)m));
+          tmem_ld_wait();
+          int sv = 0;
+          if (live) {
+            const int wi = m >> 5;
+            const uint32_t bit = 1u << (m & 31);
+            const bool xm = (xs[wi * kBM + row] & bit) != 0u;
+            const float d = xm ? -g : g;
+            if (d <= 0.0f || (double)d < thr) {
+              sv = xm ? -1 : 1;
+              xs[wi * kBM + row] ^= bit;
+              E += (double)d;
+            }
+          }
+          sS[row] = sv;
+          tc_fence_before();
+        }
+        named_bar_sync(1, 256);
+        const int sv = sS[row];
+        const uint32_t sgn = sv < 0 ? 0x80008000u : 0u;
+        for (int q = 0; q < p.nq; ++q, ++n) {
+          if ((q & 1) != h) continue;
+          const uint32_t s = n % NST;
+          mbar_wait(EMPTY(s), ((n / NST) & 1u) ^ 1u);
+          const int kb = sa_site_kb(p, q);
+          uint64_t bits = 0;
+          if (sv != 0) {
+            if (kb == p.nkb1 - 1) bits = 1ull;
+            else bits = block_bits(xs, row, __ldg(p.kdesc + 2 * kb), __ldg(p.kdesc + 2 * kb + 1), p.runs);
+          }
+          uint32_t w[32];
+          expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+          expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
+          const uint32_t rowaddr = sSt + s * SBYTES + (uint32_t)SB * C::BOX + (uint32_t)(row >> 3) * 1024u +
+                                   (uint32_t)(row & 7) * 128u;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            st_shared_v4(rowaddr + (uint32_t)((c ^ (row & 7)) << 4), w[4 * c] ^ sgn, w[4 * c + 1] ^ sgn,
+                         w[4 * c + 2] ^ sgn, w[4 * c + 3] ^ sgn);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(FULL(s));
+        }
+      }
+      if (p.steps > 0) {
+        mbar_wait(SITE, nsite & 1u);
+        ++nsite;
+        tc_fence_after();
+      }
+      if (h == 0 && live) {
+        p.E[b] = E;
+        for (int w = 0; w < p.W; ++w) p.bits[(size_t)b * p.W + w] = xs[w * kBM + row];
+      }
+      tc_fence_before();
+      named_bar_sync(1, 256);
+    }
+  }
+#undef FULL
+#undef EMPTY
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, (uint32_t)NPAD);
+}
+
 }  // namespace hobo
