@@ -111,6 +111,19 @@ hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X_dev, int64_t B, int64_t
 hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X_dev, int64_t B, int64_t row0,
                              float* G_dev, float* E_dev, hobo_best* best, void* stream);
 
+/* hobo_local_field_host — hobo_local_field for candidates in HOST memory, end to end:
+ * X_host [B*N] u8 (page-locked memory lets the copies overlap), E_host [B] f32 (nullable)
+ * and best (nullable) are host outputs; the fields are computed on the device (scratch,
+ * not returned).  The batch runs in chunks of whole waves; chunk i+1's host->device copy
+ * (on an internal copy stream ordered after the caller's stream) overlaps chunk i's
+ * contraction.  Results equal hobo_local_field's.  Synchronises the stream.             */
+hobo_status hobo_local_field_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0,
+                                  float* E_host, hobo_best* best, void* stream);
+/* hobo_energy_host — hobo_energy for candidates in host memory, the same pipeline (energy
+ * layout; no fields).  Results equal hobo_energy's.  Synchronises the stream.            */
+hobo_status hobo_energy_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0,
+                             float* E_host, hobo_best* best, void* stream);
+
 /* hobo_multilinear_field — the same contraction on REAL candidates p in [0,1]^N, the
  * multilinear relaxation used by gradient descent ("the gradient is computed based
  * on tensor contraction results"):

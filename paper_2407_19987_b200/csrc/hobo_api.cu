@@ -72,6 +72,10 @@ struct hobo_tensor {
   uint16_t* d_P = nullptr; size_t P_cap = 0;
   uint32_t* d_starts = nullptr; size_t starts_cap = 0;
   double* d_Qpart = nullptr; size_t Qpart_cap = 0;
+  uint8_t* d_xh[2] = {nullptr, nullptr}; size_t xh_cap = 0;   // host-input path: staged X chunks
+  float* d_Eh = nullptr; size_t Eh_cap = 0;
+  cudaStream_t cs = nullptr;                            // its copy stream
+  cudaEvent_t ev_in = nullptr, ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   std::vector<hobo_tensor*> sa_child;                   // annealing: P_m = dE/dx_m per site m
   bool sa_borrowed = false;                             // a site tensor: its tables belong to the parent
   uint4* d_sa_runs = nullptr;                           // the site tensors' shared tables (same order, N)
@@ -494,6 +498,14 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
   for (hobo_tensor* c : t->sa_child) hobo_tensor_free(c);
+  if (t->cs) {
+    cudaStreamDestroy(t->cs);
+    cudaEventDestroy(t->ev_in);
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(t->ev_copied[i]); cudaEventDestroy(t->ev_free[i]); }
+  }
+  for (int i = 0; i < 2; ++i)
+    if (t->d_xh[i]) cudaFree(t->d_xh[i]);
+  if (t->d_Eh) cudaFree(t->d_Eh);
   if (t->d_sa_s) cudaFree(t->d_sa_s);
   if (t->d_sa_E) cudaFree(t->d_sa_E);
   void* ptrs[] = {t->d_tt, t->d_tt_meta, t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
@@ -584,6 +596,93 @@ hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_
     best->e = key_energy(key);
   }
   return HOBO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// host-input path of hobo_energy_host / hobo_local_field_host (whole-wave chunks, copy stream)
+hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
+                     hobo_best* best, void* stream) {
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (B < 0 || (B > 0 && !X_host) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF)
+    return fail(HOBO_EINVAL, "bad batch (B >= 0, X non-null, row0 + B < 2^32)");
+  if (hobo_status st = check_device(t)) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (B == 0) {
+    if (best) { best->e = INFINITY; best->idx = -1; }
+    return HOBO_OK;
+  }
+  if (hobo_status st = ensure_layout(t, field)) return st;
+  const DevLayout& L = t->lay[field];
+  const int N = t->host.N;
+  // chunks of whole waves: 2 waves of (candidate block x column tile) CTAs
+  const long long per_wave = std::max<long long>(1, 148 / L.n_ct) * kBM;
+  const long long chunk = std::min<long long>(B, 2 * per_wave);
+  if (!t->cs) {
+    CK(cudaStreamCreateWithFlags(&t->cs, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&t->ev_copied[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&t->ev_free[i], cudaEventDisableTiming));
+    }
+  }
+  if ((size_t)chunk * N > t->xh_cap) {
+    for (int i = 0; i < 2; ++i) {
+      if (t->d_xh[i]) cudaFree(t->d_xh[i]);
+      t->d_xh[i] = nullptr;
+    }
+    t->xh_cap = 0;
+    for (int i = 0; i < 2; ++i) CK(cudaMalloc(&t->d_xh[i], (size_t)chunk * N));
+    t->xh_cap = (size_t)chunk * N;
+  }
+  if (hobo_status st = grow(t, t->d_Eh, t->Eh_cap, (size_t)B)) return st;
+  if (field)
+    if (hobo_status st = grow(t, t->d_G, t->G_cap, (size_t)chunk * N)) return st;
+  if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  CK(cudaEventRecord(t->ev_in, s));             // the copies follow the caller's prior work
+  CK(cudaStreamWaitEvent(t->cs, t->ev_in, 0));
+  int64_t launches = 0;
+  for (long long off = 0, i = 0; off < B; off += chunk, ++i) {
+    const long long n = std::min<long long>(chunk, B - off);
+    const int slot = (int)(i & 1);
+    if (i >= 2) CK(cudaStreamWaitEvent(t->cs, t->ev_free[slot], 0));   // its previous chunk is packed
+    CK(cudaMemcpyAsync(t->d_xh[slot], X_host + (size_t)off * N, (size_t)n * N, cudaMemcpyHostToDevice, t->cs));
+    CK(cudaEventRecord(t->ev_copied[slot], t->cs));
+    CK(cudaStreamWaitEvent(s, t->ev_copied[slot], 0));
+    if (hobo_status st = contract(t, field, t->d_xh[slot], n, field ? t->d_G : nullptr, s)) return st;
+    CK(cudaEventRecord(t->ev_free[slot], s));
+    finalize_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, s>>>(
+        t->d_Q, L.n_ct, n, L.lcm, row0 + off, t->d_Eh + off, best ? t->d_key : nullptr);
+    CK(cudaGetLastError());
+    launches += t->last_launches + 1;
+    if (E_host) CK(cudaMemcpyAsync(E_host + off, t->d_Eh + off, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, s));
+  }
+  unsigned long long key = 0;
+  if (best) CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (best) {
+    best->idx = (int64_t)(key & 0xFFFFFFFFull);
+    best->e = key_energy(key);
+  }
+  t->last_launches = launches;
+  t->last_mma_macs = exec_macs(t, L, B);
+  t->last_algo_macs = algo_macs(t, field != 0, B);
+  return HOBO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hobo_status hobo_energy_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
+                             hobo_best* best, void* stream) {
+  return run_host(t, 0, X_host, B, row0, E_host, best, stream);
+}
+
+hobo_status hobo_local_field_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
+                                  hobo_best* best, void* stream) {
+  return run_host(t, 1, X_host, B, row0, E_host, best, stream);
 }
 
 }  // extern "C"

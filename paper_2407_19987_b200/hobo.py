@@ -16,7 +16,7 @@ _STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ES
 
 EXPORTED = [
     "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_free", "hobo_tensor_info",
-    "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field",
+    "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field", "hobo_local_field_host", "hobo_energy_host",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
     "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats",
     "hobo_set_profiling", "hobo_last_error",
@@ -55,6 +55,8 @@ def lib():
         L.hobo_tensor_export_dense.argtypes = [P, P]
         L.hobo_energy.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_local_field.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
+        L.hobo_local_field_host.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
+        L.hobo_energy_host.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_search.argtypes = [P, U64, I64, I64, P, C.POINTER(C.c_float), P]
         L.hobo_search_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, C.POINTER(C.c_float),
                                         C.POINTER(I64), P]
@@ -201,6 +203,31 @@ class HoboTensor:
                                       _dev_ptr(E, torch.float32, (B,)) if E is not None else None,
                                       C.byref(best) if want_best else None, _stream_handle(stream)))
         return (G, E, (best.e, best.idx)) if want_best else (G, E)
+
+    def local_field_host(self, X, E=None, row0=0, want_best=True, stream=None, fields=True):
+        """hobo_local_field_host (fields=True) / hobo_energy_host (fields=False): candidates in
+        host memory (numpy u8 B x N, or a CPU torch tensor, ideally pinned); energies into the
+        host array E (f32, allocated if None).  Returns (E, best)."""
+        def host_ptr(a, dtype, shape):
+            if hasattr(a, "data_ptr"):
+                if a.is_cuda or tuple(a.shape) != shape or not a.is_contiguous():
+                    raise ValueError(f"expected a contiguous CPU tensor of shape {shape}")
+                return a.data_ptr()
+            if a.dtype != dtype or a.shape != shape or not a.flags.c_contiguous:
+                raise ValueError(f"expected a C-contiguous {dtype} array of shape {shape}")
+            return a.ctypes.data
+        B = X.shape[0]
+        xp = host_ptr(X, np.uint8, (B, self.N))
+        if E is None:
+            E = np.empty(B, np.float32)
+        best = HoboBest()
+        fn = lib().hobo_local_field_host if fields else lib().hobo_energy_host
+        _check(fn(self._h, xp, B, row0, host_ptr(E, np.float32, (B,)), C.byref(best) if want_best else None,
+                  _stream_handle(stream)))
+        return E, ((best.e, best.idx) if want_best else None)
+
+    def energy_host(self, X, E=None, row0=0, want_best=True, stream=None):
+        return self.local_field_host(X, E, row0, want_best, stream, fields=False)
 
     def multilinear_field(self, P, G=None, E=None, stream=None):
         """Gradient and value of the multilinear relaxation at real p (CUDA bf16 tensor B x N)."""

@@ -499,3 +499,22 @@ def test_sa_run_sample_set(H, torch, name, emin):
         assert np.array_equal(gx, wx) and ge == we and gc == wc
     assert got[0][1] == emin
     assert sum(c for _, _, c in t.sa_run(7, shots, sweeps, topk=1 << 12)) == shots
+
+
+# ---- host-buffer entry points (the e2e path): chunked copies overlapped with compute ---------
+def test_host_entry_points_match_device_path(H, torch):
+    """cfg3 at the full 65,536 (4 chunks, ragged last) and small / offset batches: energies
+    and argmin from host buffers equal the device-buffer calls bit for bit."""
+    p = cfg3_problem()
+    t = H.HoboTensor.from_problem(p)
+    for B, row0, pinned in ((65536, 0, True), (1000, 5, False), (1, 0, False), (19000, 77, True)):
+        Xh = x_bits(3, B, t.N)
+        Xd = dev(torch, Xh)
+        G, E, best = t.local_field(Xd, row0=row0, want_best=True)
+        Ed, bestd = t.energy(Xd, row0=row0)
+        torch.cuda.synchronize()
+        src = torch.from_numpy(Xh).pin_memory() if pinned else Xh
+        Eh, besth = t.local_field_host(src, row0=row0)
+        assert np.array_equal(Eh, E.cpu().numpy()) and besth == best
+        Eh2, besth2 = t.energy_host(src, row0=row0)
+        assert np.array_equal(Eh2, Ed.cpu().numpy()) and besth2 == bestd
