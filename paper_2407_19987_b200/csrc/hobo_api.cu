@@ -1461,11 +1461,29 @@ hobo_status hobo_tt_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t 
   if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * W)) return st;
   const long long nw = B * W;
   pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, N, W, t->d_bits);
-  const unsigned g = (unsigned)std::min<long long>((B + 127) / 128, 148 * 32);
+  int ncores = 0;
+  for (const auto& c : t->tt.cores) ncores += (int)c.size();
+  const size_t smem = (size_t)ncores * sizeof(double);
   if (t->profile) CK(cudaEventRecord(t->ev0, s));
-  if (rmax <= 4) tt_energy_kernel<4><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
-  else if (rmax <= 16) tt_energy_kernel<16><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
-  else tt_energy_kernel<32><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+  if (smem <= 48 * 1024 && k <= 16) {   // cores staged in shared memory, 4 (rank <= 4) or 2 candidates per thread
+    const int cpt = rmax <= 4 ? 4 : 2;
+    const unsigned g = (unsigned)std::min<long long>((B + 128 * cpt - 1) / (128 * cpt), 148 * 16);
+    if (rmax <= 4)
+      tt_energy_smem_kernel<4, 4><<<g, 128, smem, s>>>(t->d_tt, ncores, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+    else if (rmax <= 8)
+      tt_energy_smem_kernel<8, 2><<<g, 128, smem, s>>>(t->d_tt, ncores, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+    else if (rmax <= 16)
+      tt_energy_smem_kernel<16, 1><<<(unsigned)std::min<long long>((B + 127) / 128, 148 * 16), 128, smem, s>>>(
+          t->d_tt, ncores, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+    else
+      tt_energy_smem_kernel<32, 1><<<(unsigned)std::min<long long>((B + 127) / 128, 148 * 16), 128, smem, s>>>(
+          t->d_tt, ncores, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+  } else {
+    const unsigned g = (unsigned)std::min<long long>((B + 127) / 128, 148 * 32);
+    if (rmax <= 4) tt_energy_kernel<4><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+    else if (rmax <= 16) tt_energy_kernel<16><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+    else tt_energy_kernel<32><<<g, 128, 0, s>>>(t->d_tt, t->d_tt_meta, t->d_tt_meta + k, k, N, W, t->d_bits, B, E);
+  }
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
   CK(cudaGetLastError());
   t->last_launches = 2;

@@ -1042,4 +1042,71 @@ __global__ void tt_energy_kernel(const double* __restrict__ cores, const int* __
     E[b] = (float)v[0];
   }
 }
+
+// The same chain product with the cores staged in shared memory (warp-uniform reads are
+// broadcasts) and CPT candidates per thread, so each core element loaded feeds CPT fp64
+// FMAs; a candidate's bit word is loaded once per 32 indices.  Same summation order as
+// tt_energy_kernel (x_i = 0 contributes an exact zero instead of being skipped).
+template <int RM, int CPT>
+__global__ void tt_energy_smem_kernel(const double* __restrict__ cores, int ncores, const int* __restrict__ off,
+                                      const int* __restrict__ ranks, int k, int N, int W,
+                                      const uint32_t* __restrict__ bits, long long B, float* __restrict__ E) {
+  extern __shared__ double sc[];
+  __shared__ int soff[16], sr[17];
+  for (int i = threadIdx.x; i < ncores; i += blockDim.x) sc[i] = cores[i];
+  if (threadIdx.x < k) soff[threadIdx.x] = off[threadIdx.x];
+  if (threadIdx.x <= k) sr[threadIdx.x] = ranks[threadIdx.x];
+  __syncthreads();
+  const long long per_block = (long long)blockDim.x * CPT;
+  for (long long base = blockIdx.x * per_block; base < B; base += (long long)gridDim.x * per_block) {
+    long long bj[CPT];
+    double v[CPT][RM];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      bj[j] = base + (long long)j * blockDim.x + threadIdx.x;   // coalesced bits / E accesses
+#pragma unroll
+      for (int a = 0; a < RM; ++a) v[j][a] = a == 0 ? 1.0 : 0.0;
+    }
+    int rp = 1;
+    for (int p = 0; p < k; ++p) {
+      const int rn = sr[p + 1];
+      const double* G = sc + soff[p];
+      double nv[CPT][RM];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j)
+#pragma unroll
+        for (int c = 0; c < RM; ++c) nv[j][c] = 0.0;
+      uint32_t xw[CPT];
+      for (int i = 0; i < N; ++i) {
+        if ((i & 31) == 0) {
+#pragma unroll
+          for (int j = 0; j < CPT; ++j) xw[j] = bj[j] < B ? __ldg(bits + bj[j] * W + (i >> 5)) : 0u;
+        }
+#pragma unroll
+        for (int a = 0; a < RM; ++a) {
+          if (a >= rp) break;
+          double va[CPT];
+#pragma unroll
+          for (int j = 0; j < CPT; ++j) va[j] = ((xw[j] >> (i & 31)) & 1u) ? v[j][a] : 0.0;
+          const double* g = G + ((size_t)a * N + i) * rn;
+#pragma unroll
+          for (int c = 0; c < RM; ++c)
+            if (c < rn) {
+              const double gc = g[c];
+#pragma unroll
+              for (int j = 0; j < CPT; ++j) nv[j][c] = fma(va[j], gc, nv[j][c]);
+            }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CPT; ++j)
+#pragma unroll
+        for (int c = 0; c < RM; ++c) v[j][c] = nv[j][c];
+      rp = rn;
+    }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j)
+      if (bj[j] < B) E[bj[j]] = (float)v[j][0];
+  }
+}
 }  // namespace hobo

@@ -2,6 +2,7 @@
 into profiles/: a markdown table plus a JSON with the numbers bench.py's roofline cites.
 
   python tools/ncu_summary.py gpurun_out/launches_r1.csv gpurun_out/prof_r1.ncu-rep profiles/r01
+  python tools/ncu_summary.py --capture gpurun_out/sa.ncu-rep profiles/r01_sa "what was captured"
 """
 import csv
 import io
@@ -41,6 +42,10 @@ WANT = {
     "launch__block_size": "block",
     "gpc__cycles_elapsed.max": "cycles",
     "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed": "smem_pipe_pct",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    "l1tex__throughput.avg.pct_of_peak_sustained_elapsed": "l1tex_throughput_pct",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
 }
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
          "ms": 1e-3, "msecond": 1e-3, "s": 1.0}
@@ -60,7 +65,23 @@ def full_capture(rep):
     return d
 
 
+def capture_only(rep, prefix, what):
+    F = full_capture(rep)
+    traffic = F.get("dram_read", 0.0) + F.get("dram_write", 0.0)
+    json.dump({"capture": F, "traffic_bytes_per_launch": traffic, "what": what, "source": rep},
+              open(prefix + "_ncu.json", "w"), indent=1)
+    with open(prefix + "_ncu.md", "w") as f:
+        f.write(f"# ncu --set full capture\n\n{what}\n\n| metric | value |\n|---|---|\n")
+        for k, v in F.items():
+            f.write(f"| {k} | {v:.6g} |\n" if isinstance(v, float) else f"| {k} | {v} |\n")
+        f.write(f"| traffic = dram read + write (bytes/launch) | {traffic:.6g} |\n")
+    print(json.dumps(F, indent=1))
+
+
 def main():
+    if sys.argv[1] == "--capture":
+        capture_only(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "")
+        return
     launches, rep, prefix = sys.argv[1:4]
     L = launch_shares(launches)
     F = full_capture(rep)

@@ -15,7 +15,8 @@ elif cfg == "cfg4":
     t, B = HoboTensor.import_colex(4, 128, uniform_colex(4, 128, 4)), 262144
 t0 = t.default_t_start() if cfg == "cfg3" else 5.0
 t.sa_shard(1, 0, 128, 1, t0, t0)
-for kind in ("ring", "stage"):
+kinds = sys.argv[2:] or ["ring", "stage"]
+for kind in kinds:
     os.environ["HOBO_SA_KERNEL"] = kind
     t.set_profiling(True)
     t.sa_shard(2, 0, B, 1, t0, t0 / 10)
