@@ -362,7 +362,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
 int choose_split(hobo_tensor* t, const DevLayout& L, long long B) {
   const long long tiles = ((B + kBM - 1) / kBM) * L.n_ct;
   if (tiles >= 148) return 1;
-  const int KPS = KrCfg<256>::kps(t->host.limbs);
+  const int KPS = L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
   int stages = 0;
   for (int ct = 0; ct < L.n_ct; ++ct) {
     int s = 0;

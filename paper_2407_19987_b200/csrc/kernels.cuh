@@ -73,8 +73,10 @@ struct KrCfg {
   static size_t smem_bytes(int W) {
     return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)(W + 2) * kBM * 4 + 128;
   }
-  // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages
-  __host__ __device__ static constexpr int kps(int L) { return L == 1 ? 2 : 1; }
+  // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages.  Two
+  // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
+  // boxes that fits only at L = 1, with 128-column boxes at every L <= 3
+  __host__ __device__ static constexpr int kps(int L) { return (L == 1 || NT <= 128) ? 2 : 1; }
   __host__ __device__ static constexpr int nst(int L) { return RING_BOXES / (kps(L) * L) < MAXST ? RING_BOXES / (kps(L) * L) : MAXST; }
   // real-valued A: one K-block per stage, LA limb tiles of A in TMEM, ring sized at run time
   __host__ __device__ static int nst_real(int L, int LA, int ring) {
