@@ -1080,17 +1080,17 @@ cudaError_t launch_sa(const CUtensorMap& tmap, const SaParams& p, unsigned grid,
   return cudaGetLastError();
 }
 
-template <int NT>
+template <int NT, bool TS>
 cudaError_t launch_sa_stage(const CUtensorMap& tmap, const SaParams& p, int SB, unsigned grid, cudaStream_t s) {
-  auto* k = sa_stage_kernel<NT>;
-  const size_t smem = SaStCfg<NT>::smem_bytes(SB, p.W);
+  auto* k = sa_stage_kernel<NT, TS>;
+  const size_t smem = SaStCfg<NT, TS>::smem_bytes(SB, p.W);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  k<<<grid, kThreads, smem, s>>>(tmap, p, SB, SaStCfg<NT>::nst(SB));
+  k<<<grid, kThreads, smem, s>>>(tmap, p, SB, SaStCfg<NT, TS>::nst(SB));
   return cudaGetLastError();
 }
 
@@ -1154,15 +1154,21 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
     const long long n_cb = (B + kBM - 1) / kBM;
     if (t->profile) CK(cudaEventRecord(t->ev0, s));
     const unsigned grid = (unsigned)std::min<long long>(n_cb, 148);
-    // 128-column tiles (64-cycle MMAs): the staged kernel, one barrier pair per K-block, when
-    // two stages fit; 256-column tiles: the box ring (measured faster there)
+    // one column tile (Npad <= 256): the staged kernel (one barrier pair per K-block); two
+    // tiles: the box ring (measured faster there).  The A-in-TMEM staged variant ('t') is an
+    // A/B option: measured 4% slower than smem A at cfg4.
     int Lmax = 1;
     for (int l : t->sa_L) Lmax = std::max(Lmax, l);
     const int SB = Lmax * t->sa_nct;
-    bool staged = t->sa_NT == 128 && SaStCfg<128>::nst(SB) >= 2;
-    if (const char* e = getenv("HOBO_SA_KERNEL")) staged = e[0] == 's';   // A/B measurement switch
-    if (staged)
-      CK(t->sa_NT == 128 ? launch_sa_stage<128>(t->sa_tmap, q, SB, grid, s) : launch_sa_stage<256>(t->sa_tmap, q, SB, grid, s));
+    char kind = t->sa_nct == 1 ? 's' : 'r';
+    if ((t->sa_NT == 128 ? SaStCfg<128, false>::nst(SB) : SaStCfg<256, false>::nst(SB)) < 2) kind = 'r';
+    if (const char* e = getenv("HOBO_SA_KERNEL")) kind = e[0];   // A/B measurement switch: ring|stage|ts
+    if (kind == 't' && t->sa_nct == 1)
+      CK((t->sa_NT == 128 ? launch_sa_stage<128, true>(t->sa_tmap, q, SB, grid, s)
+                          : launch_sa_stage<256, true>(t->sa_tmap, q, SB, grid, s)));
+    else if (kind == 's')
+      CK((t->sa_NT == 128 ? launch_sa_stage<128, false>(t->sa_tmap, q, SB, grid, s)
+                          : launch_sa_stage<256, false>(t->sa_tmap, q, SB, grid, s)));
     else
       CK(t->sa_NT == 128 ? launch_sa<128>(t->sa_tmap, q, grid, s) : launch_sa<256>(t->sa_tmap, q, grid, s));
     if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }

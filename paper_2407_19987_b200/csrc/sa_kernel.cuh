@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: G[:, tile h] += A_q * W_m,q (accumulate, never cleared) ---------
-    if (lane == 0) {
+    // whole warp in the loop (uniform registers), one elected lane issues
+    {
       constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
       uint32_t nw = 0, na = 0;
       PT(unsigned long long wa = 0, ww = 0; const long long tbeg = clock64(); long long t0;)
@@ -152,16 +153,21 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
                 PT(ww += clock64() - t0;)
                 tc_fence_after();
                 const uint64_t bdesc = sw128_kmajor_desc(sW + s * C::BOX);
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k)
-                  umma_bf16_ss(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
-                umma_commit(EMPTYW(s));
+                  for (int k = 0; k < kBK / 16; ++k)
+                    umma_bf16_ss(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
+                  umma_commit(EMPTYW(s));
+                }
+                __syncwarp();
               }
-            umma_commit(EMPTYA(a));
+            if (elect_one()) umma_commit(EMPTYA(a));
+            __syncwarp();
           }
-          umma_commit(SITE);   // this site's G update is complete when this arrives
+          if (elect_one()) umma_commit(SITE);   // this site's G update is complete when this arrives
+          __syncwarp();
         }
-      PT(PSTAT_FLUSH(0, clock64() - tbeg); PSTAT_FLUSH(1, wa); PSTAT_FLUSH(2, ww);)
+      PT(if (lane == 0) { PSTAT_FLUSH(0, clock64() - tbeg); PSTAT_FLUSH(1, wa); PSTAT_FLUSH(2, ww); })
     }
   } else {
     // ---------------- decisions (team 0) + A generator (both teams), one row per thread -----------
@@ -288,22 +294,27 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
 // and ONE empty barrier (a single tcgen05.commit).  The box-ring kernel above pays a wait,
 // a fence and a commit per W box and per A tile; with 128-column tiles (64-cycle MMAs) that
 // bookkeeping is what the lone MMA-issuing thread cannot hide.
-template <int NT>
+// TS (one column tile, Npad <= 256): the A tiles go to tensor memory next to G (tcgen05.st,
+// A-in-TMEM MMAs), so shared memory carries only the W stream — with A in smem its writes
+// and the MMAs' A reads push shared-memory traffic past the port at 128-column tiles.
+template <int NT, bool TS>
 struct SaStCfg {
   static constexpr int BOX = NT * 128;
-  static constexpr int ABOX = kBM * 128;
+  static constexpr int ABOX = TS ? 0 : kBM * 128;
+  static constexpr int MAXST = 8;
   static constexpr int BUDGET = 232448 - 1024 - 1024 - 16 * 1024;   // ring bytes (bits, barriers after it)
   static int stage_bytes(int boxes) { return boxes * BOX + ABOX; }
-  static int nst(int boxes) { return std::min(4, BUDGET / stage_bytes(boxes)); }
+  static int nst(int boxes) { return std::min(TS ? MAXST : 4, BUDGET / stage_bytes(boxes)); }
   static size_t smem_bytes(int boxes, int W) {
-    return 1024 + (size_t)nst(boxes) * stage_bytes(boxes) + 8 * 9 + 16 + (size_t)(W + 2) * kBM * 4 + kBM * 4 + 128;
+    return 1024 + (size_t)nst(boxes) * stage_bytes(boxes) + 8 * (2 * MAXST + 1) + 16 + (size_t)(W + 2) * kBM * 4 +
+           kBM * 4 + 128;
   }
 };
 
-template <int NT>
+template <int NT, bool TS>
 __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_constant__ CUtensorMap tmap, const SaParams p,
                                                                int SB, int NST) {
-  using C = SaStCfg<NT>;
+  using C = SaStCfg<NT, TS>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -312,8 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
   const uint32_t sSt = base;                                  // stage s: SB W boxes, then the A tile
   const uint32_t sBar = sSt + (uint32_t)NST * SBYTES;
 #define FULL(s) (sBar + 8u * (s))
-#define EMPTY(s) (sBar + 8u * (4 + (s)))
-  const uint32_t SITE = sBar + 8u * 8;
+#define EMPTY(s) (sBar + 8u * (C::MAXST + (s)))
+  const uint32_t SITE = sBar + 8u * (2 * C::MAXST);
   const uint32_t tslot = SITE + 8;
   const uint32_t sX = (tslot + 16 + 127u) & ~127u;
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
@@ -322,6 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NPAD = NT * p.n_ct;
+  // TMEM: G in [0, NPAD), then (TS) one 32-column A tile per stage
+  const uint32_t TCOLS = TS ? (NPAD + NST * 32 <= 256 ? 256u : 512u) : (uint32_t)NPAD;
   const long long n_cb = (p.B + kBM - 1) / kBM;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(FULL(s), 5); mbar_init(EMPTY(s), 1); }
@@ -329,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
-  if (warp == 1) tmem_alloc(tslot, (uint32_t)NPAD);
+  if (warp == 1) tmem_alloc(tslot, TCOLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -357,7 +370,9 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: one wait + one commit per K-block ----------------------------
-    if (lane == 0) {
+    // The whole warp runs the loop (warp-uniform descriptors live in uniform registers) and one
+    // elected lane issues; a single-lane loop pays register->uniform moves on every MMA.
+    {
       constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
       uint32_t n = 0;
       for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x)
@@ -369,17 +384,24 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
             mbar_wait(FULL(s), (n / NST) & 1u);
             tc_fence_after();
             const uint32_t st = sSt + s * SBYTES;
-            const uint64_t adesc = sw128_kmajor_desc(st + (uint32_t)SB * C::BOX);
-            for (int l = 0; l < L; ++l)
-              for (int h = 0; h < p.n_ct; ++h) {
-                const uint64_t bdesc = sw128_kmajor_desc(st + (uint32_t)(l * p.n_ct + h) * C::BOX);
+            const uint64_t adesc = TS ? 0ull : sw128_kmajor_desc(st + (uint32_t)SB * C::BOX);
+            const uint32_t a_t = tmem + (uint32_t)(NPAD + 32 * s);
+            if (elect_one()) {
+              for (int l = 0; l < L; ++l)
+                for (int h = 0; h < p.n_ct; ++h) {
+                  const uint64_t bdesc = sw128_kmajor_desc(st + (uint32_t)(l * p.n_ct + h) * C::BOX);
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k)
-                  umma_bf16_ss(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
-              }
-            umma_commit(EMPTY(s));
+                  for (int k = 0; k < kBK / 16; ++k) {
+                    if constexpr (TS) umma_bf16_ts(tmem + (uint32_t)(h * NT), a_t + 8u * k, bdesc + 2u * k, idesc, 1u);
+                    else umma_bf16_ss(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
+                  }
+                }
+              umma_commit(EMPTY(s));
+            }
+            __syncwarp();
           }
-          umma_commit(SITE);
+          if (elect_one()) umma_commit(SITE);
+          __syncwarp();
         }
     }
   } else {
@@ -456,13 +478,22 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
           uint32_t w[32];
           expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
           expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
-          const uint32_t rowaddr = sSt + s * SBYTES + (uint32_t)SB * C::BOX + (uint32_t)(row >> 3) * 1024u +
-                                   (uint32_t)(row & 7) * 128u;
+          if constexpr (TS) {
+            tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            st_shared_v4(rowaddr + (uint32_t)((c ^ (row & 7)) << 4), w[4 * c] ^ sgn, w[4 * c + 1] ^ sgn,
-                         w[4 * c + 2] ^ sgn, w[4 * c + 3] ^ sgn);
-          fence_async_smem();
+            for (int c = 0; c < 32; ++c) w[c] ^= sgn;
+            tmem_st32(lane_base + (uint32_t)(NPAD + 32 * s), w);
+            tmem_st_wait();
+            tc_fence_before();
+          } else {
+            const uint32_t rowaddr = sSt + s * SBYTES + (uint32_t)SB * C::BOX + (uint32_t)(row >> 3) * 1024u +
+                                     (uint32_t)(row & 7) * 128u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              st_shared_v4(rowaddr + (uint32_t)((c ^ (row & 7)) << 4), w[4 * c] ^ sgn, w[4 * c + 1] ^ sgn,
+                           w[4 * c + 2] ^ sgn, w[4 * c + 3] ^ sgn);
+            fence_async_smem();
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(FULL(s));
         }
@@ -484,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
 #undef EMPTY
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, (uint32_t)NPAD);
+  if (warp == 1) tmem_dealloc(tmem, TCOLS);
 }
 
 }  // namespace hobo
