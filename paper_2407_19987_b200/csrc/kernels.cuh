@@ -363,8 +363,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       PSTAT_FLUSH(6, w_tma);
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread): D[tmem] += A[tmem] * B[smem] ------------------
-    if (lane == 0) {
+    // ---------------- MMA issuer: D[tmem] += A[tmem] * B[smem] -------------------------------
+    // The whole warp runs the loop, so descriptors are warp-uniform and stay in uniform
+    // registers; one elected lane issues the MMAs and commits.
+    {
       constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
       int n = 0, snap = 0;
       uint32_t issued = 0;
@@ -378,43 +380,52 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           mbar_wait(FULL(st), (uint32_t)((n / NST) & 1));
           PT(stt[1] += clock64() - t0; stt[2] += 1; stt[3] += nkb; t0 = clock64();)
           tc_fence_after();
-          if constexpr (REAL) {   // one K-block: LA limb tiles of A x L limb boxes of W
-            for (int la = 0; la < p.LA; ++la) {
-              const uint32_t a_t = tmem + (uint32_t)(NT + st * ACOLS + la * C::A_COLS);
-              for (int l = 0; l < p.L; ++l) {
-                const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)l * C::BOX);
+          if (elect_one()) {
+            if constexpr (REAL) {   // one K-block: LA limb tiles of A x L limb boxes of W
+              for (int la = 0; la < p.LA; ++la) {
+                const uint32_t a_t = tmem + (uint32_t)(NT + st * ACOLS + la * C::A_COLS);
+                for (int l = 0; l < p.L; ++l) {
+                  const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)l * C::BOX);
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k)
-                  umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(la | l | k));
+                  for (int k = 0; k < kBK / 16; ++k)
+                    umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(la | l | k));
+                }
+              }
+            } else {
+              for (int q = 0; q < nkb; ++q) {
+                const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
+                for (int l = 0; l < p.L; ++l) {
+                  const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX);
+#pragma unroll
+                  for (int k = 0; k < kBK / 16; ++k)
+                    umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
+                }
               }
             }
-          } else {
-            for (int q = 0; q < nkb; ++q) {
-              const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
-              for (int l = 0; l < p.L; ++l) {
-                const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX);
-#pragma unroll
-                for (int k = 0; k < kBK / 16; ++k)
-                  umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
-              }
-            }
+            PT(stt[4] += clock64() - t0; t0 = clock64();)
+            umma_commit(EMPTY(st));
+            PT(stt[5] += clock64() - t0;)
           }
-          PT(stt[4] += clock64() - t0; t0 = clock64();)
-          umma_commit(EMPTY(st));
-          PT(stt[5] += clock64() - t0;)
+          __syncwarp();
           issued = 1;
         }
         if (snaps && j > 0) {  // hand the degree-(k-j) partial sum to the epilogue warps
-          if (issued) umma_commit(snap_full);
-          else mbar_arrive(snap_full);
+          if (elect_one()) {
+            if (issued) umma_commit(snap_full);
+            else mbar_arrive(snap_full);
+          }
+          __syncwarp();
           mbar_wait(snap_empty, (uint32_t)(snap & 1));
           tc_fence_after();
           ++snap;
         }
       }
-      if (issued) umma_commit(acc_full);
-      else mbar_arrive(acc_full);
-      PT(stt[0] = clock64() - t_start; for (int i = 0; i < 6; ++i) PSTAT_FLUSH(i, stt[i]);)
+      if (elect_one()) {
+        if (issued) umma_commit(acc_full);
+        else mbar_arrive(acc_full);
+      }
+      __syncwarp();
+      PT(if (lane == 0) { stt[0] = clock64() - t_start; for (int i = 0; i < 6; ++i) PSTAT_FLUSH(i, stt[i]); })
     }
   } else {
     // ---------------- A generator (warps 2..9), then epilogue --------------------------------
