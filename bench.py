@@ -382,9 +382,10 @@ def main():
     except Exception:
         pass
     import math
-    Npad = (N + 255) // 256 * 256
+    NTt = 128 if N <= 128 else 256                                  # the layout's column tile
+    Npad = (N + NTt - 1) // NTt * NTt
     Tpad = sum((math.comb(N, r - 1) + 63) // 64 * 64 for r in range(2, t.order + 1))
-    nct = Npad // 256
+    nct = Npad // NTt
     algo_bytes = (t.limbs * Npad * Tpad * 2 + B * ((N + 31) // 32) * 4 + (B * N * 4 if mode == "field" else B * 4)
                   + nct * B * 8)                                    # W once, X bits, G (or E), Q
     # below the ridge (few candidates per W byte) the W stream from HBM binds instead
@@ -396,11 +397,18 @@ def main():
             "achieved": achieved_b if hbm_bound else achieved, "peak": hbm_peak if hbm_bound else peak,
             "unit": "GB/s" if hbm_bound else "TFLOP/s",
             "frac": (achieved_b / hbm_peak) if hbm_bound else achieved / peak, "tflops_algorithmic": achieved,
-            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": "kr_gemm_kernel<256,2> (open-index contraction, field mode)",
+            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": f"kr_gemm_kernel<{NTt}> (open-index contraction, {mode} mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms, "launches_per_step": launches / max(1, a.steps),
             "algorithmic_flops_per_launch": algo_flops, "executed_mma_flops_per_launch": exec_flops,
             "executed_tflops": exec_flops / (kms / 1e3) / 1e12, "frac_of_sustained": achieved / sustained,
             "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s"}
+    # the tensor cores' own rate at this run's clock (4096 bf16 MAC/clk/SM, measured by
+    # tools/mma_ceiling.cu); the cuBLAS-measured burst above is taken on random operands,
+    # which toggle more than this path's {0,1} x small-integer operands, so frac can exceed 1
+    mhz = clocks.get("sm_mhz") or 1965.0
+    hw = 2 * 4096 * 148 * mhz * 1e6 / 1e12
+    roof["hw_nominal_tflops"] = hw
+    roof["frac_exec_of_hw_nominal"] = roof["executed_tflops"] / hw
 
     extras = {}
     if not a.no_extras:
