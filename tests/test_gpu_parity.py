@@ -323,7 +323,7 @@ def _p_bf16(torch, seed, B, N):
 
 @pytest.mark.parametrize("kind,order,N,B,seed", [("int", 3, 40, 300, 1), ("int", 2, 100, 129, 2), ("int", 4, 20, 200, 3),
                                                  ("u", 3, 130, 257, 4), ("u", 3, 512, 64, 5), ("u", 2, 300, 500, 6),
-                                                 ("cfg3", 3, 512, 1000, 7)])
+                                                 ("cfg3", 3, 512, 1000, 7), ("int", 3, 37, 131, 8)])   # odd N
 def test_multilinear_field(H, torch, kind, order, N, B, seed):
     from workloads import h  # noqa: F401
     if kind == "int":
