@@ -282,12 +282,18 @@ def main():
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
     cdev = dev if backend == "nccl" else None     # where the combine's key tensor lives
-    if world > 1:
+    # NCCL runs combine the per-rank bests inside the library (hobo_dist_init: ncclAllReduce on
+    # the compute stream); gloo runs (host-path tests) combine in Python.
+    # HOBO_BENCH_LIBCOMM=1 joins the library communicator even at world size 1.
+    lib_comm = backend == "nccl" and (world > 1 or os.environ.get("HOBO_BENCH_LIBCOMM") == "1")
+    if world > 1 or lib_comm:
         dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     from paper_2407_19987_b200 import HoboTensor, build
-    from paper_2407_19987_b200.dist import combine_best
+    from paper_2407_19987_b200.dist import combine_best, init_library_comm
     from workloads import x_bits
     build.build()
+    if lib_comm:
+        init_library_comm(dev_index)
 
     from paper_2407_19987_b200.dist import shard
     wl_text, factory, N, xseed, per_gpu, mode, scaling = CONFIGS[a.config]
@@ -320,7 +326,8 @@ def main():
         else:
             _, best = t.energy(Xd, E, row0=row0)
         if world > 1:
-            best = combine_best(best[0], best[1], device=cdev)
+            if not lib_comm:
+                best = combine_best(best[0], best[1], device=cdev)
         return best
 
     clk = ClockSampler(local).__enter__()
@@ -422,7 +429,8 @@ def main():
             s.record(stream)
             _, hb = t.local_field_host(Xh, Eh, row0=row0, stream=stream, fields=(mode == "field"))
             if world > 1:
-                hb = combine_best(hb[0], hb[1], device=cdev)
+                if not lib_comm:
+                    hb = combine_best(hb[0], hb[1], device=cdev)
             e.record(stream)
             e.synchronize()
             if i >= a.warmup:
@@ -502,7 +510,10 @@ def main():
         if "e2e" not in line:
             line["e2e"] = None
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if lib_comm:
+        from paper_2407_19987_b200 import hobo as _hobo
+        _hobo.dist_finalize()
+    if world > 1 or lib_comm:
         dist.destroy_process_group()
 
 

@@ -210,6 +210,26 @@ hobo_status hobo_sa_run(hobo_tensor* t, uint64_t seed, int64_t shots, int64_t sw
                         double t_start, double t_end, int64_t topk, uint8_t* x_host,
                         float* e_host, int64_t* count_host, int64_t* n_out, void* stream);
 
+/* ---- multi-GPU: one process per GPU, one NCCL communicator per
+ * process.  H is replicated (each rank builds its own handle); candidates / chains are
+ * sharded by the caller (row0) or, for hobo_search, by rank.  Once a communicator is
+ * initialised (any world size), every call that returns a `best` combines it over the ranks on
+ * the compute stream (C1: ncclAllReduce MIN of the packed 64-bit (E, global index) key)
+ * before reading it back, and hobo_search runs chains [lo_r, lo_{r+1}) of the global batch
+ * (lo_r = r*(batch/P) + min(r, batch%P)) and broadcasts the winner's bits from the rank that
+ * owns its chain (C2: ncclBroadcast).  All ranks must make the same calls in the same order
+ * (collectives).  Sample-set calls (hobo_*_samples, hobo_sa_run, hobo_gd_run) and the
+ * *_shard calls stay per rank.  libnccl.so.2 is loaded on first use (the process's own
+ * NCCL when one is already loaded).
+ * hobo_dist_unique_id: 128 bytes to hand from rank 0 to every rank (e.g. via
+ * torch.distributed.broadcast_object_list).  hobo_dist_init: makes `device` current and
+ * joins the communicator; HOBO_ESTATE if one exists.  hobo_dist_finalize: destroys it.
+ * hobo_dist_info: (rank, world), (0, 1) without a communicator.                            */
+hobo_status hobo_dist_unique_id(void* id_out);
+hobo_status hobo_dist_init(int rank, int world, const void* id, int device);
+hobo_status hobo_dist_finalize(void);
+hobo_status hobo_dist_info(int* rank, int* world);
+
 /* Launch statistics of the last call on this handle: number of kernel launches issued,
  * the executed tensor-core MACs of its contraction kernel(s), the algorithmic MACs
  * (DESIGN.md "Roofline"), and — when profiling is on — the CUDA-event time in ms of its

@@ -1,6 +1,8 @@
 // hobo_api.cu — the C ABI of include/hobo.h: device layouts, launches, search loop.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -27,6 +29,42 @@ hobo_status fail(hobo_status s, const std::string& msg) {
   g_err = msg;
   return s;
 }
+
+// ---- multi-GPU: one NCCL communicator per process, resolved with dlopen so
+// the library uses the NCCL already loaded in the process (torch's) or the system one ----
+struct Dist {
+  void* lib = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*err)(ncclResult_t) = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1, device = -1;
+};
+Dist g_dist;
+
+hobo_status nccl_load(std::string& msg) {
+  if (g_dist.lib) return HOBO_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) { msg = std::string("libnccl.so.2 not loadable: ") + dlerror(); return HOBO_ENCCL; }
+  g_dist.get_unique_id = (decltype(g_dist.get_unique_id))dlsym(h, "ncclGetUniqueId");
+  g_dist.init_rank = (decltype(g_dist.init_rank))dlsym(h, "ncclCommInitRank");
+  g_dist.all_reduce = (decltype(g_dist.all_reduce))dlsym(h, "ncclAllReduce");
+  g_dist.broadcast = (decltype(g_dist.broadcast))dlsym(h, "ncclBroadcast");
+  g_dist.destroy = (decltype(g_dist.destroy))dlsym(h, "ncclCommDestroy");
+  g_dist.err = (decltype(g_dist.err))dlsym(h, "ncclGetErrorString");
+  if (!g_dist.get_unique_id || !g_dist.init_rank || !g_dist.all_reduce || !g_dist.broadcast || !g_dist.destroy ||
+      !g_dist.err) {
+    msg = "libnccl.so.2 lacks a required symbol";
+    return HOBO_ENCCL;
+  }
+  g_dist.lib = h;
+  return HOBO_OK;
+}
+
+bool dist_active() { return g_dist.comm != nullptr; }   // world 1 runs the same path (identity collectives)
 
 struct DevLayout {
   bool built = false;
@@ -73,6 +111,7 @@ struct hobo_tensor {
   uint32_t* d_starts = nullptr; size_t starts_cap = 0;
   double* d_Qpart = nullptr; size_t Qpart_cap = 0;
   uint8_t* d_xh[2] = {nullptr, nullptr}; size_t xh_cap = 0;   // host-input path: staged X chunks
+  uint32_t* d_xbc = nullptr; size_t xbc_cap = 0;        // multi-GPU search: the winner's bits
   float* d_Eh = nullptr; size_t Eh_cap = 0;
   cudaStream_t cs = nullptr;                            // its copy stream
   cudaEvent_t ev_in = nullptr, ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
@@ -386,6 +425,14 @@ double algo_macs(hobo_tensor* t, bool field, long long B) {
   return s * (double)B;
 }
 
+// C1: the global lexicographic (E, idx) minimum over ranks, on the compute stream
+hobo_status key_allreduce(hobo_tensor* t, cudaStream_t s) {
+  if (!dist_active()) return HOBO_OK;
+  ncclResult_t r = g_dist.all_reduce(t->d_key, t->d_key, 1, ncclUint64, ncclMin, g_dist.comm, s);
+  if (r != ncclSuccess) return fail(HOBO_ENCCL, std::string("ncclAllReduce: ") + g_dist.err(r));
+  return HOBO_OK;
+}
+
 float key_energy(unsigned long long key) {
   uint32_t u = (uint32_t)(key >> 32) ^ 0x80000000u;
   int32_t i = (int32_t)u;
@@ -393,6 +440,34 @@ float key_energy(unsigned long long key) {
   float f;
   std::memcpy(&f, &i, 4);
   return f;
+}
+
+// the argmin key (device) -> host best, after the multi-GPU combine when one is active
+hobo_status finish_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
+  if (hobo_status st = key_allreduce(t, s)) return st;
+  unsigned long long key = 0;
+  CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (key == ~0ull) {
+    best->e = INFINITY;
+    best->idx = -1;
+  } else {
+    best->idx = (int64_t)(key & 0xFFFFFFFFull);
+    best->e = key_energy(key);
+  }
+  return HOBO_OK;
+}
+
+// an empty local batch still takes part in the combine (the other ranks wait for it)
+hobo_status empty_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
+  if (!best) return HOBO_OK;
+  if (!dist_active()) {
+    best->e = INFINITY;
+    best->idx = -1;
+    return HOBO_OK;
+  }
+  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  return finish_best(t, best, s);
 }
 
 hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
@@ -506,6 +581,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   for (int i = 0; i < 2; ++i)
     if (t->d_xh[i]) cudaFree(t->d_xh[i]);
   if (t->d_Eh) cudaFree(t->d_Eh);
+  if (t->d_xbc) cudaFree(t->d_xbc);
   if (t->d_sa_s) cudaFree(t->d_sa_s);
   if (t->d_sa_E) cudaFree(t->d_sa_E);
   void* ptrs[] = {t->d_tt, t->d_tt_meta, t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
@@ -547,10 +623,7 @@ hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row
     return fail(HOBO_EINVAL, "bad batch (B >= 0, X non-null, row0 + B < 2^32)");
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  if (B == 0) {
-    if (best) { best->e = INFINITY; best->idx = -1; }
-    return HOBO_OK;
-  }
+  if (B == 0) return empty_best(t, best, s);
   if (hobo_status st = contract(t, 0, X, B, nullptr, s)) return st;
   const DevLayout& L = t->lay[0];
   CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
@@ -558,13 +631,8 @@ hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row
       t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
   CK(cudaGetLastError());
   t->last_launches += 1;
-  if (best) {
-    unsigned long long key = 0;
-    CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    best->idx = (int64_t)(key & 0xFFFFFFFFull);
-    best->e = key_energy(key);
-  }
+  if (best)
+    if (hobo_status st = finish_best(t, best, s)) return st;
   return HOBO_OK;
 }
 
@@ -575,10 +643,7 @@ hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_
     return fail(HOBO_EINVAL, "bad batch (B >= 0, X and G non-null, row0 + B < 2^32)");
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  if (B == 0) {
-    if (best) { best->e = INFINITY; best->idx = -1; }
-    return HOBO_OK;
-  }
+  if (B == 0) return empty_best(t, best, s);
   if (hobo_status st = contract(t, 1, X, B, G, s)) return st;
   if (E || best) {
     const DevLayout& L = t->lay[1];
@@ -588,13 +653,8 @@ hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_
     CK(cudaGetLastError());
     t->last_launches += 1;
   }
-  if (best) {
-    unsigned long long key = 0;
-    CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    best->idx = (int64_t)(key & 0xFFFFFFFFull);
-    best->e = key_energy(key);
-  }
+  if (best)
+    if (hobo_status st = finish_best(t, best, s)) return st;
   return HOBO_OK;
 }
 
@@ -609,10 +669,7 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
     return fail(HOBO_EINVAL, "bad batch (B >= 0, X non-null, row0 + B < 2^32)");
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  if (B == 0) {
-    if (best) { best->e = INFINITY; best->idx = -1; }
-    return HOBO_OK;
-  }
+  if (B == 0) return empty_best(t, best, s);
   if (hobo_status st = ensure_layout(t, field)) return st;
   const DevLayout& L = t->lay[field];
   const int N = t->host.N;
@@ -660,12 +717,10 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
     launches += t->last_launches + 1;
     if (E_host) CK(cudaMemcpyAsync(E_host + off, t->d_Eh + off, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, s));
   }
-  unsigned long long key = 0;
-  if (best) CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
   if (best) {
-    best->idx = (int64_t)(key & 0xFFFFFFFFull);
-    best->e = key_energy(key);
+    if (hobo_status st = finish_best(t, best, s)) return st;
+  } else {
+    CK(cudaStreamSynchronize(s));
   }
   t->last_launches = launches;
   t->last_mma_macs = exec_macs(t, L, B);
@@ -1462,10 +1517,7 @@ hobo_status hobo_tt_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t 
     if (!t->d_tt_meta) CK(cudaMalloc(&t->d_tt_meta, 16 * sizeof(int)));
     CK(cudaMemcpy(t->d_tt_meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
-  if (B == 0) {
-    if (best) { best->e = INFINITY; best->idx = -1; }
-    return HOBO_OK;
-  }
+  if (B == 0) return empty_best(t, best, (cudaStream_t)stream);
   if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * W)) return st;
   const long long nw = B * W;
   pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, N, W, t->d_bits);
@@ -1500,18 +1552,103 @@ hobo_status hobo_tt_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t 
     search_best_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(E, B, row0, t->d_key);
     CK(cudaGetLastError());
     t->last_launches += 1;
-    unsigned long long key = 0;
-    CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    best->idx = (int64_t)(key & 0xFFFFFFFFull);
-    best->e = key_energy(key);
+    if (hobo_status st = finish_best(t, best, s)) return st;
   }
   return HOBO_OK;
 }
 
 hobo_status hobo_search(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t iters, uint8_t* x_best_host,
                         float* e_best_host, void* stream) {
-  return hobo_search_shard(t, seed, 0, batch, iters, 0.5, 0.005, x_best_host, e_best_host, nullptr, stream);
+  if (!dist_active())
+    return hobo_search_shard(t, seed, 0, batch, iters, 0.5, 0.005, x_best_host, e_best_host, nullptr, stream);
+  // multi-GPU: this rank's contiguous shard of the global chains (the first ranks take the
+  // remainder), C1 all-reduce(MIN) of the packed (E_best, chain) key, C2 broadcast of the
+  // winner's bits from the rank that owns its chain.  Per-chain RNG streams are keyed by the
+  // global chain id, so the result equals the single-GPU search.
+  if (!t) return fail(HOBO_EINVAL, "null handle");
+  if (batch < 1 || batch > (int64_t)0xFFFFFFFF) return fail(HOBO_EINVAL, "bad search batch");
+  if (hobo_status st = check_device(t)) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int R = g_dist.rank, P = g_dist.world;
+  auto lo_of = [&](int r) { return r * (batch / P) + std::min<int64_t>(r, batch % P); };
+  const int64_t lo = lo_of(R), n = lo_of(R + 1) - lo;
+  const int N = t->host.N, W = t->W;
+  int64_t launches = 0;
+  if (n > 0) {
+    if (hobo_status st = run_search(t, seed, lo, n, iters, 0.5, 0.005, s, launches)) return st;
+  } else if (hobo_status st = check_device(t)) {
+    return st;
+  }
+  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  if (n > 0) {
+    search_best_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_ebest, n, lo,
+                                                                                               t->d_key);
+    CK(cudaGetLastError());
+    ++launches;
+  }
+  hobo_best b;
+  if (hobo_status st = finish_best(t, &b, s)) return st;   // C1 (synchronises the stream)
+  const int64_t c = b.idx;
+  int owner = 0;
+  while (owner + 1 < P && lo_of(owner + 1) <= c) ++owner;
+  if (hobo_status st = grow(t, t->d_xbc, t->xbc_cap, (size_t)W)) return st;
+  if (R == owner)
+    CK(cudaMemcpyAsync(t->d_xbc, t->d_xbest + (size_t)(c - lo) * W, (size_t)W * 4, cudaMemcpyDeviceToDevice, s));
+  ncclResult_t r = g_dist.broadcast(t->d_xbc, t->d_xbc, (size_t)W * 4, ncclUint8, owner, g_dist.comm, s);   // C2
+  if (r != ncclSuccess) return fail(HOBO_ENCCL, std::string("ncclBroadcast: ") + g_dist.err(r));
+  std::vector<uint32_t> xb(W);
+  CK(cudaMemcpyAsync(xb.data(), t->d_xbc, (size_t)W * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (x_best_host)
+    for (int m = 0; m < N; ++m) x_best_host[m] = (uint8_t)((xb[m >> 5] >> (m & 31)) & 1u);
+  if (e_best_host) *e_best_host = b.e;
+  t->last_launches = launches + 2;
+  return HOBO_OK;
+}
+
+hobo_status hobo_dist_unique_id(void* id_out) {
+  if (!id_out) return fail(HOBO_EINVAL, "null id buffer");
+  std::string msg;
+  if (hobo_status st = nccl_load(msg)) return fail(st, msg);
+  ncclUniqueId id;
+  ncclResult_t r = g_dist.get_unique_id(&id);
+  if (r != ncclSuccess) return fail(HOBO_ENCCL, std::string("ncclGetUniqueId: ") + g_dist.err(r));
+  std::memcpy(id_out, &id, sizeof(id));
+  return HOBO_OK;
+}
+
+hobo_status hobo_dist_init(int rank, int world, const void* id, int device) {
+  if (world < 1 || rank < 0 || rank >= world || !id || device < 0) return fail(HOBO_EINVAL, "bad rank / world / id / device");
+  if (g_dist.comm) return fail(HOBO_ESTATE, "a communicator is already initialised (hobo_dist_finalize first)");
+  std::string msg;
+  if (hobo_status st = nccl_load(msg)) return fail(st, msg);
+  if (cudaSetDevice(device) != cudaSuccess) return fail(HOBO_ECUDA, "cudaSetDevice failed");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = g_dist.init_rank(&comm, world, uid, rank);
+  if (r != ncclSuccess) return fail(HOBO_ENCCL, std::string("ncclCommInitRank: ") + g_dist.err(r));
+  g_dist.comm = comm;
+  g_dist.rank = rank;
+  g_dist.world = world;
+  g_dist.device = device;
+  return HOBO_OK;
+}
+
+hobo_status hobo_dist_finalize(void) {
+  if (!g_dist.comm) return HOBO_OK;
+  ncclResult_t r = g_dist.destroy(g_dist.comm);
+  g_dist.comm = nullptr;
+  g_dist.rank = 0;
+  g_dist.world = 1;
+  if (r != ncclSuccess) return fail(HOBO_ENCCL, std::string("ncclCommDestroy: ") + g_dist.err(r));
+  return HOBO_OK;
+}
+
+hobo_status hobo_dist_info(int* rank, int* world) {
+  if (rank) *rank = g_dist.comm ? g_dist.rank : 0;
+  if (world) *world = g_dist.comm ? g_dist.world : 1;
+  return HOBO_OK;
 }
 
 hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mma_macs, double* algo,

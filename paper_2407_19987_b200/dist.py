@@ -78,3 +78,18 @@ def search_sharded(t, seed: int, total_chains: int, iters: int, rank: int, world
     ge, gc = combine_best(e, c, device=device)
     xb = broadcast_x(x, owner_of(gc, total_chains, world), t.N, device=device)
     return xb, ge, gc
+
+
+def init_library_comm(device_index: int, group=None):
+    """Join the C library's own NCCL communicator (hobo_dist_init) using an initialised
+    torch.distributed group for the bootstrap: rank 0 creates the 128-byte unique id and
+    broadcasts it.  Afterwards every `best` the library returns is already global (C1)
+    and hobo_search shards its chains by rank (C1 + C2)."""
+    import torch.distributed as dist
+
+    from . import hobo
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [hobo.dist_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    hobo.dist_init(rank, world, obj[0], device_index)
+    return rank, world

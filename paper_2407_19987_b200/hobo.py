@@ -19,7 +19,8 @@ EXPORTED = [
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field", "hobo_local_field_host", "hobo_energy_host",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
     "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats",
-    "hobo_set_profiling", "hobo_last_error",
+    "hobo_set_profiling", "hobo_dist_unique_id", "hobo_dist_init", "hobo_dist_finalize", "hobo_dist_info",
+    "hobo_last_error",
 ]
 
 
@@ -69,6 +70,10 @@ def lib():
         L.hobo_sa_run.argtypes = [P, U64, I64, I64, D, D, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_last_launch_stats.argtypes = [P, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]
         L.hobo_set_profiling.argtypes = [P, I]
+        L.hobo_dist_unique_id.argtypes = [P]
+        L.hobo_dist_init.argtypes = [I, I, P, I]
+        L.hobo_dist_finalize.argtypes = []
+        L.hobo_dist_info.argtypes = [C.POINTER(I), C.POINTER(I)]
         L.hobo_last_error.restype = C.c_char_p
         for name in EXPORTED:
             if name != "hobo_last_error":
@@ -253,6 +258,14 @@ class HoboTensor:
                                        C.byref(c), _stream_handle(stream)))
         return x, e.value, c.value
 
+    def search_global(self, seed, batch, iters, stream=None):
+        """hobo_search: the global batch of chains; with a library communicator (dist_init) the
+        chains are sharded by rank and the winner combined over ranks.  Returns (x u8[N], e)."""
+        x = np.zeros(self.N, np.uint8)
+        e = C.c_float()
+        _check(lib().hobo_search(self._h, seed, batch, iters, _np_ptr(x), C.byref(e), _stream_handle(stream)))
+        return x, e.value
+
     def search_samples(self, seed, batch, iters, topk=10, stream=None):
         """hobo_search_samples: list of (x u8[N], energy, occurrence), the paper's result format."""
         x = np.zeros((topk, self.N), np.uint8)
@@ -332,3 +345,25 @@ class HoboTensor:
         n, mm, am, ms = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
         _check(lib().hobo_last_launch_stats(self._h, C.byref(n), C.byref(mm), C.byref(am), C.byref(ms)))
         return dict(launches=n.value, mma_macs=mm.value, algo_macs=am.value, kernel_ms=ms.value)
+
+
+# ---- multi-GPU communicator of the library (include/hobo.h) ------------------
+def dist_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().hobo_dist_unique_id(buf))
+    return buf.raw
+
+
+def dist_init(rank: int, world: int, uid: bytes, device: int):
+    buf = C.create_string_buffer(bytes(uid), 128)
+    _check(lib().hobo_dist_init(rank, world, buf, device))
+
+
+def dist_finalize():
+    _check(lib().hobo_dist_finalize())
+
+
+def dist_info():
+    r, w = C.c_int(), C.c_int()
+    _check(lib().hobo_dist_info(C.byref(r), C.byref(w)))
+    return r.value, w.value

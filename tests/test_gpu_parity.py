@@ -521,3 +521,36 @@ def test_host_entry_points_match_device_path(H, torch):
         assert np.array_equal(Eh, E.cpu().numpy()) and besth == best
         Eh2, besth2 = t.energy_host(src, row0=row0)
         assert np.array_equal(Eh2, Ed.cpu().numpy()) and besth2 == bestd
+
+
+
+# ---- the library's own NCCL communicator (hobo_dist_*), exercised at world size 1 -----------
+def test_library_comm_world1_matches_single_gpu(H, torch):
+    """With a communicator every best goes through ncclAllReduce(MIN) and hobo_search through
+    the rank-sharded path + ncclBroadcast; at world 1 those are identities, so every result
+    equals the communicator-free call and the oracle replay."""
+    p = random_integer_problem(3, 40, 77, nterms=500)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    ref_x, ref_e = t.search_global(9, 300, 20)
+    r = o.search(9, 0, 300, 20)
+    assert ref_e == r["e_best"] and np.array_equal(ref_x, r["chain_xbest"][r["best_chain"]])
+    Xh = x_bits(5, 1000, 40)
+    X = dev(torch, Xh)
+    _, ref_b = t.energy(X, row0=3)
+    dev_index = torch.cuda.current_device()
+    uid = H.dist_unique_id()
+    H.dist_init(0, 1, uid, dev_index)
+    try:
+        assert H.dist_info() == (0, 1)
+        with pytest.raises(H.HoboError) as e:
+            H.dist_init(0, 1, uid, dev_index)
+        assert e.value.status == H.HOBO_ESTATE
+        x, e = t.search_global(9, 300, 20)
+        assert e == ref_e and np.array_equal(x, ref_x)
+        assert t.energy(X, row0=3)[1] == ref_b
+        assert t.local_field(X, row0=3, want_best=True)[2] == ref_b
+        assert t.local_field_host(Xh, row0=3)[1] == ref_b
+        assert t.energy(X[:0])[1] == (float("inf"), -1)
+    finally:
+        H.dist_finalize()
+    assert H.dist_info() == (0, 1)

@@ -138,3 +138,14 @@ def test_tt_build_reproduces_paper_core_shapes(H, pins):
     r = t.tt_build(0.0)
     shapes = [[6, r[1]]] + [[r[p], 6, r[p + 1]] for p in range(1, 5)] + [[r[5], 6]]
     assert shapes == pins["tt_core_shapes_tsp"]["value"] and r[0] == r[6] == 1
+
+
+def test_dist_entry_points_validate_arguments(H):
+    """Multi-GPU communicator calls: argument checks happen before any NCCL or CUDA work."""
+    assert H.dist_info() == (0, 1)
+    for rank, world in ((1, 1), (-1, 2), (0, 0)):
+        with pytest.raises(H.HoboError) as e:
+            H.dist_init(rank, world, bytes(128), 0)
+        assert e.value.status == H.HOBO_EINVAL
+    H.dist_finalize()                      # no communicator: a no-op
+    assert H.dist_info() == (0, 1)
