@@ -554,3 +554,38 @@ def test_library_comm_world1_matches_single_gpu(H, torch):
     finally:
         H.dist_finalize()
     assert H.dist_info() == (0, 1)
+
+
+# ---- edge cases of every batch entry point --------------------------------------------------
+def test_empty_batches_and_argument_errors(H, torch):
+    p = random_integer_problem(3, 24, 5, nterms=200)
+    t = H.HoboTensor.from_problem(p)
+    X0 = torch.empty(0, t.N, dtype=torch.uint8, device="cuda")
+    none = (float("inf"), -1)
+    assert t.energy(X0)[1] == none
+    assert t.local_field(X0, want_best=True)[2] == none
+    assert t.local_field_host(np.zeros((0, t.N), np.uint8))[1] == none
+    assert t.energy_host(np.zeros((0, t.N), np.uint8))[1] == none
+    with pytest.raises(H.HoboError) as e:                 # TT energies before the TT cores exist
+        t.tt_energy(X0)
+    assert e.value.status == H.HOBO_ESTATE
+    t.tt_build(0.0)
+    assert t.tt_energy(X0)[1] == none
+    G, E = t.multilinear_field(torch.empty(0, t.N, dtype=torch.bfloat16, device="cuda"))
+    assert G.shape == (0, t.N)
+    # annealing and search arguments (0 < t_end <= t_start, >= 1 chain / shot, step > 0)
+    for bad in (lambda: t.sa_shard(1, 0, 10, 2, 1.0, 2.0), lambda: t.sa_shard(1, 0, 0, 2, 2.0, 1.0),
+                lambda: t.sa_shard(1, 0, 10, 2, 0.0, 0.0), lambda: t.sa_run(1, 0, 2),
+                lambda: t.search(1, 0, 4), lambda: t.gd_run(1, 16, 4, 0.0),
+                lambda: t.search_global(1, 0, 4)):
+        with pytest.raises(H.HoboError) as e:
+            bad()
+        assert e.value.status == H.HOBO_EINVAL
+    # device path limit: N <= 1024
+    from workloads import TermBuilder
+    tb = TermBuilder()
+    tb.add(1.0, [(0.0, [(0, 1.0)]), (0.0, [(1024, 1.0)])])
+    big = H.HoboTensor.from_problem(tb.problem(2, 1025))
+    with pytest.raises(H.HoboError) as e:
+        big.energy(torch.zeros(1, 1025, dtype=torch.uint8, device="cuda"))
+    assert e.value.status == H.HOBO_EINVAL
