@@ -132,7 +132,9 @@ hobo_status hobo_energy_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, i
  *   P_dev        device bf16 (raw 16-bit patterns), row-major B x N.  The products of up to
  *                three bf16 values are exact in fp32 and are split exactly into bf16 limbs,
  *                so the result is the gradient AT the bf16 p (fp32 accumulation).
- * Requires N <= 512 (p rows are staged in shared memory) at L = 1.                       */
+ * The p rows are staged in shared memory next to the W ring: N up to ~800 (HOBO_EINVAL
+ * beyond); when 256-column W boxes do not fit beside them (e.g. N = 512 at L = 3) the call
+ * uses a copy of the field layout with 128-column tiles (one-time extra device memory).    */
 hobo_status hobo_multilinear_field(hobo_tensor* t, const uint16_t* P_dev, int64_t B, float* G_dev,
                                    float* E_dev, void* stream);
 

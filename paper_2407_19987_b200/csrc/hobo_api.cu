@@ -91,7 +91,8 @@ struct hobo_tensor {
   uint32_t* d_runoff = nullptr;
   float* d_p1 = nullptr;   // padded to 256-multiples
   int W = 0;               // 32-bit words per candidate bit row
-  DevLayout lay[2];        // 0 = energy (strict), 1 = field (open index)
+  DevLayout lay[3];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
+                           // tiles for the real-valued path (p rows + a deeper W ring in smem)
   // scratch (grown on demand)
   uint32_t* d_bits = nullptr; size_t bits_cap = 0;
   double* d_Q = nullptr; size_t Q_cap = 0;
@@ -275,12 +276,13 @@ hobo_status init_device(hobo_tensor* t) {
 }
 
 // builds W (bf16 limb planes) of one layout on the device, plus its TMA map and schedule
-hobo_status ensure_layout(hobo_tensor* t, int field) {
-  DevLayout& L = t->lay[field];
+hobo_status ensure_layout(hobo_tensor* t, int slot) {
+  DevLayout& L = t->lay[slot];
   if (L.built) return HOBO_OK;
+  const int field = slot != 0;
   const HostTensor& H = t->host;
   const int N = H.N, k = H.order;
-  L.NT = N <= 128 ? 128 : 256;     // a 128-column tile when N fits (no padded columns)
+  L.NT = (N <= 128 || slot == 2) ? 128 : 256;   // a 128-column tile when N fits (no padded columns)
   if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
   L.n_ct = (N + L.NT - 1) / L.NT;
   L.Npad = L.n_ct * L.NT;
@@ -386,7 +388,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.pstride = 0;
   p.nseg = t->kl.nseg;
   p.L = t->host.limbs;
-  p.field_mode = (&L == &t->lay[1]) ? 1 : 0;
+  p.field_mode = (&L == &t->lay[0]) ? 0 : 1;
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
   p.dbg = 0;
@@ -470,10 +472,21 @@ hobo_status empty_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
   return finish_best(t, best, s);
 }
 
+// layout slot of the real-valued path: the field layout, or, when its p rows plus L limb
+// boxes of 256 columns do not fit in shared memory (e.g. N = 512 at L = 3), the same layout
+// with 128-column tiles (half-size boxes).  (128-column tiles everywhere measured 1.8x slower
+// at cfg3: twice the CTAs generate A.)
+int real_slot(hobo_tensor* t) {
+  if (t->host.N <= 128) return 1;
+  int ps = 0, ring = 0, la = 0;
+  return real_geometry(t, 256, ps, ring, la) ? 1 : 2;
+}
+
 hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
                      const uint16_t* P = nullptr) {
-  if (hobo_status st = ensure_layout(t, field)) return st;
-  const DevLayout& L = t->lay[field];
+  const int slot = P ? real_slot(t) : field;
+  if (hobo_status st = ensure_layout(t, slot)) return st;
+  const DevLayout& L = t->lay[slot];
   if (hobo_status st = grow(t, t->d_Q, t->Q_cap, (size_t)B * L.n_ct)) return st;
   if (!P) {
     if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * t->W)) return st;
@@ -799,7 +812,7 @@ hobo_status hobo_multilinear_field(hobo_tensor* t, const uint16_t* P, int64_t B,
   if (B == 0) return HOBO_OK;
   if (hobo_status st = contract(t, 1, nullptr, B, G, s, P)) return st;
   if (E) {
-    const DevLayout& L = t->lay[1];
+    const DevLayout& L = t->lay[real_slot(t)];
     finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_Q, L.n_ct, B, L.lcm, 0,
                                                                                           E, nullptr);
     CK(cudaGetLastError());

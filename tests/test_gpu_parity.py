@@ -336,12 +336,7 @@ def test_multilinear_field(H, torch, kind, order, N, B, seed):
         idx, val = uniform_cells(order, N, seed)
         t, o = H.HoboTensor.import_cells(order, N, idx, val), Oracle.from_cells(order, N, idx, val)
     Pd, P = _p_bf16(torch, seed, B, N)
-    if t.limbs > 1 and N > 300:   # p rows + a 3-limb W ring exceed shared memory: documented EINVAL
-        with pytest.raises(H.HoboError) as e:
-            t.multilinear_field(Pd)
-        assert e.value.status == H.HOBO_EINVAL
-        return
-    G, E = t.multilinear_field(Pd)
+    G, E = t.multilinear_field(Pd)   # N=512 at L=3 runs on the 128-column-tile layout
     torch.cuda.synchronize()
     Gr, Er = o.mfield(P), o.menergy(P)
     assert np.max(np.abs(G.cpu().numpy() - Gr)) <= o.tau
