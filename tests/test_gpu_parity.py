@@ -422,6 +422,8 @@ SA_CASES = {
     "o2n600": lambda: random_integer_problem(2, 600, 34, 900),  # N > 512: the per-site launch path
     "o3n520": lambda: random_integer_problem(3, 520, 35, 900),
     "wide3limb": _wide_int_problem,
+    "o3n300": lambda: random_integer_problem(3, 300, 37, 700),  # two column tiles (box ring)
+    "o2n400": lambda: random_integer_problem(2, 400, 38, 700),
 }
 
 
