@@ -220,12 +220,16 @@ def cpu_baseline(seconds=12.0):
     from workloads import cfg3_problem, x_bits
     o = Oracle.from_problem(cfg3_problem())
     cores = os.cpu_count() or 1
-    S = cores * 2
-    X = x_bits(3, S, 512)
-    t0 = time.perf_counter()
-    o.field(X, nthreads=cores)
-    o.energy(X, nthreads=cores)
-    dt = time.perf_counter() - t0
+    S, dt = cores * 2, 0.0
+    while S < 65536:                       # calibrate on a sample long enough to amortise start-up
+        X = x_bits(3, S, 512)
+        t0 = time.perf_counter()
+        o.field(X, nthreads=cores)
+        o.energy(X, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if dt >= 1.5:
+            break
+        S = min(65536, S * 4)
     S2 = int(min(65536, max(S, S * seconds / max(dt, 1e-3))))
     X = x_bits(3, S2, 512)
     t0 = time.perf_counter()
