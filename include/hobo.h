@@ -70,6 +70,13 @@ hobo_status hobo_tensor_build(int order, int N, const hobo_term* terms, size_t n
 hobo_status hobo_tensor_import_cells(int order, int N, int64_t ncells, const int32_t* idx,
                                      const float* val, hobo_tensor** out);
 
+/* hobo_tensor_import_dense — SURVEY 8(b) dense import: a host tensor of N^order fp32
+ * cells, row-major with the last index fastest (the layout hobo_tensor_export_dense writes).
+ * Every nonzero cell is added to the canonical cell of its index SET (as in
+ * hobo_tensor_import_cells), so energies on binary x are unchanged.  N^order <= 2^28 cells
+ * (HOBO_ENOMEM otherwise); other errors as hobo_tensor_import_cells.                      */
+hobo_status hobo_tensor_import_dense(int order, int N, const float* dense_host, hobo_tensor** out);
+
 /* hobo_tensor_import_colex — the canonical cells themselves (the upper-triangular tensor
  * without its replicated copies): cells_by_degree[r-1] is a host float array of
  * C(N, r) entries, entry colex_rank(S) = sum_i C(s_i, i) holding c(S) for the r-subset

@@ -557,6 +557,28 @@ hobo_status hobo_tensor_import_cells(int order, int N, int64_t ncells, const int
   return HOBO_OK;
 }
 
+hobo_status hobo_tensor_import_dense(int order, int N, const float* dense, hobo_tensor** out) {
+  if (!out || !dense) return fail(HOBO_EINVAL, "null argument");
+  if (order < 1 || order > 6 || N < 1) return fail(HOBO_EINVAL, "order must be in 1..6 and N >= 1");
+  const double cells = std::pow((double)N, order);
+  if (cells > (double)(1u << 28)) return fail(HOBO_ENOMEM, "dense import limited to N^order <= 2^28 cells");
+  // every nonzero cell (row-major, last index fastest) goes to the canonical cell of its index SET
+  std::vector<int32_t> idx;
+  std::vector<float> val;
+  std::vector<int32_t> ix(order, 0);
+  for (int64_t lin = 0; lin < (int64_t)cells; ++lin) {
+    if (dense[lin] != 0.0f) {
+      idx.insert(idx.end(), ix.begin(), ix.end());
+      val.push_back(dense[lin]);
+    }
+    for (int p = order - 1; p >= 0; --p) {   // odometer increment of the index tuple
+      if (++ix[p] < N) break;
+      ix[p] = 0;
+    }
+  }
+  return hobo_tensor_import_cells(order, N, (int64_t)val.size(), idx.data(), val.data(), out);
+}
+
 hobo_status hobo_tensor_import_colex(int order, int N, const float* const* cells_by_degree, hobo_tensor** out) {
   if (!out) return fail(HOBO_EINVAL, "null output handle");
   std::unique_ptr<hobo_tensor> t(new hobo_tensor());

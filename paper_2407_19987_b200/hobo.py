@@ -15,7 +15,7 @@ HOBO_OK, HOBO_EINVAL, HOBO_ERANGE, HOBO_ENOMEM, HOBO_ECUDA, HOBO_ENCCL, HOBO_EST
 _STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
 
 EXPORTED = [
-    "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_free", "hobo_tensor_info",
+    "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_import_dense", "hobo_tensor_free", "hobo_tensor_info",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field", "hobo_local_field_host", "hobo_energy_host",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
     "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats",
@@ -49,6 +49,7 @@ def lib():
         L.hobo_tensor_build.argtypes = [I, I, P, SZ, P, P, C.POINTER(P), C.POINTER(D)]
         L.hobo_tensor_import_cells.argtypes = [I, I, I64, P, P, C.POINTER(P)]
         L.hobo_tensor_import_colex.argtypes = [I, I, P, C.POINTER(P)]
+        L.hobo_tensor_import_dense.argtypes = [I, I, P, C.POINTER(P)]
         L.hobo_tensor_free.argtypes = [P]
         L.hobo_tensor_info.argtypes = [P, C.POINTER(I), C.POINTER(I), C.POINTER(I64), C.POINTER(I),
                                        C.POINTER(D), C.POINTER(I), C.POINTER(D)]
@@ -151,6 +152,16 @@ class HoboTensor:
         ptrs = (C.c_void_p * order)(*[a.ctypes.data for a in arrs])
         h = C.c_void_p()
         _check(lib().hobo_tensor_import_colex(order, N, C.cast(ptrs, C.c_void_p), C.byref(h)))
+        return cls(h, 0.0)
+
+    @classmethod
+    def import_dense(cls, order, N, dense):
+        """A dense N^order fp32 tensor (row-major, last index fastest), canonicalised by index set."""
+        d = np.ascontiguousarray(dense, np.float32).reshape(-1)
+        if d.size != N ** order:
+            raise ValueError(f"expected {N}^{order} cells")
+        h = C.c_void_p()
+        _check(lib().hobo_tensor_import_dense(order, N, d.ctypes.data, C.byref(h)))
         return cls(h, 0.0)
 
     def close(self):

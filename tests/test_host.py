@@ -149,3 +149,26 @@ def test_dist_entry_points_validate_arguments(H):
         assert e.value.status == H.HOBO_EINVAL
     H.dist_finalize()                      # no communicator: a no-op
     assert H.dist_info() == (0, 1)
+
+
+@pytest.mark.parametrize("maker", [tsp, lambda: seating(4), lambda: random_integer_problem(3, 12, 2, 150)])
+def test_import_dense_round_trip(H, maker):
+    """Export the dense N^k tensor, import it back: the same canonical cells, bit for bit."""
+    p = maker()
+    t = H.HoboTensor.from_problem(p)
+    back = H.HoboTensor.import_dense(t.order, t.N, t.dense())
+    i1, v1 = t.cells()
+    i2, v2 = back.cells()
+    assert np.array_equal(i1, i2) and np.array_equal(v1.view(np.uint32), v2.view(np.uint32))
+
+
+def test_import_dense_canonicalises_like_the_oracle(H):
+    """A raw (non-canonical) dense tensor: every cell lands on the canonical cell of its index
+    set, the same cells the oracle builds from the same raw cells."""
+    rng = np.random.default_rng(9)
+    order, N = 3, 7
+    dense = np.where(rng.random((N,) * order) < 0.2, rng.integers(-5, 6, (N,) * order), 0).astype(np.float32)
+    t = H.HoboTensor.import_dense(order, N, dense)
+    nz = np.argwhere(dense != 0).astype(np.int32)
+    o = Oracle.from_cells(order, N, nz, dense[tuple(nz.T)])
+    _same_cells(t, o)
