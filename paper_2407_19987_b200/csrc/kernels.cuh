@@ -391,6 +391,15 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
                     umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(la | l | k));
                 }
               }
+            } else if (p.L == 1 && nkb == 2 && KPS == 2) {   // the common stage, fully unrolled
+              const uint32_t a_t = tmem + (uint32_t)(NT + st * 2 * C::A_COLS);
+              const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes);
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                  umma_bf16_ts(tmem, a_t + (uint32_t)(q * C::A_COLS) + 8u * k,
+                               bdesc + (uint64_t)((q * C::BOX) >> 4) + 2u * k, idesc, issued | (uint32_t)(q | k));
             } else {
               for (int q = 0; q < nkb; ++q) {
                 const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
