@@ -73,6 +73,7 @@ struct DevLayout {
   int2* d_sched = nullptr;
   std::vector<int32_t> sched;
   alignas(64) CUtensorMap tmap;
+  alignas(64) CUtensorMap tmap_half;   // CTA pairs: NT/2-row boxes (each CTA loads its half)
   double lcm = 1.0;
   double wdeg[8] = {1, 1, 1, 1, 1, 1, 1, 1};
   double wp = 1.0;
@@ -207,7 +208,46 @@ cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) 
   return cudaGetLastError();
 }
 
+// CTA pairs: clusters of 2 (adjacent candidate blocks of one column tile), cta_group::2 MMAs
+template <int NT>
+cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  auto* k = kr_gemm_kernel<NT, false, false, true>;
+  const size_t smem = KrCfg<NT>::smem_bytes(p.W);
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, L.tmap_half, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// CTA pairs for 256-column tiles at L >= 2 with long K loops (measured: cfg3-fp32 +19%, cfg5
+// +12%); at L = 1 the single-CTA kernel is 5% faster (cfg3), and short K loops (cfg2's QUBO,
+// 4-16 K-blocks per CTA) do not amortise the pair's cluster synchronisation (-8%).
+// HOBO_PAIR=1 / =0 forces the choice (A/B runs, tests of both paths).
+bool use_pairs(const DevLayout& L, const KrParams& p) {
+  if (p.preal || p.n_split != 1 || L.NT != 256) return false;
+  if (const char* e = getenv("HOBO_PAIR")) return e[0] == '1';
+  return p.L >= 2 && p.n_kb >= 64;
+}
+
 cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  if (use_pairs(L, p)) return launch_kr_pair<256>(L, p, s);
   if (L.NT == 128) return p.preal ? launch_kr<128, true>(L, p, s) : launch_kr<128, false>(L, p, s);
   return p.preal ? launch_kr<256, true>(L, p, s) : launch_kr<256, false>(L, p, s);
 }
@@ -346,6 +386,11 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   CUresult cr = enc(&L.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.W, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+  cuuint32_t box_half[3] = {(cuuint32_t)kBK, (cuuint32_t)(L.NT / 2), 1};
+  cr = enc(&L.tmap_half, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.W, dims, strides, box_half, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
   L.sched = schedule(t->kl, L.NT, L.n_ct, field != 0);
   CK(cudaMalloc(&L.d_sched, L.sched.size() * sizeof(int32_t)));

@@ -65,7 +65,7 @@ template <int NT>
 struct KrCfg {
   static constexpr int BOX = NT * 128;                   // one TMA box: NT rows x 64 bf16 (SW128)
   static constexpr int RING_BOXES = 6 * 256 / NT;        // shared-memory budget for W (192 KB), in boxes
-  static constexpr int MAXST = NT >= 256 ? 3 : 6;        // max pipeline stages
+  static constexpr int MAXST = NT >= 256 ? 4 : 6;        // max pipeline stages (4 at NT=256: CTA pairs' half boxes)
   static constexpr int A_COLS = kBK / 2;                 // TMEM columns of one K-block of A (64 bf16 / lane)
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator, then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
@@ -210,8 +210,13 @@ __device__ unsigned long long g_pipe_stats[8192][8];
 // Ring slot s holds the stage's W boxes in shared memory and its A K-blocks in TMEM;
 // FULL(s) completes when the 8 generator warps arrived and the TMA bytes landed, EMPTY(s)
 // when the MMAs reading the slot completed (one tcgen05.commit).
-template <int NT, bool REAL, bool SA = false>
+// PAIR: the two CTAs of a cluster (launched with cluster dimension 2) take adjacent candidate
+// blocks of one column tile and share every W box: each loads half of its NT rows, the
+// leader issues cta_group::2 MMAs (M = 256: 128 rows of A in each CTA's TMEM), so one MMA
+// instruction covers both SMs and each SM's shared memory carries half the W stream.
+template <int NT, bool REAL, bool SA = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
+  static_assert(!(PAIR && (REAL || SA)), "CTA pairs: binary contraction only");
   using C = KrCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -234,13 +239,20 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // block order: candidate block fastest, then column tile, then K split (concurrent CTAs
-  // share W tiles in L2)
-  const int cb = blockIdx.x % p.n_cb;
-  const int ct = (blockIdx.x / p.n_cb) % p.n_ct;
-  const int split = blockIdx.x / (p.n_cb * p.n_ct);
+  // share W tiles in L2); pairs: cluster c holds candidate blocks 2c', 2c'+1 of one tile
+  const uint32_t prank = PAIR ? cluster_ctarank() : 0u;
+  const bool leader = !PAIR || prank == 0;
+  const int ncb_eff = PAIR ? (p.n_cb + 1) / 2 : p.n_cb;
+  const int bid = PAIR ? (int)(blockIdx.x / 2) : (int)blockIdx.x;
+  const int cb = PAIR ? 2 * (bid % ncb_eff) + (int)prank : bid % ncb_eff;
+  const int ct = (bid / ncb_eff) % p.n_ct;
+  const int split = bid / (ncb_eff * p.n_ct);
   const long long b0 = (long long)cb * kBM;
+  constexpr uint32_t BOXB = PAIR ? C::BOX / 2 : C::BOX;   // shared-memory bytes of one W box per CTA
   const int KPS = REAL ? 1 : C::kps(p.L);
-  const int NST = REAL ? C::nst_real(p.L, p.LA, ring) : C::nst(p.L);
+  // CTA pairs hold half boxes, so the same ring fits twice the stages (TMEM: 256 + 4 x 64 columns)
+  const int NST = REAL ? C::nst_real(p.L, p.LA, ring)
+                       : (PAIR ? min(2 * C::RING_BOXES / (KPS * p.L), C::MAXST) : C::nst(p.L));
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
   __shared__ int ssa[SA ? kBM : 1];   // annealing: this CTA's decisions for site sa_m
@@ -260,20 +272,24 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       s0 += ns;
     }
   }
-  const uint32_t stage_bytes = (uint32_t)(KPS * p.L) * C::BOX;
+  const uint32_t stage_bytes = (uint32_t)(KPS * p.L) * BOXB;
   // segments run in ascending degree order (j = nseg-1 .. 0); in field mode the single
   // accumulator is snapshot after each degree so the energy can weight degree r by 1/r
   const bool snaps = p.field_mode != 0 && !SA;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), 9); mbar_init(EMPTY(s), 1); }
+    // FULL: the TMA arrive + 8 generator warps (pairs: + the peer's 8, on the leader only)
+    for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), PAIR ? 17 : 9); mbar_init(EMPTY(s), 1); }
     mbar_init(acc_full, 1);
     mbar_init(snap_full, 1);
-    mbar_init(snap_empty, 8);
+    mbar_init(snap_empty, PAIR ? 16 : 8);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
-  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair(tslot, C::TMEM_COLS);
+    else tmem_alloc(tslot, C::TMEM_COLS);
+  }
   if constexpr (REAL) {
     // this CTA's p rows (bf16), zero past N and past B; +64 slack for window over-reads
     for (int i = threadIdx.x; i < kBM * p.pstride + 64; i += kThreads) {
@@ -293,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();   // both CTAs' barriers initialised, TMEM allocated
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot_g;
   bool sa_any = true;
@@ -352,12 +369,15 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           PT(const long long t0 = clock64();)
           mbar_wait(EMPTY(st), (uint32_t)(((n / NST) & 1) ^ 1));
           PT(w_tma += clock64() - t0;)
-          mbar_arrive_expect_tx(FULL(st), (uint32_t)(nkb * p.L) * C::BOX);
+          if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)(nkb * p.L) * C::BOX);   // pairs: both halves
           for (int q = 0; q < nkb; ++q)
-            for (int l = 0; l < p.L; ++l)
+            for (int l = 0; l < p.L; ++l) {
               // W is tile-blocked: box (l, ct, kb) is one contiguous NT x 64 block
-              tma_load_3d(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX, &tmap, FULL(st), 0, 0,
-                          (l * p.n_ct + ct) * p.n_kb + kb0 + q);
+              const int box = (l * p.n_ct + ct) * p.n_kb + kb0 + q;
+              const uint32_t dst = sB + st * stage_bytes + (uint32_t)(q * p.L + l) * BOXB;
+              if constexpr (PAIR) tma_load_3d_pair(dst, &tmap, mapa_shared(FULL(st), 0), 0, (int)prank * (NT / 2), box);
+              else tma_load_3d(dst, &tmap, FULL(st), 0, 0, box);
+            }
         }
       }
       PSTAT_FLUSH(6, w_tma);
@@ -366,8 +386,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     // ---------------- MMA issuer: D[tmem] += A[tmem] * B[smem] -------------------------------
     // The whole warp runs the loop, so descriptors are warp-uniform and stay in uniform
     // registers; one elected lane issues the MMAs and commits.
-    {
-      constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, NT);
       int n = 0, snap = 0;
       uint32_t issued = 0;
       PT(unsigned long long stt[6] = {0, 0, 0, 0, 0, 0}; const long long t_start = clock64(); long long t0;)
@@ -397,22 +417,28 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #pragma unroll
               for (int q = 0; q < 2; ++q)
 #pragma unroll
-                for (int k = 0; k < kBK / 16; ++k)
-                  umma_bf16_ts(tmem, a_t + (uint32_t)(q * C::A_COLS) + 8u * k,
-                               bdesc + (uint64_t)((q * C::BOX) >> 4) + 2u * k, idesc, issued | (uint32_t)(q | k));
+                for (int k = 0; k < kBK / 16; ++k) {
+                  const uint32_t at = a_t + (uint32_t)(q * C::A_COLS) + 8u * k;
+                  const uint64_t bd = bdesc + (uint64_t)((q * BOXB) >> 4) + 2u * k;
+                  if constexpr (PAIR) umma_bf16_ts_pair(tmem, at, bd, idesc, issued | (uint32_t)(q | k));
+                  else umma_bf16_ts(tmem, at, bd, idesc, issued | (uint32_t)(q | k));
+                }
             } else {
               for (int q = 0; q < nkb; ++q) {
                 const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
                 for (int l = 0; l < p.L; ++l) {
-                  const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * C::BOX);
+                  const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * BOXB);
 #pragma unroll
-                  for (int k = 0; k < kBK / 16; ++k)
-                    umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
+                  for (int k = 0; k < kBK / 16; ++k) {
+                    if constexpr (PAIR) umma_bf16_ts_pair(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
+                    else umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(q | l | k));
+                  }
                 }
               }
             }
             PT(stt[4] += clock64() - t0; t0 = clock64();)
-            umma_commit(EMPTY(st));
+            if constexpr (PAIR) umma_commit_pair(EMPTY(st), 3);
+            else umma_commit(EMPTY(st));
             PT(stt[5] += clock64() - t0;)
           }
           __syncwarp();
@@ -420,8 +446,13 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
         if (snaps && j > 0) {  // hand the degree-(k-j) partial sum to the epilogue warps
           if (elect_one()) {
-            if (issued) umma_commit(snap_full);
-            else mbar_arrive(snap_full);
+            if constexpr (PAIR) {
+              if (issued) umma_commit_pair(snap_full, 3);
+              else { mbar_arrive(snap_full); mbar_arrive_remote(mapa_shared(snap_full, 1)); }
+            } else {
+              if (issued) umma_commit(snap_full);
+              else mbar_arrive(snap_full);
+            }
           }
           __syncwarp();
           mbar_wait(snap_empty, (uint32_t)(snap & 1));
@@ -430,8 +461,13 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
       }
       if (elect_one()) {
-        if (issued) umma_commit(acc_full);
-        else mbar_arrive(acc_full);
+        if constexpr (PAIR) {
+          if (issued) umma_commit_pair(acc_full, 3);
+          else { mbar_arrive(acc_full); mbar_arrive_remote(mapa_shared(acc_full, 1)); }
+        } else {
+          if (issued) umma_commit(acc_full);
+          else mbar_arrive(acc_full);
+        }
       }
       __syncwarp();
       PT(if (lane == 0) { stt[0] = clock64() - t_start; for (int i = 0; i < 6; ++i) PSTAT_FLUSH(i, stt[i]); })
@@ -527,7 +563,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           tc_fence_before();
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(FULL(st));
+        if (lane == 0) {
+          if (PAIR && !leader) mbar_arrive_remote(mapa_shared(FULL(st), 0));
+          else mbar_arrive(FULL(st));
+        }
         d0 = n0;
         d1 = n1;
       }
@@ -539,7 +578,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         S[nsnap] = any ? xsum() : 0.0;
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(snap_empty);
+        if (lane == 0) {
+          if (PAIR && !leader) mbar_arrive_remote(mapa_shared(snap_empty, 0));
+          else mbar_arrive(snap_empty);
+        }
         ++nsnap;
       }
     }
@@ -635,8 +677,13 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #undef FULL
 #undef EMPTY
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if constexpr (PAIR) {
+    cluster_sync_all();   // the leader's last MMAs wrote both CTAs' TMEM
+    if (warp == 1) tmem_dealloc_pair(tmem, C::TMEM_COLS);
+  } else {
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  }
 }
 
 // ------------------------------------------------------------------------------------------

@@ -586,3 +586,32 @@ def test_empty_batches_and_argument_errors(H, torch):
     with pytest.raises(H.HoboError) as e:
         big.energy(torch.zeros(1, 1025, dtype=torch.uint8, device="cuda"))
     assert e.value.status == H.HOBO_EINVAL
+
+
+
+# ---- CTA pairs (cta_group::2) and the single-CTA kernel, each forced on both limb regimes ----
+@pytest.mark.parametrize("force", ["1", "0"])
+def test_cta_pair_and_single_paths(H, torch, force):
+    """HOBO_PAIR=1 runs every 256-column contraction on CTA pairs (M = 256 MMAs over two SMs),
+    =0 on single CTAs: integer instances stay bit-exact, fp32 ones within tau, either way."""
+    import os
+    old = os.environ.get("HOBO_PAIR")
+    os.environ["HOBO_PAIR"] = force
+    try:
+        for p in (random_integer_problem(3, 300, 41, nterms=800), cfg3_problem()):   # L = 1
+            t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+            X = x_bits(6, 1000, t.N)                           # 8 candidate blocks: odd pairs too
+            G, E = fields(H, torch, t, X)
+            assert np.array_equal(E, o.energy(X)) and np.array_equal(G, o.field(X))
+        idx, val = uniform_cells(3, 260, 3)                    # L = 3, two column tiles
+        t, o = H.HoboTensor.import_cells(3, 260, idx, val), Oracle.from_cells(3, 260, idx, val)
+        X = x_bits(7, 383, 260)                                # 3 candidate blocks: a lone last block
+        G, E = fields(H, torch, t, X)
+        assert np.max(np.abs(E - o.energy(X))) <= o.tau and np.max(np.abs(G - o.field(X))) <= o.tau
+        Ee, _ = energies(H, torch, t, X)
+        assert np.max(np.abs(Ee - o.energy(X))) <= o.tau
+    finally:
+        if old is None:
+            del os.environ["HOBO_PAIR"]
+        else:
+            os.environ["HOBO_PAIR"] = old
