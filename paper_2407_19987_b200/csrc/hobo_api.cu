@@ -130,6 +130,7 @@ struct hobo_tensor {
   int* d_sa_base = nullptr;
   double* d_sa_T = nullptr; size_t sa_T_cap = 0;
   alignas(64) CUtensorMap sa_tmap;
+  alignas(64) CUtensorMap sa_tmap2;   // CTA-pair kernel: half boxes (NT/2 rows)
   int sa_NT = 256, sa_nct = 1, sa_nkb1 = 1, sa_nseg = 0, sa_nq = 1;
   int sa_seg_kb0[8] = {0}, sa_seg_cnt[8] = {0};
   std::vector<int> sa_L;
@@ -1178,6 +1179,11 @@ hobo_status ensure_sa_persistent(hobo_tensor* t) {
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+  cuuint32_t box2[3] = {(cuuint32_t)kBK, (cuuint32_t)(NT / 2), 1};
+  cr = enc(&t->sa_tmap2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, t->d_sa_W, dims, strides, box2, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
   t->sa_NT = NT;
   t->sa_nct = n_ct;
   t->sa_nkb1 = nkb1;
@@ -1228,6 +1234,33 @@ cudaError_t launch_sa_stage(const CUtensorMap& tmap, const SaParams& p, int SB, 
     configured = smem;
   }
   k<<<grid, kThreads, smem, s>>>(tmap, p, SB, SaStCfg<NT, TS>::nst(SB));
+  return cudaGetLastError();
+}
+
+template <int NT>
+cudaError_t launch_sa2(const CUtensorMap& tmap, const SaParams& p, unsigned grid, cudaStream_t s) {
+  auto* k = sa2_kernel<NT>;
+  const size_t smem = Sa2Cfg<NT>::smem_bytes(p.W);
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, tmap, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1292,21 +1325,24 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
     if (t->profile) CK(cudaEventRecord(t->ev0, s));
     const unsigned grid = (unsigned)std::min<long long>(n_cb, 148);
     // one column tile (Npad <= 256): the staged kernel (one barrier pair per K-block); two
-    // tiles: the box ring (measured faster there).  The A-in-TMEM staged variant ('t') is an
-    // A/B option: measured 4% slower than smem A at cfg4.
+    // tiles: CTA pairs sharing every W box (the box ring is the single-block fallback).  The
+    // A-in-TMEM staged variant ('t') is an A/B option: measured 4% slower than smem A at cfg4.
     int Lmax = 1;
     for (int l : t->sa_L) Lmax = std::max(Lmax, l);
     const int SB = Lmax * t->sa_nct;
-    char kind = t->sa_nct == 1 ? 's' : 'r';
+    char kind = t->sa_nct == 1 ? 's' : 'p';   // two 256-column tiles: CTA pairs (cfg3 15.3 -> 13.3 ms)
     if ((t->sa_NT == 128 ? SaStCfg<128, false>::nst(SB) : SaStCfg<256, false>::nst(SB)) < 2) kind = 'r';
-    if (const char* e = getenv("HOBO_SA_KERNEL")) kind = e[0];   // A/B measurement switch: ring|stage|ts
+    if (const char* e = getenv("HOBO_SA_KERNEL")) kind = e[0];   // A/B measurement switch: ring|stage|ts|pair
     if (kind == 't' && t->sa_nct == 1)
       CK((t->sa_NT == 128 ? launch_sa_stage<128, true>(t->sa_tmap, q, SB, grid, s)
                           : launch_sa_stage<256, true>(t->sa_tmap, q, SB, grid, s)));
     else if (kind == 's')
       CK((t->sa_NT == 128 ? launch_sa_stage<128, false>(t->sa_tmap, q, SB, grid, s)
                           : launch_sa_stage<256, false>(t->sa_tmap, q, SB, grid, s)));
-    else
+    else if (kind == 'p' && n_cb >= 2) {
+      const unsigned g2 = (unsigned)(2 * std::min<long long>((n_cb + 1) / 2, 74));
+      CK(t->sa_NT == 128 ? launch_sa2<128>(t->sa_tmap2, q, g2, s) : launch_sa2<256>(t->sa_tmap2, q, g2, s));
+    } else
       CK(t->sa_NT == 128 ? launch_sa<128>(t->sa_tmap, q, grid, s) : launch_sa<256>(t->sa_tmap, q, grid, s));
     if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
     launches += 1;

@@ -518,4 +518,225 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
   if (warp == 1) tmem_dealloc(tmem, TCOLS);
 }
 
+// ---------------------------------------------------------------------------------------------
+// The same sweep on a CTA pair (cta_group::2): the two CTAs of a cluster own two 128-chain
+// blocks and share every W box — each loads half of its NT rows, and the leader's MMAs
+// (M = 256, 128 rows per CTA) read both halves.  Per SM this halves the W stream through
+// shared memory and the MMA instructions per site.  The peer's A-tile arrivals on the
+// leader's barriers are plain remote arrivals (see ptx.cuh: mbar_arrive_remote).
+template <int NT>
+struct Sa2Cfg {
+  static constexpr int HBOX = (NT / 2) * 128;   // this CTA's half of a W box
+  static constexpr int RW = 8;
+  static constexpr int ABOX = kBM * 128;
+  static constexpr int RA = 4;
+  static constexpr int NBAR = 2 * RW + 2 * RA + 1;
+  static size_t smem_bytes(int W) {
+    return 1024 + (size_t)RW * HBOX + (size_t)RA * ABOX + 8 * NBAR + 16 + (size_t)(W + 2) * kBM * 4 + kBM * 4 + 128;
+  }
+};
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1) sa2_kernel(const __grid_constant__ CUtensorMap tmap, const SaParams p) {
+  using C = Sa2Cfg<NT>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sW = base;
+  const uint32_t sA = sW + C::RW * C::HBOX;
+  const uint32_t sBar = sA + C::RA * C::ABOX;
+#define FULLW(s) (sBar + 8u * (s))
+#define EMPTYW(s) (sBar + 8u * (C::RW + (s)))
+#define FULLA(s) (sBar + 8u * (2 * C::RW + (s)))
+#define EMPTYA(s) (sBar + 8u * (2 * C::RW + C::RA + (s)))
+  const uint32_t SITE = sBar + 8u * (2 * C::RW + 2 * C::RA);
+  const uint32_t tslot = SITE + 8;
+  const uint32_t sX = (tslot + 16 + 127u) & ~127u;
+  uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
+  int* sS = reinterpret_cast<int*>(gbase + (sX - base) + (size_t)(p.W + 2) * kBM * 4);
+  volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int NPAD = NT * p.n_ct;
+  const long long n_cb = (p.B + kBM - 1) / kBM;
+  const long long n_pairs = (n_cb + 1) / 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::RW; ++s) { mbar_init(FULLW(s), 1); mbar_init(EMPTYW(s), 1); }
+    for (int s = 0; s < C::RA; ++s) { mbar_init(FULLA(s), 8); mbar_init(EMPTYA(s), 1); }
+    mbar_init(SITE, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
+  if (warp == 1) tmem_alloc_pair(tslot, (uint32_t)NPAD);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tslot_g;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t nw = 0;
+      for (long long pr = blockIdx.x / 2; pr < n_pairs; pr += gridDim.x / 2)
+        for (long long step = 0; step < p.steps; ++step) {
+          const int m = (int)(step % p.N);
+          const int L = __ldg(p.site_L + m), sb = __ldg(p.site_base + m);
+          for (int q = 0; q < p.nq; ++q) {
+            const int kb = sa_site_kb(p, q);
+            for (int l = 0; l < L; ++l)
+              for (int h = 0; h < p.n_ct; ++h, ++nw) {
+                const uint32_t s = nw % C::RW;
+                mbar_wait(EMPTYW(s), ((nw / C::RW) & 1u) ^ 1u);
+                if (leader) mbar_arrive_expect_tx(FULLW(s), 2 * C::HBOX);
+                tma_load_3d_pair(sW + s * C::HBOX, &tmap, mapa_shared(FULLW(s), 0), 0, (int)rank * (NT / 2),
+                                 sb + (l * p.n_ct + h) * p.nkb1 + kb);
+              }
+          }
+        }
+    }
+  } else if (warp == 1) {
+    if (leader) {   // whole warp in the loop, one elected lane issues
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * kBM, NT);
+      uint32_t nw = 0, na = 0;
+      for (long long pr = blockIdx.x / 2; pr < n_pairs; pr += gridDim.x / 2)
+        for (long long step = 0; step < p.steps; ++step) {
+          const int m = (int)(step % p.N);
+          const int L = __ldg(p.site_L + m);
+          for (int q = 0; q < p.nq; ++q, ++na) {
+            const uint32_t a = na % C::RA;
+            mbar_wait(FULLA(a), (na / C::RA) & 1u);
+            tc_fence_after();
+            const uint64_t adesc = sw128_kmajor_desc(sA + a * C::ABOX);
+            for (int l = 0; l < L; ++l)
+              for (int h = 0; h < p.n_ct; ++h, ++nw) {
+                const uint32_t s = nw % C::RW;
+                mbar_wait(FULLW(s), (nw / C::RW) & 1u);
+                tc_fence_after();
+                const uint64_t bdesc = sw128_kmajor_desc(sW + s * C::HBOX);
+                if (elect_one()) {
+#pragma unroll
+                  for (int k = 0; k < kBK / 16; ++k)
+                    umma_bf16_ss_pair(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
+                  umma_commit_pair(EMPTYW(s), 3);
+                }
+                __syncwarp();
+              }
+            if (elect_one()) umma_commit_pair(EMPTYA(a), 3);
+            __syncwarp();
+          }
+          if (elect_one()) umma_commit_pair(SITE, 3);
+          __syncwarp();
+        }
+    }
+  } else {
+    const int qd = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int row = qd * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(qd * 32) << 16);
+    const int gtid = threadIdx.x - 64;
+    uint32_t na = 0, nsite = 0;
+    for (long long pr = blockIdx.x / 2; pr < n_pairs; pr += gridDim.x / 2) {
+      const long long cb = 2 * pr + rank;
+      const long long b0 = cb * kBM, b = b0 + row;
+      const bool live = b < p.B;
+      const int Wp = p.W + 2;
+      for (int i = gtid; i < Wp * kBM; i += 256) {
+        const int r = i / Wp, w = i % Wp;
+        xs[w * kBM + r] = (w < p.W && b0 + r < p.B) ? p.bits[(size_t)(b0 + r) * p.W + w] : 0u;
+      }
+      for (int c0 = h * (NPAD / 2); c0 < (h + 1) * (NPAD / 2); c0 += 32) {
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          v[c] = (live && c0 + c < p.N) ? __float_as_uint(__ldg(p.G0 + (size_t)b * p.N + c0 + c)) : 0u;
+        tmem_st32(lane_base + (uint32_t)c0, v);
+      }
+      tmem_st_wait();
+      double E = (h == 0 && live) ? p.E[b] : 0.0;
+      tc_fence_before();
+      named_bar_sync(1, 256);
+      tc_fence_after();
+      for (long long step = 0; step < p.steps; ++step) {
+        const int m = (int)(step % p.N);
+        double thr = 0.0;
+        if (h == 0 && live) {
+          const double u = (double)(d_hash(p.seed, 4, (uint64_t)(p.chain0 + b), (uint64_t)step) >> 11) * 0x1.0p-53;
+          thr = -__ldg(p.temps + step / p.N) * log(u);
+        }
+        if (step > 0) {
+          mbar_wait(SITE, nsite & 1u);
+          ++nsite;
+          tc_fence_after();
+        }
+        if (h == 0) {
+          const float g = __uint_as_float(tmem_ld1(lane_base + (uint32_t)m));
+          tmem_ld_wait();
+          int sv = 0;
+          if (live) {
+            const int wi = m >> 5;
+            const uint32_t bit = 1u << (m & 31);
+            const bool xm = (xs[wi * kBM + row] & bit) != 0u;
+            const float d = xm ? -g : g;
+            if (d <= 0.0f || (double)d < thr) {
+              sv = xm ? -1 : 1;
+              xs[wi * kBM + row] ^= bit;
+              E += (double)d;
+            }
+          }
+          sS[row] = sv;
+          tc_fence_before();
+        }
+        named_bar_sync(1, 256);
+        const int sv = sS[row];
+        const uint32_t sgn = sv < 0 ? 0x80008000u : 0u;
+        for (int q = 0; q < p.nq; ++q, ++na) {
+          if ((q & 1) != h) continue;
+          const uint32_t a = na % C::RA;
+          mbar_wait(EMPTYA(a), ((na / C::RA) & 1u) ^ 1u);
+          const int kb = sa_site_kb(p, q);
+          uint64_t bits = 0;
+          if (sv != 0) {
+            if (kb == p.nkb1 - 1) bits = 1ull;
+            else bits = block_bits(xs, row, __ldg(p.kdesc + 2 * kb), __ldg(p.kdesc + 2 * kb + 1), p.runs);
+          }
+          uint32_t w[32];
+          expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+          expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
+          const uint32_t rowaddr = sA + a * C::ABOX + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            st_shared_v4(rowaddr + (uint32_t)((c ^ (row & 7)) << 4), w[4 * c] ^ sgn, w[4 * c + 1] ^ sgn,
+                         w[4 * c + 2] ^ sgn, w[4 * c + 3] ^ sgn);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader) mbar_arrive(FULLA(a));
+            else mbar_arrive_remote(mapa_shared(FULLA(a), 0));
+          }
+        }
+      }
+      if (p.steps > 0) {
+        mbar_wait(SITE, nsite & 1u);
+        ++nsite;
+        tc_fence_after();
+      }
+      if (h == 0 && live) {
+        p.E[b] = E;
+        for (int w = 0; w < p.W; ++w) p.bits[(size_t)b * p.W + w] = xs[w * kBM + row];
+      }
+      tc_fence_before();
+      named_bar_sync(1, 256);
+    }
+  }
+#undef FULLW
+#undef EMPTYW
+#undef FULLA
+#undef EMPTYA
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) tmem_dealloc_pair(tmem, (uint32_t)NPAD);
+}
+
 }  // namespace hobo
