@@ -237,18 +237,18 @@ cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s
   return cudaGetLastError();
 }
 
-// CTA pairs for 256-column tiles at L >= 2 with long K loops (measured: cfg3-fp32 +19%, cfg5
-// +12%); at L = 1 the single-CTA kernel is 5% faster (cfg3), and short K loops (cfg2's QUBO,
-// 4-16 K-blocks per CTA) do not amortise the pair's cluster synchronisation (-8%).
+// CTA pairs at L >= 2 with long K loops (measured: cfg3-fp32 +19%, cfg5 +12%, cfg4 (128-column
+// tiles) +21%); at L = 1 the single-CTA kernel is 5% faster (cfg3), and short K loops (cfg2's
+// QUBO, 4-16 K-blocks per CTA) do not amortise the pair's cluster synchronisation (-8%).
 // HOBO_PAIR=1 / =0 forces the choice (A/B runs, tests of both paths).
 bool use_pairs(const DevLayout& L, const KrParams& p) {
-  if (p.preal || p.n_split != 1 || L.NT != 256) return false;
+  if (p.preal || p.n_split != 1) return false;
   if (const char* e = getenv("HOBO_PAIR")) return e[0] == '1';
   return p.L >= 2 && p.n_kb >= 64;
 }
 
 cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  if (use_pairs(L, p)) return launch_kr_pair<256>(L, p, s);
+  if (use_pairs(L, p)) return L.NT == 128 ? launch_kr_pair<128>(L, p, s) : launch_kr_pair<256>(L, p, s);
   if (L.NT == 128) return p.preal ? launch_kr<128, true>(L, p, s) : launch_kr<128, false>(L, p, s);
   return p.preal ? launch_kr<256, true>(L, p, s) : launch_kr<256, false>(L, p, s);
 }
