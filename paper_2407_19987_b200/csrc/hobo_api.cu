@@ -210,10 +210,10 @@ cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) 
 }
 
 // CTA pairs: clusters of 2 (adjacent candidate blocks of one column tile), cta_group::2 MMAs
-template <int NT>
+template <int NT, bool REAL>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  auto* k = kr_gemm_kernel<NT, false, false, true>;
-  const size_t smem = KrCfg<NT>::smem_bytes(p.W);
+  auto* k = kr_gemm_kernel<NT, REAL, false, true>;
+  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT>::smem_bytes(p.W);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -242,13 +242,17 @@ cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s
 // QUBO, 4-16 K-blocks per CTA) do not amortise the pair's cluster synchronisation (-8%).
 // HOBO_PAIR=1 / =0 forces the choice (A/B runs, tests of both paths).
 bool use_pairs(const DevLayout& L, const KrParams& p) {
-  if (p.preal || p.n_split != 1) return false;
+  if (p.n_split != 1) return false;
   if (const char* e = getenv("HOBO_PAIR")) return e[0] == '1';
-  return p.L >= 2 && p.n_kb >= 64;
+  const int limb_mmas = p.preal ? p.LA * p.L : p.L;   // MMA passes per W box (real-valued: x A limbs)
+  return limb_mmas >= 2 && p.n_kb >= 64;              // (real-valued cfg3: 14.7 -> 13.6 ms)
 }
 
 cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  if (use_pairs(L, p)) return L.NT == 128 ? launch_kr_pair<128>(L, p, s) : launch_kr_pair<256>(L, p, s);
+  if (use_pairs(L, p)) {
+    if (p.preal) return L.NT == 128 ? launch_kr_pair<128, true>(L, p, s) : launch_kr_pair<256, true>(L, p, s);
+    return L.NT == 128 ? launch_kr_pair<128, false>(L, p, s) : launch_kr_pair<256, false>(L, p, s);
+  }
   if (L.NT == 128) return p.preal ? launch_kr<128, true>(L, p, s) : launch_kr<128, false>(L, p, s);
   return p.preal ? launch_kr<256, true>(L, p, s) : launch_kr<256, false>(L, p, s);
 }

@@ -216,7 +216,7 @@ __device__ unsigned long long g_pipe_stats[8192][8];
 // instruction covers both SMs and each SM's shared memory carries half the W stream.
 template <int NT, bool REAL, bool SA = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
-  static_assert(!(PAIR && (REAL || SA)), "CTA pairs: binary contraction only");
+  static_assert(!(PAIR && SA), "CTA pairs: not for the per-site annealing launch");
   using C = KrCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   constexpr uint32_t BOXB = PAIR ? C::BOX / 2 : C::BOX;   // shared-memory bytes of one W box per CTA
   const int KPS = REAL ? 1 : C::kps(p.L);
   // CTA pairs hold half boxes, so the same ring fits twice the stages (TMEM: 256 + 4 x 64 columns)
-  const int NST = REAL ? C::nst_real(p.L, p.LA, ring)
+  const int NST = REAL ? C::nst_real(p.L, p.LA, PAIR ? 2 * ring : ring)
                        : (PAIR ? min(2 * C::RING_BOXES / (KPS * p.L), C::MAXST) : C::nst(p.L));
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
@@ -405,10 +405,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
               for (int la = 0; la < p.LA; ++la) {
                 const uint32_t a_t = tmem + (uint32_t)(NT + st * ACOLS + la * C::A_COLS);
                 for (int l = 0; l < p.L; ++l) {
-                  const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)l * C::BOX);
+                  const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)l * BOXB);
 #pragma unroll
-                  for (int k = 0; k < kBK / 16; ++k)
-                    umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(la | l | k));
+                  for (int k = 0; k < kBK / 16; ++k) {
+                    if constexpr (PAIR) umma_bf16_ts_pair(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(la | l | k));
+                    else umma_bf16_ts(tmem, a_t + 8u * k, bdesc + 2u * k, idesc, issued | (uint32_t)(la | l | k));
+                  }
                 }
               }
             } else if (p.L == 1 && nkb == 2 && KPS == 2) {   // the common stage, fully unrolled
@@ -536,7 +538,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(FULL(st));
+          if (lane == 0) {
+            if (PAIR && !leader) mbar_arrive_remote(mapa_shared(FULL(st), 0));
+            else mbar_arrive(FULL(st));
+          }
           d0 = n0;
           d1 = n1;
         }
