@@ -787,8 +787,10 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   CK(cudaEventRecord(t->ev_in, s));             // the copies follow the caller's prior work
   CK(cudaStreamWaitEvent(t->cs, t->ev_in, 0));
   int64_t launches = 0;
-  for (long long off = 0, i = 0; off < B; off += chunk, ++i) {
-    const long long n = std::min<long long>(chunk, B - off);
+  // the first chunk is a single wave: its copy is the one nothing overlaps
+  const long long first = std::min<long long>(chunk, per_wave);
+  for (long long off = 0, i = 0, n = 0; off < B; off += n, ++i) {
+    n = std::min<long long>(i == 0 ? first : chunk, B - off);
     const int slot = (int)(i & 1);
     if (i >= 2) CK(cudaStreamWaitEvent(t->cs, t->ev_free[slot], 0));   // its previous chunk is packed
     CK(cudaMemcpyAsync(t->d_xh[slot], X_host + (size_t)off * N, (size_t)n * N, cudaMemcpyHostToDevice, t->cs));
