@@ -17,6 +17,10 @@
  *     handle (later calls return HOBO_ECUDA).
  *   - Energies EXCLUDE the compile offset, like the paper's printed "Energy"
  *     (Energy -30 reported together with offset 30).
+ *   - Kernel choice is automatic; two environment variables override it for A/B
+ *     measurements and tests (results are identical either way):
+ *       HOBO_PAIR=1|0        CTA-pair (cta_group::2) contraction on / off
+ *       HOBO_SA_KERNEL=ring|stage|ts|pair   the persistent annealing kernel
  */
 #ifndef HOBO_H_
 #define HOBO_H_
@@ -33,8 +37,9 @@ typedef enum {
   HOBO_ERANGE = 2,  /* a compiled cell exceeds FLT_MAX                                     */
   HOBO_ENOMEM = 3,  /* host or device allocation failed / size budget exceeded             */
   HOBO_ECUDA = 4,   /* CUDA error (sticky per handle) or no sm_100 device                  */
-  HOBO_ENCCL = 5,   /* reserved for the multi-GPU combine                                  */
-  HOBO_ESTATE = 6   /* handle poisoned by an earlier error                                 */
+  HOBO_ENCCL = 5,   /* NCCL error in the multi-GPU combine (hobo_dist_*)                   */
+  HOBO_ESTATE = 6   /* handle poisoned, call out of order (e.g. TT energy before the TT
+                       build), or a communicator already initialised                       */
 } hobo_status;
 
 typedef struct hobo_tensor hobo_tensor;   /* opaque; owns host cells + one device replica */
