@@ -17,10 +17,14 @@
  *     handle (later calls return HOBO_ECUDA).
  *   - Energies EXCLUDE the compile offset, like the paper's printed "Energy"
  *     (Energy -30 reported together with offset 30).
- *   - Kernel choice is automatic; two environment variables override it for A/B
- *     measurements and tests (results are identical either way):
+ *   - Kernel choice is automatic; environment variables override it for A/B
+ *     measurements and tests (read when the handle first uses the choice):
  *       HOBO_PAIR=1|0        CTA-pair (cta_group::2) contraction on / off
  *       HOBO_SA_KERNEL=ring|stage|ts|pair   the persistent annealing kernel
+ *       HOBO_I8=1|0          int8 digit planes (kind::i8) whenever exact / never
+ *     Pairs and annealing kernels give identical results.  The int8 path computes the
+ *     contraction exactly (integer accumulation), the bf16 path within the fp32
+ *     tolerance; both are exact on integer instances with sum|H| < 2^24.
  */
 #ifndef HOBO_H_
 #define HOBO_H_
@@ -250,6 +254,10 @@ hobo_status hobo_dist_info(int* rank, int* world);
  * contraction kernel(s), recorded on the launch stream (this call synchronises on it).  */
 hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mma_macs,
                                    double* algo_macs, double* kernel_ms);
+/* The MMA kind of the last call's contraction: *i8_planes = the number of int8 digit planes
+ * (tcgen05.mma kind::i8), or 0 for bf16 limbs (kind::f16).
+ * mma_macs above counts 8-bit MACs in the first case, bf16 MACs in the second.            */
+hobo_status hobo_last_launch_kind(const hobo_tensor* t, int* i8_planes);
 /* profiling on/off: record CUDA events around every contraction-kernel launch.         */
 hobo_status hobo_set_profiling(hobo_tensor* t, int enable);
 

@@ -69,7 +69,9 @@ bool dist_active() { return g_dist.comm != nullptr; }   // world 1 runs the same
 struct DevLayout {
   bool built = false;
   int NT = 256, n_ct = 0, Npad = 0;
-  __nv_bfloat16* W = nullptr;
+  __nv_bfloat16* W = nullptr;          // bf16 limb planes, or (i8 > 0) int8 digit planes
+  int i8 = 0;                          // int8 digit planes: their count; 0 = bf16 limbs
+  double qscale = 1.0;                 // int8: cell = qscale * (digit integer)
   int2* d_sched = nullptr;
   std::vector<int32_t> sched;
   alignas(64) CUtensorMap tmap;
@@ -92,8 +94,10 @@ struct hobo_tensor {
   uint32_t* d_runoff = nullptr;
   float* d_p1 = nullptr;   // padded to 256-multiples
   int W = 0;               // 32-bit words per candidate bit row
-  DevLayout lay[3];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
-                           // tiles for the real-valued path (p rows + a deeper W ring in smem)
+  DevLayout lay[4];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
+                           // tiles for the real-valued path (p rows + a deeper W ring in smem),
+                           // 3 = bf16 field layout for the real-valued path when 1 holds int8 digits
+  int dig = -1;            // int8 digit planes of slots 0/1 (0 = bf16 limbs; -1 = not decided yet)
   // scratch (grown on demand)
   uint32_t* d_bits = nullptr; size_t bits_cap = 0;
   double* d_Q = nullptr; size_t Q_cap = 0;
@@ -138,6 +142,7 @@ struct hobo_tensor {
   double* d_sa_E = nullptr; size_t sa_E_cap = 0;        // tracked energies
   int64_t last_launches = 0;
   double last_mma_macs = 0, last_algo_macs = 0;
+  int last_i8 = 0;                                      // MMA kind of the last call: int8 digit planes (count) or 0 = bf16
   bool profile = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // around the contraction kernel(s) of the last call
   bool ev_valid = false;
@@ -181,10 +186,10 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int NT, bool REAL>
+template <int NT, bool REAL, bool I8 = false>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  auto* k = kr_gemm_kernel<NT, REAL>;
-  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT>::smem_bytes(p.W);
+  auto* k = kr_gemm_kernel<NT, REAL, false, false, I8>;
+  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -210,10 +215,10 @@ cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) 
 }
 
 // CTA pairs: clusters of 2 (adjacent candidate blocks of one column tile), cta_group::2 MMAs
-template <int NT, bool REAL>
+template <int NT, bool REAL, bool I8 = false>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  auto* k = kr_gemm_kernel<NT, REAL, false, true>;
-  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT>::smem_bytes(p.W);
+  auto* k = kr_gemm_kernel<NT, REAL, false, true, I8>;
+  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -249,6 +254,10 @@ bool use_pairs(const DevLayout& L, const KrParams& p) {
 }
 
 cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  if (L.i8) {
+    if (use_pairs(L, p)) return L.NT == 128 ? launch_kr_pair<128, false, true>(L, p, s) : launch_kr_pair<256, false, true>(L, p, s);
+    return L.NT == 128 ? launch_kr<128, false, true>(L, p, s) : launch_kr<256, false, true>(L, p, s);
+  }
   if (use_pairs(L, p)) {
     if (p.preal) return L.NT == 128 ? launch_kr_pair<128, true>(L, p, s) : launch_kr_pair<256, true>(L, p, s);
     return L.NT == 128 ? launch_kr_pair<128, false>(L, p, s) : launch_kr_pair<256, false>(L, p, s);
@@ -280,6 +289,25 @@ bool real_geometry(hobo_tensor* t, int NT, int& pstride, int& ring, int& LA) {
 }
 
 hobo_status init_device(hobo_tensor* t);
+
+// int8 digit planes for the binary energy / field layouts (slots 0 and 1): used when the degree
+// >= 2 cells are a fixed-point grid of <= 3 bytes (exact), the int32 accumulators cannot
+// overflow (255 x tuples < 2^31) and they take fewer tensor-core cycles than the bf16 limbs
+// (an int8 MMA runs at twice the bf16 rate: d digits cost d/2 vs L limbs).  HOBO_I8=0 / =1
+// forces bf16 / int8 (when exact).
+int digit_planes(hobo_tensor* t) {
+  if (t->dig >= 0) return t->dig;
+  const HostTensor& H = t->host;
+  int d = H.digits;
+  if (d > 0 && 255.0 * (double)std::max<int64_t>(t->kl.Tpad, kBK) >= 2147483648.0) d = 0;
+  if (d > 0) {
+    const char* e = getenv("HOBO_I8");
+    if (e && e[0] == '0') d = 0;
+    else if (!(e && e[0] == '1') && d >= 2 * H.limbs) d = 0;
+  }
+  t->dig = d;
+  return d;
+}
 
 hobo_status check_device(hobo_tensor* t) {
   if (t->poisoned) return fail(HOBO_ESTATE, "handle poisoned by an earlier CUDA error");
@@ -327,17 +355,21 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   const int field = slot != 0;
   const HostTensor& H = t->host;
   const int N = H.N, k = H.order;
+  L.i8 = slot <= 1 ? digit_planes(t) : 0;
   L.NT = (N <= 128 || slot == 2) ? 128 : 256;   // a 128-column tile when N fits (no padded columns)
+  if (L.i8 >= 2) L.NT = 128;                    // TMEM: i8 accumulators of NT columns + the A stages
+  L.qscale = std::ldexp(1.0, H.qexp);
+  const int planes = L.i8 ? L.i8 : H.limbs;
   if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
   L.n_ct = (N + L.NT - 1) / L.NT;
   L.Npad = L.n_ct * L.NT;
   const int64_t Tpad = std::max<int64_t>(t->kl.Tpad, kBK);
-  const double bytes = (double)H.limbs * L.Npad * Tpad * 2.0;
+  const double bytes = (double)planes * L.Npad * Tpad * (L.i8 ? 1.0 : 2.0);
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   if (bytes > 0.8 * (double)free_b)
     return fail(HOBO_ENOMEM, "device layout needs " + std::to_string(bytes / 1e9) + " GB (N=" + std::to_string(N) +
-                                 ", order=" + std::to_string(k) + ", limbs=" + std::to_string(H.limbs) + ")");
+                                 ", order=" + std::to_string(k) + ", planes=" + std::to_string(planes) + ")");
   CK(cudaMalloc(&L.W, (size_t)bytes));
   if (t->kl.Tpad > 0) {
     // temporaries: per-degree cells, binomials, tuple list
@@ -366,9 +398,13 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
     lp.Tpad = t->kl.Tpad;
     lp.N = N;
     lp.Npad = L.Npad;
-    lp.L = H.limbs;
+    lp.L = planes;
     lp.field_mode = field;
     lp.NT = L.NT;
+    if (L.i8) {
+      lp.Wout8 = reinterpret_cast<uint8_t*>(L.W);
+      lp.inv_qscale = std::ldexp(1.0, -H.qexp);
+    }
     layout_kernel<<<148 * 8, 256>>>(lp);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
@@ -383,19 +419,21 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled unavailable");
   // 3-D view of the tile-blocked planes: (64 tuples, NT rows, box index), box = one block
+  // (int8 digit planes: 64-byte rows, 64-byte swizzle)
   const int64_t n_kb = Tpad / kBK;
-  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)L.NT, (cuuint64_t)H.limbs * L.n_ct * n_kb};
-  cuuint64_t strides[2] = {(cuuint64_t)kBK * 2, (cuuint64_t)kBK * 2 * L.NT};
+  const cuuint64_t esz = L.i8 ? 1 : 2;
+  const CUtensorMapDataType dt = L.i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUtensorMapSwizzle sw = L.i8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)L.NT, (cuuint64_t)planes * L.n_ct * n_kb};
+  cuuint64_t strides[2] = {(cuuint64_t)kBK * esz, (cuuint64_t)kBK * esz * L.NT};
   cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)L.NT, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = enc(&L.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.W, dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult cr = enc(&L.tmap, dt, 3, L.W, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
   cuuint32_t box_half[3] = {(cuuint32_t)kBK, (cuuint32_t)(L.NT / 2), 1};
-  cr = enc(&L.tmap_half, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, L.W, dims, strides, box_half, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cr = enc(&L.tmap_half, dt, 3, L.W, dims, strides, box_half, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
   L.sched = schedule(t->kl, L.NT, L.n_ct, field != 0);
   CK(cudaMalloc(&L.d_sched, L.sched.size() * sizeof(int32_t)));
@@ -437,7 +475,8 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.ring_boxes = L.NT == 128 ? ring_boxes_for<128>() : ring_boxes_for<256>();
   p.pstride = 0;
   p.nseg = t->kl.nseg;
-  p.L = t->host.limbs;
+  p.L = L.i8 ? L.i8 : t->host.limbs;
+  p.qscale = L.qscale;
   p.field_mode = (&L == &t->lay[0]) ? 0 : 1;
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
@@ -453,7 +492,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
 int choose_split(hobo_tensor* t, const DevLayout& L, long long B) {
   const long long tiles = ((B + kBM - 1) / kBM) * L.n_ct;
   if (tiles >= 148) return 1;
-  const int KPS = L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
+  const int KPS = L.i8 ? 2 : L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
   int stages = 0;
   for (int ct = 0; ct < L.n_ct; ++ct) {
     int s = 0;
@@ -468,7 +507,7 @@ double exec_macs(hobo_tensor* t, const DevLayout& L, long long B) {
   double kb = 0;
   for (int ct = 0; ct < L.n_ct; ++ct)
     for (int j = 0; j < t->kl.nseg; ++j) kb += L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1];
-  return kb * kBK * (double)L.NT * kBM * (double)((B + kBM - 1) / kBM) * t->host.limbs;
+  return kb * kBK * (double)L.NT * kBM * (double)((B + kBM - 1) / kBM) * (L.i8 ? L.i8 : t->host.limbs);
 }
 
 double algo_macs(hobo_tensor* t, bool field, long long B) {
@@ -527,9 +566,10 @@ hobo_status empty_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
 // with 128-column tiles (half-size boxes).  (128-column tiles everywhere measured 1.8x slower
 // at cfg3: twice the CTAs generate A.)
 int real_slot(hobo_tensor* t) {
-  if (t->host.N <= 128) return 1;
+  const int full = digit_planes(t) ? 3 : 1;   // the real-valued path needs bf16 limb planes
+  if (t->host.N <= 128) return digit_planes(t) ? 2 : 1;
   int ps = 0, ring = 0, la = 0;
-  return real_geometry(t, 256, ps, ring, la) ? 1 : 2;
+  return real_geometry(t, 256, ps, ring, la) ? full : 2;
 }
 
 hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
@@ -555,7 +595,7 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   p.n_split = choose_split(t, L, B);
   if (p.n_split > 1) {
     if (field) {
-      if (hobo_status st = grow(t, t->d_Gpart, t->Gpart_cap, (size_t)p.n_split * B * t->host.N)) return st;
+      if (hobo_status st = grow(t, t->d_Gpart, t->Gpart_cap, (size_t)p.n_split * B * t->host.N * (L.i8 ? 2 : 1))) return st;
       p.G = t->d_Gpart;
     }
     if (hobo_status st = grow(t, t->d_Qpart, t->Qpart_cap, (size_t)p.n_split * L.n_ct * B)) return st;
@@ -568,11 +608,12 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   if (p.n_split > 1) {
     const long long nG = field ? B * t->host.N : 0, nQ = (long long)L.n_ct * B;
     splitk_reduce_kernel<<<(unsigned)std::min<long long>((std::max(nG, nQ) + 255) / 256, 148 * 8), 256, 0, s>>>(
-        t->d_Gpart, G, nG, t->d_Qpart, t->d_Q, nQ, p.n_split);
+        t->d_Gpart, G, nG, t->d_Qpart, t->d_Q, nQ, p.n_split, L.i8 ? 1 : 0);
     CK(cudaGetLastError());
     t->last_launches += 1;
   }
   t->last_mma_macs = exec_macs(t, L, B) * p.LA;
+  t->last_i8 = L.i8;
   t->last_algo_macs = algo_macs(t, field != 0, B);
   return HOBO_OK;
 }
@@ -811,6 +852,7 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   }
   t->last_launches = launches;
   t->last_mma_macs = exec_macs(t, L, B);
+  t->last_i8 = L.i8;
   t->last_algo_macs = algo_macs(t, field != 0, B);
   return HOBO_OK;
 }
@@ -871,6 +913,7 @@ hobo_status run_search(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nc
   }
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
   t->last_mma_macs = exec_macs(t, L, B) * (double)(iters + 1);
+  t->last_i8 = L.i8;
   t->last_algo_macs = algo_macs(t, true, B) * (double)(iters + 1);
   return HOBO_OK;
 }
@@ -1355,6 +1398,7 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
     double per_sweep = 0;
     for (int m = 0; m < N; ++m) per_sweep += (double)t->sa_L[m] * t->sa_nq * t->sa_nct * t->sa_NT * kBK * kBM;
     t->last_mma_macs = per_sweep * (double)n_cb * (double)sweeps;
+    t->last_i8 = 0;
     t->last_algo_macs = 0;   // site tensors are not kept on the host in this layout
     return HOBO_OK;
   }
@@ -1387,6 +1431,7 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
   }
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
   launches += step;
+  t->last_i8 = 0;
   t->last_mma_macs = macs * (double)sweeps;   // upper bound: blocks whose chains all reject skip the MMA
   t->last_algo_macs = 0;
   for (int m = 0; m < N; ++m) t->last_algo_macs += algo_macs(t->sa_child[m], true, B);
@@ -1788,6 +1833,12 @@ hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mm
       *kernel_ms = ms;
     }
   }
+  return HOBO_OK;
+}
+
+hobo_status hobo_last_launch_kind(const hobo_tensor* t, int* i8_planes) {
+  if (!t || !i8_planes) return fail(HOBO_EINVAL, "null argument");
+  *i8_planes = t->last_i8;
   return HOBO_OK;
 }
 

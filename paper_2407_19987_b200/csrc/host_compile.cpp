@@ -7,6 +7,8 @@
 // layout needs; the tuple form (s,..,s,v2..vr) is produced only by the export helpers.
 #include "host_compile.h"
 
+#include <climits>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -103,6 +105,28 @@ void cell_stats(HostTensor& out) {
       if (f != std::nearbyint(f)) out.is_integer = false;
       out.limbs = std::max(out.limbs, limbs_needed(f));
     }
+  // fixed-point quantum of the degree >= 2 cells: the smallest exponent of a cell's lowest set bit
+  int qe = INT_MAX;
+  for (int r = 2; r <= out.order; ++r)
+    for (float f : out.strict[r]) {
+      if (f == 0.0f) continue;
+      int e = 0;
+      const double m = std::frexp(std::fabs((double)f), &e);     // |f| = m 2^e, m in [0.5, 1)
+      uint32_t M = (uint32_t)std::ldexp(m, 24);                 // the 24-bit significand
+      qe = std::min(qe, e - 24 + __builtin_ctz(M));
+    }
+  out.qexp = qe == INT_MAX ? 0 : qe;
+  out.digits = 1;
+  double qmax = 0.0, qmin = 0.0;
+  for (int r = 2; r <= out.order; ++r)
+    for (float f : out.strict[r]) {
+      const double q = std::ldexp((double)f, -out.qexp);
+      qmax = std::max(qmax, q);
+      qmin = std::min(qmin, q);
+    }
+  while (out.digits <= 3 && (qmax > std::ldexp(1.0, 8 * out.digits - 1) - 1.0 || qmin < -std::ldexp(1.0, 8 * out.digits - 1)))
+    ++out.digits;
+  if (out.digits > 3) out.digits = 0;
 }
 
 template <class Num>

@@ -20,6 +20,9 @@ struct HostTensor {
   bool is_integer = true;
   double sum_abs = 0.0;
   int limbs = 1;
+  // int8 digit planes: every cell of degree >= 2 is q * 2^qexp with q an integer of `digits`
+  // two's-complement bytes (1..3); digits = 0 when no such q fits in 3 bytes
+  int digits = 1, qexp = 0;
 };
 
 struct TermView {  // mirrors hobo_term / hobo_factor / hobo_lin

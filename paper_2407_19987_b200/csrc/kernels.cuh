@@ -47,6 +47,7 @@ struct KrParams {
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
   double wp;                // weight of the degree-1 term
   int dbg;                  // debug builds only (HOBO_PIPE_STATS): pipeline bisection switches
+  double qscale;            // int8 digit planes (kr_gemm_kernel<..., I8>): cell = qscale * sum_l 256^l d_l
   // simulated annealing (kr_gemm_kernel<NT, false, true>): one launch per visited site m with
   // the layout of P_m = dE/dx_m; every CTA decides site m for its chains, column tile 0
   // commits the decisions, and the epilogue adds s_b * (field of P_m) to G
@@ -61,13 +62,15 @@ struct KrParams {
   int sa_m, sa_prev;        // visited site, previous site (-1: none)
 };
 
-template <int NT>
+// I8: W as int8 digit planes (one byte per tuple: NT rows x 64 bytes, SW64) against A as
+// {0,1} bytes, tcgen05.mma kind::i8 at twice the bf16 rate, one s32 accumulator per digit plane
+template <int NT, bool I8 = false>
 struct KrCfg {
-  static constexpr int BOX = NT * 128;                   // one TMA box: NT rows x 64 bf16 (SW128)
-  static constexpr int RING_BOXES = 6 * 256 / NT;        // shared-memory budget for W (192 KB), in boxes
-  static constexpr int MAXST = NT >= 256 ? 4 : 6;        // max pipeline stages (4 at NT=256: CTA pairs' half boxes)
-  static constexpr int A_COLS = kBK / 2;                 // TMEM columns of one K-block of A (64 bf16 / lane)
-  static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator, then the A stages
+  static constexpr int BOX = NT * (I8 ? 64 : 128);       // one TMA box: NT rows x 64 tuples (bf16 SW128 / int8 SW64)
+  static constexpr int RING_BOXES = (I8 ? 12 : 6) * 256 / NT;   // shared-memory budget for W (192 KB), in boxes
+  static constexpr int MAXST = (I8 || NT < 256) ? 6 : 4; // max pipeline stages (4 at NT=256: CTA pairs' half boxes)
+  static constexpr int A_COLS = I8 ? kBK / 4 : kBK / 2;  // TMEM columns of one K-block of A (64 bf16 / 64 bytes per lane)
+  static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator (I8: L of them), then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
   static constexpr int NBAR = 2 * MAXST + 3;
   static size_t smem_bytes(int W) {
@@ -76,7 +79,12 @@ struct KrCfg {
   // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages.  Two
   // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
   // boxes that fits only at L = 1, with 128-column boxes at every L <= 3
-  __host__ __device__ static constexpr int kps(int L) { return (L == 1 || NT <= 128) ? 2 : 1; }
+  __host__ __device__ static constexpr int kps(int L) { return (I8 || L == 1 || NT <= 128) ? 2 : 1; }
+  // I8 stages: bounded by the ring (pairs: twice the boxes), MAXST and the TMEM left after the L accumulators
+  __host__ __device__ static constexpr int nst_i8(int L, int ring) {
+    return ring / (2 * L) < MAXST ? (ring / (2 * L) < (TMEM_COLS - L * NT) / (2 * A_COLS) ? ring / (2 * L) : (TMEM_COLS - L * NT) / (2 * A_COLS))
+                                  : (MAXST < (TMEM_COLS - L * NT) / (2 * A_COLS) ? MAXST : (TMEM_COLS - L * NT) / (2 * A_COLS));
+  }
   __host__ __device__ static constexpr int nst(int L) { return RING_BOXES / (kps(L) * L) < MAXST ? RING_BOXES / (kps(L) * L) : MAXST; }
   // real-valued A: one K-block per stage, LA limb tiles of A in TMEM, ring sized at run time
   __host__ __device__ static int nst_real(int L, int LA, int ring) {
@@ -214,10 +222,11 @@ __device__ unsigned long long g_pipe_stats[8192][8];
 // blocks of one column tile and share every W box: each loads half of its NT rows, the
 // leader issues cta_group::2 MMAs (M = 256: 128 rows of A in each CTA's TMEM), so one MMA
 // instruction covers both SMs and each SM's shared memory carries half the W stream.
-template <int NT, bool REAL, bool SA = false, bool PAIR = false>
+template <int NT, bool REAL, bool SA = false, bool PAIR = false, bool I8 = false>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
   static_assert(!(PAIR && SA), "CTA pairs: not for the per-site annealing launch");
-  using C = KrCfg<NT>;
+  static_assert(!(I8 && (REAL || SA)), "int8 digit planes: binary candidates, energy / field launches");
+  using C = KrCfg<NT, I8>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 atoms need 1024-byte alignment
@@ -252,7 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const int KPS = REAL ? 1 : C::kps(p.L);
   // CTA pairs hold half boxes, so the same ring fits twice the stages (TMEM: 256 + 4 x 64 columns)
   const int NST = REAL ? C::nst_real(p.L, p.LA, PAIR ? 2 * ring : ring)
-                       : (PAIR ? min(2 * C::RING_BOXES / (KPS * p.L), C::MAXST) : C::nst(p.L));
+                 : I8 ? C::nst_i8(p.L, PAIR ? 2 * ring : ring)
+                      : (PAIR ? min(2 * C::RING_BOXES / (KPS * p.L), C::MAXST) : C::nst(p.L));
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
   __shared__ int ssa[SA ? kBM : 1];   // annealing: this CTA's decisions for site sa_m
@@ -401,7 +411,23 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           PT(stt[1] += clock64() - t0; stt[2] += 1; stt[3] += nkb; t0 = clock64();)
           tc_fence_after();
           if (elect_one()) {
-            if constexpr (REAL) {   // one K-block: LA limb tiles of A x L limb boxes of W
+            if constexpr (I8) {   // KPS K-blocks x L digit planes, each into its own accumulator
+              const uint32_t abase = tmem + (uint32_t)(p.L * NT);
+              for (int q = 0; q < nkb; ++q) {
+                const uint32_t a_t = abase + (uint32_t)((st * KPS + q) * C::A_COLS);
+                for (int l = 0; l < p.L; ++l) {
+                  const uint64_t bdesc = sw64_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * BOXB);
+                  const uint32_t id = l == p.L - 1 ? idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 1)    // top digit signed
+                                                   : idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 0);
+                  const uint32_t d = tmem + (uint32_t)(l * NT);
+#pragma unroll
+                  for (int k = 0; k < kBK / 32; ++k) {
+                    if constexpr (PAIR) umma_i8_ts_pair(d, a_t + 8u * k, bdesc + 2u * k, id, issued | (uint32_t)(q | k));
+                    else umma_i8_ts(d, a_t + 8u * k, bdesc + 2u * k, id, issued | (uint32_t)(q | k));
+                  }
+                }
+              }
+            } else if constexpr (REAL) {   // one K-block: LA limb tiles of A x L limb boxes of W
               for (int la = 0; la < p.LA; ++la) {
                 const uint32_t a_t = tmem + (uint32_t)(NT + st * ACOLS + la * C::A_COLS);
                 for (int l = 0; l < p.L; ++l) {
@@ -489,7 +515,34 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     bool any = false;                // has any MMA been issued yet (else F = 0)
     PT(unsigned long long w_gen = 0;)
     const uint16_t* prow_r = prow + (size_t)row * (REAL ? p.pstride : 0);
+    // I8: F_m = qscale * sum_l 256^l acc_l[m], exact in int64
+    auto load_i8 = [&](int c0, long long (&v)[32]) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + (uint32_t)c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = (long long)(int32_t)r[c];
+      for (int l = 1; l < p.L; ++l) {
+        tmem_ld32(lane_base + (uint32_t)(l * NT + c0), r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] += (long long)(int32_t)r[c] << (8 * l);
+      }
+    };
     auto xsum = [&](void) -> double {  // sum over this warp's columns of x_m * F_m (p_m * F_m)
+      if constexpr (I8) {
+        long long acc = 0;
+        for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+          const int mbase = ct * NT + c0;
+          long long v[32];
+          load_i8(c0, v);
+          const uint32_t xw = (mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u;
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if ((xw >> c) & 1u) acc += v[c];
+        }
+        return (double)acc * p.qscale;
+      }
       double acc = 0.0;
       for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
         const int mbase = ct * NT + c0;
@@ -557,7 +610,16 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         PT(const long long tg = clock64();)
         mbar_wait(EMPTY(st), (uint32_t)(((n / NST) & 1) ^ 1));
         PT(w_gen += clock64() - tg;)
-        if (mine) {
+        if (I8 && mine) {
+          tc_fence_after();
+          const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
+          uint32_t w[16];   // byte t of the K-block = bit t: nibble * 0x204081 spreads 4 bits to 4 bytes
+#pragma unroll
+          for (int c = 0; c < 16; ++c) w[c] = (((uint32_t)(bits >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+          tmem_st16(lane_base + (uint32_t)(p.L * NT + (st * KPS + h) * C::A_COLS), w);
+          tmem_st_wait();
+          tc_fence_before();
+        } else if (mine) {
           tc_fence_after();
           const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
           uint32_t w[32];
@@ -601,6 +663,30 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
       const int mbase = ct * NT + c0;
       const uint32_t xw = REAL ? 0u : ((mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u);
+      float g[32];
+      if constexpr (I8) {   // exact integer field; one rounding to fp32 after adding the degree-1 cell
+        long long v[32];
+        if (any) load_i8(c0, v);
+        else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = 0;
+        }
+        // split-K partial fields stay exact: doubles, summed in a fixed order by splitk_reduce
+        double* gdp = (p.field_mode && live && p.n_split > 1)
+                          ? reinterpret_cast<double*>(p.G) + ((size_t)split * p.B + b) * p.N + mbase : nullptr;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const double vd = (double)v[c] * p.qscale;
+          const float pm = split == 0 ? __ldg(p.p1 + mbase + c) : 0.0f;
+          g[c] = (float)(vd + (double)pm);
+          if (gdp && mbase + c < p.N) gdp[c] = vd + (double)pm;
+          if ((xw >> c) & 1u) {
+            sfin += vd;
+            sp += (double)pm;
+          }
+        }
+      }
+      else {
       uint32_t r[32];
       if (any) {
         tmem_ld32(lane_base + (uint32_t)c0, r);
@@ -609,7 +695,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #pragma unroll
         for (int c = 0; c < 32; ++c) r[c] = 0u;
       }
-      float g[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         const float v = __uint_as_float(r[c]);
@@ -623,6 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           sfin += (double)v;
           sp += (double)pm;
         }
+      }
       }
       if constexpr (SA) {   // G[b, j] += s_b * (field of P_m)[j]; column m is unchanged
         const int sv = ssa[row];
@@ -646,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
               if (c < nvalid) gout[c] += sf * g[c];
           }
         }
-      } else if (p.field_mode && live) {
+      } else if (p.field_mode && live && !(I8 && p.n_split > 1)) {
         float* gout = p.G + ((size_t)split * p.B + b) * p.N + mbase;
         const int nvalid = min(32, p.N - mbase);
         if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(gout) & 15) == 0)) {
@@ -707,10 +793,18 @@ __global__ void pack_x_kernel(const uint8_t* __restrict__ X, long long B, int N,
 }
 
 // split-K: sum the per-split partials in a fixed order (deterministic)
+// (gp_double: the int8 path's exact partials, one rounding to fp32 after the sum)
 __global__ void splitk_reduce_kernel(const float* __restrict__ Gp, float* __restrict__ G, long long nG,
-                                     const double* __restrict__ Qp, double* __restrict__ Q, long long nQ, int n_split) {
+                                     const double* __restrict__ Qp, double* __restrict__ Q, long long nQ, int n_split,
+                                     int gp_double) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nG; i += stride) {
+    if (gp_double) {
+      double g = 0.0;
+      for (int s = 0; s < n_split; ++s) g += reinterpret_cast<const double*>(Gp)[(size_t)s * nG + i];
+      G[i] = (float)g;
+      continue;
+    }
     float g = 0.0f;
     for (int s = 0; s < n_split; ++s) g += Gp[(size_t)s * nG + i];
     G[i] = g;
@@ -776,6 +870,8 @@ struct LayoutParams {
   const float* const* strict;    // strict[r] device pointers (r = 0..order)
   const long long* binomT;       // [(N+1) * 7]: C(n, i)
   __nv_bfloat16* Wout;           // [L][Npad][Tpad]
+  uint8_t* Wout8 = nullptr;      // int8 digit planes instead (non-null): [L][n_ct][n_kb][NT][64] bytes
+  double inv_qscale = 1.0;       // cell / qscale = the integer the digits encode
   long long Tpad;
   int N, Npad, L, field_mode, NT;
 };
@@ -809,6 +905,15 @@ __global__ void layout_kernel(const LayoutParams lp) {
       }
     } else if (r == 1 && m < lp.N) {   // the empty tuple (annealing site layouts): W[m, {}] = c({m})
       c = lp.strict[1][m];
+    }
+    if (lp.Wout8) {
+      // two's-complement base-256 digits of q = c / qscale: unsigned low digits, signed top digit
+      const long long q = __double2ll_rn((double)c * lp.inv_qscale);
+      const size_t plane = (size_t)lp.Npad * lp.Tpad;
+      const long long n_kb = lp.Tpad / 64;
+      const size_t off = ((size_t)((m / lp.NT) * n_kb + t / 64) * lp.NT + (m % lp.NT)) * 64 + (t % 64);
+      for (int l = 0; l < lp.L; ++l) lp.Wout8[(size_t)l * plane + off] = (uint8_t)((q >> (8 * l)) & 0xFF);
+      continue;
     }
     // exact split into bf16 limbs: hi + mid + lo
     const __nv_bfloat16 hi = __float2bfloat16_rn(c);

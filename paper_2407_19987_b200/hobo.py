@@ -18,7 +18,7 @@ EXPORTED = [
     "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_import_dense", "hobo_tensor_free", "hobo_tensor_info",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field", "hobo_local_field_host", "hobo_energy_host",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
-    "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats",
+    "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats", "hobo_last_launch_kind",
     "hobo_set_profiling", "hobo_dist_unique_id", "hobo_dist_init", "hobo_dist_finalize", "hobo_dist_info",
     "hobo_last_error",
 ]
@@ -70,6 +70,7 @@ def lib():
         L.hobo_sa_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, P, P, P]
         L.hobo_sa_run.argtypes = [P, U64, I64, I64, D, D, I64, P, P, P, C.POINTER(I64), P]
         L.hobo_last_launch_stats.argtypes = [P, C.POINTER(I64), C.POINTER(D), C.POINTER(D), C.POINTER(D)]
+        L.hobo_last_launch_kind.argtypes = [P, C.POINTER(I)]
         L.hobo_set_profiling.argtypes = [P, I]
         L.hobo_dist_unique_id.argtypes = [P]
         L.hobo_dist_init.argtypes = [I, I, P, I]
@@ -352,10 +353,12 @@ class HoboTensor:
         _check(lib().hobo_set_profiling(self._h, 1 if enable else 0))
 
     def launch_stats(self):
-        """Launches, executed MMA MACs, algorithmic MACs and (profiling on) kernel ms of the last call."""
-        n, mm, am, ms = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        """Launches, executed MMA MACs, algorithmic MACs, (profiling on) kernel ms of the last call, and
+        its MMA kind: i8_planes = int8 digit planes (kind::i8, MACs are 8-bit) or 0 (bf16 limbs)."""
+        n, mm, am, ms, i8 = C.c_int64(), C.c_double(), C.c_double(), C.c_double(), C.c_int()
         _check(lib().hobo_last_launch_stats(self._h, C.byref(n), C.byref(mm), C.byref(am), C.byref(ms)))
-        return dict(launches=n.value, mma_macs=mm.value, algo_macs=am.value, kernel_ms=ms.value)
+        _check(lib().hobo_last_launch_kind(self._h, C.byref(i8)))
+        return dict(launches=n.value, mma_macs=mm.value, algo_macs=am.value, kernel_ms=ms.value, i8_planes=i8.value)
 
 
 # ---- multi-GPU communicator of the library (include/hobo.h, SURVEY 8(e)) ------------------

@@ -2,6 +2,9 @@
 inputs.  Bars (BASELINE.json north_star): bit-exact on integer-coefficient instances;
 |dE|, |dG| <= tau = 1e-5 * sum|H| for fp32 coefficients; argmin exact when the energy gap
 exceeds 2 tau (reading 11), else the returned candidate is within 2 tau."""
+import contextlib
+import os
+
 import numpy as np
 import pytest
 
@@ -41,6 +44,25 @@ def fields(H, torch, t, X):
     G, E = t.local_field(dev(torch, X))
     torch.cuda.synchronize()
     return G.cpu().numpy().astype(np.float64), E.cpu().numpy().astype(np.float64)
+
+
+@contextlib.contextmanager
+def env(name, value):
+    """Set a kernel-choice override (include/hobo.h) for the tensors built inside the block."""
+    old = os.environ.get(name)
+    os.environ[name] = value
+    try:
+        yield
+    finally:
+        if old is None:
+            del os.environ[name]
+        else:
+            os.environ[name] = old
+
+
+def f32(a):
+    """The oracle's exact (long double) values rounded once to fp32, as float64."""
+    return np.asarray(a, np.float64).astype(np.float32).astype(np.float64)
 
 
 def check_argmin(best, E_or, tau, row0=0):
@@ -615,3 +637,72 @@ def test_cta_pair_and_single_paths(H, torch, force):
             del os.environ["HOBO_PAIR"]
         else:
             os.environ["HOBO_PAIR"] = old
+
+
+# ---- int8 digit planes (tcgen05.mma kind::i8): exact integer accumulation --------------------
+@pytest.mark.parametrize("i8", ["1", "0"])
+@pytest.mark.parametrize("order,N,B,seed", [(2, 300, 700, 11), (3, 130, 500, 12), (3, 260, 383, 13), (4, 30, 300, 14),
+                                            (3, 300, 37, 41), (2, 1024, 1000, 2), (5, 16, 200, 15)])
+def test_int8_digit_planes_fp32_cells(H, torch, order, N, B, seed, i8):
+    """U(-1,1) cells lie on a 2^-23 fixed-point grid, so three int8 digit planes (unsigned low
+    digits, signed top digit) hold every cell exactly and the s32 accumulators sum them without
+    rounding: the int8 path's energies and fields equal the oracle's exact values rounded once
+    to fp32 (reading 24).  HOBO_I8=0 keeps the bf16-limb path, within tau."""
+    with env("HOBO_I8", i8):
+        idx, val = uniform_cells(order, N, seed)
+        t, o = H.HoboTensor.import_cells(order, N, idx, val), Oracle.from_cells(order, N, idx, val)
+        X = x_bits(seed, B, N)
+        G, E = fields(H, torch, t, X)
+        assert t.launch_stats()["i8_planes"] == (3 if i8 == "1" else 0)
+        Ee, best = energies(H, torch, t, X)
+    Eo, Go = o.energy(X), o.field(X)
+    if i8 == "1":
+        assert np.array_equal(E, f32(Eo)) and np.array_equal(Ee, f32(Eo)) and np.array_equal(G, f32(Go))
+    else:
+        assert max(np.max(np.abs(E - Eo)), np.max(np.abs(Ee - Eo)), np.max(np.abs(G - Go))) <= o.tau
+    check_argmin(best, Eo, o.tau)
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_int8_digit_planes_integer_instances(H, torch, pair):
+    """Integer instances forced onto the int8 path (1 or 2 digit planes; CTA pairs forced on and
+    off): bit-exact against the oracle like the bf16 path."""
+    with env("HOBO_I8", "1"), env("HOBO_PAIR", pair):
+        cases = [(cfg3_problem(), 1000, 2), (random_integer_problem(3, 300, 41, nterms=800), 1000, None),
+                 (random_integer_problem(4, 40, 6, nterms=300), 200, None), (seating(4), 4096, 1), (tsp(), 64, None),
+                 (random_integer_problem(2, 37, 9, nterms=200), 5, None)]
+        for p, B, want in cases:
+            t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+            X = x_bits(8, B, t.N)
+            G, E = fields(H, torch, t, X)
+            planes = t.launch_stats()["i8_planes"]
+            assert planes >= 1 and (want is None or planes == want), (p.name, planes)
+            Ee, best = energies(H, torch, t, X)
+            Eo = o.energy(X)
+            assert np.array_equal(G, o.field(X)) and np.array_equal(E, Eo) and np.array_equal(Ee, Eo), p.name
+            check_argmin(best, Eo, 0.0)
+
+
+def test_int8_digit_planes_choice(H, torch):
+    """The automatic choice: int8 when it costs fewer tensor-core cycles (3 digit planes at twice
+    the rate vs 3 bf16 limbs; 1 digit vs 1 limb), bf16 when it does not (cfg3: 2 digits vs 1
+    limb), bf16 when the cells are not a <= 3-byte fixed-point grid."""
+    X = x_bits(1, 256, 64)
+    for make, want in ((lambda: H.HoboTensor.import_cells(3, 64, *uniform_cells(3, 64, 1)), 3),
+                       (lambda: H.HoboTensor.import_cells(3, 64, *int_twin_cells(3, 64, 1)), 1),
+                       (lambda: H.HoboTensor.from_problem(random_integer_problem(3, 64, 2, nterms=50)), None)):
+        t = make()
+        t.energy(dev(torch, X))
+        got = t.launch_stats()["i8_planes"]
+        assert (got == want) if want is not None else got in (0, 1)
+    p = cfg3_problem()
+    t = H.HoboTensor.from_problem(p)
+    t.local_field(dev(torch, x_bits(3, 128, 512)))
+    assert t.launch_stats()["i8_planes"] == 0
+    idx, val = uniform_cells(2, 64, 3)
+    val = val.copy()
+    val[np.flatnonzero(idx[:, 0] != idx[:, 1])[0]] = np.float32(3.0e-12)   # a degree-2 cell with a ~2^-62
+    # quantum next to O(1) cells: no 3-byte fixed-point grid holds both
+    t = H.HoboTensor.import_cells(2, 64, idx, val)
+    t.energy(dev(torch, X))
+    assert t.launch_stats()["i8_planes"] == 0
