@@ -379,6 +379,11 @@ def main():
     exec_flops = 2.0 * st["mma_macs"]
     kms = statistics.mean(kern_ms)
     burst, sustained, src = measured_peaks()
+    # int8 digit planes (kind::i8): the peak for that dtype is the measured bf16 peak x the
+    # nominal ratio 4.5 / 2.25 PFLOP/s = 2 (also measured: tools/mma_i8.cu, 8192 vs 4096 MAC/clk/SM)
+    i8 = st.get("i8_planes", 0)
+    kind_ratio = 2.0 if i8 else 1.0
+    burst, sustained = burst * kind_ratio, sustained * kind_ratio
     # the timed region is ~0.3 s of back-to-back ~7 ms steps with clocks at max (see "clocks"):
     # judged against the BURST figure; the sustained (power-capped) ratio is reported beside it
     peak = burst
@@ -393,11 +398,12 @@ def main():
     except Exception:
         pass
     import math
-    NTt = 128 if N <= 128 else 256                                  # the layout's column tile
+    NTt = 128 if (N <= 128 or i8 >= 2) else 256                      # the layout's column tile
     Npad = (N + NTt - 1) // NTt * NTt
     Tpad = sum((math.comb(N, r - 1) + 63) // 64 * 64 for r in range(2, t.order + 1))
     nct = Npad // NTt
-    algo_bytes = (t.limbs * Npad * Tpad * 2 + B * ((N + 31) // 32) * 4 + (B * N * 4 if mode == "field" else B * 4)
+    wbytes = i8 * Npad * Tpad if i8 else t.limbs * Npad * Tpad * 2    # int8 digit planes / bf16 limb planes
+    algo_bytes = (wbytes + B * ((N + 31) // 32) * 4 + (B * N * 4 if mode == "field" else B * 4)
                   + nct * B * 8)                                    # W once, X bits, G (or E), Q
     # below the ridge (few candidates per W byte) the W stream from HBM binds instead
     ridge = burst * 1e12 / (hbm_peak * 1e9)
@@ -408,16 +414,19 @@ def main():
             "achieved": achieved_b if hbm_bound else achieved, "peak": hbm_peak if hbm_bound else peak,
             "unit": "GB/s" if hbm_bound else "TFLOP/s",
             "frac": (achieved_b / hbm_peak) if hbm_bound else achieved / peak, "tflops_algorithmic": achieved,
-            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": f"kr_gemm_kernel<{NTt}> (open-index contraction, {mode} mode)",
+            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": f"kr_gemm_kernel<{NTt}{', I8' if i8 else ''}> (open-index contraction, {mode} mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms, "launches_per_step": launches / max(1, a.steps),
             "algorithmic_flops_per_launch": algo_flops, "executed_mma_flops_per_launch": exec_flops,
             "executed_tflops": exec_flops / (kms / 1e3) / 1e12, "frac_of_sustained": achieved / sustained,
-            "peak_source": f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s"}
+            "mma_kind": f"i8 ({i8} digit planes, s32 accumulate)" if i8 else f"bf16 ({t.limbs} limbs, fp32 accumulate)",
+            "peak_source": (f"{src} bf16 dense (MEASURED_PEAKS.json) x 2 (nominal i8/bf16 ratio): burst {burst}, "
+                            f"sustained {sustained} TOP/s" if i8 else
+                            f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s")}
     # the tensor cores' own rate at this run's clock (4096 bf16 MAC/clk/SM, measured by
     # tools/mma_ceiling.cu); the cuBLAS-measured burst above is taken on random operands,
     # which toggle more than this path's {0,1} x small-integer operands, so frac can exceed 1
     mhz = clocks.get("sm_mhz") or 1965.0
-    hw = 2 * 4096 * 148 * mhz * 1e6 / 1e12
+    hw = 2 * 4096 * 148 * mhz * 1e6 / 1e12 * kind_ratio
     roof["hw_nominal_tflops"] = hw
     roof["frac_exec_of_hw_nominal"] = roof["executed_tflops"] / hw
 
@@ -502,7 +511,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "vs_baseline": None, "dtype": "i8" if i8 else "bf16", "data": "synthetic",
                 "config": {"workload": wl_text, "name": a.config, "order": t.order, "N": N, "batch_per_gpu": B,
                            "limbs": t.limbs, "global_batch": units,
                            "parallelism": f"dp{world} (H replicated, batch sharded)",

@@ -363,7 +363,7 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
   L.n_ct = (N + L.NT - 1) / L.NT;
   L.Npad = L.n_ct * L.NT;
-  const int64_t Tpad = std::max<int64_t>(t->kl.Tpad, kBK);
+  const int64_t Tpad = std::max<int64_t>(t->kl.Tpad, 2 * kBK);   // (a multiple of 2 K-blocks)
   const double bytes = (double)planes * L.Npad * Tpad * (L.i8 ? 1.0 : 2.0);
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
@@ -395,7 +395,7 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
     lp.strict = d_strict_ptrs;
     lp.binomT = d_bt;
     lp.Wout = L.W;
-    lp.Tpad = t->kl.Tpad;
+    lp.Tpad = Tpad;
     lp.N = N;
     lp.Npad = L.Npad;
     lp.L = planes;
@@ -419,19 +419,20 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled unavailable");
   // 3-D view of the tile-blocked planes: (64 tuples, NT rows, box index), box = one block
-  // (int8 digit planes: 64-byte rows, 64-byte swizzle)
+  // (int8 digit planes: 128-byte rows = K-block pairs, boxes (128 tuples, NT rows, pair index))
   const int64_t n_kb = Tpad / kBK;
-  const cuuint64_t esz = L.i8 ? 1 : 2;
+  const int inner = L.i8 ? 2 * kBK : kBK;          // elements per 128-byte box row
+  const int64_t nbox = L.i8 ? n_kb / 2 : n_kb;
   const CUtensorMapDataType dt = L.i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  const CUtensorMapSwizzle sw = L.i8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)L.NT, (cuuint64_t)planes * L.n_ct * n_kb};
-  cuuint64_t strides[2] = {(cuuint64_t)kBK * esz, (cuuint64_t)kBK * esz * L.NT};
-  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)L.NT, 1};
+  const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)L.NT, (cuuint64_t)planes * L.n_ct * nbox};
+  cuuint64_t strides[2] = {128, (cuuint64_t)128 * L.NT};
+  cuuint32_t box[3] = {(cuuint32_t)inner, (cuuint32_t)L.NT, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult cr = enc(&L.tmap, dt, 3, L.W, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-  cuuint32_t box_half[3] = {(cuuint32_t)kBK, (cuuint32_t)(L.NT / 2), 1};
+  cuuint32_t box_half[3] = {(cuuint32_t)inner, (cuuint32_t)(L.NT / 2), 1};
   cr = enc(&L.tmap_half, dt, 3, L.W, dims, strides, box_half, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(HOBO_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
@@ -468,7 +469,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.Npad = L.Npad;
   p.n_ct = L.n_ct;
   p.n_cb = (int)((B + kBM - 1) / kBM);
-  p.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, kBK) / kBK);
+  p.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, 2 * kBK) / kBK);
   p.n_split = 1;
   p.preal = nullptr;
   p.LA = 1;
@@ -1844,9 +1845,9 @@ hobo_status hobo_last_launch_kind(const hobo_tensor* t, int* i8_planes) {
 
 #ifdef HOBO_PIPE_STATS
 // debug builds only: copy (and reset) the per-CTA pipeline counters
-hobo_status hobo_debug_pipe_stats(unsigned long long* out /* 8192 x 8 */) {
+hobo_status hobo_debug_pipe_stats(unsigned long long* out /* 8192 x 16 */) {
   if (cudaMemcpyFromSymbol(out, g_pipe_stats, sizeof(g_pipe_stats)) != cudaSuccess) return HOBO_ECUDA;
-  static unsigned long long zeros[8192][8];
+  static unsigned long long zeros[8192][16];
   cudaMemcpyToSymbol(g_pipe_stats, zeros, sizeof(zeros));
   return HOBO_OK;
 }

@@ -392,8 +392,8 @@ int build_klayout(int order, int N, KLayout& k, std::string& msg) {
     const int64_t len = binom(N, r - 1);
     k.seg_t0.push_back(T);
     k.seg_len.push_back(len);
-    T += (len + KBLK - 1) / KBLK * KBLK;
-  }
+    T += (len + 2 * KBLK - 1) / (2 * KBLK) * (2 * KBLK);   // segments start at even K-blocks (int8
+  }                                                       // boxes hold K-block pairs)
   k.Tpad = T;
   if ((double)T * 12.0 > 4.0e9) { msg = "K dimension too large"; return 3; }
   k.tuples.assign((size_t)T * 6, 0);

@@ -44,7 +44,8 @@ void export_cells(const HostTensor& t, int32_t* idx, float* val);   // lexicogra
 int export_dense(const HostTensor& t, float* out);                   // 0 ok, 3 too large
 
 // K-dimension of the open-index contraction: segments of (r-1)-subsets (r = order..2), each
-// in colex order and padded to a multiple of KBLK tuples.
+// in colex order and padded to a multiple of 2 KBLK tuples (so every segment starts at an
+// even K-block: the int8 digit planes' 128-byte boxes hold K-block pairs).
 constexpr int KBLK = 64;
 struct KLayout {
   int order = 0, N = 0, nseg = 0;

@@ -62,17 +62,19 @@ struct KrParams {
   int sa_m, sa_prev;        // visited site, previous site (-1: none)
 };
 
-// I8: W as int8 digit planes (one byte per tuple: NT rows x 64 bytes, SW64) against A as
-// {0,1} bytes, tcgen05.mma kind::i8 at twice the bf16 rate, one s32 accumulator per digit plane
+// I8: W as int8 digit planes (one byte per tuple; a box row = 128 bytes = the K-block pair
+// (2i, 2i+1), SW128) against A as {0,1} bytes, tcgen05.mma kind::i8 at twice the bf16 rate,
+// one s32 accumulator per digit plane
 template <int NT, bool I8 = false>
 struct KrCfg {
-  static constexpr int BOX = NT * (I8 ? 64 : 128);       // one TMA box: NT rows x 64 tuples (bf16 SW128 / int8 SW64)
-  static constexpr int RING_BOXES = (I8 ? 12 : 6) * 256 / NT;   // shared-memory budget for W (192 KB), in boxes
-  static constexpr int MAXST = (I8 || NT < 256) ? 6 : 4; // max pipeline stages (4 at NT=256: CTA pairs' half boxes)
+  static constexpr int BOX = NT * 128;                   // one TMA box: NT rows x 64 bf16 tuples / 128 int8 tuples (SW128)
+  static constexpr int RING_BOXES = 6 * 256 / NT;        // shared-memory budget for W (192 KB), in boxes
+  static constexpr int MAXST = I8 ? 8 : NT < 256 ? 6 : 4;  // max W stages (4 at NT=256: CTA pairs' half boxes)
+  static constexpr int MAXA = I8 ? 8 : 0;                // I8: A stages, a ring of their own (TMEM-bound)
   static constexpr int A_COLS = I8 ? kBK / 4 : kBK / 2;  // TMEM columns of one K-block of A (64 bf16 / 64 bytes per lane)
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator (I8: L of them), then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
-  static constexpr int NBAR = 2 * MAXST + 3;
+  static constexpr int NBAR = 2 * MAXST + 2 * MAXA + 3;
   static size_t smem_bytes(int W) {
     return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)(W + 2) * kBM * 4 + 128;
   }
@@ -80,10 +82,12 @@ struct KrCfg {
   // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
   // boxes that fits only at L = 1, with 128-column boxes at every L <= 3
   __host__ __device__ static constexpr int kps(int L) { return (I8 || L == 1 || NT <= 128) ? 2 : 1; }
-  // I8 stages: bounded by the ring (pairs: twice the boxes), MAXST and the TMEM left after the L accumulators
-  __host__ __device__ static constexpr int nst_i8(int L, int ring) {
-    return ring / (2 * L) < MAXST ? (ring / (2 * L) < (TMEM_COLS - L * NT) / (2 * A_COLS) ? ring / (2 * L) : (TMEM_COLS - L * NT) / (2 * A_COLS))
-                                  : (MAXST < (TMEM_COLS - L * NT) / (2 * A_COLS) ? MAXST : (TMEM_COLS - L * NT) / (2 * A_COLS));
+  // I8 stages (one box per digit plane = 2 K-blocks).  The W ring and the A ring are separate:
+  // W stages are bounded by shared memory (pairs: twice the boxes) and MAXST, A stages by the
+  // TMEM left after the L accumulators
+  __host__ __device__ static constexpr int nst_i8(int L, int ring) { return ring / L < MAXST ? ring / L : MAXST; }
+  __host__ __device__ static constexpr int nsta_i8(int L) {
+    return (TMEM_COLS - L * NT) / (2 * A_COLS) < MAXA ? (TMEM_COLS - L * NT) / (2 * A_COLS) : MAXA;
   }
   __host__ __device__ static constexpr int nst(int L) { return RING_BOXES / (kps(L) * L) < MAXST ? RING_BOXES / (kps(L) * L) : MAXST; }
   // real-valued A: one K-block per stage, LA limb tiles of A in TMEM, ring sized at run time
@@ -205,14 +209,34 @@ __device__ __forceinline__ void real_block(const uint16_t* pr, const uint4 d0, c
 #ifdef HOBO_PIPE_STATS
 // debug builds only: per-CTA pipeline accounting (clock64 cycles), accumulated in registers
 //  [0] MMA loop  [1] MMA waiting FULL  [2] stages  [3] K-blocks  [4] issuing MMAs  [5] commits
-//  [6] TMA waiting EMPTY  [7] gen warp waiting EMPTY
-__device__ unsigned long long g_pipe_stats[8192][8];
+//  [6] TMA waiting EMPTY  [7] gen warp waiting EMPTY  [8] gen A bits  [9] gen TMEM store + wait
+//  [10] gen arrive
+__device__ unsigned long long g_pipe_stats[8192][16];
 #define PSTAT_FLUSH(i, v) atomicAdd(&g_pipe_stats[blockIdx.x & 8191][i], (unsigned long long)(v))
 #define PT(...) __VA_ARGS__
 #else
 #define PSTAT_FLUSH(i, v)
 #define PT(...)
 #endif
+
+// int8 digit planes, the common stage (both K-blocks of the box pair) fully unrolled: L planes
+// x 4 MMAs of K = 32, each plane into its own s32 accumulator (top digit signed); only the
+// first MMA of a plane in the first stage starts the accumulator
+template <int L, int NT, bool PAIR>
+__device__ __forceinline__ void issue_i8_stage(uint32_t tmem, uint32_t a_t, uint32_t sbase, uint32_t boxb, uint32_t issued) {
+  constexpr uint32_t id_u = idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 0), id_s = idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 1);
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const uint64_t bd = sw128_kmajor_desc(sbase + (uint32_t)l * boxb);
+    const uint32_t d = tmem + (uint32_t)(l * NT);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint32_t acc = kk ? 1u : issued;
+      if constexpr (PAIR) umma_i8_ts_pair(d, a_t + 8u * kk, bd + 2u * kk, l == L - 1 ? id_s : id_u, acc);
+      else umma_i8_ts(d, a_t + 8u * kk, bd + 2u * kk, l == L - 1 ? id_s : id_u, acc);
+    }
+  }
+}
 
 // One pipeline stage = KPS consecutive K-blocks of one segment (x L limb boxes of W).
 // Ring slot s holds the stage's W boxes in shared memory and its A K-blocks in TMEM;
@@ -234,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t sB = base;
   const int ring = REAL ? p.ring_boxes : C::RING_BOXES;
   const uint32_t sBar = sB + ring * C::BOX;
-  const uint32_t acc_full = sBar + 8 * (2 * C::MAXST);
+  const uint32_t acc_full = sBar + 8 * (2 * C::MAXST + 2 * C::MAXA);
   const uint32_t snap_full = acc_full + 8, snap_empty = acc_full + 16;
   const uint32_t tslot = acc_full + 24;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
@@ -245,6 +269,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
 #define FULL(s) (sBar + 8u * (s))
 #define EMPTY(s) (sBar + 8u * (C::MAXST + (s)))
+#define FULLA(s) (sBar + 8u * (2 * C::MAXST + (s)))
+#define EMPTYA(s) (sBar + 8u * (2 * C::MAXST + C::MAXA + (s)))
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // block order: candidate block fastest, then column tile, then K split (concurrent CTAs
@@ -264,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
                  : I8 ? C::nst_i8(p.L, PAIR ? 2 * ring : ring)
                       : (PAIR ? min(2 * C::RING_BOXES / (KPS * p.L), C::MAXST) : C::nst(p.L));
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
+  const int NSTA = I8 ? C::nsta_i8(p.L) : NST;                     // A stages (I8: own ring)
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
   __shared__ int ssa[SA ? kBM : 1];   // annealing: this CTA's decisions for site sa_m
   if (threadIdx.x == 0) {
@@ -282,14 +309,15 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       s0 += ns;
     }
   }
-  const uint32_t stage_bytes = (uint32_t)(KPS * p.L) * BOXB;
+  const uint32_t stage_bytes = (uint32_t)((I8 ? 1 : KPS) * p.L) * BOXB;
   // segments run in ascending degree order (j = nseg-1 .. 0); in field mode the single
   // accumulator is snapshot after each degree so the energy can weight degree r by 1/r
   const bool snaps = p.field_mode != 0 && !SA;
 
   if (threadIdx.x == 0) {
     // FULL: the TMA arrive + 8 generator warps (pairs: + the peer's 8, on the leader only)
-    for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), PAIR ? 17 : 9); mbar_init(EMPTY(s), 1); }
+    for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), I8 ? 1 : PAIR ? 17 : 9); mbar_init(EMPTY(s), 1); }
+    for (int s = 0; s < C::MAXA; ++s) { mbar_init(FULLA(s), PAIR ? 16 : 8); mbar_init(EMPTYA(s), 1); }
     mbar_init(acc_full, 1);
     mbar_init(snap_full, 1);
     mbar_init(snap_empty, PAIR ? 16 : 8);
@@ -369,25 +397,36 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   } else if (warp == 0) {
     // ---------------- TMA producer: W limb boxes (NT rows x 64 tuples, SW128) ---------------
     if (lane == 0) {
-      int n = 0;
+      int st = 0;                    // ring slot and phase, advanced per stage (no divisions)
+      uint32_t ph = 0;
       PT(unsigned long long w_tma = 0;)
       for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
-        for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS, ++n) {
+        for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
           const int nkb = min(KPS, s.x + s.y - kb0);
-          const int st = n % NST;
           PT(const long long t0 = clock64();)
-          mbar_wait(EMPTY(st), (uint32_t)(((n / NST) & 1) ^ 1));
+          mbar_wait(EMPTY(st), ph ^ 1u);
           PT(w_tma += clock64() - t0;)
-          if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)(nkb * p.L) * C::BOX);   // pairs: both halves
-          for (int q = 0; q < nkb; ++q)
+          if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
+            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)p.L * C::BOX);
             for (int l = 0; l < p.L; ++l) {
-              // W is tile-blocked: box (l, ct, kb) is one contiguous NT x 64 block
-              const int box = (l * p.n_ct + ct) * p.n_kb + kb0 + q;
-              const uint32_t dst = sB + st * stage_bytes + (uint32_t)(q * p.L + l) * BOXB;
+              const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1);
+              const uint32_t dst = sB + st * stage_bytes + (uint32_t)l * BOXB;
               if constexpr (PAIR) tma_load_3d_pair(dst, &tmap, mapa_shared(FULL(st), 0), 0, (int)prank * (NT / 2), box);
               else tma_load_3d(dst, &tmap, FULL(st), 0, 0, box);
             }
+          } else {
+            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)(nkb * p.L) * C::BOX);   // pairs: both halves
+            for (int q = 0; q < nkb; ++q)
+              for (int l = 0; l < p.L; ++l) {
+                // W is tile-blocked: box (l, ct, kb) is one contiguous NT x 64 block
+                const int box = (l * p.n_ct + ct) * p.n_kb + kb0 + q;
+                const uint32_t dst = sB + st * stage_bytes + (uint32_t)(q * p.L + l) * BOXB;
+                if constexpr (PAIR) tma_load_3d_pair(dst, &tmap, mapa_shared(FULL(st), 0), 0, (int)prank * (NT / 2), box);
+                else tma_load_3d(dst, &tmap, FULL(st), 0, 0, box);
+              }
+          }
+          if (++st == NST) { st = 0; ph ^= 1u; }
         }
       }
       PSTAT_FLUSH(6, w_tma);
@@ -398,34 +437,40 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     // registers; one elected lane issues the MMAs and commits.
     if (leader) {
       constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * kBM : kBM, NT);
-      int n = 0, snap = 0;
+      int snap = 0;
+      int st = 0, sa = 0;            // W and A ring slots and phases, advanced per stage
+      uint32_t ph = 0, pha = 0;
       uint32_t issued = 0;
       PT(unsigned long long stt[6] = {0, 0, 0, 0, 0, 0}; const long long t_start = clock64(); long long t0;)
       for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
-        for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS, ++n) {
+        for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
           const int nkb = min(KPS, s.x + s.y - kb0);
-          const int st = n % NST;
           PT(t0 = clock64();)
-          mbar_wait(FULL(st), (uint32_t)((n / NST) & 1));
+          mbar_wait(FULL(st), ph);
+          if (I8) mbar_wait(FULLA(sa), pha);
           PT(stt[1] += clock64() - t0; stt[2] += 1; stt[3] += nkb; t0 = clock64();)
           tc_fence_after();
           if (elect_one()) {
             if constexpr (I8) {   // KPS K-blocks x L digit planes, each into its own accumulator
-              const uint32_t abase = tmem + (uint32_t)(p.L * NT);
-              for (int q = 0; q < nkb; ++q) {
-                const uint32_t a_t = abase + (uint32_t)((st * KPS + q) * C::A_COLS);
-                for (int l = 0; l < p.L; ++l) {
-                  const uint64_t bdesc = sw64_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * BOXB);
-                  const uint32_t id = l == p.L - 1 ? idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 1)    // top digit signed
-                                                   : idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 0);
-                  const uint32_t d = tmem + (uint32_t)(l * NT);
+              const uint32_t a_t = tmem + (uint32_t)(p.L * NT + sa * KPS * C::A_COLS);
+              const uint32_t sbase = sB + st * stage_bytes;
+              if (nkb == 2 && p.L == 3) issue_i8_stage<3, NT, PAIR>(tmem, a_t, sbase, BOXB, issued);
+              else if (nkb == 2 && p.L == 2) issue_i8_stage<2, NT, PAIR>(tmem, a_t, sbase, BOXB, issued);
+              else if (nkb == 2 && p.L == 1) issue_i8_stage<1, NT, PAIR>(tmem, a_t, sbase, BOXB, issued);
+              else
+              for (int l = 0; l < p.L; ++l) {
+                const uint64_t bdesc = sw128_kmajor_desc(sbase + (uint32_t)l * BOXB);
+                const uint32_t id = l == p.L - 1 ? idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 1)    // top digit signed
+                                                 : idesc_i8_s32(PAIR ? 2 * kBM : kBM, NT, 0);
+                const uint32_t d = tmem + (uint32_t)(l * NT);
+                for (int q = 0; q < nkb; ++q)
 #pragma unroll
-                  for (int k = 0; k < kBK / 32; ++k) {
-                    if constexpr (PAIR) umma_i8_ts_pair(d, a_t + 8u * k, bdesc + 2u * k, id, issued | (uint32_t)(q | k));
-                    else umma_i8_ts(d, a_t + 8u * k, bdesc + 2u * k, id, issued | (uint32_t)(q | k));
+                  for (int k = 0; k < kBK / 32; ++k) {   // 32 bytes of K per MMA: 8 A columns, 2 descriptor units
+                    const uint32_t kk = (uint32_t)(2 * q + k);
+                    if constexpr (PAIR) umma_i8_ts_pair(d, a_t + 8u * kk, bdesc + 2u * kk, id, issued | kk);
+                    else umma_i8_ts(d, a_t + 8u * kk, bdesc + 2u * kk, id, issued | kk);
                   }
-                }
               }
             } else if constexpr (REAL) {   // one K-block: LA limb tiles of A x L limb boxes of W
               for (int la = 0; la < p.LA; ++la) {
@@ -467,10 +512,16 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             PT(stt[4] += clock64() - t0; t0 = clock64();)
             if constexpr (PAIR) umma_commit_pair(EMPTY(st), 3);
             else umma_commit(EMPTY(st));
+            if constexpr (I8) {
+              if constexpr (PAIR) umma_commit_pair(EMPTYA(sa), 3);
+              else umma_commit(EMPTYA(sa));
+            }
             PT(stt[5] += clock64() - t0;)
           }
           __syncwarp();
           issued = 1;
+          if (++st == NST) { st = 0; ph ^= 1u; }
+          if (I8 && ++sa == NSTA) { sa = 0; pha ^= 1u; }
         }
         if (snaps && j > 0) {  // hand the degree-(k-j) partial sum to the epilogue warps
           if (elect_one()) {
@@ -512,8 +563,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     double S[8];                     // S[r]: sum_m x_m F_m over this warp's columns after degree r
     int nsnap = 0;
     int n = 0;                       // stage counter (same sequence as the MMA issuer)
+    int gst = 0;                     // binary path: A slot and phase, advanced per stage
+    uint32_t gph = 0;
     bool any = false;                // has any MMA been issued yet (else F = 0)
-    PT(unsigned long long w_gen = 0;)
+    PT(unsigned long long w_gen = 0, w_bits = 0, w_st = 0, w_arr = 0;)
     const uint16_t* prow_r = prow + (size_t)row * (REAL ? p.pstride : 0);
     // I8: F_m = qscale * sum_l 256^l acc_l[m], exact in int64
     auto load_i8 = [&](int c0, long long (&v)[32]) {
@@ -599,20 +652,41 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           d1 = n1;
         }
       } else {
-      uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
-      if (h < s.y) { d0 = __ldg(p.kdesc + 2 * (s.x + h)); d1 = __ldg(p.kdesc + 2 * (s.x + h) + 1); }
-      for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS, ++n) {
+      // this team's K-block descriptors, prefetched three stages ahead (d: this stage, e, f:
+      // the next two)
+      const int kend = s.x + s.y;
+      auto ldk = [&](int kb, uint4& a, uint4& b) {
+        if (kb < kend) { a = __ldg(p.kdesc + 2 * kb); b = __ldg(p.kdesc + 2 * kb + 1); }
+      };
+      uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0, e0 = d0, e1 = d0, f0 = d0, f1 = d0;
+      ldk(s.x + h, d0, d1);
+      ldk(s.x + h + KPS, e0, e1);
+      ldk(s.x + h + 2 * KPS, f0, f1);
+      for (int kb0 = s.x; kb0 < kend; kb0 += KPS) {
         const int kb = kb0 + h;                       // this team's K-block of the stage
-        const bool mine = h < KPS && kb < s.x + s.y;
-        uint4 n0 = d0, n1 = d1;                       // prefetch the next stage's descriptor
-        if (kb + KPS < s.x + s.y) { n0 = __ldg(p.kdesc + 2 * (kb + KPS)); n1 = __ldg(p.kdesc + 2 * (kb + KPS) + 1); }
-        const int st = n % NST;
+        const bool mine = h < KPS && kb < kend;
+        uint4 n0 = f0, n1 = f1;
+#ifdef HOBO_PIPE_STATS
+        if (!(p.dbg & 1))   // bisection: 1 = reuse the descriptors (wrong A, timing only)
+#endif
+        ldk(kb + 3 * KPS, n0, n1);
+        const int st = gst;                           // A slot (I8: its own ring; else == the W slot)
+        // the A bits depend only on the candidates: computed before the slot frees up
+        PT(const long long tb = clock64();)
+        uint64_t bits = 0ull;
+#ifdef HOBO_PIPE_STATS
+        if (p.dbg & 2) bits = mine ? (uint64_t)d0.x * 0x9E3779B97F4A7C15ull ^ xs[row] : 0ull;   // 2 = no run decoding
+        else
+#endif
+        bits = mine ? block_bits(xs, row, d0, d1, p.runs) : 0ull;
+        PT(w_bits += clock64() - tb;)
         PT(const long long tg = clock64();)
-        mbar_wait(EMPTY(st), (uint32_t)(((n / NST) & 1) ^ 1));
+        mbar_wait(I8 ? EMPTYA(st) : EMPTY(st), gph ^ 1u);
         PT(w_gen += clock64() - tg;)
+        if (++gst == NSTA) { gst = 0; gph ^= 1u; }
+        PT(const long long ts = clock64();)
         if (I8 && mine) {
           tc_fence_after();
-          const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
           uint32_t w[16];   // byte t of the K-block = bit t: nibble * 0x204081 spreads 4 bits to 4 bytes
 #pragma unroll
           for (int c = 0; c < 16; ++c) w[c] = (((uint32_t)(bits >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
@@ -621,7 +695,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           tc_fence_before();
         } else if (mine) {
           tc_fence_after();
-          const uint64_t bits = block_bits(xs, row, d0, d1, p.runs);
           uint32_t w[32];
           expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
           expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
@@ -629,13 +702,21 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           tmem_st_wait();
           tc_fence_before();
         }
+        PT(w_st += clock64() - ts;)
+        PT(const long long ta = clock64();)
         __syncwarp();
         if (lane == 0) {
-          if (PAIR && !leader) mbar_arrive_remote(mapa_shared(FULL(st), 0));
-          else mbar_arrive(FULL(st));
+          const uint32_t fb = I8 ? FULLA(st) : FULL(st);
+          if (PAIR && !leader) mbar_arrive_remote(mapa_shared(fb, 0));
+          else mbar_arrive(fb);
         }
-        d0 = n0;
-        d1 = n1;
+        PT(w_arr += clock64() - ta;)
+        d0 = e0;
+        d1 = e1;
+        e0 = f0;
+        e1 = f1;
+        f0 = n0;
+        f1 = n1;
       }
       }
       any = any || s.y > 0;
@@ -654,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     }
 
     // ---------------- epilogue: fields, energy partial (this warp's column half) ---------------
-    PT(if (warp == 2 && lane == 0) PSTAT_FLUSH(7, w_gen);)
+    PT(if (warp == 2 && lane == 0) { PSTAT_FLUSH(7, w_gen); PSTAT_FLUSH(8, w_bits); PSTAT_FLUSH(9, w_st); PSTAT_FLUSH(10, w_arr); })
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const long long b = b0 + row;
@@ -767,6 +848,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   }
 #undef FULL
 #undef EMPTY
+#undef FULLA
+#undef EMPTYA
   tc_fence_before();
   if constexpr (PAIR) {
     cluster_sync_all();   // the leader's last MMAs wrote both CTAs' TMEM
@@ -870,7 +953,7 @@ struct LayoutParams {
   const float* const* strict;    // strict[r] device pointers (r = 0..order)
   const long long* binomT;       // [(N+1) * 7]: C(n, i)
   __nv_bfloat16* Wout;           // [L][Npad][Tpad]
-  uint8_t* Wout8 = nullptr;      // int8 digit planes instead (non-null): [L][n_ct][n_kb][NT][64] bytes
+  uint8_t* Wout8 = nullptr;      // int8 digit planes instead (non-null): [L][n_ct][n_kb/2][NT][128] bytes
   double inv_qscale = 1.0;       // cell / qscale = the integer the digits encode
   long long Tpad;
   int N, Npad, L, field_mode, NT;
@@ -910,8 +993,8 @@ __global__ void layout_kernel(const LayoutParams lp) {
       // two's-complement base-256 digits of q = c / qscale: unsigned low digits, signed top digit
       const long long q = __double2ll_rn((double)c * lp.inv_qscale);
       const size_t plane = (size_t)lp.Npad * lp.Tpad;
-      const long long n_kb = lp.Tpad / 64;
-      const size_t off = ((size_t)((m / lp.NT) * n_kb + t / 64) * lp.NT + (m % lp.NT)) * 64 + (t % 64);
+      const long long n_kbp = lp.Tpad / 128;   // boxes of 128-byte rows: K-block pairs
+      const size_t off = ((size_t)((m / lp.NT) * n_kbp + t / 128) * lp.NT + (m % lp.NT)) * 128 + (t % 128);
       for (int l = 0; l < lp.L; ++l) lp.Wout8[(size_t)l * plane + off] = (uint8_t)((q >> (8 * l)) & 0xFF);
       continue;
     }

@@ -112,16 +112,6 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
-// K-major operand in SWIZZLE_64B (8-row x 64-byte atoms, SBO = 512 B): the int8 W boxes
-// (64 tuples = 64 bytes per row)
-__device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t smem_addr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-  d |= (uint64_t)(512 >> 4) << 32;   // SBO
-  d |= (uint64_t)1 << 46;            // version (sm_100)
-  d |= (uint64_t)4 << 61;            // SWIZZLE_64B
-  return d;
-}
 // kind::i8 instruction descriptor: A unsigned 8-bit, B unsigned (bsigned = 0) or signed 8-bit,
 // D s32
 __host__ __device__ constexpr uint32_t idesc_i8_s32(int M, int N, int bsigned) {

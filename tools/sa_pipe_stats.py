@@ -23,7 +23,7 @@ t0 = t.default_t_start()
 t.sa_shard(1, 0, B, 1, t0, t0 / 10)
 torch.cuda.synchronize()
 L = hobo.lib()
-buf = np.zeros((8192, 8), np.uint64)
+buf = np.zeros((8192, 16), np.uint64)
 L.hobo_debug_pipe_stats(buf.ctypes.data_as(C.c_void_p))        # read + clear
 t.set_profiling(True)
 t.sa_shard(1, 0, B, 1, t0, t0 / 10)
