@@ -75,8 +75,9 @@ struct KrCfg {
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator (I8: L of them), then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
   static constexpr int NBAR = 2 * MAXST + 2 * MAXA + 3;
+  static constexpr int DESC_BYTES = I8 ? MAXST * 64 : 0;   // I8: the stages' K-block descriptors, copied by TMA
   static size_t smem_bytes(int W) {
-    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)(W + 2) * kBM * 4 + 128;
+    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + DESC_BYTES + (size_t)(W + 2) * kBM * 4 + 128;
   }
   // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages.  Two
   // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
@@ -262,7 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t snap_full = acc_full + 8, snap_empty = acc_full + 16;
   const uint32_t tslot = acc_full + 24;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
-  const uint32_t sX = sQ + kBM * 8;
+  const uint32_t sD = sQ + kBM * 8;                               // I8: descriptor ring (one slot per W stage)
+  const uint32_t sX = sD + C::DESC_BYTES;
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
   uint16_t* prow = reinterpret_cast<uint16_t*>(gbase + (sX - base));   // REAL: p rows [128][pstride]
   double* qpart = reinterpret_cast<double*>(gbase + (sQ - base));
@@ -408,7 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           mbar_wait(EMPTY(st), ph ^ 1u);
           PT(w_tma += clock64() - t0;)
           if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
-            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)p.L * C::BOX);
+            // + the stage's K-block descriptors for this CTA's A generator, on this CTA's FULL
+            // (the peer of a pair: its FULL carries only them)
+            const uint32_t dbytes = (uint32_t)nkb * 32u;
+            mbar_arrive_expect_tx(FULL(st), (leader ? (uint32_t)p.L * C::BOX : 0u) + dbytes);
+            bulk_g2s(sD + (uint32_t)st * 64u, p.kdesc + 2 * kb0, dbytes, FULL(st));
             for (int l = 0; l < p.L; ++l) {
               const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1);
               const uint32_t dst = sB + st * stage_bytes + (uint32_t)l * BOXB;
@@ -565,6 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     int n = 0;                       // stage counter (same sequence as the MMA issuer)
     int gst = 0;                     // binary path: A slot and phase, advanced per stage
     uint32_t gph = 0;
+    int wst = 0;                     // I8: the W slot and phase (its descriptors)
+    uint32_t wph = 0;
     bool any = false;                // has any MMA been issued yet (else F = 0)
     PT(unsigned long long w_gen = 0, w_bits = 0, w_st = 0, w_arr = 0;)
     const uint16_t* prow_r = prow + (size_t)row * (REAL ? p.pstride : 0);
@@ -659,17 +667,26 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         if (kb < kend) { a = __ldg(p.kdesc + 2 * kb); b = __ldg(p.kdesc + 2 * kb + 1); }
       };
       uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0, e0 = d0, e1 = d0, f0 = d0, f1 = d0;
-      ldk(s.x + h, d0, d1);
-      ldk(s.x + h + KPS, e0, e1);
-      ldk(s.x + h + 2 * KPS, f0, f1);
+      if (!I8) {
+        ldk(s.x + h, d0, d1);
+        ldk(s.x + h + KPS, e0, e1);
+        ldk(s.x + h + 2 * KPS, f0, f1);
+      }
       for (int kb0 = s.x; kb0 < kend; kb0 += KPS) {
         const int kb = kb0 + h;                       // this team's K-block of the stage
         const bool mine = h < KPS && kb < kend;
         uint4 n0 = f0, n1 = f1;
+        if constexpr (I8) {   // the descriptors arrive with the stage's W boxes (TMA)
+          mbar_wait(FULL(wst), wph);
+          const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base)) + wst * 4 + 2 * h;
+          if (mine) { d0 = dsm[0]; d1 = dsm[1]; }
+          if (++wst == NST) { wst = 0; wph ^= 1u; }
+        } else {
 #ifdef HOBO_PIPE_STATS
         if (!(p.dbg & 1))   // bisection: 1 = reuse the descriptors (wrong A, timing only)
 #endif
         ldk(kb + 3 * KPS, n0, n1);
+        }
         const int st = gst;                           // A slot (I8: its own ring; else == the W slot)
         // the A bits depend only on the candidates: computed before the slot frees up
         PT(const long long tb = clock64();)
