@@ -696,6 +696,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         else
 #endif
         bits = mine ? block_bits(xs, row, d0, d1, p.runs) : 0ull;
+        uint32_t w8[16];   // I8: byte t of the K-block = bit t (nibble * 0x204081 spreads 4 bits to 4 bytes)
+        if constexpr (I8) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) w8[c] = (((uint32_t)(bits >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+        }
         PT(w_bits += clock64() - tb;)
         PT(const long long tg = clock64();)
         mbar_wait(I8 ? EMPTYA(st) : EMPTY(st), gph ^ 1u);
@@ -704,10 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         PT(const long long ts = clock64();)
         if (I8 && mine) {
           tc_fence_after();
-          uint32_t w[16];   // byte t of the K-block = bit t: nibble * 0x204081 spreads 4 bits to 4 bytes
-#pragma unroll
-          for (int c = 0; c < 16; ++c) w[c] = (((uint32_t)(bits >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-          tmem_st16(lane_base + (uint32_t)(p.L * NT + (st * KPS + h) * C::A_COLS), w);
+          tmem_st16(lane_base + (uint32_t)(p.L * NT + (st * KPS + h) * C::A_COLS), w8);
           tmem_st_wait();
           tc_fence_before();
         } else if (mine) {
