@@ -74,8 +74,10 @@ struct KrCfg {
   static constexpr int A_COLS = I8 ? kBK / 4 : kBK / 2;  // TMEM columns of one K-block of A (64 bf16 / 64 bytes per lane)
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator (I8: L of them), then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
-  static constexpr int NBAR = 2 * MAXST + 2 * MAXA + 3;
-  static constexpr int DESC_BYTES = I8 ? MAXST * 64 : 0;   // I8: the stages' K-block descriptors, copied by TMA
+  static constexpr int MAXD = I8 ? 16 : 0;               // I8: descriptor ring slots (>= DAHEAD + MAXST)
+  static constexpr int DAHEAD = 8;                       // I8: descriptors run this many stages ahead of W
+  static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 3;
+  static constexpr int DESC_BYTES = MAXD * 64;          // I8: the stages' K-block descriptors, copied by TMA
   static size_t smem_bytes(int W) {
     return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + DESC_BYTES + (size_t)(W + 2) * kBM * 4 + 128;
   }
@@ -112,12 +114,12 @@ __device__ __forceinline__ uint64_t run_bits(const uint32_t* xs, int row, const 
 #pragma unroll
   for (int q = 0; q < 4; ++q)
     if ((uint32_t)q < nfix) on &= xs[(f[q] >> 5) * kBM + row] >> (f[q] & 31);
+  // the 64-bit window x[lo .. lo+64) from three words, branch-free (funnel shifts)
   const uint32_t w = lo >> 5, sh = lo & 31;
-  uint64_t v = ((uint64_t)xs[(w + 1) * kBM + row] << 32) | xs[w * kBM + row];
-  v >>= sh;
-  if (sh) v |= (uint64_t)xs[(w + 2) * kBM + row] << (64 - sh);
+  const uint32_t w0 = xs[w * kBM + row], w1 = xs[(w + 1) * kBM + row], w2 = xs[(w + 2) * kBM + row];
+  const uint64_t v = ((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
   const uint64_t mask = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1ull);
-  return (on & 1u) ? (v & mask) << start : 0ull;
+  return (v & mask & (0ull - (uint64_t)(on & 1u))) << start;
 }
 
 // the candidate row's 64 A bits of one K-block from its descriptor (d0, d1)
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t sB = base;
   const int ring = REAL ? p.ring_boxes : C::RING_BOXES;
   const uint32_t sBar = sB + ring * C::BOX;
-  const uint32_t acc_full = sBar + 8 * (2 * C::MAXST + 2 * C::MAXA);
+  const uint32_t acc_full = sBar + 8 * (2 * C::MAXST + 2 * C::MAXA + C::MAXD);
   const uint32_t snap_full = acc_full + 8, snap_empty = acc_full + 16;
   const uint32_t tslot = acc_full + 24;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #define EMPTY(s) (sBar + 8u * (C::MAXST + (s)))
 #define FULLA(s) (sBar + 8u * (2 * C::MAXST + (s)))
 #define EMPTYA(s) (sBar + 8u * (2 * C::MAXST + C::MAXA + (s)))
+#define DFULL(s) (sBar + 8u * (2 * C::MAXST + 2 * C::MAXA + (s)))
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // block order: candidate block fastest, then column tile, then K split (concurrent CTAs
@@ -320,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     // FULL: the TMA arrive + 8 generator warps (pairs: + the peer's 8, on the leader only)
     for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), I8 ? 1 : PAIR ? 17 : 9); mbar_init(EMPTY(s), 1); }
     for (int s = 0; s < C::MAXA; ++s) { mbar_init(FULLA(s), PAIR ? 16 : 8); mbar_init(EMPTYA(s), 1); }
+    for (int s = 0; s < C::MAXD; ++s) mbar_init(DFULL(s), 1);
     mbar_init(acc_full, 1);
     mbar_init(snap_full, 1);
     mbar_init(snap_empty, PAIR ? 16 : 8);
@@ -402,6 +406,27 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       int st = 0;                    // ring slot and phase, advanced per stage (no divisions)
       uint32_t ph = 0;
       PT(unsigned long long w_tma = 0;)
+      // I8: the A generator's K-block descriptors, bulk-copied DAHEAD stages ahead of the W
+      // boxes into a ring of their own (slot m % MAXD is reused only after the generator is
+      // done with stage m - MAXD <= the stage whose W slot was just freed)
+      int dj = p.nseg - 1, dkb = 0, dslot = 0;
+      auto dskip = [&]() {
+        while (dj >= 0 && dkb >= sched[dj].x + sched[dj].y) { --dj; if (dj >= 0) dkb = sched[dj].x; }
+      };
+      auto dissue = [&]() {
+        if (dj < 0) return;
+        const uint32_t dbytes = (uint32_t)min(KPS, sched[dj].x + sched[dj].y - dkb) * 32u;
+        mbar_arrive_expect_tx(DFULL(dslot), dbytes);
+        bulk_g2s(sD + (uint32_t)dslot * 64u, p.kdesc + 2 * dkb, dbytes, DFULL(dslot));
+        if (++dslot == C::MAXD) dslot = 0;
+        dkb += KPS;
+        dskip();
+      };
+      if constexpr (I8) {
+        if (dj >= 0) dkb = sched[dj].x;
+        dskip();
+        for (int i = 0; i < C::DAHEAD; ++i) dissue();
+      }
       for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
@@ -410,11 +435,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           mbar_wait(EMPTY(st), ph ^ 1u);
           PT(w_tma += clock64() - t0;)
           if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
-            // + the stage's K-block descriptors for this CTA's A generator, on this CTA's FULL
-            // (the peer of a pair: its FULL carries only them)
-            const uint32_t dbytes = (uint32_t)nkb * 32u;
-            mbar_arrive_expect_tx(FULL(st), (leader ? (uint32_t)p.L * C::BOX : 0u) + dbytes);
-            bulk_g2s(sD + (uint32_t)st * 64u, p.kdesc + 2 * kb0, dbytes, FULL(st));
+            dissue();
+            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)p.L * C::BOX);
             for (int l = 0; l < p.L; ++l) {
               const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1);
               const uint32_t dst = sB + st * stage_bytes + (uint32_t)l * BOXB;
@@ -571,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     int n = 0;                       // stage counter (same sequence as the MMA issuer)
     int gst = 0;                     // binary path: A slot and phase, advanced per stage
     uint32_t gph = 0;
-    int wst = 0;                     // I8: the W slot and phase (its descriptors)
+    int wst = 0;                     // I8: the descriptor slot and phase
     uint32_t wph = 0;
     bool any = false;                // has any MMA been issued yet (else F = 0)
     PT(unsigned long long w_gen = 0, w_bits = 0, w_st = 0, w_arr = 0;)
@@ -659,6 +681,68 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           d0 = n0;
           d1 = n1;
         }
+      } else if constexpr (I8) {
+        // int8: two stages per iteration (team h builds K-block h of each), so one TMEM-store
+        // round trip (tcgen05.st -> wait::st, ~400 cycles) covers two stages.  The stage
+        // descriptors come by TMA with the W boxes (FULL of the W ring).
+        const int kend = s.x + s.y;
+        const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
+        for (int kb0 = s.x; kb0 < kend; kb0 += 2 * KPS) {
+          const bool two = kb0 + KPS < kend;
+          const bool mineA = kb0 + h < kend, mineB = two && kb0 + KPS + h < kend;
+          PT(const long long tb = clock64();)
+          uint32_t wA[16], wB[16];
+          {
+            mbar_wait(DFULL(wst), wph);
+            uint64_t b = 0ull;
+            if (mineA) b = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) wA[c] = (((uint32_t)(b >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+            if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
+          }
+          if (two) {
+            mbar_wait(DFULL(wst), wph);
+            uint64_t b = 0ull;
+            if (mineB) b = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) wB[c] = (((uint32_t)(b >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+            if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
+          }
+          PT(w_bits += clock64() - tb;)
+          PT(const long long tg = clock64();)
+          const int sA = gst;
+          mbar_wait(EMPTYA(sA), gph ^ 1u);
+          if (++gst == NSTA) { gst = 0; gph ^= 1u; }
+          PT(w_gen += clock64() - tg;)
+          PT(const long long ts = clock64();)
+          tc_fence_after();
+          if (mineA) tmem_st16(lane_base + (uint32_t)(p.L * NT + (sA * KPS + h) * C::A_COLS), wA);
+          int sB = -1;
+          if (two) {
+            sB = gst;
+            PT(const long long tg2 = clock64();)
+            mbar_wait(EMPTYA(sB), gph ^ 1u);
+            if (++gst == NSTA) { gst = 0; gph ^= 1u; }
+            PT(w_gen += clock64() - tg2;)
+            tc_fence_after();
+            if (mineB) tmem_st16(lane_base + (uint32_t)(p.L * NT + (sB * KPS + h) * C::A_COLS), wB);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          PT(w_st += clock64() - ts;)
+          PT(const long long ta = clock64();)
+          __syncwarp();
+          if (lane == 0) {
+            if (PAIR && !leader) {
+              mbar_arrive_remote(mapa_shared(FULLA(sA), 0));
+              if (sB >= 0) mbar_arrive_remote(mapa_shared(FULLA(sB), 0));
+            } else {
+              mbar_arrive(FULLA(sA));
+              if (sB >= 0) mbar_arrive(FULLA(sB));
+            }
+          }
+          PT(w_arr += clock64() - ta;)
+        }
       } else {
       // this team's K-block descriptors, prefetched three stages ahead (d: this stage, e, f:
       // the next two)
@@ -667,27 +751,18 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         if (kb < kend) { a = __ldg(p.kdesc + 2 * kb); b = __ldg(p.kdesc + 2 * kb + 1); }
       };
       uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0, e0 = d0, e1 = d0, f0 = d0, f1 = d0;
-      if (!I8) {
-        ldk(s.x + h, d0, d1);
-        ldk(s.x + h + KPS, e0, e1);
-        ldk(s.x + h + 2 * KPS, f0, f1);
-      }
+      ldk(s.x + h, d0, d1);
+      ldk(s.x + h + KPS, e0, e1);
+      ldk(s.x + h + 2 * KPS, f0, f1);
       for (int kb0 = s.x; kb0 < kend; kb0 += KPS) {
         const int kb = kb0 + h;                       // this team's K-block of the stage
         const bool mine = h < KPS && kb < kend;
         uint4 n0 = f0, n1 = f1;
-        if constexpr (I8) {   // the descriptors arrive with the stage's W boxes (TMA)
-          mbar_wait(FULL(wst), wph);
-          const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base)) + wst * 4 + 2 * h;
-          if (mine) { d0 = dsm[0]; d1 = dsm[1]; }
-          if (++wst == NST) { wst = 0; wph ^= 1u; }
-        } else {
 #ifdef HOBO_PIPE_STATS
         if (!(p.dbg & 1))   // bisection: 1 = reuse the descriptors (wrong A, timing only)
 #endif
         ldk(kb + 3 * KPS, n0, n1);
-        }
-        const int st = gst;                           // A slot (I8: its own ring; else == the W slot)
+        const int st = gst;                           // A slot (== the W slot)
         // the A bits depend only on the candidates: computed before the slot frees up
         PT(const long long tb = clock64();)
         uint64_t bits = 0ull;
@@ -696,23 +771,13 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         else
 #endif
         bits = mine ? block_bits(xs, row, d0, d1, p.runs) : 0ull;
-        uint32_t w8[16];   // I8: byte t of the K-block = bit t (nibble * 0x204081 spreads 4 bits to 4 bytes)
-        if constexpr (I8) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) w8[c] = (((uint32_t)(bits >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-        }
         PT(w_bits += clock64() - tb;)
         PT(const long long tg = clock64();)
-        mbar_wait(I8 ? EMPTYA(st) : EMPTY(st), gph ^ 1u);
+        mbar_wait(EMPTY(st), gph ^ 1u);
         PT(w_gen += clock64() - tg;)
         if (++gst == NSTA) { gst = 0; gph ^= 1u; }
         PT(const long long ts = clock64();)
-        if (I8 && mine) {
-          tc_fence_after();
-          tmem_st16(lane_base + (uint32_t)(p.L * NT + (st * KPS + h) * C::A_COLS), w8);
-          tmem_st_wait();
-          tc_fence_before();
-        } else if (mine) {
+        if (mine) {
           tc_fence_after();
           uint32_t w[32];
           expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
@@ -725,9 +790,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         PT(const long long ta = clock64();)
         __syncwarp();
         if (lane == 0) {
-          const uint32_t fb = I8 ? FULLA(st) : FULL(st);
-          if (PAIR && !leader) mbar_arrive_remote(mapa_shared(fb, 0));
-          else mbar_arrive(fb);
+          if (PAIR && !leader) mbar_arrive_remote(mapa_shared(FULL(st), 0));
+          else mbar_arrive(FULL(st));
         }
         PT(w_arr += clock64() - ta;)
         d0 = e0;
@@ -869,6 +933,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #undef EMPTY
 #undef FULLA
 #undef EMPTYA
+#undef DFULL
   tc_fence_before();
   if constexpr (PAIR) {
     cluster_sync_all();   // the leader's last MMAs wrote both CTAs' TMEM
