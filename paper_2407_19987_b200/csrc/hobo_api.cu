@@ -293,8 +293,8 @@ hobo_status init_device(hobo_tensor* t);
 // int8 digit planes for the binary energy / field layouts (slots 0 and 1): used when the degree
 // >= 2 cells are a fixed-point grid of <= 3 bytes (exact), the int32 accumulators cannot
 // overflow (255 x tuples < 2^31) and they take fewer tensor-core cycles than the bf16 limbs
-// (an int8 MMA runs at twice the bf16 rate: d digits cost d/2 vs L limbs).  HOBO_I8=0 / =1
-// forces bf16 / int8 (when exact).
+// (an int8 MMA runs at twice the bf16 rate: d digits cost d/2 vs L limbs) over K loops of
+// >= 64 K-blocks.  HOBO_I8=0 / =1 forces bf16 / int8 (when exact).
 int digit_planes(hobo_tensor* t) {
   if (t->dig >= 0) return t->dig;
   const HostTensor& H = t->host;
@@ -303,7 +303,9 @@ int digit_planes(hobo_tensor* t) {
   if (d > 0) {
     const char* e = getenv("HOBO_I8");
     if (e && e[0] == '0') d = 0;
-    else if (!(e && e[0] == '1') && d >= 2 * H.limbs) d = 0;
+    // default: only when it saves tensor-core cycles and the K loops are long enough (>= 64
+    // K-blocks) to amortise the per-CTA cost of L accumulators (cfg2's 16-K-block QUBO: -12%)
+    else if (!(e && e[0] == '1') && (d >= 2 * H.limbs || t->kl.Tpad / kBK < 64)) d = 0;
   }
   t->dig = d;
   return d;

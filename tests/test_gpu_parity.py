@@ -685,12 +685,13 @@ def test_int8_digit_planes_integer_instances(H, torch, pair):
 
 def test_int8_digit_planes_choice(H, torch):
     """The automatic choice: int8 when it costs fewer tensor-core cycles (3 digit planes at twice
-    the rate vs 3 bf16 limbs; 1 digit vs 1 limb), bf16 when it does not (cfg3: 2 digits vs 1
-    limb), bf16 when the cells are not a <= 3-byte fixed-point grid."""
-    X = x_bits(1, 256, 64)
-    for make, want in ((lambda: H.HoboTensor.import_cells(3, 64, *uniform_cells(3, 64, 1)), 3),
-                       (lambda: H.HoboTensor.import_cells(3, 64, *int_twin_cells(3, 64, 1)), 1),
-                       (lambda: H.HoboTensor.from_problem(random_integer_problem(3, 64, 2, nterms=50)), None)):
+    the rate vs 3 bf16 limbs; 1 digit vs 1 limb) over K loops of >= 64 K-blocks; bf16 when it
+    does not (cfg3: 2 digits vs 1 limb), for short K loops (N=64 at order 3: 33 K-blocks), and
+    when the cells are not a <= 3-byte fixed-point grid."""
+    X = x_bits(1, 256, 200)
+    for make, want in ((lambda: H.HoboTensor.import_cells(3, 200, *uniform_cells(3, 200, 1)), 3),
+                       (lambda: H.HoboTensor.import_cells(3, 200, *int_twin_cells(3, 200, 1)), 1),
+                       (lambda: H.HoboTensor.from_problem(random_integer_problem(3, 200, 2, nterms=50)), None)):
         t = make()
         t.energy(dev(torch, X))
         got = t.launch_stats()["i8_planes"]
@@ -699,10 +700,15 @@ def test_int8_digit_planes_choice(H, torch):
     t = H.HoboTensor.from_problem(p)
     t.local_field(dev(torch, x_bits(3, 128, 512)))
     assert t.launch_stats()["i8_planes"] == 0
+    t = H.HoboTensor.import_cells(3, 64, *uniform_cells(3, 64, 1))
+    t.energy(dev(torch, x_bits(1, 256, 64)))
+    assert t.launch_stats()["i8_planes"] == 0              # 33 K-blocks: bf16
+    X = x_bits(1, 256, 64)
     idx, val = uniform_cells(2, 64, 3)
     val = val.copy()
     val[np.flatnonzero(idx[:, 0] != idx[:, 1])[0]] = np.float32(3.0e-12)   # a degree-2 cell with a ~2^-62
     # quantum next to O(1) cells: no 3-byte fixed-point grid holds both
-    t = H.HoboTensor.import_cells(2, 64, idx, val)
-    t.energy(dev(torch, X))
+    with env("HOBO_I8", "1"):                                # even when forced: not exact in 3 bytes
+        t = H.HoboTensor.import_cells(2, 64, idx, val)
+        t.energy(dev(torch, X))
     assert t.launch_stats()["i8_planes"] == 0
