@@ -242,15 +242,15 @@ cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s
   return cudaGetLastError();
 }
 
-// CTA pairs at L >= 2 with long K loops (measured: cfg3-fp32 +19%, cfg5 +12%, cfg4 (128-column
-// tiles) +21%); at L = 1 the single-CTA kernel is 5% faster (cfg3), and short K loops (cfg2's
-// QUBO, 4-16 K-blocks per CTA) do not amortise the pair's cluster synchronisation (-8%).
+// CTA pairs for long K loops (measured: cfg3-fp32 +19%, cfg5 +12%, cfg4 (128-column tiles)
+// +21% at L = 3; cfg3 at L = 1 +2.3% since the ring counters and descriptor prefetch (it was
+// 5% slower before); the real-valued cfg3 14.7 -> 13.6 ms).  Short K loops (cfg2's QUBO, 4-16
+// K-blocks per CTA) do not amortise the pair's cluster synchronisation (-8%).
 // HOBO_PAIR=1 / =0 forces the choice (A/B runs, tests of both paths).
 bool use_pairs(const DevLayout& L, const KrParams& p) {
   if (p.n_split != 1) return false;
   if (const char* e = getenv("HOBO_PAIR")) return e[0] == '1';
-  const int limb_mmas = p.preal ? p.LA * p.L : p.L;   // MMA passes per W box (real-valued: x A limbs)
-  return limb_mmas >= 2 && p.n_kb >= 64;              // (real-valued cfg3: 14.7 -> 13.6 ms)
+  return p.n_kb >= 64;
 }
 
 cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
