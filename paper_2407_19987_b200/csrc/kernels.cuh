@@ -69,15 +69,16 @@ template <int NT, bool I8 = false>
 struct KrCfg {
   static constexpr int BOX = NT * 128;                   // one TMA box: NT rows x 64 bf16 tuples / 128 int8 tuples (SW128)
   static constexpr int RING_BOXES = 6 * 256 / NT;        // shared-memory budget for W (192 KB), in boxes
-  static constexpr int MAXST = I8 ? 8 : NT < 256 ? 6 : 4;  // max W stages (4 at NT=256: CTA pairs' half boxes)
-  static constexpr int MAXA = I8 ? 8 : 0;                // I8: A stages, a ring of their own (TMEM-bound)
+  static constexpr int MAXST = 8;                        // max W stages
+  static constexpr int MAXA = 8;                         // binary energy/field launches: A stages, a ring of their
+                                                         // own (TMEM-bound), decoupled from the W ring
   static constexpr int A_COLS = I8 ? kBK / 4 : kBK / 2;  // TMEM columns of one K-block of A (64 bf16 / 64 bytes per lane)
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator (I8: L of them), then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
-  static constexpr int MAXD = I8 ? 16 : 0;               // I8: descriptor ring slots (>= DAHEAD + MAXST)
-  static constexpr int DAHEAD = 8;                       // I8: descriptors run this many stages ahead of W
+  static constexpr int MAXD = 16;                        // descriptor ring slots (>= DAHEAD + MAXST)
+  static constexpr int DAHEAD = 8;                       // descriptors run this many stages ahead of W
   static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 3;
-  static constexpr int DESC_BYTES = MAXD * 64;          // I8: the stages' K-block descriptors, copied by TMA
+  static constexpr int DESC_BYTES = MAXD * 64;          // the stages' K-block descriptors, copied by TMA
   static size_t smem_bytes(int W) {
     return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + DESC_BYTES + (size_t)(W + 2) * kBM * 4 + 128;
   }
@@ -85,14 +86,23 @@ struct KrCfg {
   // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
   // boxes that fits only at L = 1, with 128-column boxes at every L <= 3
   __host__ __device__ static constexpr int kps(int L) { return (I8 || L == 1 || NT <= 128) ? 2 : 1; }
-  // I8 stages (one box per digit plane = 2 K-blocks).  The W ring and the A ring are separate:
-  // W stages are bounded by shared memory (pairs: twice the boxes) and MAXST, A stages by the
-  // TMEM left after the L accumulators
-  __host__ __device__ static constexpr int nst_i8(int L, int ring) { return ring / L < MAXST ? ring / L : MAXST; }
-  __host__ __device__ static constexpr int nsta_i8(int L) {
-    return (TMEM_COLS - L * NT) / (2 * A_COLS) < MAXA ? (TMEM_COLS - L * NT) / (2 * A_COLS) : MAXA;
+  // decoupled rings (binary energy/field launches): W stages are bounded by shared memory
+  // (pairs: twice the boxes) and MAXST, A stages by the TMEM left after the accumulator(s)
+  // (I8: L of them).  A bf16 stage is KPS boxes per limb, an I8 stage one box per plane (the
+  // box holds the K-block pair).
+  __host__ __device__ static constexpr int nstw(int L, int ring) {
+    return ring / ((I8 ? 1 : kps(L)) * L) < MAXST ? ring / ((I8 ? 1 : kps(L)) * L) : MAXST;
   }
-  __host__ __device__ static constexpr int nst(int L) { return RING_BOXES / (kps(L) * L) < MAXST ? RING_BOXES / (kps(L) * L) : MAXST; }
+  __host__ __device__ static constexpr int nsta(int L) {
+    return (TMEM_COLS - (I8 ? L : 1) * NT) / (kps(L) * A_COLS) < MAXA ? (TMEM_COLS - (I8 ? L : 1) * NT) / (kps(L) * A_COLS) : MAXA;
+  }
+  __host__ __device__ static constexpr int nst(int L) { return nst_c(L, RING_BOXES); }
+  // one ring (W boxes + A K-blocks per slot): bounded by shared memory, MAXST and TMEM
+  __host__ __device__ static constexpr int nst_c(int L, int ring) {
+    return ring / (kps(L) * L) < MAXST
+               ? (ring / (kps(L) * L) < (TMEM_COLS - NT) / (kps(L) * A_COLS) ? ring / (kps(L) * L) : (TMEM_COLS - NT) / (kps(L) * A_COLS))
+               : (MAXST < (TMEM_COLS - NT) / (kps(L) * A_COLS) ? MAXST : (TMEM_COLS - NT) / (kps(L) * A_COLS));
+  }
   // real-valued A: one K-block per stage, LA limb tiles of A in TMEM, ring sized at run time
   __host__ __device__ static int nst_real(int L, int LA, int ring) {
     int n = ring / L;
@@ -101,7 +111,7 @@ struct KrCfg {
     return n < t ? n : t;
   }
   static size_t smem_bytes_real(int ring, int pstride) {
-    return 1024 + (size_t)ring * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + (size_t)kBM * pstride * 2 + 256;
+    return 1024 + (size_t)ring * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + DESC_BYTES + (size_t)kBM * pstride * 2 + 256;
   }
 };
 
@@ -291,11 +301,14 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   constexpr uint32_t BOXB = PAIR ? C::BOX / 2 : C::BOX;   // shared-memory bytes of one W box per CTA
   const int KPS = REAL ? 1 : C::kps(p.L);
   // CTA pairs hold half boxes, so the same ring fits twice the stages (TMEM: 256 + 4 x 64 columns)
+  // DEC: the int8 launches run decoupled W / A / descriptor rings (for bf16 limbs the single
+  // ring measured faster: cfg3 15.2 vs 14.2 M cand/s)
+  constexpr bool DEC = I8;
   const int NST = REAL ? C::nst_real(p.L, p.LA, PAIR ? 2 * ring : ring)
-                 : I8 ? C::nst_i8(p.L, PAIR ? 2 * ring : ring)
-                      : (PAIR ? min(2 * C::RING_BOXES / (KPS * p.L), C::MAXST) : C::nst(p.L));
+                 : DEC ? C::nstw(p.L, PAIR ? 2 * ring : ring)
+                       : C::nst_c(p.L, PAIR ? 2 * ring : ring);
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
-  const int NSTA = I8 ? C::nsta_i8(p.L) : NST;                     // A stages (I8: own ring)
+  const int NSTA = DEC ? C::nsta(p.L) : NST;                       // A stages (DEC: own ring)
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
   __shared__ int ssa[SA ? kBM : 1];   // annealing: this CTA's decisions for site sa_m
   if (threadIdx.x == 0) {
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     // FULL: the TMA arrive + 8 generator warps (pairs: + the peer's 8, on the leader only)
-    for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), I8 ? 1 : PAIR ? 17 : 9); mbar_init(EMPTY(s), 1); }
+    for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), DEC ? 1 : PAIR ? 17 : 9); mbar_init(EMPTY(s), 1); }
     for (int s = 0; s < C::MAXA; ++s) { mbar_init(FULLA(s), PAIR ? 16 : 8); mbar_init(EMPTYA(s), 1); }
     for (int s = 0; s < C::MAXD; ++s) mbar_init(DFULL(s), 1);
     mbar_init(acc_full, 1);
@@ -422,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         dkb += KPS;
         dskip();
       };
-      if constexpr (I8) {
+      if constexpr (DEC) {
         if (dj >= 0) dkb = sched[dj].x;
         dskip();
         for (int i = 0; i < C::DAHEAD; ++i) dissue();
@@ -434,8 +447,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           PT(const long long t0 = clock64();)
           mbar_wait(EMPTY(st), ph ^ 1u);
           PT(w_tma += clock64() - t0;)
+          if constexpr (DEC) dissue();
           if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
-            dissue();
             if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)p.L * C::BOX);
             for (int l = 0; l < p.L; ++l) {
               const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1);
@@ -476,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           const int nkb = min(KPS, s.x + s.y - kb0);
           PT(t0 = clock64();)
           mbar_wait(FULL(st), ph);
-          if (I8) mbar_wait(FULLA(sa), pha);
+          if (DEC) mbar_wait(FULLA(sa), pha);
           PT(stt[1] += clock64() - t0; stt[2] += 1; stt[3] += nkb; t0 = clock64();)
           tc_fence_after();
           if (elect_one()) {
@@ -513,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
                 }
               }
             } else if (p.L == 1 && nkb == 2 && KPS == 2) {   // the common stage, fully unrolled
-              const uint32_t a_t = tmem + (uint32_t)(NT + st * 2 * C::A_COLS);
+              const uint32_t a_t = tmem + (uint32_t)(NT + (DEC ? sa : st) * 2 * C::A_COLS);
               const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes);
 #pragma unroll
               for (int q = 0; q < 2; ++q)
@@ -526,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
                 }
             } else {
               for (int q = 0; q < nkb; ++q) {
-                const uint32_t a_t = tmem + (uint32_t)(NT + (st * KPS + q) * C::A_COLS);
+                const uint32_t a_t = tmem + (uint32_t)(NT + ((DEC ? sa : st) * KPS + q) * C::A_COLS);
                 for (int l = 0; l < p.L; ++l) {
                   const uint64_t bdesc = sw128_kmajor_desc(sB + st * stage_bytes + (uint32_t)(q * p.L + l) * BOXB);
 #pragma unroll
@@ -540,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             PT(stt[4] += clock64() - t0; t0 = clock64();)
             if constexpr (PAIR) umma_commit_pair(EMPTY(st), 3);
             else umma_commit(EMPTY(st));
-            if constexpr (I8) {
+            if constexpr (DEC) {
               if constexpr (PAIR) umma_commit_pair(EMPTYA(sa), 3);
               else umma_commit(EMPTYA(sa));
             }
@@ -549,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           __syncwarp();
           issued = 1;
           if (++st == NST) { st = 0; ph ^= 1u; }
-          if (I8 && ++sa == NSTA) { sa = 0; pha ^= 1u; }
+          if (DEC && ++sa == NSTA) { sa = 0; pha ^= 1u; }
         }
         if (snaps && j > 0) {  // hand the degree-(k-j) partial sum to the epilogue warps
           if (elect_one()) {
@@ -681,34 +694,44 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           d0 = n0;
           d1 = n1;
         }
-      } else if constexpr (I8) {
-        // int8: two stages per iteration (team h builds K-block h of each), so one TMEM-store
-        // round trip (tcgen05.st -> wait::st, ~400 cycles) covers two stages.  The stage
-        // descriptors come by TMA with the W boxes (FULL of the W ring).
+      } else if constexpr (DEC) {
+        // two stages per iteration (team h builds K-block h of each), so one TMEM-store round
+        // trip (tcgen05.st -> wait::st, ~400 cycles) covers two stages.  The stage descriptors
+        // come by TMA bulk copy, DAHEAD stages ahead, in a ring of their own (DFULL).
         const int kend = s.x + s.y;
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
-        for (int kb0 = s.x; kb0 < kend; kb0 += 2 * KPS) {
-          const bool two = kb0 + KPS < kend;
-          const bool mineA = kb0 + h < kend, mineB = two && kb0 + KPS + h < kend;
+        for (int kb0 = s.x; kb0 < kend; kb0 += (I8 ? 2 : 1) * KPS) {
+          const bool two = I8 && kb0 + KPS < kend;   // (bf16: one stage per iteration measured faster)
+          const bool mineA = h < KPS && kb0 + h < kend, mineB = two && h < KPS && kb0 + KPS + h < kend;
           PT(const long long tb = clock64();)
-          uint32_t wA[16], wB[16];
-          {
-            mbar_wait(DFULL(wst), wph);
-            uint64_t b = 0ull;
-            if (mineA) b = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
-#pragma unroll
-            for (int c = 0; c < 16; ++c) wA[c] = (((uint32_t)(b >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-            if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
-          }
+          uint64_t bA = 0ull, bB = 0ull;
+          mbar_wait(DFULL(wst), wph);
+          if (mineA) bA = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
+          if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
           if (two) {
             mbar_wait(DFULL(wst), wph);
-            uint64_t b = 0ull;
-            if (mineB) b = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
-#pragma unroll
-            for (int c = 0; c < 16; ++c) wB[c] = (((uint32_t)(b >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+            if (mineB) bB = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
             if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
           }
+          uint32_t wA[16], wB[16];   // I8: byte t of the K-block = bit t (nibble * 0x204081)
+          if constexpr (I8) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) wA[c] = (((uint32_t)(bA >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) wB[c] = (((uint32_t)(bB >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+          }
           PT(w_bits += clock64() - tb;)
+          // store one K-block of A into A slot sl: int8 bytes (16 columns) / bf16 pairs (32)
+          auto store = [&](int sl, uint64_t bits, const uint32_t (&w8)[16]) {
+            if constexpr (I8) {
+              tmem_st16(lane_base + (uint32_t)(p.L * NT + (sl * KPS + h) * C::A_COLS), w8);
+            } else {
+              uint32_t w[32];
+              expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+              expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
+              tmem_st32(lane_base + (uint32_t)(NT + (sl * KPS + h) * C::A_COLS), w);
+            }
+          };
           PT(const long long tg = clock64();)
           const int sA = gst;
           mbar_wait(EMPTYA(sA), gph ^ 1u);
@@ -716,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           PT(w_gen += clock64() - tg;)
           PT(const long long ts = clock64();)
           tc_fence_after();
-          if (mineA) tmem_st16(lane_base + (uint32_t)(p.L * NT + (sA * KPS + h) * C::A_COLS), wA);
+          if (mineA) store(sA, bA, wA);
           int sB = -1;
           if (two) {
             sB = gst;
@@ -725,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             if (++gst == NSTA) { gst = 0; gph ^= 1u; }
             PT(w_gen += clock64() - tg2;)
             tc_fence_after();
-            if (mineB) tmem_st16(lane_base + (uint32_t)(p.L * NT + (sB * KPS + h) * C::A_COLS), wB);
+            if (mineB) store(sB, bB, wB);
           }
           tmem_st_wait();
           tc_fence_before();
