@@ -712,3 +712,32 @@ def test_int8_digit_planes_choice(H, torch):
         t = H.HoboTensor.import_cells(2, 64, idx, val)
         t.energy(dev(torch, X))
     assert t.launch_stats()["i8_planes"] == 0
+
+
+def test_int8_host_entry_points_and_search(H, torch):
+    """The int8 path behind the host-buffer entry points (chunked copies, ragged last chunk)
+    and inside the search loop: host calls equal the device calls bit for bit on U(-1,1)
+    cells, and a forced-int8 search replays the oracle chain for chain on an integer
+    instance."""
+    idx, val = uniform_cells(3, 200, 17)
+    t, o = H.HoboTensor.import_cells(3, 200, idx, val), Oracle.from_cells(3, 200, idx, val)
+    for B, row0 in ((20000, 0), (333, 9)):
+        Xh = x_bits(17, B, 200)
+        Xd = dev(torch, Xh)
+        G, E, best = t.local_field(Xd, row0=row0, want_best=True)
+        assert t.launch_stats()["i8_planes"] == 3
+        Ed, bestd = t.energy(Xd, row0=row0)
+        torch.cuda.synchronize()
+        Eh, besth = t.local_field_host(Xh, row0=row0)
+        assert np.array_equal(Eh, E.cpu().numpy()) and besth == best
+        Eh2, besth2 = t.energy_host(Xh, row0=row0)
+        assert np.array_equal(Eh2, Ed.cpu().numpy()) and besth2 == bestd
+        rows = np.arange(0, B, 97)
+        assert np.array_equal(E.cpu().numpy().astype(np.float64)[rows], f32(o.energy(Xh[rows])))
+    with env("HOBO_I8", "1"):
+        p = random_integer_problem(3, 40, 77, nterms=500)
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        x, e, c = t.search(9, None, 20, chain0=0, nchains=300)
+        assert t.launch_stats()["i8_planes"] >= 1
+    r = o.search(9, 0, 300, 20)
+    assert (e, c) == (r["e_best"], r["best_chain"]) and np.array_equal(x, r["chain_xbest"][c])
