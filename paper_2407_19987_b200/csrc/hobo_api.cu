@@ -92,6 +92,8 @@ struct hobo_tensor {
   uint4* d_runs = nullptr;
   uint4* d_kdesc = nullptr;
   uint32_t* d_runoff = nullptr;
+  uint4* d_srec = nullptr;  // int8 path: per K-block pair, a header + all its generator runs
+  int srec_u4 = 0;          // uint4s per record (1 + the most runs of any pair)
   float* d_p1 = nullptr;   // padded to 256-multiples
   int W = 0;               // 32-bit words per candidate bit row
   DevLayout lay[4];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
@@ -189,7 +191,7 @@ EncodeTiledFn encode_fn() {
 template <int NT, bool REAL, bool I8 = false>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, false, I8>;
-  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W);
+  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -218,7 +220,7 @@ cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) 
 template <int NT, bool REAL, bool I8 = false>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, true, I8>;
-  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W);
+  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
   static size_t configured = 0;
   if (configured < smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -295,11 +297,21 @@ hobo_status init_device(hobo_tensor* t);
 // overflow (255 x tuples < 2^31) and they take fewer tensor-core cycles than the bf16 limbs
 // (an int8 MMA runs at twice the bf16 rate: d digits cost d/2 vs L limbs) over K loops of
 // >= 64 K-blocks.  HOBO_I8=0 / =1 forces bf16 / int8 (when exact).
+// the most generator runs of any K-block pair (the int8 path's stage records)
+uint32_t pair_runs_max(const KLayout& kl) {
+  const size_t nkb = kl.run_off.size() - 1;
+  uint32_t rmax = 0;
+  for (size_t a = 0; a < nkb; a += 2) rmax = std::max(rmax, kl.run_off[std::min(a + 2, nkb)] - kl.run_off[a]);
+  return rmax;
+}
+
 int digit_planes(hobo_tensor* t) {
   if (t->dig >= 0) return t->dig;
   const HostTensor& H = t->host;
   int d = H.digits;
   if (d > 0 && 255.0 * (double)std::max<int64_t>(t->kl.Tpad, kBK) >= 2147483648.0) d = 0;
+  // shared memory: W ring + 16 run-record slots + the candidates' bits must fit one CTA
+  if (d > 0 && KrCfg<128, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl)) > kMaxSmem) d = 0;
   if (d > 0) {
     const char* e = getenv("HOBO_I8");
     if (e && e[0] == '0') d = 0;
@@ -367,6 +379,29 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   L.Npad = L.n_ct * L.NT;
   const int64_t Tpad = std::max<int64_t>(t->kl.Tpad, 2 * kBK);   // (a multiple of 2 K-blocks)
   const double bytes = (double)planes * L.Npad * Tpad * (L.i8 ? 1.0 : 2.0);
+  if (L.i8 && !t->d_srec) {
+    // stage records: for K-block pair P, uint4 {runs of 2P, runs of 2P+1, nfix, 0} followed by
+    // the pair's runs (contiguous in kl.runs), padded to the most runs of any pair; one TMA
+    // bulk copy brings a stage's whole generator input (no dependent global loads)
+    const KLayout& kl = t->kl;
+    const int64_t npair = Tpad / (2 * kBK);
+    t->srec_u4 = 1 + (int)pair_runs_max(kl);
+    std::vector<uint32_t> rec((size_t)npair * t->srec_u4 * 4, 0);
+    for (int64_t P = 0; P < npair; ++P) {
+      uint32_t* r = &rec[(size_t)P * t->srec_u4 * 4];
+      const size_t nkb = kl.run_off.size() - 1;
+      if ((size_t)(2 * P) >= nkb) continue;
+      const uint32_t a = kl.run_off[2 * P], b = kl.run_off[2 * P + 1];
+      const uint32_t c = (size_t)(2 * P + 2) <= nkb ? kl.run_off[2 * P + 2] : b;
+      r[0] = b - a;
+      r[1] = c - b;
+      r[2] = kl.kdesc[(size_t)(2 * P) * 8 + 3] & 7u;   // nfix (a pair never spans two segments)
+      for (uint32_t i = a; i < c; ++i)
+        for (int f = 0; f < 4; ++f) r[4 * (1 + i - a) + f] = kl.runs[(size_t)i * 4 + f];
+    }
+    CK(cudaMalloc(&t->d_srec, rec.size() * 4));
+    CK(cudaMemcpy(t->d_srec, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice));
+  }
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   if (bytes > 0.8 * (double)free_b)
@@ -480,6 +515,8 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.nseg = t->kl.nseg;
   p.L = L.i8 ? L.i8 : t->host.limbs;
   p.qscale = L.qscale;
+  p.srec = t->d_srec;
+  p.srec_u4 = L.i8 ? t->srec_u4 : 0;
   p.field_mode = (&L == &t->lay[0]) ? 0 : 1;
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
@@ -713,6 +750,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (t->d_xbc) cudaFree(t->d_xbc);
   if (t->d_sa_s) cudaFree(t->d_sa_s);
   if (t->d_sa_E) cudaFree(t->d_sa_E);
+  if (t->d_srec) cudaFree(t->d_srec);
   void* ptrs[] = {t->d_tt, t->d_tt_meta, t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);

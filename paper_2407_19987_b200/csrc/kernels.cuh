@@ -48,6 +48,8 @@ struct KrParams {
   double wp;                // weight of the degree-1 term
   int dbg;                  // debug builds only (HOBO_PIPE_STATS): pipeline bisection switches
   double qscale;            // int8 digit planes (kr_gemm_kernel<..., I8>): cell = qscale * sum_l 256^l d_l
+  const uint4* srec;        // int8: per K-block pair, {runs of 2P, runs of 2P+1, nfix, 0} + the runs
+  int srec_u4;              // int8: uint4s per record (the descriptor ring's slot size)
   // simulated annealing (kr_gemm_kernel<NT, false, true>): one launch per visited site m with
   // the layout of P_m = dE/dx_m; every CTA decides site m for its chains, column tile 0
   // commits the decisions, and the epilogue adds s_b * (field of P_m) to G
@@ -79,8 +81,10 @@ struct KrCfg {
   static constexpr int DAHEAD = 8;                       // descriptors run this many stages ahead of W
   static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 3;
   static constexpr int DESC_BYTES = MAXD * 64;          // the stages' K-block descriptors, copied by TMA
-  static size_t smem_bytes(int W) {
-    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + DESC_BYTES + (size_t)(W + 2) * kBM * 4 + 128;
+  // I8: the descriptor ring holds the stages' run records (srec_u4 uint4s per slot)
+  __host__ __device__ static size_t desc_bytes(int srec_u4) { return I8 ? (size_t)MAXD * srec_u4 * 16 : DESC_BYTES; }
+  static size_t smem_bytes(int W, int srec_u4 = 0) {
+    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + desc_bytes(srec_u4) + (size_t)(W + 2) * kBM * 4 + 128;
   }
   // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages.  Two
   // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t tslot = acc_full + 24;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
   const uint32_t sD = sQ + kBM * 8;                               // I8: descriptor ring (one slot per W stage)
-  const uint32_t sX = sD + C::DESC_BYTES;
+  const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4);
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
   uint16_t* prow = reinterpret_cast<uint16_t*>(gbase + (sX - base));   // REAL: p rows [128][pstride]
   double* qpart = reinterpret_cast<double*>(gbase + (sQ - base));
@@ -428,9 +432,15 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       };
       auto dissue = [&]() {
         if (dj < 0) return;
-        const uint32_t dbytes = (uint32_t)min(KPS, sched[dj].x + sched[dj].y - dkb) * 32u;
-        mbar_arrive_expect_tx(DFULL(dslot), dbytes);
-        bulk_g2s(sD + (uint32_t)dslot * 64u, p.kdesc + 2 * dkb, dbytes, DFULL(dslot));
+        if constexpr (I8) {   // the K-block pair's run record (dkb even)
+          const uint32_t rbytes = (uint32_t)p.srec_u4 * 16u;
+          mbar_arrive_expect_tx(DFULL(dslot), rbytes);
+          bulk_g2s(sD + (uint32_t)dslot * rbytes, p.srec + (size_t)(dkb >> 1) * p.srec_u4, rbytes, DFULL(dslot));
+        } else {
+          const uint32_t dbytes = (uint32_t)min(KPS, sched[dj].x + sched[dj].y - dkb) * 32u;
+          mbar_arrive_expect_tx(DFULL(dslot), dbytes);
+          bulk_g2s(sD + (uint32_t)dslot * 64u, p.kdesc + 2 * dkb, dbytes, DFULL(dslot));
+        }
         if (++dslot == C::MAXD) dslot = 0;
         dkb += KPS;
         dskip();
@@ -705,12 +715,21 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           const bool mineA = h < KPS && kb0 + h < kend, mineB = two && h < KPS && kb0 + KPS + h < kend;
           PT(const long long tb = clock64();)
           uint64_t bA = 0ull, bB = 0ull;
+          // I8: K-block h of the pair from its run record in shared memory
+          auto rec_bits = [&](int slot) -> uint64_t {
+            const uint4* rec = dsm + (size_t)slot * p.srec_u4;
+            const uint4 hd = rec[0];
+            const uint32_t n = h ? hd.y : hd.x, off = h ? hd.x : 0u;
+            uint64_t bits = 0ull;
+            for (uint32_t i = 0; i < n; ++i) bits |= run_bits(xs, row, rec[1 + off + i], hd.z);
+            return bits;
+          };
           mbar_wait(DFULL(wst), wph);
-          if (mineA) bA = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
+          if (mineA) bA = I8 ? rec_bits(wst) : block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
           if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
           if (two) {
             mbar_wait(DFULL(wst), wph);
-            if (mineB) bB = block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
+            if (mineB) bB = I8 ? rec_bits(wst) : block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
             if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
           }
           uint32_t wA[16], wB[16];   // I8: byte t of the K-block = bit t (nibble * 0x204081)
