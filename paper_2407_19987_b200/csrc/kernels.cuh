@@ -80,7 +80,7 @@ struct KrCfg {
   static constexpr int MAXD = 16;                        // descriptor ring slots (>= DAHEAD + MAXST)
   static constexpr int DAHEAD = 8;                       // descriptors run this many stages ahead of W
   static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 3;
-  static constexpr int DESC_BYTES = MAXD * 64;          // the stages' K-block descriptors, copied by TMA
+  static constexpr int DESC_BYTES = 0;                   // (bf16 launches read their descriptors with __ldg)
   // I8: the descriptor ring holds the stages' run records (srec_u4 uint4s per slot)
   __host__ __device__ static size_t desc_bytes(int srec_u4) { return I8 ? (size_t)MAXD * srec_u4 * 16 : DESC_BYTES; }
   static size_t smem_bytes(int W, int srec_u4 = 0) {
@@ -432,15 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       };
       auto dissue = [&]() {
         if (dj < 0) return;
-        if constexpr (I8) {   // the K-block pair's run record (dkb even)
-          const uint32_t rbytes = (uint32_t)p.srec_u4 * 16u;
-          mbar_arrive_expect_tx(DFULL(dslot), rbytes);
-          bulk_g2s(sD + (uint32_t)dslot * rbytes, p.srec + (size_t)(dkb >> 1) * p.srec_u4, rbytes, DFULL(dslot));
-        } else {
-          const uint32_t dbytes = (uint32_t)min(KPS, sched[dj].x + sched[dj].y - dkb) * 32u;
-          mbar_arrive_expect_tx(DFULL(dslot), dbytes);
-          bulk_g2s(sD + (uint32_t)dslot * 64u, p.kdesc + 2 * dkb, dbytes, DFULL(dslot));
-        }
+        // the K-block pair's run record (dkb even)
+        const uint32_t rbytes = (uint32_t)p.srec_u4 * 16u;
+        mbar_arrive_expect_tx(DFULL(dslot), rbytes);
+        bulk_g2s(sD + (uint32_t)dslot * rbytes, p.srec + (size_t)(dkb >> 1) * p.srec_u4, rbytes, DFULL(dslot));
         if (++dslot == C::MAXD) dslot = 0;
         dkb += KPS;
         dskip();
@@ -710,8 +705,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         // come by TMA bulk copy, DAHEAD stages ahead, in a ring of their own (DFULL).
         const int kend = s.x + s.y;
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
-        for (int kb0 = s.x; kb0 < kend; kb0 += (I8 ? 2 : 1) * KPS) {
-          const bool two = I8 && kb0 + KPS < kend;   // (bf16: one stage per iteration measured faster)
+        for (int kb0 = s.x; kb0 < kend; kb0 += 2 * KPS) {
+          const bool two = kb0 + KPS < kend;
           const bool mineA = h < KPS && kb0 + h < kend, mineB = two && h < KPS && kb0 + KPS + h < kend;
           PT(const long long tb = clock64();)
           uint64_t bA = 0ull, bB = 0ull;
@@ -725,31 +720,22 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             return bits;
           };
           mbar_wait(DFULL(wst), wph);
-          if (mineA) bA = I8 ? rec_bits(wst) : block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
+          if (mineA) bA = rec_bits(wst);
           if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
           if (two) {
             mbar_wait(DFULL(wst), wph);
-            if (mineB) bB = I8 ? rec_bits(wst) : block_bits(xs, row, dsm[wst * 4 + 2 * h], dsm[wst * 4 + 2 * h + 1], p.runs);
+            if (mineB) bB = rec_bits(wst);
             if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
           }
-          uint32_t wA[16], wB[16];   // I8: byte t of the K-block = bit t (nibble * 0x204081)
-          if constexpr (I8) {
+          uint32_t wA[16], wB[16];   // byte t of the K-block = bit t (nibble * 0x204081 spreads 4 bits)
 #pragma unroll
-            for (int c = 0; c < 16; ++c) wA[c] = (((uint32_t)(bA >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+          for (int c = 0; c < 16; ++c) wA[c] = (((uint32_t)(bA >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
 #pragma unroll
-            for (int c = 0; c < 16; ++c) wB[c] = (((uint32_t)(bB >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-          }
+          for (int c = 0; c < 16; ++c) wB[c] = (((uint32_t)(bB >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
           PT(w_bits += clock64() - tb;)
-          // store one K-block of A into A slot sl: int8 bytes (16 columns) / bf16 pairs (32)
-          auto store = [&](int sl, uint64_t bits, const uint32_t (&w8)[16]) {
-            if constexpr (I8) {
-              tmem_st16(lane_base + (uint32_t)(p.L * NT + (sl * KPS + h) * C::A_COLS), w8);
-            } else {
-              uint32_t w[32];
-              expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
-              expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
-              tmem_st32(lane_base + (uint32_t)(NT + (sl * KPS + h) * C::A_COLS), w);
-            }
+          // one K-block of A (int8 bytes, 16 TMEM columns) into A slot sl
+          auto store = [&](int sl, const uint32_t (&w8)[16]) {
+            tmem_st16(lane_base + (uint32_t)(p.L * NT + (sl * KPS + h) * C::A_COLS), w8);
           };
           PT(const long long tg = clock64();)
           const int sA = gst;
@@ -758,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           PT(w_gen += clock64() - tg;)
           PT(const long long ts = clock64();)
           tc_fence_after();
-          if (mineA) store(sA, bA, wA);
+          if (mineA) store(sA, wA);
           int sB = -1;
           if (two) {
             sB = gst;
@@ -767,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             if (++gst == NSTA) { gst = 0; gph ^= 1u; }
             PT(w_gen += clock64() - tg2;)
             tc_fence_after();
-            if (mineB) store(sB, bB, wB);
+            if (mineB) store(sB, wB);
           }
           tmem_st_wait();
           tc_fence_before();
