@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   if (threadIdx.x == 0) {
     // FULL: the TMA arrive + 8 generator warps (pairs: + the peer's 8, on the leader only)
     for (int s = 0; s < C::MAXST; ++s) { mbar_init(FULL(s), DEC ? 1 : PAIR ? 17 : 9); mbar_init(EMPTY(s), 1); }
-    for (int s = 0; s < C::MAXA; ++s) { mbar_init(FULLA(s), PAIR ? 16 : 8); mbar_init(EMPTYA(s), 1); }
+    for (int s = 0; s < C::MAXA; ++s) { mbar_init(FULLA(s), (PAIR ? 2 : 1) * (I8 ? 4 : 8)); mbar_init(EMPTYA(s), 1); }
     for (int s = 0; s < C::MAXD; ++s) mbar_init(DFULL(s), 1);
     mbar_init(acc_full, 1);
     mbar_init(snap_full, 1);
@@ -613,6 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     uint32_t gph = 0;
     int wst = 0;                     // I8: the descriptor slot and phase
     uint32_t wph = 0;
+    int gn = 0;                      // I8: stage counter (the teams alternate stages)
     bool any = false;                // has any MMA been issued yet (else F = 0)
     PT(unsigned long long w_gen = 0, w_bits = 0, w_st = 0, w_arr = 0;)
     const uint16_t* prow_r = prow + (size_t)row * (REAL ? p.pstride : 0);
@@ -700,76 +701,47 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           d1 = n1;
         }
       } else if constexpr (DEC) {
-        // two stages per iteration (team h builds K-block h of each), so one TMEM-store round
-        // trip (tcgen05.st -> wait::st, ~400 cycles) covers two stages.  The stage descriptors
-        // come by TMA bulk copy, DAHEAD stages ahead, in a ring of their own (DFULL).
+        // int8: the teams take whole stages in turn (team h: stages with gn % 2 == h).  A team
+        // decodes both K-blocks of its stage from the stage's run record (TMA bulk copy,
+        // DAHEAD stages ahead, DFULL ring) and writes them with ONE tcgen05.st (32 columns),
+        // so one store round trip (~400 cycles) covers two K-blocks and each team has two
+        // stage times per stage.  FULLA counts the one team's 4 warps (pairs: 8).
         const int kend = s.x + s.y;
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
-        for (int kb0 = s.x; kb0 < kend; kb0 += 2 * KPS) {
-          const bool two = kb0 + KPS < kend;
-          const bool mineA = h < KPS && kb0 + h < kend, mineB = two && h < KPS && kb0 + KPS + h < kend;
-          PT(const long long tb = clock64();)
-          uint64_t bA = 0ull, bB = 0ull;
-          // I8: K-block h of the pair from its run record in shared memory
-          auto rec_bits = [&](int slot) -> uint64_t {
-            const uint4* rec = dsm + (size_t)slot * p.srec_u4;
-            const uint4 hd = rec[0];
-            const uint32_t n = h ? hd.y : hd.x, off = h ? hd.x : 0u;
-            uint64_t bits = 0ull;
-            for (uint32_t i = 0; i < n; ++i) bits |= run_bits(xs, row, rec[1 + off + i], hd.z);
-            return bits;
-          };
-          mbar_wait(DFULL(wst), wph);
-          if (mineA) bA = rec_bits(wst);
-          if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
-          if (two) {
+        for (int kb0 = s.x; kb0 < kend; kb0 += KPS, ++gn) {
+          if ((gn & 1) == h) {
+            PT(const long long tb = clock64();)
             mbar_wait(DFULL(wst), wph);
-            if (mineB) bB = rec_bits(wst);
-            if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
-          }
-          uint32_t wA[16], wB[16];   // byte t of the K-block = bit t (nibble * 0x204081 spreads 4 bits)
+            const uint4* rec = dsm + (size_t)wst * p.srec_u4;
+            const uint4 hd = rec[0];
+            uint64_t b0 = 0ull, b1 = 0ull;
+            for (uint32_t i = 0; i < hd.x; ++i) b0 |= run_bits(xs, row, rec[1 + i], hd.z);
+            for (uint32_t i = 0; i < hd.y; ++i) b1 |= run_bits(xs, row, rec[1 + hd.x + i], hd.z);
+            uint32_t w[32];   // byte t of the K-block = bit t (nibble * 0x204081 spreads 4 bits)
 #pragma unroll
-          for (int c = 0; c < 16; ++c) wA[c] = (((uint32_t)(bA >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+            for (int c = 0; c < 16; ++c) w[c] = (((uint32_t)(b0 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
 #pragma unroll
-          for (int c = 0; c < 16; ++c) wB[c] = (((uint32_t)(bB >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-          PT(w_bits += clock64() - tb;)
-          // one K-block of A (int8 bytes, 16 TMEM columns) into A slot sl
-          auto store = [&](int sl, const uint32_t (&w8)[16]) {
-            tmem_st16(lane_base + (uint32_t)(p.L * NT + (sl * KPS + h) * C::A_COLS), w8);
-          };
-          PT(const long long tg = clock64();)
-          const int sA = gst;
-          mbar_wait(EMPTYA(sA), gph ^ 1u);
-          if (++gst == NSTA) { gst = 0; gph ^= 1u; }
-          PT(w_gen += clock64() - tg;)
-          PT(const long long ts = clock64();)
-          tc_fence_after();
-          if (mineA) store(sA, wA);
-          int sB = -1;
-          if (two) {
-            sB = gst;
-            PT(const long long tg2 = clock64();)
-            mbar_wait(EMPTYA(sB), gph ^ 1u);
-            if (++gst == NSTA) { gst = 0; gph ^= 1u; }
-            PT(w_gen += clock64() - tg2;)
+            for (int c = 0; c < 16; ++c) w[16 + c] = (((uint32_t)(b1 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+            PT(w_bits += clock64() - tb;)
+            PT(const long long tg = clock64();)
+            mbar_wait(EMPTYA(gst), gph ^ 1u);
+            PT(w_gen += clock64() - tg;)
+            PT(const long long ts = clock64();)
             tc_fence_after();
-            if (mineB) store(sB, wB);
-          }
-          tmem_st_wait();
-          tc_fence_before();
-          PT(w_st += clock64() - ts;)
-          PT(const long long ta = clock64();)
-          __syncwarp();
-          if (lane == 0) {
-            if (PAIR && !leader) {
-              mbar_arrive_remote(mapa_shared(FULLA(sA), 0));
-              if (sB >= 0) mbar_arrive_remote(mapa_shared(FULLA(sB), 0));
-            } else {
-              mbar_arrive(FULLA(sA));
-              if (sB >= 0) mbar_arrive(FULLA(sB));
+            tmem_st32(lane_base + (uint32_t)(p.L * NT + gst * KPS * C::A_COLS), w);
+            tmem_st_wait();
+            tc_fence_before();
+            PT(w_st += clock64() - ts;)
+            PT(const long long ta = clock64();)
+            __syncwarp();
+            if (lane == 0) {
+              if (PAIR && !leader) mbar_arrive_remote(mapa_shared(FULLA(gst), 0));
+              else mbar_arrive(FULLA(gst));
             }
+            PT(w_arr += clock64() - ta;)
           }
-          PT(w_arr += clock64() - ta;)
+          if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
+          if (++gst == NSTA) { gst = 0; gph ^= 1u; }
         }
       } else {
       // this team's K-block descriptors, prefetched three stages ahead (d: this stage, e, f:
