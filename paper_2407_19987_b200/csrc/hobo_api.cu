@@ -1091,6 +1091,7 @@ hobo_status ensure_sa_sites(hobo_tensor* t) {
     hobo_tensor* c = new hobo_tensor();
     kids.push_back(c);
     c->sa_borrowed = true;
+    c->dig = 0;               // site tensors keep bf16 limb layouts (built below)
     // order 1: the fields never change (P_m is a constant): an all-zero order-1 tensor
     const int st = k >= 2 ? derive(t->host, m, c->host, msg) : compile_colex(1, N, &zp, c->host, msg);
     if (st) return drop(fail(st == 3 ? HOBO_ENOMEM : HOBO_EINVAL, "annealing site tensor: " + msg));
