@@ -101,6 +101,11 @@ hobo_status hobo_tensor_free(hobo_tensor* t);
  * the least L such that hi+mid+lo represents every fp32 cell exactly), offset.          */
 hobo_status hobo_tensor_info(const hobo_tensor* t, int* order, int* N, int64_t* ncells,
                              int* is_integer, double* sum_abs, int* limbs, double* offset);
+/* The fixed-point decomposition behind the int8 path, host
+ * only: every cell of degree >= 2 equals q * 2^qexp with q an integer of `digits`
+ * two's-complement bytes (1..3; 0 = no such q fits in 3 bytes).  Whether a call takes the
+ * int8 path also depends on its cost (hobo_last_launch_kind reports the path taken).      */
+hobo_status hobo_tensor_digits(const hobo_tensor* t, int* digits, int* qexp);
 
 /* host export of the canonical cells (lexicographic by index tuple): idx[ncells*order],
  * val[ncells]; and of the dense N^order fp32 tensor (row-major, last index fastest;

@@ -758,6 +758,13 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   return HOBO_OK;
 }
 
+hobo_status hobo_tensor_digits(const hobo_tensor* t, int* digits, int* qexp) {
+  if (!t || !digits || !qexp) return fail(HOBO_EINVAL, "null argument");
+  *digits = t->host.digits;
+  *qexp = t->host.qexp;
+  return HOBO_OK;
+}
+
 hobo_status hobo_tensor_info(const hobo_tensor* t, int* order, int* N, int64_t* ncells, int* is_integer,
                              double* sum_abs, int* limbs, double* offset) {
   if (!t) return fail(HOBO_EINVAL, "null handle");

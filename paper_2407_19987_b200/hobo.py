@@ -15,7 +15,7 @@ HOBO_OK, HOBO_EINVAL, HOBO_ERANGE, HOBO_ENOMEM, HOBO_ECUDA, HOBO_ENCCL, HOBO_EST
 _STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
 
 EXPORTED = [
-    "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_import_dense", "hobo_tensor_free", "hobo_tensor_info",
+    "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_import_dense", "hobo_tensor_free", "hobo_tensor_info", "hobo_tensor_digits",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field", "hobo_local_field_host", "hobo_energy_host",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
     "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats", "hobo_last_launch_kind",
@@ -51,6 +51,7 @@ def lib():
         L.hobo_tensor_import_colex.argtypes = [I, I, P, C.POINTER(P)]
         L.hobo_tensor_import_dense.argtypes = [I, I, P, C.POINTER(P)]
         L.hobo_tensor_free.argtypes = [P]
+        L.hobo_tensor_digits.argtypes = [P, C.POINTER(I), C.POINTER(I)]
         L.hobo_tensor_info.argtypes = [P, C.POINTER(I), C.POINTER(I), C.POINTER(I64), C.POINTER(I),
                                        C.POINTER(D), C.POINTER(I), C.POINTER(D)]
         L.hobo_tensor_export_cells.argtypes = [P, P, P]
@@ -122,6 +123,13 @@ class HoboTensor:
                                       C.byref(lb), C.byref(off)))
         self.order, self.N, self.ncells = o.value, n.value, nc.value
         self.is_integer, self.sum_abs, self.limbs, self.offset = bool(ii.value), sa.value, lb.value, off.value
+
+    def digits(self):
+        """(digits, qexp): the cells of degree >= 2 are q * 2^qexp with q a `digits`-byte
+        two's-complement integer (0: not representable in 3 bytes)."""
+        d, q = C.c_int(), C.c_int()
+        _check(lib().hobo_tensor_digits(self._h, C.byref(d), C.byref(q)))
+        return d.value, q.value
 
     # -- construction ---------------------------------------------------------------------
     @classmethod

@@ -103,6 +103,29 @@ def test_limb_counts(H):
     assert H.HoboTensor.import_cells(3, 20, *uniform_cells(3, 20, 1)).limbs == 3
 
 
+def test_int8_digit_decomposition(H):
+    """The fixed-point grid behind the int8 path (host side, no GPU): U(-1,1) cells are
+    (q - 2^23) 2^-23, so 3 bytes at 2^-23; cfg3's integer cells (|c| <= 1216, lowest set bit
+    2^0 somewhere) need 2 bytes at 2^0; seating's +10 cubic cells fit 1 byte (the -1 cells
+    are degree 1, held in fp32 beside the planes); a 2^-62-quantum cell next to O(1) cells
+    fits no 3-byte grid."""
+    assert H.HoboTensor.import_cells(3, 20, *uniform_cells(3, 20, 1)).digits() == (3, -23)
+    assert H.HoboTensor.from_problem(cfg3_problem()).digits() == (2, 0)
+    d, q = H.HoboTensor.from_problem(seating(4)).digits()
+    assert d == 1 and 10 * 2.0 ** -q < 128 and (10 * 2.0 ** -q) == int(10 * 2.0 ** -q)
+    idx, val = uniform_cells(2, 16, 3)
+    val = val.copy()
+    val[np.flatnonzero(idx[:, 0] != idx[:, 1])[0]] = np.float32(3.0e-12)
+    assert H.HoboTensor.import_cells(2, 16, idx, val).digits()[0] == 0
+    # exactness of the decomposition: every cell = q 2^qexp with q in the d-byte range
+    idx, val = uniform_cells(3, 24, 5)
+    t = H.HoboTensor.import_cells(3, 24, idx, val)
+    d, q = t.digits()
+    deg = np.array([len(set(r)) for r in idx])
+    qs = val[deg >= 2].astype(np.float64) * 2.0 ** -q
+    assert np.array_equal(qs, np.round(qs)) and qs.min() >= -2 ** (8 * d - 1) and qs.max() <= 2 ** (8 * d - 1) - 1
+
+
 def test_errors(H):
     tb = TermBuilder()
     tb.add(1.0, [(0.0, [(0, 1.0)]), (0.0, [(1, 1.0)]), (0.0, [(2, 1.0)])])
