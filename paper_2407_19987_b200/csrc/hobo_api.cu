@@ -847,13 +847,15 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   if (hobo_status st = ensure_layout(t, field)) return st;
   const DevLayout& L = t->lay[field];
   const int N = t->host.N;
-  // chunks of whole waves (>= 2 waves of (candidate block x column tile) CTAs; CTA pairs take
-  // candidate blocks two by two): a one-wave first chunk (its copy is the exposed one), then
-  // halves of the batch, each copy hidden behind the previous chunk's contraction; fewer
-  // launches keep their fill and drain small (8 chunks -> 3: cfg3 e2e 14.4 -> 14.8 M cand/s)
+  // chunks of whole waves of (candidate block x column tile) CTAs (CTA pairs take candidate
+  // blocks two by two): a one-wave first chunk (its copy is the exposed one), then chunks
+  // growing 6x, each copy (PCIe, ~10-20 ns per candidate) hidden behind the previous chunk's
+  // contraction (>= 60 ns per candidate); few launches keep their fill and drain small
   const long long per_wave = std::max<long long>(2, 148 / L.n_ct / 2 * 2) * kBM;
-  const long long waves = std::max<long long>(2, ((B + 1) / 2 + per_wave - 1) / per_wave);
-  const long long chunk = std::min<long long>(B, waves * per_wave);
+  std::vector<long long> sizes;
+  for (long long off = 0, n = per_wave; off < B; off += sizes.back(), n *= 6)
+    sizes.push_back(std::min(n, B - off));
+  const long long chunk = *std::max_element(sizes.begin(), sizes.end());
   if (!t->cs) {
     CK(cudaStreamCreateWithFlags(&t->cs, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
@@ -878,10 +880,8 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   CK(cudaEventRecord(t->ev_in, s));             // the copies follow the caller's prior work
   CK(cudaStreamWaitEvent(t->cs, t->ev_in, 0));
   int64_t launches = 0;
-  // the first chunk is a single wave: its copy is the one nothing overlaps
-  const long long first = std::min<long long>(chunk, per_wave);
   for (long long off = 0, i = 0, n = 0; off < B; off += n, ++i) {
-    n = std::min<long long>(i == 0 ? first : chunk, B - off);
+    n = sizes[(size_t)i];
     const int slot = (int)(i & 1);
     if (i >= 2) CK(cudaStreamWaitEvent(t->cs, t->ev_free[slot], 0));   // its previous chunk is packed
     CK(cudaMemcpyAsync(t->d_xh[slot], X_host + (size_t)off * N, (size_t)n * N, cudaMemcpyHostToDevice, t->cs));
