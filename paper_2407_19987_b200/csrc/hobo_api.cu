@@ -508,6 +508,17 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.n_cb = (int)((B + kBM - 1) / kBM);
   p.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, 2 * kBK) / kBK);
   p.n_split = 1;
+  {
+    // longest-first: the open index's last column tile has the most rows,
+    // and issuing it first keeps the short tiles for the tail of the last wave
+    auto kbs = [&](int ct) {
+      long long kb = 0;
+      for (int j = 0; j < t->kl.nseg; ++j) kb += L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1];
+      return kb;
+    };
+    p.ct_desc = (L.n_ct > 1 && kbs(L.n_ct - 1) > kbs(0)) ? 1 : 0;
+    if (const char* e = getenv("HOBO_CT_DESC")) p.ct_desc = e[0] == '1';
+  }
   p.preal = nullptr;
   p.LA = 1;
   p.ring_boxes = L.NT == 128 ? ring_boxes_for<128>() : ring_boxes_for<256>();

@@ -42,6 +42,8 @@ struct KrParams {
   int LA;                   // bf16 limbs of the Khatri-Rao products of p (exact for <= 3 factors)
   int ring_boxes;           // W boxes that fit next to the p rows in shared memory
   int pstride;              // p row stride in shared memory (elements, odd word count)
+  int ct_desc;              // 1: column tiles in descending order (the heaviest K schedules start
+                            // first, so the light tiles fill the tail of the last wave)
   int n_split;              // split-K: CTAs of one (candidate block, column tile) split the K
                             // schedule; split s writes partials G + s*B*N, Q[(s*n_ct + ct)*B + b]
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
@@ -299,7 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const int ncb_eff = PAIR ? (p.n_cb + 1) / 2 : p.n_cb;
   const int bid = PAIR ? (int)(blockIdx.x / 2) : (int)blockIdx.x;
   const int cb = PAIR ? 2 * (bid % ncb_eff) + (int)prank : bid % ncb_eff;
-  const int ct = (bid / ncb_eff) % p.n_ct;
+  const int ct_i = (bid / ncb_eff) % p.n_ct;
+  const int ct = (!SA && p.ct_desc) ? p.n_ct - 1 - ct_i : ct_i;
   const int split = bid / (ncb_eff * p.n_ct);
   const long long b0 = (long long)cb * kBM;
   constexpr uint32_t BOXB = PAIR ? C::BOX / 2 : C::BOX;   // shared-memory bytes of one W box per CTA
