@@ -457,6 +457,34 @@ def main():
         extras["e2e"] = {"value": units / (m2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * N,
                          "d2h_bytes_per_step": B * 4 + 8, "ms_per_step": m2,
                          "api": "hobo_local_field_host" if mode == "field" else "hobo_energy_host"}
+        # the same through the packed-candidate host entry point (hobo_*_host_bits): X arrives as
+        # bit rows (ceil(N/32) words per candidate), 1/8 of the bytes over PCIe
+        from paper_2407_19987_b200.hobo import pack_rows
+        Xph = torch.from_numpy(pack_rows(Xh.numpy()).view(np.int32)).pin_memory()
+        e2p_ms = []
+        for i in range(a.warmup + a.steps):
+            flush_l2()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            _, hb = t.local_field_host_bits(Xph, Eh, row0=row0, stream=stream, fields=(mode == "field"))
+            if world > 1:
+                if not lib_comm:
+                    hb = combine_best(hb[0], hb[1], device=cdev)
+            e.record(stream)
+            e.synchronize()
+            if i >= a.warmup:
+                e2p_ms.append(s.elapsed_time(e))
+        assert tuple(hb) == tuple(best), (hb, best)
+        m3 = statistics.mean(e2p_ms)
+        if world > 1:
+            mm = torch.tensor([m3], dtype=torch.float64, device=cdev)
+            dist.all_reduce(mm, op=dist.ReduceOp.MAX)
+            m3 = float(mm.item())
+        extras["e2e_packed"] = {"value": units / (m3 / 1e3), "unit": UNIT,
+                                "h2d_bytes_per_step": int(Xph.numel()) * 4, "d2h_bytes_per_step": B * 4 + 8,
+                                "ms_per_step": m3,
+                                "api": "hobo_local_field_host_bits" if mode == "field" else "hobo_energy_host_bits",
+                                "input": "bit-packed candidate rows (packed on the host before the timed region)"}
         if mode == "field":
             # the search loop (16 iterations of field + move over B chains), context only
             t.search(3, B, 1)                     # warm the search scratch buffers

@@ -22,6 +22,8 @@
  *       HOBO_PAIR=1|0        CTA-pair (cta_group::2) contraction on / off
  *       HOBO_SA_KERNEL=ring|stage|ts|pair   the persistent annealing kernel
  *       HOBO_I8=1|0          int8 digit planes (kind::i8) whenever exact / never
+ *       HOBO_CT_DESC=1|0     column tiles longest-first (default when the last tile is the
+ *                            heaviest) / in index order
  *     Pairs and annealing kernels give identical results.  The int8 path computes the
  *     contraction exactly (integer accumulation), the bf16 path within the fp32
  *     tolerance; both are exact on integer instances with sum|H| < 2^24.
@@ -144,6 +146,24 @@ hobo_status hobo_local_field_host(hobo_tensor* t, const uint8_t* X_host, int64_t
  * layout; no fields).  Results equal hobo_energy's.  Synchronises the stream.            */
 hobo_status hobo_energy_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0,
                              float* E_host, hobo_best* best, void* stream);
+
+/* Packed candidates — the same four calls with X given as bit rows instead of bytes
+ * (the candidates are binary vectors; a byte per bit is 8x the bytes the
+ * contraction needs, and through host buffers the host->device copy of X is the cost):
+ *   Xbits    u32, row-major B x W with W = ceil(N / 32); bit (m mod 32) of word m / 32 of
+ *            row b is x_bm (LSB first).  Bits at positions >= N are ignored (cleared on
+ *            the device).  _bits: device pointer; _host_bits: host pointer (page-locked
+ *            lets the copies overlap), B*W*4 bytes copied instead of B*N.
+ * Everything else (outputs, row0, best, errors, streams) is as in the byte-input call;
+ * results are identical to it for the same candidates.                                  */
+hobo_status hobo_energy_bits(hobo_tensor* t, const uint32_t* Xbits_dev, int64_t B, int64_t row0,
+                             float* E_dev, hobo_best* best, void* stream);
+hobo_status hobo_local_field_bits(hobo_tensor* t, const uint32_t* Xbits_dev, int64_t B, int64_t row0,
+                                  float* G_dev, float* E_dev, hobo_best* best, void* stream);
+hobo_status hobo_energy_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0,
+                                  float* E_host, hobo_best* best, void* stream);
+hobo_status hobo_local_field_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0,
+                                       float* E_host, hobo_best* best, void* stream);
 
 /* hobo_multilinear_field — the same contraction on REAL candidates p in [0,1]^N, the
  * multilinear relaxation used by gradient descent ("the gradient is computed based

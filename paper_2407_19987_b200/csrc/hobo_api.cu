@@ -624,7 +624,7 @@ int real_slot(hobo_tensor* t) {
 }
 
 hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
-                     const uint16_t* P = nullptr) {
+                     const uint16_t* P = nullptr, bool packed = false) {
   const int slot = P ? real_slot(t) : field;
   if (hobo_status st = ensure_layout(t, slot)) return st;
   const DevLayout& L = t->lay[slot];
@@ -632,8 +632,12 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   if (!P) {
     if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * t->W)) return st;
     const long long nw = B * t->W;
-    pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, t->host.N, t->W,
-                                                                                             t->d_bits);
+    if (packed)
+      mask_bits_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(
+          reinterpret_cast<const uint32_t*>(X), B, t->host.N, t->W, t->d_bits);
+    else
+      pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, t->host.N, t->W,
+                                                                                               t->d_bits);
     CK(cudaGetLastError());
   }
   KrParams p = make_params(t, L, t->d_bits, B, G, t->d_Q);
@@ -801,15 +805,18 @@ hobo_status hobo_tensor_export_dense(const hobo_tensor* t, float* host_out) {
   return HOBO_OK;
 }
 
-hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row0, float* E, hobo_best* best,
-                        void* stream) {
+}  // extern "C"
+
+namespace {
+hobo_status energy_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B, int64_t row0, float* E,
+                        hobo_best* best, void* stream) {
   if (!t) return fail(HOBO_EINVAL, "null handle");
   if (B < 0 || (B > 0 && !X) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF)
     return fail(HOBO_EINVAL, "bad batch (B >= 0, X non-null, row0 + B < 2^32)");
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (B == 0) return empty_best(t, best, s);
-  if (hobo_status st = contract(t, 0, X, B, nullptr, s)) return st;
+  if (hobo_status st = contract(t, 0, X, B, nullptr, s, nullptr, packed)) return st;
   const DevLayout& L = t->lay[0];
   CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
   finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
@@ -821,15 +828,15 @@ hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row
   return HOBO_OK;
 }
 
-hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row0, float* G, float* E,
-                             hobo_best* best, void* stream) {
+hobo_status field_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B, int64_t row0, float* G, float* E,
+                       hobo_best* best, void* stream) {
   if (!t) return fail(HOBO_EINVAL, "null handle");
   if (B < 0 || (B > 0 && (!X || !G)) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF)
     return fail(HOBO_EINVAL, "bad batch (B >= 0, X and G non-null, row0 + B < 2^32)");
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (B == 0) return empty_best(t, best, s);
-  if (hobo_status st = contract(t, 1, X, B, G, s)) return st;
+  if (hobo_status st = contract(t, 1, X, B, G, s, nullptr, packed)) return st;
   if (E || best) {
     const DevLayout& L = t->lay[1];
     if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
@@ -842,13 +849,36 @@ hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_
     if (hobo_status st = finish_best(t, best, s)) return st;
   return HOBO_OK;
 }
+}  // namespace
+
+extern "C" {
+
+hobo_status hobo_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row0, float* E, hobo_best* best,
+                        void* stream) {
+  return energy_impl(t, X, false, B, row0, E, best, stream);
+}
+
+hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t row0, float* G, float* E,
+                             hobo_best* best, void* stream) {
+  return field_impl(t, X, false, B, row0, G, E, best, stream);
+}
+
+hobo_status hobo_energy_bits(hobo_tensor* t, const uint32_t* Xbits, int64_t B, int64_t row0, float* E,
+                             hobo_best* best, void* stream) {
+  return energy_impl(t, reinterpret_cast<const uint8_t*>(Xbits), true, B, row0, E, best, stream);
+}
+
+hobo_status hobo_local_field_bits(hobo_tensor* t, const uint32_t* Xbits, int64_t B, int64_t row0, float* G, float* E,
+                                  hobo_best* best, void* stream) {
+  return field_impl(t, reinterpret_cast<const uint8_t*>(Xbits), true, B, row0, G, E, best, stream);
+}
 
 }  // extern "C"
 
 namespace {
 // host-input path of hobo_energy_host / hobo_local_field_host (whole-wave chunks, copy stream)
 hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
-                     hobo_best* best, void* stream) {
+                     hobo_best* best, void* stream, bool packed = false) {
   if (!t) return fail(HOBO_EINVAL, "null handle");
   if (B < 0 || (B > 0 && !X_host) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF)
     return fail(HOBO_EINVAL, "bad batch (B >= 0, X non-null, row0 + B < 2^32)");
@@ -858,6 +888,7 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   if (hobo_status st = ensure_layout(t, field)) return st;
   const DevLayout& L = t->lay[field];
   const int N = t->host.N;
+  const size_t row_bytes = packed ? (size_t)t->W * 4 : (size_t)N;   // one candidate's input bytes
   // chunks of whole waves of (candidate block x column tile) CTAs (CTA pairs take candidate
   // blocks two by two): a one-wave first chunk (its copy is the exposed one), then chunks
   // growing 6x, each copy (PCIe, ~10-20 ns per candidate) hidden behind the previous chunk's
@@ -875,14 +906,14 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
       CK(cudaEventCreateWithFlags(&t->ev_free[i], cudaEventDisableTiming));
     }
   }
-  if ((size_t)chunk * N > t->xh_cap) {
+  if ((size_t)chunk * row_bytes > t->xh_cap) {
     for (int i = 0; i < 2; ++i) {
       if (t->d_xh[i]) cudaFree(t->d_xh[i]);
       t->d_xh[i] = nullptr;
     }
     t->xh_cap = 0;
-    for (int i = 0; i < 2; ++i) CK(cudaMalloc(&t->d_xh[i], (size_t)chunk * N));
-    t->xh_cap = (size_t)chunk * N;
+    for (int i = 0; i < 2; ++i) CK(cudaMalloc(&t->d_xh[i], (size_t)chunk * row_bytes));
+    t->xh_cap = (size_t)chunk * row_bytes;
   }
   if (hobo_status st = grow(t, t->d_Eh, t->Eh_cap, (size_t)B)) return st;
   if (field)
@@ -895,10 +926,11 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
     n = sizes[(size_t)i];
     const int slot = (int)(i & 1);
     if (i >= 2) CK(cudaStreamWaitEvent(t->cs, t->ev_free[slot], 0));   // its previous chunk is packed
-    CK(cudaMemcpyAsync(t->d_xh[slot], X_host + (size_t)off * N, (size_t)n * N, cudaMemcpyHostToDevice, t->cs));
+    CK(cudaMemcpyAsync(t->d_xh[slot], X_host + (size_t)off * row_bytes, (size_t)n * row_bytes, cudaMemcpyHostToDevice,
+                       t->cs));
     CK(cudaEventRecord(t->ev_copied[slot], t->cs));
     CK(cudaStreamWaitEvent(s, t->ev_copied[slot], 0));
-    if (hobo_status st = contract(t, field, t->d_xh[slot], n, field ? t->d_G : nullptr, s)) return st;
+    if (hobo_status st = contract(t, field, t->d_xh[slot], n, field ? t->d_G : nullptr, s, nullptr, packed)) return st;
     CK(cudaEventRecord(t->ev_free[slot], s));
     finalize_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, s>>>(
         t->d_Q, L.n_ct, n, L.lcm, row0 + off, t->d_Eh + off, best ? t->d_key : nullptr);
@@ -930,6 +962,16 @@ hobo_status hobo_energy_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, i
 hobo_status hobo_local_field_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
                                   hobo_best* best, void* stream) {
   return run_host(t, 1, X_host, B, row0, E_host, best, stream);
+}
+
+hobo_status hobo_energy_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0, float* E_host,
+                                  hobo_best* best, void* stream) {
+  return run_host(t, 0, reinterpret_cast<const uint8_t*>(Xbits_host), B, row0, E_host, best, stream, true);
+}
+
+hobo_status hobo_local_field_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0,
+                                       float* E_host, hobo_best* best, void* stream) {
+  return run_host(t, 1, reinterpret_cast<const uint8_t*>(Xbits_host), B, row0, E_host, best, stream, true);
 }
 
 }  // extern "C"

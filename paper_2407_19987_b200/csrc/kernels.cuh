@@ -962,6 +962,18 @@ __global__ void pack_x_kernel(const uint8_t* __restrict__ X, long long B, int N,
   }
 }
 
+// packed candidates (hobo_*_bits): the caller's rows of W words, bit m of word m/32; the bits
+// past N are cleared here, so the generator and the epilogue masks see the same rows as
+// pack_x_kernel would produce
+__global__ void mask_bits_kernel(const uint32_t* __restrict__ in, long long B, int N, int W, uint32_t* __restrict__ bits) {
+  const long long total = B * W;
+  const uint32_t last = (N & 31) ? ((1u << (N & 31)) - 1u) : 0xFFFFFFFFu;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t v = in[i];
+    bits[i] = ((int)(i % W) == W - 1) ? (v & last) : v;
+  }
+}
+
 // split-K: sum the per-split partials in a fixed order (deterministic)
 // (gp_double: the int8 path's exact partials, one rounding to fp32 after the sum)
 __global__ void splitk_reduce_kernel(const float* __restrict__ Gp, float* __restrict__ G, long long nG,

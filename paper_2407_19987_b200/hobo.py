@@ -17,6 +17,7 @@ _STATUS = {1: "EINVAL", 2: "ERANGE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ES
 EXPORTED = [
     "hobo_tensor_build", "hobo_tensor_import_cells", "hobo_tensor_import_colex", "hobo_tensor_import_dense", "hobo_tensor_free", "hobo_tensor_info", "hobo_tensor_digits",
     "hobo_tensor_export_cells", "hobo_tensor_export_dense", "hobo_energy", "hobo_local_field", "hobo_local_field_host", "hobo_energy_host",
+    "hobo_energy_bits", "hobo_local_field_bits", "hobo_energy_host_bits", "hobo_local_field_host_bits",
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
     "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats", "hobo_last_launch_kind",
     "hobo_set_profiling", "hobo_dist_unique_id", "hobo_dist_init", "hobo_dist_finalize", "hobo_dist_info",
@@ -60,6 +61,10 @@ def lib():
         L.hobo_local_field.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
         L.hobo_local_field_host.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_energy_host.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
+        L.hobo_energy_bits.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
+        L.hobo_local_field_bits.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
+        L.hobo_energy_host_bits.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
+        L.hobo_local_field_host_bits.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_search.argtypes = [P, U64, I64, I64, P, C.POINTER(C.c_float), P]
         L.hobo_search_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, C.POINTER(C.c_float),
                                         C.POINTER(I64), P]
@@ -110,6 +115,17 @@ def _dev_ptr(t, dtype, shape=None):
     if shape is not None and tuple(t.shape) != tuple(shape):
         raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
     return C.c_void_p(t.data_ptr())
+
+
+def pack_rows(X):
+    """u8 candidates (numpy B x N, nonzero = 1) -> the packed rows the *_bits calls take:
+    uint32 B x ceil(N/32), bit (m mod 32) of word m/32 = x_m.  Format conversion only."""
+    X = np.ascontiguousarray(X)
+    B, N = X.shape
+    W = (N + 31) // 32
+    Xp = np.zeros((B, W * 32), np.uint8)
+    Xp[:, :N] = X != 0
+    return np.packbits(Xp, axis=1, bitorder="little").view("<u4").reshape(B, W)
 
 
 class HoboTensor:
@@ -253,6 +269,62 @@ class HoboTensor:
 
     def energy_host(self, X, E=None, row0=0, want_best=True, stream=None):
         return self.local_field_host(X, E, row0, want_best, stream, fields=False)
+
+    # ---- packed candidates (hobo_*_bits): rows of ceil(N/32) words, see pack_rows ----
+    def energy_bits(self, Xb, E=None, row0=0, want_best=True, stream=None):
+        """hobo_energy_bits: E_b for a CUDA int32 tensor of packed rows (B x ceil(N/32))."""
+        import torch
+        B = Xb.shape[0]
+        xp = _dev_ptr(Xb, torch.int32, (B, (self.N + 31) // 32))
+        if E is None:
+            E = torch.empty(B, dtype=torch.float32, device=Xb.device)
+        best = HoboBest()
+        _check(lib().hobo_energy_bits(self._h, xp, B, row0, _dev_ptr(E, torch.float32, (B,)),
+                                      C.byref(best) if want_best else None, _stream_handle(stream)))
+        return E, ((best.e, best.idx) if want_best else None)
+
+    def local_field_bits(self, Xb, G=None, E=None, row0=0, want_best=False, stream=None):
+        """hobo_local_field_bits: fields, energies (and the argmin) for packed CUDA rows."""
+        import torch
+        B = Xb.shape[0]
+        xp = _dev_ptr(Xb, torch.int32, (B, (self.N + 31) // 32))
+        if G is None:
+            G = torch.empty(B, self.N, dtype=torch.float32, device=Xb.device)
+        if E is None:
+            E = torch.empty(B, dtype=torch.float32, device=Xb.device)
+        best = HoboBest()
+        _check(lib().hobo_local_field_bits(self._h, xp, B, row0, _dev_ptr(G, torch.float32, (B, self.N)),
+                                           _dev_ptr(E, torch.float32, (B,)), C.byref(best) if want_best else None,
+                                           _stream_handle(stream)))
+        return (G, E, (best.e, best.idx)) if want_best else (G, E)
+
+    def local_field_host_bits(self, Xb, E=None, row0=0, want_best=True, stream=None, fields=True):
+        """hobo_local_field_host_bits (fields=True) / hobo_energy_host_bits: packed rows in host
+        memory (numpy uint32 or a CPU int32 tensor, B x ceil(N/32), ideally pinned)."""
+        W = (self.N + 31) // 32
+        B = Xb.shape[0]
+        if hasattr(Xb, "data_ptr"):
+            if Xb.is_cuda or tuple(Xb.shape) != (B, W) or not Xb.is_contiguous() or Xb.element_size() != 4:
+                raise ValueError(f"expected a contiguous 4-byte CPU tensor of shape {(B, W)}")
+            xp = Xb.data_ptr()
+        else:
+            if Xb.dtype.itemsize != 4 or Xb.shape != (B, W) or not Xb.flags.c_contiguous:
+                raise ValueError(f"expected a C-contiguous 4-byte array of shape {(B, W)}")
+            xp = Xb.ctypes.data
+        if E is None:
+            E = np.empty(B, np.float32)
+        if hasattr(E, "data_ptr"):
+            if E.is_cuda or tuple(E.shape) != (B,) or not E.is_contiguous() or E.dtype != __import__("torch").float32:
+                raise ValueError(f"expected a contiguous float32 CPU tensor of shape {(B,)}")
+            ep = E.data_ptr()
+        else:
+            if E.dtype != np.float32 or E.shape != (B,) or not E.flags.c_contiguous:
+                raise ValueError(f"expected a C-contiguous float32 array of shape {(B,)}")
+            ep = E.ctypes.data
+        best = HoboBest()
+        fn = lib().hobo_local_field_host_bits if fields else lib().hobo_energy_host_bits
+        _check(fn(self._h, xp, B, row0, ep, C.byref(best) if want_best else None, _stream_handle(stream)))
+        return E, ((best.e, best.idx) if want_best else None)
 
     def multilinear_field(self, P, G=None, E=None, stream=None):
         """Gradient and value of the multilinear relaxation at real p (CUDA bf16 tensor B x N)."""

@@ -543,6 +543,56 @@ def test_host_entry_points_match_device_path(H, torch):
 
 
 
+# ---- packed candidates (hobo_*_bits): B x ceil(N/32) words instead of B x N bytes ------------
+@pytest.mark.parametrize("case", ["cfg3", "ragged", "fp32"])
+def test_packed_entry_points_match_byte_path(H, torch, case):
+    """Every *_bits call (device and host buffers) equals its byte-input call bit for bit, on
+    the packed rows of the same candidates; garbage in the pad bits past N is ignored.  Byte
+    path results are themselves pinned to the oracle by the tests above; here the oracle is
+    checked again on the packed call."""
+    if case == "cfg3":
+        p = cfg3_problem()
+        t, o = H.HoboTensor.from_problem(p), None
+        B, row0 = 20000, 11
+    elif case == "ragged":
+        p = random_integer_problem(3, 300, 41, nterms=800)          # N = 300: a 12-bit last word
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        B, row0 = 1000, 0
+    else:
+        idx, val = uniform_cells(3, 130, 12)                       # int8 planes, 2-bit last word
+        t, o = H.HoboTensor.import_cells(3, 130, idx, val), Oracle.from_cells(3, 130, idx, val)
+        B, row0 = 500, 3
+    Xh = x_bits(21, B, t.N)
+    Xp = H.pack_rows(Xh)
+    assert Xp.shape == (B, (t.N + 31) // 32) and Xp.dtype == np.uint32
+    if t.N % 32:
+        Xp[:, -1] |= np.uint32(0xFFFFFFFF) << np.uint32(t.N % 32)   # pad bits set: must be ignored
+    Xd, Xpd = dev(torch, Xh), torch.from_numpy(Xp.view(np.int32)).cuda()
+    G, E, best = t.local_field(Xd, row0=row0, want_best=True)
+    Ee, beste = t.energy(Xd, row0=row0)
+    Gb, Eb, bestb = t.local_field_bits(Xpd, row0=row0, want_best=True)
+    Eeb, besteb = t.energy_bits(Xpd, row0=row0)
+    torch.cuda.synchronize()
+    assert torch.equal(G, Gb) and torch.equal(E, Eb) and best == bestb
+    assert torch.equal(Ee, Eeb) and beste == besteb
+    pinned = torch.from_numpy(Xp.view(np.int32)).pin_memory()
+    for src in (Xp, pinned):
+        Eh, besth = t.local_field_host_bits(src, row0=row0)
+        assert np.array_equal(Eh, E.cpu().numpy()) and besth == best
+        Eh2, besth2 = t.local_field_host_bits(src, row0=row0, fields=False)
+        assert np.array_equal(Eh2, Ee.cpu().numpy()) and besth2 == beste
+    if o is not None:
+        Eo = o.energy(Xh)
+        if t.is_integer:
+            assert np.array_equal(Eb.cpu().numpy(), Eo) and np.array_equal(Gb.cpu().numpy(), o.field(Xh))
+        else:
+            assert np.max(np.abs(Eeb.cpu().numpy() - Eo)) <= o.tau
+    # empty batches
+    none = (float("inf"), -1)
+    assert t.energy_bits(Xpd[:0])[1] == none
+    assert t.local_field_host_bits(Xp[:0])[1] == none
+
+
 # ---- the library's own NCCL communicator (hobo_dist_*), exercised at world size 1 -----------
 def test_library_comm_world1_matches_single_gpu(H, torch):
     """With a communicator every best goes through ncclAllReduce(MIN) and hobo_search through
@@ -637,6 +687,35 @@ def test_cta_pair_and_single_paths(H, torch, force):
             del os.environ["HOBO_PAIR"]
         else:
             os.environ["HOBO_PAIR"] = old
+
+
+# ---- column tiles longest-first (HOBO_CT_DESC) ---------------------------------------------
+@pytest.mark.parametrize("desc", ["1", "0"])
+def test_column_tile_order(H, torch, desc):
+    """The triangular (energy-mode) schedules give later column tiles more K-blocks, so they
+    are issued first by default; either order gives the same per-candidate results (each tile
+    is one CTA's independent work): bit-exact on integer cells (bf16 and int8), within tau on
+    fp32 cells, with several column tiles and a ragged candidate tail."""
+    with env("HOBO_CT_DESC", desc):
+        p = random_integer_problem(3, 300, 41, nterms=800)
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        X = x_bits(9, 700, t.N)
+        Ee, best = energies(H, torch, t, X)
+        G, E = fields(H, torch, t, X)
+        Eo = o.energy(X)
+        assert np.array_equal(Ee, Eo) and np.array_equal(E, Eo) and np.array_equal(G, o.field(X))
+        check_argmin(best, Eo, 0.0)
+        for i8 in ("1", "0"):
+            with env("HOBO_I8", i8):
+                idx, val = uniform_cells(3, 300, 5)                # 2-3 column tiles
+                t, o = H.HoboTensor.import_cells(3, 300, idx, val), Oracle.from_cells(3, 300, idx, val)
+                X = x_bits(10, 300, 300)
+                Ee, best = energies(H, torch, t, X)
+                Eo = o.energy(X)
+                if i8 == "1" and t.launch_stats()["i8_planes"]:
+                    assert np.array_equal(Ee, f32(Eo))
+                assert np.max(np.abs(Ee - Eo)) <= o.tau
+                check_argmin(best, Eo, o.tau)
 
 
 # ---- int8 digit planes (tcgen05.mma kind::i8): exact integer accumulation --------------------

@@ -195,3 +195,20 @@ def test_import_dense_canonicalises_like_the_oracle(H):
     nz = np.argwhere(dense != 0).astype(np.int32)
     o = Oracle.from_cells(order, N, nz, dense[tuple(nz.T)])
     _same_cells(t, o)
+
+
+def test_pack_rows_bit_order(H):
+    """hobo_*_bits row format (include/hobo.h): bit (m mod 32) of word m/32 is x_m, LSB first,
+    pad bits zero.  Checked against the definition written out with Python integers."""
+    rng = np.random.default_rng(5)
+    for N in (1, 31, 32, 33, 300, 512):
+        X = (rng.random((7, N)) < 0.5).astype(np.uint8)
+        X[0] = 0
+        X[1] = 1
+        P = H.pack_rows(X * 3)                                      # any nonzero byte is a 1
+        assert P.dtype == np.uint32 and P.shape == (7, (N + 31) // 32)
+        for b in range(7):
+            for w in range(P.shape[1]):
+                want = sum(int(X[b, m]) << (m - 32 * w) for m in range(32 * w, min(N, 32 * w + 32)))
+                assert int(P[b, w]) == want
+
