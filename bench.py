@@ -392,9 +392,9 @@ def main():
     traffic, traffic_src = None, None
     try:   # dram read+write bytes per launch of this kernel from the committed ncu --set full capture
         if a.config == "cfg3" and B == 65536:
-            with open(os.path.join(ROOT, "profiles", "r01_cfg3_ncu.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r01_cfg3_final_ncu.json")) as f:
                 traffic = json.load(f)["traffic_bytes_per_launch"]
-                traffic_src = "profiles/r01_cfg3_ncu.json (ncu --set full, dram__bytes_read+write)"
+                traffic_src = "profiles/r01_cfg3_final_ncu.json (ncu --set full, dram__bytes_read+write)"
     except Exception:
         pass
     import math
