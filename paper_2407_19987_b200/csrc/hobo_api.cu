@@ -612,6 +612,19 @@ hobo_status empty_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
   return finish_best(t, best, s);
 }
 
+// stage X: u8 B x N -> bit rows; whole-word rows from an aligned buffer
+// take the vectorised kernel (cfg2: 65 -> ~12 us per 64 MB)
+void launch_pack_x(const uint8_t* X, long long B, int N, int W, uint32_t* bits, cudaStream_t s) {
+  if (N % 32 == 0 && ((uintptr_t)X & 15) == 0) {
+    const long long nchunks = B * (long long)N / 16;
+    pack_x16_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>((nchunks + 255) / 256, 148 * 16)), 256, 0, s>>>(
+        reinterpret_cast<const uint4*>(X), nchunks, bits);
+  } else {
+    const long long nw = B * W;
+    pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, N, W, bits);
+  }
+}
+
 // layout slot of the real-valued path: the field layout, or, when its p rows plus L limb
 // boxes of 256 columns do not fit in shared memory (e.g. N = 512 at L = 3), the same layout
 // with 128-column tiles (half-size boxes).  (128-column tiles everywhere measured 1.8x slower
@@ -636,8 +649,7 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
       mask_bits_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(
           reinterpret_cast<const uint32_t*>(X), B, t->host.N, t->W, t->d_bits);
     else
-      pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, t->host.N, t->W,
-                                                                                               t->d_bits);
+      launch_pack_x(X, B, t->host.N, t->W, t->d_bits, s);
     CK(cudaGetLastError());
   }
   KrParams p = make_params(t, L, t->d_bits, B, G, t->d_Q);
@@ -1790,8 +1802,7 @@ hobo_status hobo_tt_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t 
   }
   if (B == 0) return empty_best(t, best, (cudaStream_t)stream);
   if (hobo_status st = grow(t, t->d_bits, t->bits_cap, (size_t)B * W)) return st;
-  const long long nw = B * W;
-  pack_x_kernel<<<(unsigned)std::min<long long>((nw + 255) / 256, 148 * 16), 256, 0, s>>>(X, B, N, W, t->d_bits);
+  launch_pack_x(X, B, N, W, t->d_bits, s);
   int ncores = 0;
   for (const auto& c : t->tt.cores) ncores += (int)c.size();
   const size_t smem = (size_t)ncores * sizeof(double);

@@ -962,6 +962,32 @@ __global__ void pack_x_kernel(const uint8_t* __restrict__ X, long long B, int N,
   }
 }
 
+// the same for N % 32 == 0 and a 16-byte aligned X: rows are whole words, so the batch is one
+// flat stream of 16-byte chunks; lane l loads chunk l of its warp's 32 (coalesced 512 B per
+// load), turns it into a 16-bit nonzero mask, and the even lane joins its odd neighbour's
+// mask into one output word (flat word c/2 == row b, word w)
+__global__ void pack_x16_kernel(const uint4* __restrict__ X, long long nchunks, uint32_t* __restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long base = warp * 32; base < nchunks; base += nwarps * 32) {
+    const long long c = base + lane;
+    uint32_t m = 0;
+    if (c < nchunks) {
+      const uint4 v = X[c];
+      const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // 0xFF per nonzero byte -> byte k of (.. & 0x08040201) holds 2^k -> byte sum = the 4-bit mask
+        const uint32_t ne = __vcmpne4(q[k], 0u) & 0x08040201u;
+        m |= ((ne * 0x01010101u) >> 24) << (4 * k);
+      }
+    }
+    const uint32_t hi = __shfl_down_sync(0xFFFFFFFFu, m, 1);
+    if (!(lane & 1) && c < nchunks) bits[c >> 1] = m | (hi << 16);
+  }
+}
+
 // packed candidates (hobo_*_bits): the caller's rows of W words, bit m of word m/32; the bits
 // past N are cleared here, so the generator and the epilogue masks see the same rows as
 // pack_x_kernel would produce

@@ -593,6 +593,25 @@ def test_packed_entry_points_match_byte_path(H, torch, case):
     assert t.local_field_host_bits(Xp[:0])[1] == none
 
 
+def test_stage_x_vectorised_and_bytewise_paths(H, torch):
+    """Stage X: rows of whole words from a 16-byte aligned buffer take the
+    vectorised packer, anything else the bytewise one; both give the same bits, so the same
+    energies and fields (any nonzero byte counts as 1)."""
+    p = random_integer_problem(3, 64, 17, nterms=400)            # N = 64: whole words
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    Xh = x_bits(23, 777, t.N)
+    Xd = dev(torch, Xh * np.uint8(200))                           # nonzero bytes other than 1
+    buf = torch.zeros(Xh.size + 1, dtype=torch.uint8, device="cuda")
+    buf[1:].copy_(Xd.reshape(-1))
+    Xu = buf[1:].view(777, t.N)                                    # unaligned: the bytewise path
+    assert Xu.data_ptr() % 16 == 1
+    Ga, Ea = t.local_field(Xd)
+    Gu, Eu = t.local_field(Xu)
+    Eo = o.energy(Xh)
+    assert np.array_equal(Ea.cpu().numpy(), Eo) and torch.equal(Ea, Eu) and torch.equal(Ga, Gu)
+    assert np.array_equal(Ga.cpu().numpy(), o.field(Xh))
+
+
 # ---- the library's own NCCL communicator (hobo_dist_*), exercised at world size 1 -----------
 def test_library_comm_world1_matches_single_gpu(H, torch):
     """With a communicator every best goes through ncclAllReduce(MIN) and hobo_search through
