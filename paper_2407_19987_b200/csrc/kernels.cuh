@@ -363,13 +363,24 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       prow[i] = v;
     }
   } else {
-    // this CTA's candidate bits, column-major xs[w][row] (+2 zero words for window reads)
+    // this CTA's candidate bits, column-major xs[w][row] (+2 zero words for window reads).
+    // Consecutive threads take consecutive rows of one word (conflict-free stores; the rows'
+    // sectors are shared through L1), and XU loads are in flight before the first store, so
+    // the staging costs ~1 global latency instead of one per 320 words
     const int Wp = p.W + 2;
-    for (int i = threadIdx.x; i < Wp * kBM; i += kThreads) {
-      const int r = i / Wp, w = i % Wp;
-      uint32_t v = 0;
-      if (w < p.W && b0 + r < p.B) v = __ldg(p.xbits + (size_t)(b0 + r) * p.W + w);
-      xs[w * kBM + r] = v;
+    constexpr int XU = 16;
+    for (int i0 = threadIdx.x; i0 < Wp * kBM; i0 += kThreads * XU) {
+      uint32_t v[XU];
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = i0 + u * kThreads, r = i % kBM, w = i / kBM;
+        v[u] = (w < p.W && b0 + r < p.B) ? __ldg(p.xbits + (size_t)(b0 + r) * p.W + w) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = i0 + u * kThreads;
+        if (i < Wp * kBM) xs[i] = v[u];   // i == w * kBM + r
+      }
     }
   }
   tc_fence_before();
