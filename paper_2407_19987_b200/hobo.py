@@ -314,7 +314,8 @@ class HoboTensor:
         if E is None:
             E = np.empty(B, np.float32)
         if hasattr(E, "data_ptr"):
-            if E.is_cuda or tuple(E.shape) != (B,) or not E.is_contiguous() or E.dtype != __import__("torch").float32:
+            import torch
+            if E.is_cuda or tuple(E.shape) != (B,) or not E.is_contiguous() or E.dtype != torch.float32:
                 raise ValueError(f"expected a contiguous float32 CPU tensor of shape {(B,)}")
             ep = E.data_ptr()
         else:
