@@ -267,10 +267,24 @@ def run_reference(a, world, rank):
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{S} cfg3 candidates per step (field + energy + argmin), {cores} threads"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(json.dumps(line))
+
+
+_JSON_FD = None
+
+
+def emit(text):
+    """The ONE JSON line, on the process's real stdout."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (text + "\n").encode())
 
 
 def main():
+    # everything else written to fd 1 (NCCL's "NCCL version ..." banner when NCCL_DEBUG is set,
+    # library or torch prints) goes to stderr, so stdout carries only the JSON line
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     a = parse()
     world, rank, local = dist_env()
     if a.impl == "reference":
@@ -550,7 +564,7 @@ def main():
         line.update(extras)
         if "e2e" not in line:
             line["e2e"] = None
-        print(json.dumps(line), flush=True)
+        emit(json.dumps(line))
     if lib_comm:
         from paper_2407_19987_b200 import hobo as _hobo
         _hobo.dist_finalize()

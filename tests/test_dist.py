@@ -113,3 +113,25 @@ def test_gloo_combine_and_sharded_search(world):
         x, e, c = res[rank]["search"]
         assert (e, c) == (float(np.float32(r["e_best"])), r["best_chain"])
         assert x == r["chain_xbest"][c].tolist()
+
+
+def test_bench_reference_arm_under_torchrun_world2():
+    """The driver's launch of the reference arm at N=2 (torchrun, one process per rank):
+    rank 0 alone times the oracle and stdout carries exactly one JSON line; the other rank
+    exits 0 without work.  CPU only (the reference arm never touches a GPU)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NCCL_DEBUG="WARN")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29611", "bench.py", "--impl", "reference",
+                        "--gpus", "2", "--steps", "1", "--warmup", "0"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
