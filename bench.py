@@ -547,7 +547,8 @@ def main():
             extras["sa_sweep"] = sa_extra(t, B, N, stream)
         if rank == 0 and a.config == "cfg3":
             extras["tt_form"] = tt_form_extra(dev, stream, flush_l2)
-            extras["cpu_baseline"] = cpu_baseline()
+            if world == 1:                    # the oracle baseline: rank 0 at N = 1 only
+                extras["cpu_baseline"] = cpu_baseline()
     if world > 1:
         dist.barrier()
     if rank == 0:
