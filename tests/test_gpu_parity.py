@@ -638,6 +638,9 @@ def test_library_comm_world1_matches_single_gpu(H, torch):
         assert t.energy(X, row0=3)[1] == ref_b
         assert t.local_field(X, row0=3, want_best=True)[2] == ref_b
         assert t.local_field_host(Xh, row0=3)[1] == ref_b
+        Xp = H.pack_rows(Xh)
+        assert t.local_field_host_bits(Xp, row0=3)[1] == ref_b
+        assert t.energy_bits(torch.from_numpy(Xp.view(np.int32)).cuda(), row0=3)[1] == ref_b
         assert t.energy(X[:0])[1] == (float("inf"), -1)
     finally:
         H.dist_finalize()
