@@ -198,7 +198,8 @@ cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  k<<<dim3((unsigned)(p.n_split * p.n_ct * p.n_cb)), dim3(kThreads), smem, s>>>(L.tmap, p);
+  const int mb = (REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
+  k<<<dim3((unsigned)(p.n_split * p.n_ct * ((p.n_cb + mb - 1) / mb))), dim3(kThreads), smem, s>>>(L.tmap, p);
   return cudaGetLastError();
 }
 
@@ -508,6 +509,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.n_cb = (int)((B + kBM - 1) / kBM);
   p.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, 2 * kBK) / kBK);
   p.n_split = 1;
+  p.cb_iters = 1;
   {
     // longest-first: the open index's last column tile has the most rows,
     // and issuing it first keeps the short tiles for the tail of the last wave
@@ -660,6 +662,14 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     p.preal = P;
   }
   p.n_split = choose_split(t, L, B);
+  // energy-mode bf16 launches on single CTAs (short K loops, e.g. cfg2): each CTA loops over
+  // cb_iters candidate blocks (HOBO_CB_ITERS overrides)
+  if (!P && !field && !L.i8 && p.n_split == 1 && !use_pairs(L, p)) {
+    // two blocks per CTA when that still leaves >= 4 waves (cfg2: 195 -> 199 M cand/s; 3-4
+    // blocks lose more to the coarser tail than they save)
+    p.cb_iters = (long long)L.n_ct * ((p.n_cb + 1) / 2) >= 4 * 148 ? 2 : 1;
+    if (const char* e = getenv("HOBO_CB_ITERS")) p.cb_iters = std::max(1, atoi(e));
+  }
   if (p.n_split > 1) {
     if (field) {
       if (hobo_status st = grow(t, t->d_Gpart, t->Gpart_cap, (size_t)p.n_split * B * t->host.N * (L.i8 ? 2 : 1))) return st;

@@ -42,6 +42,9 @@ struct KrParams {
   int LA;                   // bf16 limbs of the Khatri-Rao products of p (exact for <= 3 factors)
   int ring_boxes;           // W boxes that fit next to the p rows in shared memory
   int pstride;              // p row stride in shared memory (elements, odd word count)
+  int cb_iters;             // > 1 (single-CTA bf16 binary launches only): each CTA loops over this many
+                            // candidate blocks of one column tile, so a block's W fill and prologue
+                            // overlap the previous block's epilogue (short K loops, e.g. cfg2)
   int ct_desc;              // 1: column tiles in descending order (the heaviest K schedules start
                             // first, so the light tiles fill the tail of the last wave)
   int n_split;              // split-K: CTAs of one (candidate block, column tile) split the K
@@ -81,7 +84,7 @@ struct KrCfg {
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
   static constexpr int MAXD = 16;                        // descriptor ring slots (>= DAHEAD + MAXST)
   static constexpr int DAHEAD = 8;                       // descriptors run this many stages ahead of W
-  static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 3;
+  static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 4;
   static constexpr int DESC_BYTES = 0;                   // (bf16 launches read their descriptors with __ldg)
   // I8: the descriptor ring holds the stages' run records (srec_u4 uint4s per slot)
   __host__ __device__ static size_t desc_bytes(int srec_u4) { return I8 ? (size_t)MAXD * srec_u4 * 16 : DESC_BYTES; }
@@ -279,7 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t sBar = sB + ring * C::BOX;
   const uint32_t acc_full = sBar + 8 * (2 * C::MAXST + 2 * C::MAXA + C::MAXD);
   const uint32_t snap_full = acc_full + 8, snap_empty = acc_full + 16;
-  const uint32_t tslot = acc_full + 24;
+  const uint32_t acc_empty = acc_full + 24;                      // cb_iters > 1: epilogue done with TMEM
+  const uint32_t tslot = acc_full + 32;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
   const uint32_t sD = sQ + kBM * 8;                               // I8: descriptor ring (one slot per W stage)
   const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4);
@@ -298,13 +302,16 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   // share W tiles in L2); pairs: cluster c holds candidate blocks 2c', 2c'+1 of one tile
   const uint32_t prank = PAIR ? cluster_ctarank() : 0u;
   const bool leader = !PAIR || prank == 0;
-  const int ncb_eff = PAIR ? (p.n_cb + 1) / 2 : p.n_cb;
+  const int MB = (PAIR || SA || REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
+  const int ncb_eff = PAIR ? (p.n_cb + 1) / 2 : (p.n_cb + MB - 1) / MB;
   const int bid = PAIR ? (int)(blockIdx.x / 2) : (int)blockIdx.x;
   const int cb = PAIR ? 2 * (bid % ncb_eff) + (int)prank : bid % ncb_eff;
   const int ct_i = (bid / ncb_eff) % p.n_ct;
   const int ct = (!SA && p.ct_desc) ? p.n_ct - 1 - ct_i : ct_i;
   const int split = bid / (ncb_eff * p.n_ct);
   const long long b0 = (long long)cb * kBM;
+  // MB > 1: this CTA's candidate blocks are cb, cb + ncb_eff, ... (< n_cb)
+  const int ntile = MB == 1 ? 1 : (p.n_cb - 1 - cb) / ncb_eff + 1;
   constexpr uint32_t BOXB = PAIR ? C::BOX / 2 : C::BOX;   // shared-memory bytes of one W box per CTA
   const int KPS = REAL ? 1 : C::kps(p.L);
   // CTA pairs hold half boxes, so the same ring fits twice the stages (TMEM: 256 + 4 x 64 columns)
@@ -347,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     mbar_init(acc_full, 1);
     mbar_init(snap_full, 1);
     mbar_init(snap_empty, PAIR ? 16 : 8);
+    mbar_init(acc_empty, 8);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap);
@@ -354,6 +362,27 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     if constexpr (PAIR) tmem_alloc_pair(tslot, C::TMEM_COLS);
     else tmem_alloc(tslot, C::TMEM_COLS);
   }
+  // this CTA's candidate bits, column-major xs[w][row] (+2 zero words for window reads).
+  // Consecutive threads take consecutive rows of one word (conflict-free stores; the rows'
+  // sectors are shared through L1), and XU loads are in flight before the first store, so
+  // the staging costs ~1 global latency instead of one per 320 words
+  auto stage_x = [&](long long bb0, int tid, int nthr) {
+    const int Wp = p.W + 2;
+    constexpr int XU = 16;
+    for (int i0 = tid; i0 < Wp * kBM; i0 += nthr * XU) {
+      uint32_t v[XU];
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = i0 + u * nthr, r = i % kBM, w = i / kBM;
+        v[u] = (w < p.W && bb0 + r < p.B) ? __ldg(p.xbits + (size_t)(bb0 + r) * p.W + w) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = i0 + u * nthr;
+        if (i < Wp * kBM) xs[i] = v[u];   // i == w * kBM + r
+      }
+    }
+  };
   if constexpr (REAL) {
     // this CTA's p rows (bf16), zero past N and past B; +64 slack for window over-reads
     for (int i = threadIdx.x; i < kBM * p.pstride + 64; i += kThreads) {
@@ -363,25 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       prow[i] = v;
     }
   } else {
-    // this CTA's candidate bits, column-major xs[w][row] (+2 zero words for window reads).
-    // Consecutive threads take consecutive rows of one word (conflict-free stores; the rows'
-    // sectors are shared through L1), and XU loads are in flight before the first store, so
-    // the staging costs ~1 global latency instead of one per 320 words
-    const int Wp = p.W + 2;
-    constexpr int XU = 16;
-    for (int i0 = threadIdx.x; i0 < Wp * kBM; i0 += kThreads * XU) {
-      uint32_t v[XU];
-#pragma unroll
-      for (int u = 0; u < XU; ++u) {
-        const int i = i0 + u * kThreads, r = i % kBM, w = i / kBM;
-        v[u] = (w < p.W && b0 + r < p.B) ? __ldg(p.xbits + (size_t)(b0 + r) * p.W + w) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < XU; ++u) {
-        const int i = i0 + u * kThreads;
-        if (i < Wp * kBM) xs[i] = v[u];   // i == w * kBM + r
-      }
-    }
+    stage_x(b0, (int)threadIdx.x, kThreads);
   }
   tc_fence_before();
   if constexpr (PAIR) cluster_sync_all();   // both CTAs' barriers initialised, TMEM allocated
@@ -459,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         dskip();
         for (int i = 0; i < C::DAHEAD; ++i) dissue();
       }
+      for (int it = 0; it < ntile; ++it)   // MB > 1: the same W sequence for every block
       for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
@@ -502,6 +514,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       uint32_t ph = 0, pha = 0;
       uint32_t issued = 0;
       PT(unsigned long long stt[6] = {0, 0, 0, 0, 0, 0}; const long long t_start = clock64(); long long t0;)
+      for (int it = 0; it < ntile; ++it) {
+      if (it > 0) {   // the previous block's epilogue has read the accumulator
+        mbar_wait(acc_empty, (uint32_t)((it - 1) & 1));
+        tc_fence_after();
+        issued = 0;
+      }
       for (int j = p.nseg - 1; j >= 0; --j) {
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
@@ -609,6 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
       }
       __syncwarp();
+      }   // tiles
       PT(if (lane == 0) { stt[0] = clock64() - t_start; for (int i = 0; i < 6; ++i) PSTAT_FLUSH(i, stt[i]); })
     }
   } else {
@@ -678,6 +697,15 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       }
       return acc;
     };
+    for (int it = 0; it < ntile; ++it) {
+    const long long b0t = b0 + (long long)it * ncb_eff * kBM;   // this block's first candidate
+    if (it > 0) {   // every warp is done with the previous block's bits: stage this block's
+      named_bar_sync(1, 256);
+      stage_x(b0t, (int)threadIdx.x - 64, 256);
+      named_bar_sync(1, 256);
+      any = false;
+      nsnap = 0;
+    }
     for (int j = p.nseg - 1; j >= 0; --j) {
       const int2 s = sched[j];
       if constexpr (REAL) {
@@ -833,9 +861,9 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 
     // ---------------- epilogue: fields, energy partial (this warp's column half) ---------------
     PT(if (warp == 2 && lane == 0) { PSTAT_FLUSH(7, w_gen); PSTAT_FLUSH(8, w_bits); PSTAT_FLUSH(9, w_st); PSTAT_FLUSH(10, w_arr); })
-    mbar_wait(acc_full, 0);
+    mbar_wait(acc_full, (uint32_t)(it & 1));
     tc_fence_after();
-    const long long b = b0 + row;
+    const long long b = b0t + row;
     const bool live = b < p.B;
     double sfin = 0.0, sp = 0.0;
     for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
@@ -923,6 +951,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
       }
     }
+    if (MB > 1) {   // the accumulator is free for the next block's MMAs
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+    }
     if constexpr (!SA) {
     double qsum;
     if (snaps) {
@@ -942,6 +975,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     named_bar_sync(1, 256);
     if (h == 0 && live) p.Q[((size_t)split * p.n_ct + ct) * p.B + b] = qsum + qpart[row];
     }
+    }   // tiles
   }
 #undef FULL
 #undef EMPTY

@@ -740,6 +740,30 @@ def test_column_tile_order(H, torch, desc):
                 check_argmin(best, Eo, o.tau)
 
 
+# ---- energy launches looping each CTA over several candidate blocks (HOBO_CB_ITERS) -------------
+@pytest.mark.parametrize("iters", ["1", "2", "3", "8"])
+def test_energy_multi_block_ctas(H, torch, iters):
+    """A CTA that runs several candidate blocks back to back (the next block's W fill overlapping
+    the previous epilogue; accumulator handed back through a barrier) gives the same energies
+    and argmin: bit-exact on integer cells, within tau on fp32 cells; ragged block counts."""
+    with env("HOBO_CB_ITERS", iters), env("HOBO_PAIR", "0"), env("HOBO_I8", "0"):
+        p = random_integer_problem(3, 300, 41, nterms=800)
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        for B in (1, 700, 1300):                                   # 1, 6, 11 candidate blocks
+            X = x_bits(31, B, t.N)
+            Ee, best = energies(H, torch, t, X, row0=5)
+            Eo = o.energy(X)
+            assert np.array_equal(Ee, Eo)
+            check_argmin(best, Eo, 0.0, row0=5)
+        idx, val = uniform_cells(2, 1024, 2)                       # cfg2's shape, 4 column tiles
+        t, o = H.HoboTensor.import_cells(2, 1024, idx, val), Oracle.from_cells(2, 1024, idx, val)
+        X = x_bits(32, 1500, 1024)
+        Ee, best = energies(H, torch, t, X)
+        Eo = o.energy(X)
+        assert np.max(np.abs(Ee - Eo)) <= o.tau
+        check_argmin(best, Eo, o.tau)
+
+
 # ---- int8 digit planes (tcgen05.mma kind::i8): exact integer accumulation --------------------
 @pytest.mark.parametrize("i8", ["1", "0"])
 @pytest.mark.parametrize("order,N,B,seed", [(2, 300, 700, 11), (3, 130, 500, 12), (3, 260, 383, 13), (4, 30, 300, 14),
