@@ -869,6 +869,14 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
       const int mbase = ct * NT + c0;
       const uint32_t xw = REAL ? 0u : ((mbase >> 5) < p.W ? xs[(mbase >> 5) * kBM + row] : 0u);
+      // the chunk's degree-1 cells (counted once: split 0), 8 vector loads issued before the
+      // accumulator is read (p1 is Npad floats, mbase a multiple of 32)
+      float pmv[32];
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        const float4 v4 = split == 0 ? __ldg(reinterpret_cast<const float4*>(p.p1 + mbase + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        pmv[c] = v4.x; pmv[c + 1] = v4.y; pmv[c + 2] = v4.z; pmv[c + 3] = v4.w;
+      }
       float g[32];
       if constexpr (I8) {   // exact integer field; one rounding to fp32 after adding the degree-1 cell
         long long v[32];
@@ -883,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const double vd = (double)v[c] * p.qscale;
-          const float pm = split == 0 ? __ldg(p.p1 + mbase + c) : 0.0f;
+          const float pm = pmv[c];
           g[c] = (float)(vd + (double)pm);
           if (gdp && mbase + c < p.N) gdp[c] = vd + (double)pm;
           if ((xw >> c) & 1u) {
@@ -904,7 +912,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         const float v = __uint_as_float(r[c]);
-        const float pm = split == 0 ? __ldg(p.p1 + mbase + c) : 0.0f;   // degree 1 counted once
+        const float pm = pmv[c];   // degree 1 counted once
         g[c] = v + pm;
         if constexpr (REAL) {
           const double pw = mbase + c < p.N ? (double)bf16_bits_to_float(prow_r[mbase + c]) : 0.0;
