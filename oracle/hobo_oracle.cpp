@@ -62,9 +62,9 @@ int finish(Oracle* o, const Map& m) {
   std::vector<std::pair<std::vector<int32_t>, std::pair<Mono, float>>> cells;
   for (auto& kv : m) {
     if (kv.first.empty()) continue;                   // constant -> offset
-    if ((int)kv.first.size() > o->order) return 3;    // O2: order < degree is an error
     long double c = (long double)kv.second;
-    if (c == 0) continue;                             // exact zeros dropped
+    if (c == 0) continue;                             // O1: exact zeros dropped (a cancelled monomial is gone)
+    if ((int)kv.first.size() > o->order) return 3;    // O2, on what remains: order < degree is an error
     if (std::fabs(c) > (long double)std::numeric_limits<float>::max()) return 2;
     float f = (float)c;                               // one round-to-nearest-even
     if (f == 0.0f) continue;
@@ -510,9 +510,11 @@ int or_search_thresholds(int64_t iters, double p0, double p1, uint32_t* out) {
 
 // O8: the hobo_search rule of SURVEY 8(c) (the paper's sampler is undisclosed, P:199;
 // SA is described only qualitatively), replayed one chain at a time.
-int or_search(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
-              double p0, double p1, double* chain_ebest, uint8_t* chain_xbest,
-              double* e_best, int64_t* best_chain, int nthreads) {
+// x_trace (nullable): [nchains][iters+1][N], the state evaluated at t = 0..iters;
+// m_trace (nullable): [nchains][iters], the flipped site m* of iteration t.
+int or_search_trace(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
+                    double p0, double p1, double* chain_ebest, uint8_t* chain_xbest,
+                    double* e_best, int64_t* best_chain, int nthreads, uint8_t* x_trace, int32_t* m_trace) {
   Oracle* o = (Oracle*)h;
   if (!o || nchains < 1 || iters < 0) return 1;
   const int N = o->N;
@@ -528,7 +530,12 @@ int or_search(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t i
       float e = (float)energy_one(o, x.data());    // the kernel decides in fp32
       if (e < best) { best = e; xb = x; }            // equal E: the earliest t is kept
     };
+    auto record = [&](int64_t t) {
+      if (x_trace)
+        for (int m = 0; m < N; ++m) x_trace[((size_t)i * (size_t)(iters + 1) + (size_t)t) * N + m] = x[m];
+    };
     for (int64_t t = 0; t < iters; ++t) {
+      record(t);
       consider();
       field_one(o, x.data(), g.data());
       const uint64_t r = or_hash(seed, 2, c, (uint64_t)t);
@@ -546,8 +553,10 @@ int or_search(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t i
         }
         if (!(dmin < 0.0f)) ms = mrand;
       }
+      if (m_trace) m_trace[(size_t)i * (size_t)iters + (size_t)t] = ms;
       x[ms] ^= 1;
     }
+    record(iters);
     consider();
     chain_ebest[i] = best;
     for (int m = 0; m < N; ++m) chain_xbest[i * N + m] = xb[m];
@@ -561,6 +570,13 @@ int or_search(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t i
   return 0;
 }
 
+int or_search(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
+              double p0, double p1, double* chain_ebest, uint8_t* chain_xbest,
+              double* e_best, int64_t* best_chain, int nthreads) {
+  return or_search_trace(h, seed, chain0, nchains, iters, p0, p1, chain_ebest, chain_xbest, e_best, best_chain,
+                         nthreads, nullptr, nullptr);
+}
+
 
 // SPEC sa_run's geometric schedule: T_s = t_start (t_end/t_start)^(s/max(1,sweeps-1))
 int or_sa_temps(int64_t sweeps, double t_start, double t_end, double* out) {
@@ -569,6 +585,11 @@ int or_sa_temps(int64_t sweeps, double t_start, double t_end, double* out) {
     out[s] = t_start * std::pow(t_end / t_start, (double)s / (double)std::max<int64_t>(1, sweeps - 1));
   return 0;
 }
+
+// Metropolis acceptance of an energy change d at temperature T with the uniform u in [0, 1):
+// accept with probability min(1, exp(-d/T)), i.e. iff d <= 0 or
+// u < exp(-d/T) <=> d < -T ln u for u in (0, 1) (the log form, reading 22)
+int or_sa_accept(double d, double T, double u) { return (d <= 0.0 || d < -T * std::log(u)) ? 1 : 0; }
 
 // SPEC sa_run: Metropolis single-bit flips in index order, one chain at a time
 int or_sa(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweeps, double t_start, double t_end,
@@ -600,7 +621,7 @@ int or_sa(void* h, uint64_t seed, int64_t chain0, int64_t nchains, int64_t sweep
         // Metropolis: accept with probability min(1, exp(-d/T)), i.e. iff d <= 0 or
         // u < exp(-d/T) <=> d < -T ln u for u in (0,1)  (reading 22)
         const double u = (double)(or_hash(seed, 4, c, (uint64_t)(s * N + m)) >> 11) * 0x1.0p-53;
-        const bool accept = d <= 0.0 || d < -T[(size_t)s] * std::log(u);
+        const bool accept = or_sa_accept(d, T[(size_t)s], u) != 0;
         if (accept) {
           x[m] ^= 1;
           e += d;

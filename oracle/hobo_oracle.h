@@ -69,6 +69,13 @@ int or_brute(void* handle, double* emin, int64_t* argmin, int64_t* n_ground, dou
 int or_search(void* handle, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
               double p0, double p1, double* chain_ebest, uint8_t* chain_xbest,
               double* e_best, int64_t* best_chain, int nthreads);
+/* or_search with its trajectory: x_trace (nullable) [nchains][iters+1][N] = the state
+ * evaluated at t = 0..iters; m_trace (nullable) [nchains][iters] = the site flipped at t.  */
+int or_search_trace(void* handle, uint64_t seed, int64_t chain0, int64_t nchains, int64_t iters,
+                    double p0, double p1, double* chain_ebest, uint8_t* chain_xbest,
+                    double* e_best, int64_t* best_chain, int nthreads, uint8_t* x_trace, int32_t* m_trace);
+/* Metropolis acceptance of or_sa: 1 iff d <= 0 or d < -T ln u (= u < exp(-d/T), u in (0,1)) */
+int or_sa_accept(double d, double T, double u);
 /* Simulated annealing, SPEC sa_run ("starts at a high
  * temperature and gradually cools down"), replayed on chains [chain0, chain0+nchains):
  * chain c starts at x_m = bit (m & 63) of h(seed,1,c,m>>6); sweep s = 0..sweeps-1 at

@@ -53,6 +53,8 @@ def _L():
         _lib.or_mfield.argtypes = [P, P, I64, P, I]
         _lib.or_colex_field.argtypes = [I, I, P, P, I64, P, I]
         _lib.or_sa.argtypes = [P, U64, I64, I64, I64, D, D, P, P, I]
+        _lib.or_search_trace.argtypes = [P, U64, I64, I64, I64, D, D, P, P, C.POINTER(D), C.POINTER(I64), I, P, P]
+        _lib.or_sa_accept.argtypes = [D, D, D]
         _lib.or_sa_temps.argtypes = [I64, D, D, P]
     return _lib
 
@@ -191,6 +193,21 @@ class Oracle:
             raise ValueError(f"or_search status {st}")
         return dict(e_best=e.value, best_chain=c.value, chain_ebest=eb, chain_xbest=xb)
 
+    def search_trace(self, seed, chain0, nchains, iters, p0=0.5, p1=0.005):
+        """or_search with its trajectory: adds x_trace (nchains x (iters+1) x N, the state
+        evaluated at each t) and m_trace (nchains x iters, the flipped site)."""
+        eb = np.zeros(nchains, np.float64)
+        xb = np.zeros((nchains, self.N), np.uint8)
+        xt = np.zeros((nchains, iters + 1, self.N), np.uint8)
+        mt = np.zeros((nchains, max(iters, 1)), np.int32)
+        e, c = C.c_double(), C.c_int64()
+        st = _L().or_search_trace(self._h, seed, chain0, nchains, iters, p0, p1, _ptr(eb), _ptr(xb),
+                                  C.byref(e), C.byref(c), 1, _ptr(xt), _ptr(mt))
+        if st:
+            raise ValueError(f"or_search_trace status {st}")
+        return dict(e_best=e.value, best_chain=c.value, chain_ebest=eb, chain_xbest=xb, x_trace=xt,
+                    m_trace=mt[:, :iters])
+
     def sa(self, seed, chain0, nchains, sweeps, t_start, t_end, nthreads=0):
         """SPEC sa_run replayed per chain: (final states nchains x N, tracked energies)."""
         xs = np.zeros((nchains, self.N), np.uint8)
@@ -200,6 +217,11 @@ class Oracle:
         if st:
             raise ValueError(f"or_sa status {st}")
         return xs, es
+
+
+def sa_accept(d, T, u) -> bool:
+    """The oracle's Metropolis acceptance decision (or_sa_accept)."""
+    return bool(_L().or_sa_accept(C.c_double(d), C.c_double(T), C.c_double(u)))
 
 
 def sa_temps(sweeps, t_start, t_end):

@@ -91,6 +91,22 @@ def test_energy_tensor_seating5_printed():
     assert np.all(o.energy_tensor(paper_grids()) == -17.0)
 
 
+def test_cancellation_above_the_order_is_dropped_not_an_error():
+    """O1 before O2 (reading 7): a degree-4 monomial that cancels to
+    zero is dropped before the degree check, so an order-2 build succeeds; one that survives
+    is an error."""
+    from workloads import TermBuilder
+    tb = TermBuilder()
+    tb.add(1.0, [(0.0, [(i, 1.0)]) for i in range(4)])
+    tb.add(-1.0, [(0.0, [(i, 1.0)]) for i in range(4)])
+    tb.add(2.0, [(0.0, [(0, 1.0)])])
+    o = Oracle.from_problem(tb.problem(2, 4))
+    assert o.ncells == 1 and o.cells()[1].tolist() == [2.0]
+    tb.add(1.0, [(0.0, [(i, 1.0)]) for i in range(4)])
+    with pytest.raises(Exception):
+        Oracle.from_problem(tb.problem(2, 4))
+
+
 def test_nonzero_cells(pins):
     for name, p in (("seating5x5", seating(5)), ("pythagoras", pythagoras()), ("tsp", tsp())):
         assert Oracle.from_problem(p).ncells == pins["nonzero_cells"][name]["value"], name
@@ -295,6 +311,39 @@ def test_search_oracle_finds_brute_optimum_and_is_honest():
     assert r0["e_best"] == E0.min() and r0["best_chain"] == int(np.argmin(E0))
 
 
+def test_search_rule_golden_trace():
+    """O8 against a hand-checkable trace written from the rule text (tests/golden/search_trace.json,
+    tests/golden/make_search_trace.py): every state, flipped site and per-chain best of 2 chains x 4
+    iterations.  The trace exercises each branch a plausible slip would change: the strict
+    "(r>>32) < P_t" (chain 0, t=0 sits exactly on P_0), the lowest-m tie-break (chain 1, t=3), the
+    "Delta_min >= 0 -> random" fallback (Delta_min = 0 at chain 1, t=1) and the earliest-t best on
+    an equal-energy revisit (chain 1: E=-1 at t=1 and t=4, different states)."""
+    import json
+    import os
+    from workloads import TermBuilder
+    with open(os.path.join(os.path.dirname(__file__), "golden", "search_trace.json")) as f:
+        g = json.load(f)
+    assert all(g["coverage"].values())
+    tb = TermBuilder()
+    for c, S in g["monomials"]:
+        tb.add(float(c), [(0.0, [(v, 1.0)]) for v in S])
+    o = Oracle.from_problem(tb.problem(g["order"], g["N"]))
+    X = exhaustive_X(g["N"])
+    for t, e in zip(range(16), o.energy(X)):
+        assert g["energy_table"]["".join(str((t >> m) & 1) for m in range(4))] == e
+    assert search_thresholds(g["iters"], g["p0"], g["p1"]).tolist() == g["P"]
+    r = o.search_trace(g["seed"], 0, g["nchains"], g["iters"], g["p0"], g["p1"])
+    for i, ch in enumerate(g["chains"]):
+        assert r["x_trace"][i].tolist() == [s["x"] for s in ch["steps"]], f"chain {i} states"
+        assert r["m_trace"][i].tolist() == [s["m_star"] for s in ch["steps"][:-1]], f"chain {i} moves"
+        assert r["chain_ebest"][i] == ch["E_best"] and r["chain_xbest"][i].tolist() == ch["x_best"]
+    best = min((ch["E_best"], ch["chain"]) for ch in g["chains"])
+    assert (r["e_best"], r["best_chain"]) == best
+    # the plain search returns the same per-chain results as its traced form
+    r2 = o.search(g["seed"], 0, g["nchains"], g["iters"], g["p0"], g["p1"])
+    assert np.array_equal(r2["chain_xbest"], r["chain_xbest"]) and np.array_equal(r2["chain_ebest"], r["chain_ebest"])
+
+
 # ---- the colex-array oracle entry points used at full size ----------------------------------
 def test_colex_energy_qubo_closed_form():
     """E = x^T Q x with Q_ii = c({i}), Q_ij = c({i,j}) (i<j): numpy float64 matmul."""
@@ -456,9 +505,27 @@ def test_sa_replay_by_energy_differences():
                 y[m] ^= 1
                 d = Eall[idx(y)] - Eall[idx(x)]
                 u = int(h(13, 4, c, s * o.N + m) >> np.uint64(11)) * 2.0 ** -53
-                if d <= 0 or d < -T[s] * math.log(u):      # u < exp(-d/T) for u in (0, 1)
+                if d <= 0 or u < math.exp(-d / T[s]):      # min(1, exp(-dE/T))
                     x = y
         assert list(xs[i]) == x and es[i] == Eall[idx(x)]
+
+
+def test_sa_acceptance_is_the_metropolis_probability():
+    """The oracle's acceptance decision (log form) equals SPEC's min(1, exp(-d/T)) test
+    (S:450), u < exp(-d/T), on a grid of (d, T, u) away from the decision boundary."""
+    import math
+    from oracle import sa_accept
+    rng = np.random.default_rng(5)
+    n = 0
+    for d in np.concatenate([[-3.0, -0.5, 0.0, 1e-9], rng.uniform(-5, 40, 60)]):
+        for T in (1e-3, 0.05, 0.7, 3.0, 25.0, 1e4):
+            for u in np.concatenate([[1e-300, 2.0 ** -53, 0.5, 1 - 2.0 ** -53], rng.random(20)]):
+                ref = bool(d <= 0 or u < math.exp(-d / T))
+                if d > 0 and abs(u - math.exp(-d / T)) <= 1e-12 * max(u, 1e-300):
+                    continue                      # on the boundary the two forms may round apart
+                assert sa_accept(float(d), T, float(u)) == ref, (d, T, u)
+                n += 1
+    assert n > 9000
 
 
 def test_sa_spec_examples():
