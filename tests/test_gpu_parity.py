@@ -179,33 +179,62 @@ def test_field_fp32(H, torch, order, N, B, seed):
 
 
 # ---- full-size configs, sampled -------------------------------------------------------------
-def test_cfg3_full_batch_sampled(H, torch):
-    """BASELINE config 3 at its full size (B=65536) in the bench's launch configuration;
-    every 2048th candidate is checked against the oracle, bit-exact."""
+# Rows are sampled with a stride co-prime to 128 (the candidate block = TMEM lanes): row
+# r_i = i * stride covers every TMEM lane (r mod 128) and both CTAs of a pair (r // 128 odd and
+# even), plus the last row of the batch.
+def sample_rows(B, stride, n=None):
+    assert np.gcd(stride, 128) == 1
+    rows = np.arange(0, B, stride)[:n]
+    return np.unique(np.concatenate([rows, [B - 1]]))
+
+
+def assert_lanes_covered(rows, B):
+    if B >= 4 * 128:
+        assert len(set((rows % 128).tolist())) == 128 or len(rows) < 128
+        assert {0, 1} <= set(((rows // 128) % 2).tolist())
+
+
+def test_cfg3_full_batch(H, torch):
+    """BASELINE config 3 at its full size (B=65536) in the bench's launch configuration.
+    Energies of ALL 65,536 candidates and the full-batch argmin equal the oracle's (integer
+    instance: bit-exact, lowest index on ties); fields of 256 rows spread over every TMEM lane
+    and both CTAs of each pair equal the oracle's."""
     p = cfg3_problem()
     t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
-    X = x_bits(3, 65536, 512)
+    B = 65536
+    X = x_bits(3, B, 512)
     G, E = fields(H, torch, t, X)
-    rows = np.arange(0, 65536, 2048)
+    rows = sample_rows(B, 257)
+    assert_lanes_covered(rows, B)
     assert np.array_equal(G[rows], o.field(X[rows]))
-    assert np.array_equal(E[rows], o.energy(X[rows]))
+    Eo = o.energy(X)                                   # the whole batch (~8 s on 16 cores)
+    assert np.array_equal(E, Eo)
     Ee, best = energies(H, torch, t, X)
-    assert np.array_equal(Ee, E)                       # energy mode == field-mode energies
-    assert Ee[best[1]] == best[0] == Ee.min() and best[1] == int(np.argmin(Ee))
+    assert np.array_equal(Ee, Eo)                      # energy mode == field mode == oracle
+    assert best == (Eo.min(), int(np.argmin(Eo)))      # np.argmin: the lowest index on ties
 
 
 def test_cfg2_full_batch(H, torch):
-    """BASELINE config 2: QUBO N=1024 U(-1,1), B=65536.  Closed form x^T Q x (float64 numpy)
-    on a sample, oracle on fewer rows, and the argmin."""
+    """BASELINE config 2: QUBO N=1024 U(-1,1), B=65536.  Every energy against the float64
+    closed form x^T Q x (numpy matmul over the oracle's dense Q), the full-batch argmin against
+    it (reading 11: exact when the gap exceeds 2 tau), and 256 strided rows against the oracle."""
     idx, val = uniform_cells(2, 1024, 2)
     t, o = H.HoboTensor.import_cells(2, 1024, idx, val), Oracle.from_cells(2, 1024, idx, val)
-    X = x_bits(2, 65536, 1024)
+    B = 65536
+    X = x_bits(2, B, 1024)
     E, best = energies(H, torch, t, X)
-    rows = np.arange(0, 65536, 4096)
+    Q = o.dense().astype(np.float64)
+    ref = np.empty(B)
+    for lo in range(0, B, 8192):
+        Xc = X[lo:lo + 8192].astype(np.float64)
+        ref[lo:lo + 8192] = np.einsum("bi,bi->b", Xc @ Q, Xc)
+    assert np.max(np.abs(E - ref)) <= o.tau
+    check_argmin(best, ref, o.tau)
+    rows = sample_rows(B, 257)
+    assert_lanes_covered(rows, B)
     assert np.max(np.abs(E[rows] - o.energy(X[rows]))) <= o.tau
     assert np.allclose(E[:4], [225.87784564495087, 211.0458381175995, 31.37024474143982, 149.2058583498001],
                        rtol=0, atol=o.tau)
-    assert E[best[1]] == best[0] == E.min()
 
 
 # ---- search ---------------------------------------------------------------------------------
@@ -239,10 +268,14 @@ def test_search_shard_invariance(H, torch):
 
 
 # ---- remaining BASELINE configs at full size, sampled ----------------------------------------
+# cfg3-fp32, cfg4 and cfg5 take the int8 digit-plane path (reading 24): the contraction
+# is exact integer arithmetic rounded once, so energies and fields must EQUAL the oracle's exact
+# (long double) values rounded once to fp32 -- not merely lie within tau.
 def test_cfg5_full_batch_sampled(H, torch):
     """BASELINE config 5 at one GPU's full size: order 3, N=1024, all 178,957,824 canonical
-    cells U(-1,1) (L=3), B = 2^20 candidates, energies + argmin in the energy-mode layout.
-    Sampled rows against the oracle (subset enumeration per candidate), tolerance tau."""
+    cells U(-1,1), B = 2^20 candidates, energies + argmin in the energy-mode layout (int8).
+    Strided rows (every TMEM lane, both CTAs of a pair) equal fp32(oracle); the 16 lowest
+    energies of the batch (the argmin among them) are re-evaluated by the oracle."""
     from oracle import colex_energy
     from workloads import uniform_colex
     N, B = 1024, 1 << 20
@@ -256,42 +289,56 @@ def test_cfg5_full_batch_sampled(H, torch):
         Xd[lo:lo + (1 << 17)] = torch.from_numpy(x_bits(5, 1 << 17, N, row0=lo)).cuda()
     E, best = t.energy(Xd)
     torch.cuda.synchronize()
-    rows = np.array([0, 1, 77777, 524288, B - 1])
+    assert t.launch_stats()["i8_planes"] == 3
+    Eh = E.cpu().numpy().astype(np.float64)
+    rows = sample_rows(B, 16411, 48)
+    low = np.argsort(Eh, kind="stable")[:16]
+    rows = np.unique(np.concatenate([rows, low]))
     Xs = Xd[torch.from_numpy(rows).cuda()].cpu().numpy()
     ref = colex_energy(3, N, v, Xs)
-    tau = t.tau
-    assert np.max(np.abs(E.cpu().numpy()[rows].astype(np.float64) - ref)) <= tau
-    Eh = E.cpu().numpy()
-    assert best[0] == Eh.min() and best[1] == int(np.argmin(Eh))
+    assert np.array_equal(Eh[rows], f32(ref))
+    assert best == (Eh.min(), int(np.argmin(Eh))) and best[1] == int(low[0])
 
 
 def test_cfg4_full_batch_sampled(H, torch):
-    """BASELINE config 4: order 4, N=128, all canonical cells U(-1,1) (L=3), B=262,144:
-    local fields + energies at full size, sampled rows against the oracle."""
+    """BASELINE config 4: order 4, N=128, all canonical cells U(-1,1), B=262,144 (int8):
+    local fields + energies at full size; 64 strided rows (every lane class, both CTAs) and the
+    argmin row equal fp32(oracle)."""
     from oracle import colex_energy, colex_field
     from workloads import uniform_colex
     N, B = 128, 262144
     v = uniform_colex(4, N, 4)
     t = H.HoboTensor.import_colex(4, N, v)
     X = x_bits(4, B, N)
-    G, E = fields(H, torch, t, X)
-    rows = np.array([0, 3, 131072, B - 1])
-    assert np.max(np.abs(E[rows] - colex_energy(4, N, v, X[rows]))) <= t.tau
-    assert np.max(np.abs(G[rows] - colex_field(4, N, v, X[rows]))) <= t.tau
+    Xd = dev(torch, X)
+    G, E, best = t.local_field(Xd, want_best=True)
+    torch.cuda.synchronize()
+    assert t.launch_stats()["i8_planes"] == 3
+    G, E = G.cpu().numpy().astype(np.float64), E.cpu().numpy().astype(np.float64)
+    rows = np.unique(np.concatenate([sample_rows(B, 4099, 64), [best[1]]]))
+    assert np.array_equal(E[rows], f32(colex_energy(4, N, v, X[rows])))
+    assert np.array_equal(G[rows], f32(colex_field(4, N, v, X[rows])))
+    assert best == (E.min(), int(np.argmin(E)))
 
 
 def test_cfg3_fp32_companion_sampled(H, torch):
-    """cfg3-fp32: order 3, N=512, all 22,370,048 canonical cells U(-1,1) (L=3), B=65,536."""
+    """cfg3-fp32: order 3, N=512, all 22,370,048 canonical cells U(-1,1), B=65,536 (int8):
+    256 strided rows equal fp32(oracle) in energy and field; the argmin row too."""
     from oracle import colex_energy, colex_field
     from workloads import uniform_colex
     N, B = 512, 65536
     v = uniform_colex(3, N, 3)
     t = H.HoboTensor.import_colex(3, N, v)
     X = x_bits(3, B, N)
-    G, E = fields(H, torch, t, X)
-    rows = np.array([0, 4097, B - 1])
-    assert np.max(np.abs(E[rows] - colex_energy(3, N, v, X[rows]))) <= t.tau
-    assert np.max(np.abs(G[rows] - colex_field(3, N, v, X[rows]))) <= t.tau
+    G, E, best = t.local_field(dev(torch, X), want_best=True)
+    torch.cuda.synchronize()
+    assert t.launch_stats()["i8_planes"] == 3
+    G, E = G.cpu().numpy().astype(np.float64), E.cpu().numpy().astype(np.float64)
+    rows = np.unique(np.concatenate([sample_rows(B, 257), [best[1]]]))
+    assert_lanes_covered(rows, B)
+    assert np.array_equal(E[rows], f32(colex_energy(3, N, v, X[rows])))
+    assert np.array_equal(G[rows], f32(colex_field(3, N, v, X[rows])))
+    assert best == (E.min(), int(np.argmin(E)))
 
 
 # ---- split-K (small batches) -----------------------------------------------------------------
