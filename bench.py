@@ -2,24 +2,28 @@
 """Benchmark of the HOBOTAN hot path on B200 (BASELINE.json metric).
 
 Workload (BASELINE config 3, the headline): order-3 HOBO, N = 512 binary variables =
-128 four-bit integer variables (binary integer encoding), B = 65536
-candidates per GPU.  One STEP = one pass of the hot path over one batch: stage X, the
-open-index tensor-core contraction (energies + local fields of every candidate), the
-fused reductions and the argmin (+ the all-reduce-min combine when N > 1).
+128 four-bit integer variables (binary integer encoding), B = 65,536
+candidates in total (strong scaling, the batch sharded over the GPUs; `--scaling
+weak` keeps 65,536 per GPU).  One STEP = one pass of the hot path over one batch: stage X, the
+open-index tensor-core contraction (energies + local fields of every candidate), the fused
+reductions and the argmin (+ the library's all-reduce-min combine when N > 1).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config cfg3] [--impl reference]
   (N > 1: torchrun --nproc-per-node N bench.py --gpus N ...)
+  python bench.py --cpu-plan      # SURVEY 8(d) oracle timing plan over every config (rank 0, CPU)
 
-Prints ONE JSON line on rank 0.  `value` = candidates evaluated by all ranks / max-over-
-ranks device time, inputs resident in HBM; `e2e` = the same through host buffers (H2D of
-X and D2H of E + best inside the timed region).  L2 is flushed (256 MiB write + read) before
-every timed step.
+Prints ONE JSON line on rank 0.  `value` = candidates evaluated by all ranks / max-over-ranks
+device time, inputs resident in HBM; `e2e` = the same through the host-buffer call
+(hobo_local_field_host: H2D of X, D2H of the fields G, the energies E and the best inside the
+timed region).  L2 is flushed (256 MiB write + read) before every timed step.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -31,7 +35,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "HOBO candidate evals/sec (order-3 N=512) at 1/2/4/8 B200; % tensor-core peak"
 UNIT = "candidate evals/s"
-WORKLOAD = "cfg3: order-3 HOBO, N=512 (128 x 4-bit integer vars), B=65536 per GPU, energy + local field + argmin"
 
 
 def _cfg3():
@@ -48,19 +51,34 @@ def _colex(order, N, seed):
     return make
 
 
-# name: (workload text, tensor factory, N, seed for X, batch per GPU (None = total / world), mode, scaling)
+# name: (workload text, tensor factory, order, N, seed for X, batch, mode, default scaling)
+# strong: `batch` candidates in total, sharded over the GPUs; weak: `batch` per GPU
 CONFIGS = {
-    "cfg3": (WORKLOAD, _cfg3, 512, 3, 65536, "field", "weak"),
-    "cfg3f": ("cfg3-fp32: order-3 HOBO, N=512, all 22,370,048 canonical cells U(-1,1) (L=3), B=65536 per GPU, "
-              "energy + local field + argmin", _colex(3, 512, 3), 512, 3, 65536, "field", "weak"),
-    "cfg2": ("cfg2: QUBO N=1024, all canonical cells U(-1,1) (L=3), B=65536 per GPU, energies + argmin",
-             _colex(2, 1024, 2), 1024, 2, 65536, "energy", "weak"),
-    "cfg4": ("cfg4: order-4 HOBO, N=128, all canonical cells U(-1,1) (L=3), B=262144 per GPU, "
-             "energy + local field + argmin (one search iteration's contraction)", _colex(4, 128, 4), 128, 4, 262144,
-             "field", "weak"),
-    "cfg5": ("cfg5: order-3 HOBO, N=1024, all 178,957,824 canonical cells U(-1,1) (L=3), B=2^20 sharded over the "
-             "GPUs, energies + global argmin", _colex(3, 1024, 5), 1024, 5, None, "energy", "strong"),
+    "cfg3": ("cfg3: order-3 HOBO, N=512 (128 x 4-bit integer vars), B=65536, energy + local field + argmin",
+             _cfg3, 3, 512, 3, 65536, "field", "strong"),
+    "cfg3f": ("cfg3-fp32: order-3 HOBO, N=512, all 22,370,048 canonical cells U(-1,1), B=65536, "
+              "energy + local field + argmin", _colex(3, 512, 3), 3, 512, 3, 65536, "field", "strong"),
+    "cfg2": ("cfg2: QUBO N=1024, all canonical cells U(-1,1), B=65536, energies + argmin",
+             _colex(2, 1024, 2), 2, 1024, 2, 65536, "energy", "strong"),
+    "cfg4": ("cfg4: order-4 HOBO, N=128, all canonical cells U(-1,1), B=262144, energy + local field + argmin "
+             "(one search iteration's contraction)", _colex(4, 128, 4), 4, 128, 4, 262144, "field", "strong"),
+    "cfg5": ("cfg5: order-3 HOBO, N=1024, all 178,957,824 canonical cells U(-1,1), B=2^20 sharded over the "
+             "GPUs, energies + global argmin", _colex(3, 1024, 5), 3, 1024, 5, 1 << 20, "energy", "strong"),
 }
+
+
+def nnz_dense(order, N):
+    """canonical cells of the dense instance, nnz = sum_{d=1..k} C(N, d)."""
+    return sum(math.comb(N, d) for d in range(1, order + 1))
+
+
+def algorithmic(order, N, B, mode):
+    """SURVEY 8(d) "Algorithmic work per candidate": flops 2 nnz (E) or 4 nnz (E + field);
+    bytes N/8 (X bits) + 4 (E) [+ 4N (G)] per candidate + 4 nnz (H once per batch)."""
+    nnz = nnz_dense(order, N)
+    flops = (4 if mode == "field" else 2) * nnz * B
+    byts = B * (N / 8 + 4 + (4 * N if mode == "field" else 0)) + 4 * nnz
+    return flops, byts, nnz
 
 
 def parse():
@@ -71,8 +89,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS),
                     help="BASELINE.json config (cfg3 = the headline metric; the others for context)")
-    ap.add_argument("--batch", type=int, default=0, help="override candidates per GPU")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="strong: the config's batch in total over the GPUs; weak: that batch per GPU")
+    ap.add_argument("--batch", type=int, default=0, help="override the batch (total or per GPU, see --scaling)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / search / cpu baseline (profiling runs)")
+    ap.add_argument("--cpu-plan", action="store_true", help="SURVEY 8(d) oracle timing over every config (CPU only)")
     return ap.parse_args()
 
 
@@ -167,7 +188,7 @@ def sa_extra(t, B, N, stream, sweeps=2):
         res[label] = {"t_start": ta, "t_end": tb, "ms": ms, "ms_per_site": ms / (sweeps * N),
                       "flip_attempts_per_s": B * N * sweeps / (ms / 1e3), "launches": st["launches"],
                       "executed_tflops": 2 * st["mma_macs"] / (ms / 1e3) / 1e12,
-                      "frac_of_burst": 2 * st["mma_macs"] / (ms / 1e3) / 1e12 / 1671.8,
+                      "frac_of_burst": 2 * st["mma_macs"] / (ms / 1e3) / 1e12 / measured_peaks()[0],
                       "mean_E": float(E.double().mean().item())}
     t.set_profiling(False)
     return {"chains": B, "sweeps": sweeps, "sites": N, **res}
@@ -213,59 +234,138 @@ def tt_form_extra(dev, stream, flush, B=1 << 22):
                          "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 1.965 GHz (guide: ~45 TF nominal)"}}
 
 
-def cpu_baseline(seconds=12.0):
-    """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+# SURVEY 8(d) "Oracle timing": fixed subsets per config, term-by-term, parallel over candidates
+ORACLE_SUBSET = {"cfg1": 1024, "cfg2": 4096, "cfg3": 256, "cfg3f": 256, "cfg4": 256, "cfg5": 32}
+
+
+def oracle_workload(name):
+    """(callable(X, nthreads) doing the config's oracle work on candidates X, N, x seed, full batch,
+    what it computes).  Instances are built by the oracle itself (test infrastructure)."""
     import numpy as np
-    from oracle import Oracle
-    from workloads import cfg3_problem, x_bits
-    o = Oracle.from_problem(cfg3_problem())
+    from oracle import Oracle, colex_energy, colex_field
+    if name == "cfg1":
+        from workloads import seating
+        o = Oracle.from_problem(seating(4))
+        return (lambda X, nt: int(np.argmin(o.energy(X, nthreads=nt)))), 16, 1, 1024, "energy + argmin", o
+    if name == "cfg3":
+        from workloads import cfg3_problem
+        o = Oracle.from_problem(cfg3_problem())
+        def run(X, nt):
+            o.field(X, nthreads=nt)
+            return int(np.argmin(o.energy(X, nthreads=nt)))
+        return run, 512, 3, 65536, "field + energy + argmin (term by term)", o
+    from workloads import uniform_colex
+    order, N, seed, full, mode = {"cfg2": (2, 1024, 2, 65536, "energy"), "cfg3f": (3, 512, 3, 65536, "field"),
+                                  "cfg4": (4, 128, 4, 262144, "field"), "cfg5": (3, 1024, 5, 1 << 20, "energy")}[name]
+    v = uniform_colex(order, N, seed)
+    def run(X, nt):
+        if mode == "field":
+            colex_field(order, N, v, X, nthreads=nt)
+        return int(np.argmin(colex_energy(order, N, v, X, nthreads=nt)))
+    what = ("field + " if mode == "field" else "") + "energy + argmin (subset enumeration per candidate)"
+    return run, N, seed, full, what, None
+
+
+def time_oracle(name, single_budget_s=4.0, min_s=1.5):
+    """The oracle as it stands on this host's cores: all cores on the SURVEY 8(d) subset, and one
+    thread on as much of that subset as fits `single_budget_s` (stated).  Returns a dict."""
+    from workloads import x_bits
+    run, N, seed, full, what, o = oracle_workload(name)
+    S = ORACLE_SUBSET[name]
+    X = x_bits(seed, S, N)
     cores = os.cpu_count() or 1
-    S, dt = cores * 2, 0.0
-    while S < 65536:                       # calibrate on a sample long enough to amortise start-up
-        X = x_bits(3, S, 512)
-        t0 = time.perf_counter()
-        o.field(X, nthreads=cores)
-        o.energy(X, nthreads=cores)
-        dt = time.perf_counter() - t0
-        if dt >= 1.5:
-            break
-        S = min(65536, S * 4)
-    S2 = int(min(65536, max(S, S * seconds / max(dt, 1e-3))))
-    X = x_bits(3, S2, 512)
+
+    def timed(Xs, nt):
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            run(Xs, nt)
+            reps += 1
+            dt = time.perf_counter() - t0
+            if dt >= min_s or reps >= 50:
+                return dt / reps
+    t_all = timed(X, cores)
+    # single thread: calibrate on one candidate, then as many as the budget allows
     t0 = time.perf_counter()
-    o.field(X, nthreads=cores)
-    o.energy(X, nthreads=cores)
-    dt = time.perf_counter() - t0
-    return {"value": S2 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"cfg3 first {S2} of 65536 candidates (seed 3), field + energy term by term, {dt:.1f} s"}
+    run(X[:1], 1)
+    per = max(time.perf_counter() - t0, 1e-6)
+    S1 = int(max(1, min(S, single_budget_s / per)))
+    t_one = timed(X[:S1], 1)
+    out = {"config": name, "work": what, "subset": S, "all_cores": {"threads": cores, "seconds": t_all,
+                                                                    "cand_per_s": S / t_all},
+           "single_thread": {"candidates": S1, "seconds": t_one, "cand_per_s": S1 / t_one},
+           "full_batch": full, "extrapolated_full_batch_s_all_cores": full * t_all / S}
+    if name == "cfg1":
+        t0 = time.perf_counter()
+        r = o.brute(nthreads=cores)
+        out["brute_force_2^16"] = {"seconds": time.perf_counter() - t0, "emin": r["emin"], "argmin": r["argmin"]}
+    return out
+
+
+def cpu_baseline(name):
+    """bench.py's cpu_baseline leg: the oracle timed on this config's SURVEY 8(d) subset."""
+    name = name if name in ORACLE_SUBSET else "cfg3"
+    r = time_oracle(name)
+    return {"value": r["all_cores"]["cand_per_s"], "unit": UNIT, "cores": r["all_cores"]["threads"], "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": (f"{name}: the first {r['subset']} candidates (SURVEY 8(d) subset), {r['work']}, "
+                       f"{r['all_cores']['threads']} threads, {r['all_cores']['seconds']:.3f} s per pass"),
+            "single_thread": r["single_thread"],
+            "extrapolated_full_batch_s": r["extrapolated_full_batch_s_all_cores"]}
+
+
+def run_cpu_plan():
+    plan = {"cpu_model": cpu_model(), "cores": os.cpu_count(), "configs": []}
+    for name in ("cfg1", "cfg2", "cfg3", "cfg3f", "cfg4", "cfg5"):
+        t0 = time.perf_counter()
+        r = time_oracle(name, single_budget_s=8.0)
+        r["wall_s"] = time.perf_counter() - t0
+        plan["configs"].append(r)
+        sys.stderr.write(json.dumps(r) + "\n")
+    emit(json.dumps(plan))
 
 
 def run_reference(a, world, rank):
+    """The reference arm for this tier: the oracle (plain CPU implementation of the method) as
+    it stands, on the host cores, on a bounded sample of the same workload per step."""
     if rank != 0:
         return
-    import numpy as np
-    from oracle import Oracle
-    from workloads import cfg3_problem, x_bits
-    o = Oracle.from_problem(cfg3_problem())
+    import numpy as np  # noqa: F401
+    from workloads import x_bits
+    name = a.config
+    wl_text, _, order, N, xseed, batch, mode, scaling = CONFIGS[name]
+    run, N, seed, full, what, _ = oracle_workload(name)
     cores = os.cpu_count() or 1
-    S = cores * 4          # a bounded sample per step keeps the whole run to a few minutes
-    X = x_bits(3, S, 512)
+    S = ORACLE_SUBSET.get(name, 256)
+    if name in ("cfg3f", "cfg4"):
+        S = cores * 2           # the field by subset enumeration: ~1-2 s per candidate per core
+    elif name == "cfg5":
+        S = cores
+    X = x_bits(xseed, S, N)
     times = []
     for i in range(a.warmup + a.steps):
         t0 = time.perf_counter()
-        o.field(X, nthreads=cores)
-        E = o.energy(X, nthreads=cores)
-        int(np.argmin(E))
+        run(X, cores)
         if i >= a.warmup:
             times.append(time.perf_counter() - t0)
     ms = 1e3 * statistics.mean(times)
     v = S / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample_per_step": S},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{S} cfg3 candidates per step (field + energy + argmin), {cores} threads"},
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling or scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl_text, "name": name, "sample_per_step": S},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+                             "sample": f"{S} {name} candidates per step ({what}), {cores} threads"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(json.dumps(line))
 
@@ -278,6 +378,22 @@ def emit(text):
     os.write(_JSON_FD if _JSON_FD is not None else 1, (text + "\n").encode())
 
 
+def traffic_capture(name, B):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the contraction kernel, from the
+    committed `ncu --set full` capture of this exact launch (profiles/), with its date and commit."""
+    path = os.path.join(ROOT, "profiles", "r02", f"{name}_ncu_full.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if d.get("batch") == B:
+            return d["traffic_bytes_per_launch"], (f"{os.path.relpath(path, ROOT)} (ncu --set full, "
+                                                   f"dram__bytes_read.sum + dram__bytes_write.sum; captured "
+                                                   f"{d.get('captured', '?')} at commit {d.get('commit', '?')})")
+    except (OSError, KeyError, ValueError):
+        pass
+    return None, None
+
+
 def main():
     # everything else written to fd 1 (NCCL's "NCCL version ..." banner when NCCL_DEBUG is set,
     # library or torch prints) goes to stderr, so stdout carries only the JSON line
@@ -287,6 +403,8 @@ def main():
     os.dup2(2, 1)
     a = parse()
     world, rank, local = dist_env()
+    if a.cpu_plan:
+        return run_cpu_plan() if rank == 0 else None
     if a.impl == "reference":
         return run_reference(a, world, rank)
 
@@ -294,39 +412,42 @@ def main():
     import torch
     import torch.distributed as dist
 
-    # one process per GPU; HOBO_BENCH_BACKEND=gloo (+ ranks sharing a GPU) only for host-path tests
-    backend = os.environ.get("HOBO_BENCH_BACKEND", "nccl")
+    # one process per GPU (NCCL); the library joins its own communicator for the combine
     dev_index = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
-    cdev = dev if backend == "nccl" else None     # where the combine's key tensor lives
-    # NCCL runs combine the per-rank bests inside the library (hobo_dist_init: ncclAllReduce on
-    # the compute stream); gloo runs (host-path tests) combine in Python.
-    # HOBO_BENCH_LIBCOMM=1 joins the library communicator even at world size 1.
-    lib_comm = backend == "nccl" and (world > 1 or os.environ.get("HOBO_BENCH_LIBCOMM") == "1")
-    if world > 1 or lib_comm:
-        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
-    from paper_2407_19987_b200 import HoboTensor, build
-    from paper_2407_19987_b200.dist import combine_best, init_library_comm
-    from workloads import x_bits
+    lib_comm = world > 1 or os.environ.get("HOBO_BENCH_LIBCOMM") == "1"
+    if lib_comm:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2407_19987_b200 import build
     build.build()
+    from paper_2407_19987_b200 import hobo as H
+    from paper_2407_19987_b200.dist import init_library_comm
+    from workloads import x_bits
     if lib_comm:
         init_library_comm(dev_index)
 
-    from paper_2407_19987_b200.dist import shard
-    wl_text, factory, N, xseed, per_gpu, mode, scaling = CONFIGS[a.config]
-    if per_gpu is None:                       # strong scaling: a fixed total batch
-        total = a.batch * world if a.batch else (1 << 20)
-        row0, hi = shard(total, rank, world)
-        B = hi - row0
-    else:
-        B = a.batch or per_gpu
-        row0 = rank * B
+    wl_text, factory, order, N, xseed, batch, mode, scaling = CONFIGS[a.config]
+    scaling = a.scaling or scaling
+    batch = a.batch or batch
+
+    def shard_of(bt, sc):
+        if sc == "strong":
+            lo, hi = H.shard(bt, rank, world)
+            return lo, hi - lo, bt
+        return rank * bt, bt, bt * world
+
+    row0, B, units = shard_of(batch, scaling)
     t = factory()
-    Xh = torch.empty(B, N, dtype=torch.uint8).pin_memory()
-    for lo in range(0, B, 1 << 17):
-        n = min(1 << 17, B - lo)
-        Xh[lo:lo + n] = torch.from_numpy(x_bits(xseed, n, N, row0=row0 + lo))
+    Bmax = max(B, batch if (world > 1 and a.config == "cfg3" and scaling == "strong") else 0)
+    row0w = rank * batch
+    xlo = min(row0, row0w) if Bmax > B else row0
+    xn = max(row0 + B, row0w + batch) - xlo if Bmax > B else B
+    Xall = torch.empty(xn, N, dtype=torch.uint8).pin_memory()
+    for lo in range(0, xn, 1 << 17):
+        n = min(1 << 17, xn - lo)
+        Xall[lo:lo + n] = torch.from_numpy(x_bits(xseed, n, N, row0=xlo + lo))
+    Xh = Xall[row0 - xlo: row0 - xlo + B]
     Xd = Xh.to(dev)
     G = torch.empty(B, N, dtype=torch.float32, device=dev) if mode == "field" else None
     E = torch.empty(B, dtype=torch.float32, device=dev)
@@ -338,168 +459,157 @@ def main():
         flush_rd.sum()     # 256 MiB read: the flush's dirty lines drain to HBM here, not in the timed step
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step(Xd_, G_, E_, r0):
         if mode == "field":
-            _, _, best = t.local_field(Xd, G, E, row0=row0, want_best=True)
+            _, _, best = t.local_field(Xd_, G_, E_, row0=r0, want_best=True)
         else:
-            _, best = t.energy(Xd, E, row0=row0)
-        if world > 1:
-            if not lib_comm:
-                best = combine_best(best[0], best[1], device=cdev)
+            _, best = t.energy(Xd_, E_, row0=r0)
         return best
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        m = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        return float(m.item())
+
+    def timed_steps(fn, n):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        res, kms, launches = None, [], 0
+        for i in range(n):
+            flush_l2()
+            evs[i][0].record(stream)
+            res = fn()
+            evs[i][1].record(stream)
+            st = t.launch_stats()
+            kms.append(st["kernel_ms"])
+            launches += st["launches"]
+        torch.cuda.synchronize()
+        return res, [s.elapsed_time(e) for s, e in evs], kms, launches
 
     clk = ClockSampler(local).__enter__()
     for _ in range(a.warmup):
-        step()
+        step(Xd, G, E, row0)
     torch.cuda.synchronize()
     clk.wait_first()
-
     t.set_profiling(True)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    kern_ms, launches = [], 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     c_lo = len(clk.rows)
-    if True:
-        for i in range(a.steps):
-            flush_l2()
-            ev[i][0].record(stream)
-            best = step()
-            ev[i][1].record(stream)
-            st = t.launch_stats()
-            kern_ms.append(st["kernel_ms"])
-            launches += st["launches"]
-        torch.cuda.synchronize()
+    best, step_ms, kern_ms, launches = timed_steps(lambda: step(Xd, G, E, row0), a.steps)
     time.sleep(0.06)
     clocks = clk.summary(c_lo, len(clk.rows))
-    clk.__exit__()
     if world > 1:
         dist.barrier()
     t.set_profiling(False)
-    step_ms = [s.elapsed_time(e) for s, e in ev]
     my_ms = statistics.mean(step_ms)
-    ms = my_ms
-    if world > 1:
-        m = torch.tensor([my_ms], dtype=torch.float64, device=cdev)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX)
-        ms = float(m.item())
-    units = world * B if per_gpu is not None else (a.batch * world if a.batch else (1 << 20))
+    ms = max_over_ranks(my_ms)
     value = units / (ms / 1e3)
 
-    # roofline of the dominant kernel (the open-index contraction), live CUDA events
+    # roofline of the dominant kernel (the open-index contraction), live CUDA events on the
+    # launching stream, against SURVEY 8(d)'s algorithmic work
     st = t.launch_stats()
-    algo_flops = 2.0 * st["algo_macs"]
-    exec_flops = 2.0 * st["mma_macs"]
+    i8 = st.get("i8_planes", 0)
     kms = statistics.mean(kern_ms)
+    algo_flops, algo_bytes, nnz = algorithmic(order, N, B, mode)
+    exec_flops = 2.0 * st["mma_macs"]
     burst, sustained, src = measured_peaks()
     # int8 digit planes (kind::i8): the peak for that dtype is the measured bf16 peak x the
     # nominal ratio 4.5 / 2.25 PFLOP/s = 2 (also measured: tools/mma_i8.cu, 8192 vs 4096 MAC/clk/SM)
-    i8 = st.get("i8_planes", 0)
     kind_ratio = 2.0 if i8 else 1.0
     burst, sustained = burst * kind_ratio, sustained * kind_ratio
-    # the timed region is ~0.3 s of back-to-back ~7 ms steps with clocks at max (see "clocks"):
-    # judged against the BURST figure; the sustained (power-capped) ratio is reported beside it
+    # the timed region is back-to-back steps with clocks at max (see "clocks"): judged against
+    # the BURST figure; the sustained (power-capped) ratio is reported beside it
     peak = burst
     achieved = algo_flops / (kms / 1e3) / 1e12
     hbm_peak = measured_hbm()
-    traffic, traffic_src = None, None
-    try:   # dram read+write bytes per launch of this kernel from the committed ncu --set full capture
-        if a.config == "cfg3" and B == 65536:
-            with open(os.path.join(ROOT, "profiles", "r01_cfg3_final_ncu.json")) as f:
-                traffic = json.load(f)["traffic_bytes_per_launch"]
-                traffic_src = "profiles/r01_cfg3_final_ncu.json (ncu --set full, dram__bytes_read+write)"
-    except Exception:
-        pass
-    import math
-    NTt = 128 if (N <= 128 or i8 >= 2) else 256                      # the layout's column tile
-    Npad = (N + NTt - 1) // NTt * NTt
-    Tpad = sum((math.comb(N, r - 1) + 63) // 64 * 64 for r in range(2, t.order + 1))
-    nct = Npad // NTt
-    wbytes = i8 * Npad * Tpad if i8 else t.limbs * Npad * Tpad * 2    # int8 digit planes / bf16 limb planes
-    algo_bytes = (wbytes + B * ((N + 31) // 32) * 4 + (B * N * 4 if mode == "field" else B * 4)
-                  + nct * B * 8)                                    # W once, X bits, G (or E), Q
-    # below the ridge (few candidates per W byte) the W stream from HBM binds instead
-    ridge = burst * 1e12 / (hbm_peak * 1e9)
-    hbm_bound = exec_flops / algo_bytes < ridge
-    if hbm_bound:
-        achieved_b = algo_bytes / (kms / 1e3) / 1e9
+    achieved_b = algo_bytes / (kms / 1e3) / 1e9
+    hbm_bound = algo_flops / algo_bytes < peak * 1e12 / (hbm_peak * 1e9)   # below the ridge: the H stream binds
+    traffic, traffic_src = traffic_capture(a.config, B)
+    mhz = clocks.get("sm_mhz") or 1965.0
+    hw = 2 * 4096 * 148 * mhz * 1e6 / 1e12 * kind_ratio     # the tensor cores' own rate at this clock
     roof = {"bound": "hbm" if hbm_bound else "tensor",
             "achieved": achieved_b if hbm_bound else achieved, "peak": hbm_peak if hbm_bound else peak,
             "unit": "GB/s" if hbm_bound else "TFLOP/s",
-            "frac": (achieved_b / hbm_peak) if hbm_bound else achieved / peak, "tflops_algorithmic": achieved,
-            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes_per_launch": algo_bytes, "kernel": f"kr_gemm_kernel<{NTt}{', I8' if i8 else ''}> (open-index contraction, {mode} mode)",
+            "frac": (achieved_b / hbm_peak) if hbm_bound else achieved / peak,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "definition": ("SURVEY 8(d): algorithmic flops = " + ("4" if mode == "field" else "2") +
+                           " x nnz x B with nnz = sum_{d<=k} C(N,d) canonical cells; algorithmic bytes = "
+                           "B (N/8 + 4" + (" + 4N" if mode == "field" else "") + ") + 4 nnz; divided by the "
+                           "contraction kernel's CUDA-event time"),
+            "nnz": nnz, "algorithmic_flops_per_launch": algo_flops, "algorithmic_bytes_per_launch": algo_bytes,
+            "achieved_gbs": achieved_b, "frac_of_hbm": achieved_b / hbm_peak,
+            "kernel": f"kr_gemm_kernel<{'I8' if i8 else 'bf16'}> (open-index contraction, {mode} mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms, "launches_per_step": launches / max(1, a.steps),
-            "algorithmic_flops_per_launch": algo_flops, "executed_mma_flops_per_launch": exec_flops,
-            "executed_tflops": exec_flops / (kms / 1e3) / 1e12, "frac_of_sustained": achieved / sustained,
+            "frac_of_sustained": achieved / sustained,
+            "executed_mma_flops_per_launch": exec_flops, "executed_tflops": exec_flops / (kms / 1e3) / 1e12,
+            "frac_executed_of_peak": exec_flops / (kms / 1e3) / 1e12 / peak,
+            "hw_nominal_tflops": hw, "frac_executed_of_hw_nominal": exec_flops / (kms / 1e3) / 1e12 / hw,
             "mma_kind": f"i8 ({i8} digit planes, s32 accumulate)" if i8 else f"bf16 ({t.limbs} limbs, fp32 accumulate)",
             "peak_source": (f"{src} bf16 dense (MEASURED_PEAKS.json) x 2 (nominal i8/bf16 ratio): burst {burst}, "
                             f"sustained {sustained} TOP/s" if i8 else
-                            f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s")}
-    # the tensor cores' own rate at this run's clock (4096 bf16 MAC/clk/SM, measured by
-    # tools/mma_ceiling.cu); the cuBLAS-measured burst above is taken on random operands,
-    # which toggle more than this path's {0,1} x small-integer operands, so frac can exceed 1
-    mhz = clocks.get("sm_mhz") or 1965.0
-    hw = 2 * 4096 * 148 * mhz * 1e6 / 1e12 * kind_ratio
-    roof["hw_nominal_tflops"] = hw
-    roof["frac_exec_of_hw_nominal"] = roof["executed_tflops"] / hw
+                            f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s"),
+            "hw_nominal_source": "4096 bf16 MAC/clk/SM (x2 for i8) x 148 SMs x the run's median SM clock"}
 
     extras = {}
+    if world > 1 and a.config == "cfg3" and scaling == "strong":
+        # weak scaling beside the strong headline: 65,536 candidates per GPU
+        Xw = Xall[row0w - xlo: row0w - xlo + batch].to(dev)
+        Gw = torch.empty(batch, N, dtype=torch.float32, device=dev)
+        Ew = torch.empty(batch, dtype=torch.float32, device=dev)
+        for _ in range(a.warmup):
+            step(Xw, Gw, Ew, row0w)
+        dist.barrier()
+        torch.cuda.synchronize()
+        _, wms, _, _ = timed_steps(lambda: step(Xw, Gw, Ew, row0w), a.steps)
+        wm = max_over_ranks(statistics.mean(wms))
+        extras["weak_scaling"] = {"value": world * batch / (wm / 1e3), "unit": UNIT, "batch_per_gpu": batch,
+                                  "ms_per_step": wm}
+        del Xw, Gw, Ew
     if not a.no_extras:
-        # e2e: the same metric through the host-buffer entry point (pinned X in, E + best out;
-        # hobo_local_field_host / hobo_energy_host pipeline the copies with the contraction)
+        # e2e through the host-buffer entry points: pinned X in; the fields (field mode), the
+        # energies and the best out -- the whole result of the step, copies inside the timed region
         Eh = torch.empty(B, dtype=torch.float32).pin_memory()
-        e2e_ms = []
-        for i in range(a.warmup + a.steps):
-            flush_l2()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
-            _, hb = t.local_field_host(Xh, Eh, row0=row0, stream=stream, fields=(mode == "field"))
+        Gh = torch.empty(B, N, dtype=torch.float32).pin_memory() if mode == "field" else None
+
+        def e2e(fn, n_h2d, n_d2h, api, **kw):
+            out = None
+            for _ in range(a.warmup):
+                out = fn()
+            torch.cuda.synchronize()
             if world > 1:
-                if not lib_comm:
-                    hb = combine_best(hb[0], hb[1], device=cdev)
-            e.record(stream)
-            e.synchronize()
-            if i >= a.warmup:
-                e2e_ms.append(s.elapsed_time(e))
-        assert tuple(hb) == tuple(best), (hb, best)   # same result as the device-buffer step
-        m2 = statistics.mean(e2e_ms)
-        if world > 1:
-            mm = torch.tensor([m2], dtype=torch.float64, device=cdev)
-            dist.all_reduce(mm, op=dist.ReduceOp.MAX)
-            m2 = float(mm.item())
-        extras["e2e"] = {"value": units / (m2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * N,
-                         "d2h_bytes_per_step": B * 4 + 8, "ms_per_step": m2,
-                         "api": "hobo_local_field_host" if mode == "field" else "hobo_energy_host"}
+                dist.barrier()
+            tl = []
+            for _ in range(a.steps):
+                flush_l2()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                out = fn()
+                e.record(stream)
+                e.synchronize()
+                tl.append(s.elapsed_time(e))
+            assert tuple(out[1]) == tuple(best), (out[1], best)   # same result as the device-buffer step
+            m = max_over_ranks(statistics.mean(tl))
+            return {"value": units / (m / 1e3), "unit": UNIT, "h2d_bytes_per_step": n_h2d,
+                    "d2h_bytes_per_step": n_d2h, "ms_per_step": m, "api": api, **kw}
+        fields = mode == "field"
+        api = "hobo_local_field_host" if fields else "hobo_energy_host"
+        extras["e2e"] = e2e(lambda: t.local_field_host(Xh, Eh, row0=row0, stream=stream, fields=fields, G=Gh),
+                            B * N, B * 4 + (B * N * 4 if fields else 0) + 16, api,
+                            outputs="G (fields) + E + best" if fields else "E + best")
+        if fields:
+            extras["e2e_without_fields"] = e2e(lambda: t.local_field_host(Xh, Eh, row0=row0, stream=stream),
+                                               B * N, B * 4 + 16, api, outputs="E + best (fields left on the device)")
         # the same through the packed-candidate host entry point (hobo_*_host_bits): X arrives as
         # bit rows (ceil(N/32) words per candidate), 1/8 of the bytes over PCIe
-        from paper_2407_19987_b200.hobo import pack_rows
-        Xph = torch.from_numpy(pack_rows(Xh.numpy()).view(np.int32)).pin_memory()
-        e2p_ms = []
-        for i in range(a.warmup + a.steps):
-            flush_l2()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
-            _, hb = t.local_field_host_bits(Xph, Eh, row0=row0, stream=stream, fields=(mode == "field"))
-            if world > 1:
-                if not lib_comm:
-                    hb = combine_best(hb[0], hb[1], device=cdev)
-            e.record(stream)
-            e.synchronize()
-            if i >= a.warmup:
-                e2p_ms.append(s.elapsed_time(e))
-        assert tuple(hb) == tuple(best), (hb, best)
-        m3 = statistics.mean(e2p_ms)
-        if world > 1:
-            mm = torch.tensor([m3], dtype=torch.float64, device=cdev)
-            dist.all_reduce(mm, op=dist.ReduceOp.MAX)
-            m3 = float(mm.item())
-        extras["e2e_packed"] = {"value": units / (m3 / 1e3), "unit": UNIT,
-                                "h2d_bytes_per_step": int(Xph.numel()) * 4, "d2h_bytes_per_step": B * 4 + 8,
-                                "ms_per_step": m3,
-                                "api": "hobo_local_field_host_bits" if mode == "field" else "hobo_energy_host_bits",
-                                "input": "bit-packed candidate rows (packed on the host before the timed region)"}
-        if mode == "field":
+        Xph = torch.from_numpy(H.pack_rows(Xh.numpy()).view(np.int32)).pin_memory()
+        extras["e2e_packed"] = e2e(lambda: t.local_field_host_bits(Xph, Eh, row0=row0, stream=stream, fields=fields,
+                                                                   G=Gh),
+                                   int(Xph.numel()) * 4, B * 4 + (B * N * 4 if fields else 0) + 16, api + "_bits",
+                                   input="bit-packed candidate rows (packed on the host before the timed region)",
+                                   outputs="G + E + best" if fields else "E + best")
+        if mode == "field" and world == 1:
             # the search loop (16 iterations of field + move over B chains), context only
             t.search(3, B, 1)                     # warm the search scratch buffers
             torch.cuda.synchronize()
@@ -510,7 +620,8 @@ def main():
             e.synchronize()
             sm = s.elapsed_time(e)
             extras["search_loop"] = {"chains_per_gpu": B, "iters": 16, "ms": sm,
-                                     "chain_evals_per_s": B * 17 / (sm / 1e3), "e_best": es}
+                                     "chain_evals_per_s": B * 17 / (sm / 1e3), "e_best": es,
+                                     "launches": t.launch_stats()["launches"]}
             # the paper's result list: the same search + on-device dedupe / occurrence counts
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -518,7 +629,7 @@ def main():
             sa_ms = (time.perf_counter() - t0) * 1e3
             extras["search_samples"] = {"ms_wall": sa_ms, "aggregation_ms_wall": sa_ms - sm,
                                         "top": [[e, c] for _, e, c in samples[:3]]}
-        if mode == "field" and N <= 512 and t.limbs == 1:
+        if mode == "field" and N <= 512 and t.limbs == 1 and world == 1:
             # gradient descent's hot path: the same contraction at real p (bf16, A in 2 limbs)
             from workloads import h as _h
             u = ((_h(3, 3, np.arange(B, dtype=np.uint64)[:, None], np.arange(N, dtype=np.uint64)[None, :])
@@ -536,28 +647,29 @@ def main():
             t.set_profiling(False)
             kmm = statistics.mean(km)
             extras["multilinear_field"] = {"kernel_ms": kmm, "cand_per_s": B / (kmm / 1e3),
-                                           "algo_tflops": 2 * st2["algo_macs"] / (kmm / 1e3) / 1e12,
+                                           "algo_tflops": algorithmic(order, N, B, "field")[0] / (kmm / 1e3) / 1e12,
                                            "exec_tflops": 2 * st2["mma_macs"] / (kmm / 1e3) / 1e12}
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res = t.gd_run(3, B, 20, 0.05, greedy_iters=32, topk=3)
             extras["gd_run"] = {"shots": B, "steps": 20, "greedy_iters": 32, "ms_wall": (time.perf_counter() - t0) * 1e3,
                                 "top": [[e, c] for _, e, c in res]}
-        if mode == "field":
+        if mode == "field" and world == 1:
             extras["sa_sweep"] = sa_extra(t, B, N, stream)
-        if rank == 0 and a.config == "cfg3":
+        if rank == 0 and a.config == "cfg3" and world == 1:
             extras["tt_form"] = tt_form_extra(dev, stream, flush_l2)
-            if world == 1:                    # the oracle baseline: rank 0 at N = 1 only
-                extras["cpu_baseline"] = cpu_baseline()
+        if rank == 0 and world == 1:                 # the oracle baseline: rank 0 at N = 1 only
+            extras["cpu_baseline"] = cpu_baseline(a.config)
+    clk.__exit__()
     if world > 1:
         dist.barrier()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "i8" if i8 else "bf16", "data": "synthetic",
-                "config": {"workload": wl_text, "name": a.config, "order": t.order, "N": N, "batch_per_gpu": B,
-                           "limbs": t.limbs, "global_batch": units,
-                           "parallelism": f"dp{world} (H replicated, batch sharded)",
+                "config": {"workload": wl_text, "name": a.config, "order": order, "N": N,
+                           "global_batch": units, "batch_per_gpu": B, "limbs": t.limbs,
+                           "parallelism": f"dp{world} (H replicated, batch sharded{' by hobo_shard' if scaling == 'strong' else ''})",
                            "l2": "flushed before every timed step (256 MiB write, then a 256 MiB read so the write-backs finish outside the timed region)",
                            "inputs": f"x_bits(seed={xseed}) and the {a.config} instance (workloads/gen.py)",
                            "best": list(best)},
@@ -567,9 +679,7 @@ def main():
             line["e2e"] = None
         emit(json.dumps(line))
     if lib_comm:
-        from paper_2407_19987_b200 import hobo as _hobo
-        _hobo.dist_finalize()
-    if world > 1 or lib_comm:
+        H.dist_finalize()
         dist.destroy_process_group()
 
 

@@ -20,7 +20,7 @@
  *   - Kernel choice is automatic; environment variables override it for A/B
  *     measurements and tests (read when the handle first uses the choice):
  *       HOBO_PAIR=1|0        CTA-pair (cta_group::2) contraction on / off
- *       HOBO_SA_KERNEL=ring|stage|ts|pair   the persistent annealing kernel
+ *       HOBO_SA_KERNEL=ring|stage|pair   the persistent annealing kernel
  *       HOBO_I8=1|0          int8 digit planes (kind::i8) whenever exact / never
  *       HOBO_CT_DESC=1|0     column tiles longest-first (default when the last tile is the
  *                            heaviest) / in index order
@@ -135,13 +135,16 @@ hobo_status hobo_local_field(hobo_tensor* t, const uint8_t* X_dev, int64_t B, in
                              float* G_dev, float* E_dev, hobo_best* best, void* stream);
 
 /* hobo_local_field_host — hobo_local_field for candidates in HOST memory, end to end:
- * X_host [B*N] u8 (page-locked memory lets the copies overlap), E_host [B] f32 (nullable)
- * and best (nullable) are host outputs; the fields are computed on the device (scratch,
- * not returned).  The batch runs in chunks of whole waves; chunk i+1's host->device copy
- * (on an internal copy stream ordered after the caller's stream) overlaps chunk i's
- * contraction.  Results equal hobo_local_field's.  Synchronises the stream.             */
+ * X_host [B*N] u8 in; host outputs (each nullable): G_host [B*N] f32 the local fields,
+ * E_host [B] f32 the energies, best the argmin.  Page-locked X_host / G_host let the copies
+ * overlap the contraction: the batch runs in chunks of whole waves, chunk i+1's host->device
+ * copy (an internal copy stream ordered after the caller's stream) overlaps chunk i's
+ * contraction, and chunk i's fields go back to the host (a second internal stream) while
+ * chunk i+1 is contracted.  With G_host NULL the fields stay in device scratch.  E_host is
+ * written by one copy after the last chunk.  Results equal hobo_local_field's.  Synchronises
+ * the stream.                                                                              */
 hobo_status hobo_local_field_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0,
-                                  float* E_host, hobo_best* best, void* stream);
+                                  float* G_host, float* E_host, hobo_best* best, void* stream);
 /* hobo_energy_host — hobo_energy for candidates in host memory, the same pipeline (energy
  * layout; no fields).  Results equal hobo_energy's.  Synchronises the stream.            */
 hobo_status hobo_energy_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0,
@@ -163,7 +166,7 @@ hobo_status hobo_local_field_bits(hobo_tensor* t, const uint32_t* Xbits_dev, int
 hobo_status hobo_energy_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0,
                                   float* E_host, hobo_best* best, void* stream);
 hobo_status hobo_local_field_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0,
-                                       float* E_host, hobo_best* best, void* stream);
+                                       float* G_host, float* E_host, hobo_best* best, void* stream);
 
 /* hobo_multilinear_field — the same contraction on REAL candidates p in [0,1]^N, the
  * multilinear relaxation used by gradient descent ("the gradient is computed based
@@ -272,6 +275,24 @@ hobo_status hobo_dist_unique_id(void* id_out);
 hobo_status hobo_dist_init(int rank, int world, const void* id, int device);
 hobo_status hobo_dist_finalize(void);
 hobo_status hobo_dist_info(int* rank, int* world);
+
+/* ---- multi-GPU host logic (SURVEY 8(e) partition and C1 key).  Plain host
+ * arithmetic: no device, no communicator (callable on a machine without a GPU).  The library's
+ * own hobo_search and every best-combining call use exactly these functions.
+ * hobo_shard: rank `rank` of `world` owns items [*lo, *lo + *n) of `total` (>= 0), with
+ *   lo = rank*(total/world) + min(rank, total % world): contiguous, the first ranks take the
+ *   remainder, *n may be 0 when total < world.  EINVAL for world < 1 or rank outside [0, world).
+ * hobo_shard_owner: *owner = the rank whose shard holds `index`; EINVAL outside [0, total).
+ * hobo_best_key: the 64-bit argmin key of (e, idx):
+ *   key = (ord(e) << 32) | idx, ord(e) = the fp32 bits of e made monotone (i = bits(e); if i < 0
+ *   then i ^= 0x7FFFFFFF; -0 is +0) with the sign bit flipped, so that the UNSIGNED minimum of
+ *   keys is the lexicographic minimum of (e, idx) -- the ncclUint64 MIN of C1.  EINVAL for a NaN
+ *   e or idx outside [0, 2^32).
+ * hobo_best_from_key: its inverse into a hobo_best; key = ~0 (no candidate) gives (+inf, -1).   */
+hobo_status hobo_shard(int64_t total, int rank, int world, int64_t* lo, int64_t* n);
+hobo_status hobo_shard_owner(int64_t total, int world, int64_t index, int* owner);
+hobo_status hobo_best_key(float e, int64_t idx, uint64_t* key);
+hobo_status hobo_best_from_key(uint64_t key, hobo_best* best);
 
 /* Launch statistics of the last call on this handle: number of kernel launches issued,
  * the executed tensor-core MACs of its contraction kernel(s), the algorithmic MACs

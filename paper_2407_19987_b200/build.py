@@ -1,6 +1,14 @@
-"""Compile the CUDA library in-tree: paper_2407_19987_b200/_lib/libhobo.so (sm_100a only)."""
+"""Compile the CUDA library in-tree: paper_2407_19987_b200/_lib/libhobo.so (sm_100a only).
+
+The library is rebuilt whenever the SHA-256 of its sources (every file under csrc/ and
+include/), the compiler flags or the nvcc version differ from those recorded next to it
+(_lib/libhobo.so.sha256): a stale prebuilt library is never reused, whatever the file
+times say.
+"""
 from __future__ import annotations
 
+import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -10,9 +18,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libhobo.so")
+STAMP = LIB + ".sha256"
 SOURCES = [os.path.join(CSRC, f) for f in ("hobo_api.cu", "host_compile.cpp", "tt.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "ptx.cuh", "host_compile.h", "tt.h")] + [
-    os.path.join(ROOT, "include", "hobo.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -22,29 +29,47 @@ FLAGS = [
 ]
 
 
+def deps():
+    return sorted(glob.glob(os.path.join(CSRC, "*")) + glob.glob(os.path.join(ROOT, "include", "*.h")))
+
+
+def source_hash() -> str:
+    h = hashlib.sha256()
+    for p in deps():
+        h.update(os.path.relpath(p, ROOT).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(FLAGS).encode())
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
+    except OSError:
+        pass
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    with open(STAMP) as f:
+        return f.read().strip() != source_hash()
 
 
-def build(force: bool = False, verbose: bool = False, debug_stats: bool = False) -> str:
-    """debug_stats=True builds _lib/libhobo_dbg.so with per-CTA pipeline counters (tools only)."""
-    lib = LIB.replace("libhobo.so", "libhobo_dbg.so") if debug_stats else LIB
-    if not force and not debug_stats and not stale():
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *FLAGS, *(["-DHOBO_PIPE_STATS"] if debug_stats else []), *(["-Xptxas", "-v"] if verbose else []),
-           "-o", lib, *SOURCES]
+    digest = source_hash()
+    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", LIB, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libhobo.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    return lib
+    with open(STAMP, "w") as f:
+        f.write(digest + "\n")
+    return LIB
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug_stats="--debug-stats" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

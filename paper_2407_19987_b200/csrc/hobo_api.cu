@@ -121,8 +121,10 @@ struct hobo_tensor {
   uint8_t* d_xh[2] = {nullptr, nullptr}; size_t xh_cap = 0;   // host-input path: staged X chunks
   uint32_t* d_xbc = nullptr; size_t xbc_cap = 0;        // multi-GPU search: the winner's bits
   float* d_Eh = nullptr; size_t Eh_cap = 0;
-  cudaStream_t cs = nullptr;                            // its copy stream
+  cudaStream_t cs = nullptr;                            // its input copy stream
+  cudaStream_t cs_out = nullptr;                        // its field copy-out stream
   cudaEvent_t ev_in = nullptr, ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_gdone[2] = {nullptr, nullptr}, ev_gfree[2] = {nullptr, nullptr};
   std::vector<hobo_tensor*> sa_child;                   // annealing: P_m = dE/dx_m per site m
   bool sa_borrowed = false;                             // a site tensor: its tables belong to the parent
   uint4* d_sa_runs = nullptr;                           // the site tensors' shared tables (same order, N)
@@ -172,6 +174,20 @@ hobo_status grow(hobo_tensor* t, T*& p, size_t& cap, size_t n) {
   return HOBO_OK;
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute of a kernel: set it
+// once per (kernel, device), for the largest size requested so far
+template <class K>
+cudaError_t set_smem(K* k, size_t smem) {
+  static size_t configured[64] = {0};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (configured[dev] >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) configured[dev] = smem;
+  return e;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -192,12 +208,7 @@ template <int NT, bool REAL, bool I8 = false>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, false, I8>;
   const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
-  static size_t configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = set_smem(k, smem)) return e;
   const int mb = (REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
   k<<<dim3((unsigned)(p.n_split * p.n_ct * ((p.n_cb + mb - 1) / mb))), dim3(kThreads), smem, s>>>(L.tmap, p);
   return cudaGetLastError();
@@ -207,12 +218,7 @@ template <int NT>
 cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, false, true>;
   const size_t smem = KrCfg<NT>::smem_bytes(p.W);
-  static size_t configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = set_smem(k, smem)) return e;
   k<<<dim3((unsigned)(p.n_ct * p.n_cb)), dim3(kThreads), smem, s>>>(L.tmap, p);
   return cudaGetLastError();
 }
@@ -222,12 +228,7 @@ template <int NT, bool REAL, bool I8 = false>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, true, I8>;
   const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
-  static size_t configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
   cfg.blockDim = dim3(kThreads);
@@ -358,7 +359,7 @@ hobo_status init_device(hobo_tensor* t) {
   for (int m = 0; m < N; ++m) p1[m] = t->host.strict[1][m];
   CK(cudaMalloc(&t->d_p1, Npad * sizeof(float)));
   CK(cudaMemcpy(t->d_p1, p1.data(), Npad * sizeof(float), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&t->d_key, sizeof(unsigned long long)));
+  CK(cudaMalloc(&t->d_key, 2 * sizeof(unsigned long long)));   // [0] argmin key, [1] ~0 unless a NaN was seen
   t->dev_init = true;
   return HOBO_OK;
 }
@@ -533,10 +534,6 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.field_mode = (&L == &t->lay[0]) ? 0 : 1;
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
-  p.dbg = 0;
-#ifdef HOBO_PIPE_STATS
-  if (const char* e = getenv("HOBO_DBG")) p.dbg = atoi(e);
-#endif
   return p;
 }
 
@@ -572,34 +569,19 @@ double algo_macs(hobo_tensor* t, bool field, long long B) {
 // C1: the global lexicographic (E, idx) minimum over ranks, on the compute stream
 hobo_status key_allreduce(hobo_tensor* t, cudaStream_t s) {
   if (!dist_active()) return HOBO_OK;
-  ncclResult_t r = g_dist.all_reduce(t->d_key, t->d_key, 1, ncclUint64, ncclMin, g_dist.comm, s);
+  ncclResult_t r = g_dist.all_reduce(t->d_key, t->d_key, 2, ncclUint64, ncclMin, g_dist.comm, s);
   if (r != ncclSuccess) return fail(HOBO_ENCCL, std::string("ncclAllReduce: ") + g_dist.err(r));
   return HOBO_OK;
-}
-
-float key_energy(unsigned long long key) {
-  uint32_t u = (uint32_t)(key >> 32) ^ 0x80000000u;
-  int32_t i = (int32_t)u;
-  if (i < 0) i ^= 0x7FFFFFFF;
-  float f;
-  std::memcpy(&f, &i, 4);
-  return f;
 }
 
 // the argmin key (device) -> host best, after the multi-GPU combine when one is active
 hobo_status finish_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
   if (hobo_status st = key_allreduce(t, s)) return st;
-  unsigned long long key = 0;
-  CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+  unsigned long long key[2] = {0, 0};
+  CK(cudaMemcpyAsync(key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (key == ~0ull) {
-    best->e = INFINITY;
-    best->idx = -1;
-  } else {
-    best->idx = (int64_t)(key & 0xFFFFFFFFull);
-    best->e = key_energy(key);
-  }
-  return HOBO_OK;
+  if (key[1] != ~0ull) return fail(HOBO_ERANGE, "a candidate's energy is NaN (the argmin rejects NaN)");
+  return hobo_best_from_key(key[0], best);
 }
 
 // an empty local batch still takes part in the combine (the other ranks wait for it)
@@ -610,7 +592,7 @@ hobo_status empty_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
     best->idx = -1;
     return HOBO_OK;
   }
-  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
   return finish_best(t, best, s);
 }
 
@@ -778,8 +760,14 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   for (hobo_tensor* c : t->sa_child) hobo_tensor_free(c);
   if (t->cs) {
     cudaStreamDestroy(t->cs);
+    cudaStreamDestroy(t->cs_out);
     cudaEventDestroy(t->ev_in);
-    for (int i = 0; i < 2; ++i) { cudaEventDestroy(t->ev_copied[i]); cudaEventDestroy(t->ev_free[i]); }
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(t->ev_copied[i]);
+      cudaEventDestroy(t->ev_free[i]);
+      cudaEventDestroy(t->ev_gdone[i]);
+      cudaEventDestroy(t->ev_gfree[i]);
+    }
   }
   for (int i = 0; i < 2; ++i)
     if (t->d_xh[i]) cudaFree(t->d_xh[i]);
@@ -840,7 +828,7 @@ hobo_status energy_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B
   if (B == 0) return empty_best(t, best, s);
   if (hobo_status st = contract(t, 0, X, B, nullptr, s, nullptr, packed)) return st;
   const DevLayout& L = t->lay[0];
-  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
   finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
       t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
   CK(cudaGetLastError());
@@ -861,7 +849,7 @@ hobo_status field_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B,
   if (hobo_status st = contract(t, 1, X, B, G, s, nullptr, packed)) return st;
   if (E || best) {
     const DevLayout& L = t->lay[1];
-    if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+    if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
     finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
         t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
     CK(cudaGetLastError());
@@ -898,9 +886,9 @@ hobo_status hobo_local_field_bits(hobo_tensor* t, const uint32_t* Xbits, int64_t
 }  // extern "C"
 
 namespace {
-// host-input path of hobo_energy_host / hobo_local_field_host (whole-wave chunks, copy stream)
-hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
-                     hobo_best* best, void* stream, bool packed = false) {
+// host-input path of hobo_energy_host / hobo_local_field_host (whole-wave chunks, copy streams)
+hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B, int64_t row0, float* G_host,
+                     float* E_host, hobo_best* best, void* stream, bool packed = false) {
   if (!t) return fail(HOBO_EINVAL, "null handle");
   if (B < 0 || (B > 0 && !X_host) || row0 < 0 || row0 + B > (int64_t)0xFFFFFFFF)
     return fail(HOBO_EINVAL, "bad batch (B >= 0, X non-null, row0 + B < 2^32)");
@@ -910,22 +898,39 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   if (hobo_status st = ensure_layout(t, field)) return st;
   const DevLayout& L = t->lay[field];
   const int N = t->host.N;
+  const bool gout = field && G_host;
   const size_t row_bytes = packed ? (size_t)t->W * 4 : (size_t)N;   // one candidate's input bytes
   // chunks of whole waves of (candidate block x column tile) CTAs (CTA pairs take candidate
-  // blocks two by two): a one-wave first chunk (its copy is the exposed one), then chunks
-  // growing 6x, each copy (PCIe, ~10-20 ns per candidate) hidden behind the previous chunk's
-  // contraction (>= 60 ns per candidate); few launches keep their fill and drain small
+  // blocks two by two).  Inputs only: a one-wave first chunk (its copy is the exposed one),
+  // then chunks growing 6x, each copy (PCIe, ~10-20 ns per candidate) hidden behind the
+  // previous chunk's contraction (>= 60 ns per candidate).  With the fields coming back
+  // (4N bytes per candidate, about as long as the contraction at N = 512), chunk i's
+  // device->host copy overlaps chunk i+1's contraction, so the chunks stay two waves long and
+  // the last one is a single wave (its copy is the exposed one at the end).
   const long long per_wave = std::max<long long>(2, 148 / L.n_ct / 2 * 2) * kBM;
   std::vector<long long> sizes;
-  for (long long off = 0, n = per_wave; off < B; off += sizes.back(), n *= 6)
-    sizes.push_back(std::min(n, B - off));
+  if (!gout) {
+    for (long long off = 0, n = per_wave; off < B; off += sizes.back(), n *= 6) sizes.push_back(std::min(n, B - off));
+  } else {
+    sizes.push_back(std::min<long long>(per_wave, B));
+    for (long long off = sizes[0]; off < B;) {
+      const long long left = B - off;
+      if (left <= per_wave) { sizes.push_back(left); break; }
+      if (left <= 3 * per_wave) { sizes.push_back(left - per_wave); sizes.push_back(per_wave); break; }
+      sizes.push_back(2 * per_wave);
+      off += 2 * per_wave;
+    }
+  }
   const long long chunk = *std::max_element(sizes.begin(), sizes.end());
   if (!t->cs) {
     CK(cudaStreamCreateWithFlags(&t->cs, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&t->cs_out, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
       CK(cudaEventCreateWithFlags(&t->ev_copied[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&t->ev_free[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&t->ev_gdone[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&t->ev_gfree[i], cudaEventDisableTiming));
     }
   }
   if ((size_t)chunk * row_bytes > t->xh_cap) {
@@ -938,11 +943,14 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
     t->xh_cap = (size_t)chunk * row_bytes;
   }
   if (hobo_status st = grow(t, t->d_Eh, t->Eh_cap, (size_t)B)) return st;
+  // field chunks: two buffers when they go back to the host (chunk i's copy-out runs while
+  // chunk i+1 is computed into the other one), else one scratch buffer
   if (field)
-    if (hobo_status st = grow(t, t->d_G, t->G_cap, (size_t)chunk * N)) return st;
-  if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+    if (hobo_status st = grow(t, t->d_G, t->G_cap, (size_t)chunk * N * (gout ? 2 : 1))) return st;
+  if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
   CK(cudaEventRecord(t->ev_in, s));             // the copies follow the caller's prior work
   CK(cudaStreamWaitEvent(t->cs, t->ev_in, 0));
+  if (gout) CK(cudaStreamWaitEvent(t->cs_out, t->ev_in, 0));
   int64_t launches = 0;
   for (long long off = 0, i = 0, n = 0; off < B; off += n, ++i) {
     n = sizes[(size_t)i];
@@ -952,13 +960,27 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
                        t->cs));
     CK(cudaEventRecord(t->ev_copied[slot], t->cs));
     CK(cudaStreamWaitEvent(s, t->ev_copied[slot], 0));
-    if (hobo_status st = contract(t, field, t->d_xh[slot], n, field ? t->d_G : nullptr, s, nullptr, packed)) return st;
+    float* Gc = field ? t->d_G + (gout ? (size_t)slot * chunk * N : 0) : nullptr;
+    if (gout && i >= 2) CK(cudaStreamWaitEvent(s, t->ev_gfree[slot], 0));   // chunk i-2's fields are on the host
+    if (hobo_status st = contract(t, field, t->d_xh[slot], n, Gc, s, nullptr, packed)) return st;
     CK(cudaEventRecord(t->ev_free[slot], s));
     finalize_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, s>>>(
         t->d_Q, L.n_ct, n, L.lcm, row0 + off, t->d_Eh + off, best ? t->d_key : nullptr);
     CK(cudaGetLastError());
     launches += t->last_launches + 1;
-    if (E_host) CK(cudaMemcpyAsync(E_host + off, t->d_Eh + off, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, s));
+    if (gout) {
+      CK(cudaEventRecord(t->ev_gdone[slot], s));
+      CK(cudaStreamWaitEvent(t->cs_out, t->ev_gdone[slot], 0));
+      CK(cudaMemcpyAsync(G_host + (size_t)off * N, Gc, (size_t)n * N * sizeof(float), cudaMemcpyDeviceToHost, t->cs_out));
+      CK(cudaEventRecord(t->ev_gfree[slot], t->cs_out));
+    }
+  }
+  // energies: one copy of the whole batch at the end (a pageable E_host would otherwise make
+  // every chunk's copy synchronous and stall the next chunk's input copy)
+  if (E_host) CK(cudaMemcpyAsync(E_host, t->d_Eh, (size_t)B * sizeof(float), cudaMemcpyDeviceToHost, s));
+  if (gout) {   // the caller's stream is ordered after the last field copy
+    CK(cudaEventRecord(t->ev_gfree[0], t->cs_out));
+    CK(cudaStreamWaitEvent(s, t->ev_gfree[0], 0));
   }
   if (best) {
     if (hobo_status st = finish_best(t, best, s)) return st;
@@ -978,22 +1000,22 @@ extern "C" {
 
 hobo_status hobo_energy_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
                              hobo_best* best, void* stream) {
-  return run_host(t, 0, X_host, B, row0, E_host, best, stream);
+  return run_host(t, 0, X_host, B, row0, nullptr, E_host, best, stream);
 }
 
-hobo_status hobo_local_field_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0, float* E_host,
-                                  hobo_best* best, void* stream) {
-  return run_host(t, 1, X_host, B, row0, E_host, best, stream);
+hobo_status hobo_local_field_host(hobo_tensor* t, const uint8_t* X_host, int64_t B, int64_t row0, float* G_host,
+                                  float* E_host, hobo_best* best, void* stream) {
+  return run_host(t, 1, X_host, B, row0, G_host, E_host, best, stream);
 }
 
 hobo_status hobo_energy_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0, float* E_host,
                                   hobo_best* best, void* stream) {
-  return run_host(t, 0, reinterpret_cast<const uint8_t*>(Xbits_host), B, row0, E_host, best, stream, true);
+  return run_host(t, 0, reinterpret_cast<const uint8_t*>(Xbits_host), B, row0, nullptr, E_host, best, stream, true);
 }
 
 hobo_status hobo_local_field_host_bits(hobo_tensor* t, const uint32_t* Xbits_host, int64_t B, int64_t row0,
-                                       float* E_host, hobo_best* best, void* stream) {
-  return run_host(t, 1, reinterpret_cast<const uint8_t*>(Xbits_host), B, row0, E_host, best, stream, true);
+                                       float* G_host, float* E_host, hobo_best* best, void* stream) {
+  return run_host(t, 1, reinterpret_cast<const uint8_t*>(Xbits_host), B, row0, G_host, E_host, best, stream, true);
 }
 
 }  // extern "C"
@@ -1072,21 +1094,24 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
   if (hobo_status st = run_search(t, seed, chain0, nchains, iters, p0, p1, s, launches)) return st;
   const int N = t->host.N, W = t->W;
   const long long B = nchains;
-  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
   search_best_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_ebest, B, chain0,
                                                                                              t->d_key);
   CK(cudaGetLastError());
   ++launches;
-  unsigned long long key = 0;
-  CK(cudaMemcpyAsync(&key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+  unsigned long long key[2] = {0, 0};
+  CK(cudaMemcpyAsync(key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  const int64_t c = (int64_t)(key & 0xFFFFFFFFull);
+  if (key[1] != ~0ull) return fail(HOBO_ERANGE, "a chain's energy is NaN (the argmin rejects NaN)");
+  hobo_best b;
+  hobo_best_from_key(key[0], &b);
+  const int64_t c = b.idx;
   std::vector<uint32_t> xb(W);
   CK(cudaMemcpyAsync(xb.data(), t->d_xbest + (size_t)(c - chain0) * W, W * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (x_best_host)
     for (int m = 0; m < N; ++m) x_best_host[m] = (uint8_t)((xb[m >> 5] >> (m & 31)) & 1u);
-  if (e_best_host) *e_best_host = key_energy(key);
+  if (e_best_host) *e_best_host = b.e;
   if (best_chain) *best_chain = c;
   t->last_launches = launches;
   return HOBO_OK;
@@ -1388,27 +1413,17 @@ template <int NT>
 cudaError_t launch_sa(const CUtensorMap& tmap, const SaParams& p, unsigned grid, cudaStream_t s) {
   auto* k = sa_kernel<NT>;
   const size_t smem = SaCfg<NT>::smem_bytes(p.W);
-  static size_t configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = set_smem(k, smem)) return e;
   k<<<grid, kThreads, smem, s>>>(tmap, p);
   return cudaGetLastError();
 }
 
-template <int NT, bool TS>
+template <int NT>
 cudaError_t launch_sa_stage(const CUtensorMap& tmap, const SaParams& p, int SB, unsigned grid, cudaStream_t s) {
-  auto* k = sa_stage_kernel<NT, TS>;
-  const size_t smem = SaStCfg<NT, TS>::smem_bytes(SB, p.W);
-  static size_t configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  k<<<grid, kThreads, smem, s>>>(tmap, p, SB, SaStCfg<NT, TS>::nst(SB));
+  auto* k = sa_stage_kernel<NT>;
+  const size_t smem = SaStCfg<NT>::smem_bytes(SB, p.W);
+  if (cudaError_t e = set_smem(k, smem)) return e;
+  k<<<grid, kThreads, smem, s>>>(tmap, p, SB, SaStCfg<NT>::nst(SB));
   return cudaGetLastError();
 }
 
@@ -1416,12 +1431,7 @@ template <int NT>
 cudaError_t launch_sa2(const CUtensorMap& tmap, const SaParams& p, unsigned grid, cudaStream_t s) {
   auto* k = sa2_kernel<NT>;
   const size_t smem = Sa2Cfg<NT>::smem_bytes(p.W);
-  static size_t configured = 0;
-  if (configured < smem) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1500,20 +1510,16 @@ hobo_status run_sa(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nchain
     if (t->profile) CK(cudaEventRecord(t->ev0, s));
     const unsigned grid = (unsigned)std::min<long long>(n_cb, 148);
     // one column tile (Npad <= 256): the staged kernel (one barrier pair per K-block); two
-    // tiles: CTA pairs sharing every W box (the box ring is the single-block fallback).  The
-    // A-in-TMEM staged variant ('t') is an A/B option: measured 4% slower than smem A at cfg4.
+    // tiles: CTA pairs sharing every W box (the box ring is the single-block fallback).
     int Lmax = 1;
     for (int l : t->sa_L) Lmax = std::max(Lmax, l);
     const int SB = Lmax * t->sa_nct;
     char kind = t->sa_nct == 1 ? 's' : 'p';   // two 256-column tiles: CTA pairs (cfg3 15.3 -> 13.3 ms)
-    if ((t->sa_NT == 128 ? SaStCfg<128, false>::nst(SB) : SaStCfg<256, false>::nst(SB)) < 2) kind = 'r';
-    if (const char* e = getenv("HOBO_SA_KERNEL")) kind = e[0];   // A/B measurement switch: ring|stage|ts|pair
-    if (kind == 't' && t->sa_nct == 1)
-      CK((t->sa_NT == 128 ? launch_sa_stage<128, true>(t->sa_tmap, q, SB, grid, s)
-                          : launch_sa_stage<256, true>(t->sa_tmap, q, SB, grid, s)));
-    else if (kind == 's')
-      CK((t->sa_NT == 128 ? launch_sa_stage<128, false>(t->sa_tmap, q, SB, grid, s)
-                          : launch_sa_stage<256, false>(t->sa_tmap, q, SB, grid, s)));
+    if ((t->sa_NT == 128 ? SaStCfg<128>::nst(SB) : SaStCfg<256>::nst(SB)) < 2) kind = 'r';
+    if (const char* e = getenv("HOBO_SA_KERNEL")) kind = e[0];   // kernel override (tests run each): ring|stage|pair
+    if (kind == 's')
+      CK((t->sa_NT == 128 ? launch_sa_stage<128>(t->sa_tmap, q, SB, grid, s)
+                          : launch_sa_stage<256>(t->sa_tmap, q, SB, grid, s)));
     else if (kind == 'p' && n_cb >= 2) {
       const unsigned g2 = (unsigned)(2 * std::min<long long>((n_cb + 1) / 2, 74));
       CK(t->sa_NT == 128 ? launch_sa2<128>(t->sa_tmap2, q, g2, s) : launch_sa2<256>(t->sa_tmap2, q, g2, s));
@@ -1634,7 +1640,11 @@ hobo_status aggregate_best(hobo_tensor* t, int64_t batch, int64_t topk, uint8_t*
     for (int64_t g = 0; g < G; ++g) {
       if ((k1[g] >> 32) > (k1[kth] >> 32)) break;
       Grp r;
-      r.e = key_energy(k1[g]);
+      {
+        hobo_best bb;
+        hobo_best_from_key((k1[g] & 0xFFFFFFFF00000000ull), &bb);   // the energy half of the sort key
+        r.e = bb.e;
+      }
       r.count = (int64_t)starts[g + 1] - starts[g];
       r.chain = (uint32_t)(k2[g] & 0xFFFFFFFFull);
       std::vector<uint32_t> row(W);
@@ -1840,7 +1850,7 @@ hobo_status hobo_tt_energy(hobo_tensor* t, const uint8_t* X, int64_t B, int64_t 
   CK(cudaGetLastError());
   t->last_launches = 2;
   if (best) {
-    CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
     search_best_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(E, B, row0, t->d_key);
     CK(cudaGetLastError());
     t->last_launches += 1;
@@ -1862,8 +1872,8 @@ hobo_status hobo_search(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t it
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
   const int R = g_dist.rank, P = g_dist.world;
-  auto lo_of = [&](int r) { return r * (batch / P) + std::min<int64_t>(r, batch % P); };
-  const int64_t lo = lo_of(R), n = lo_of(R + 1) - lo;
+  int64_t lo = 0, n = 0;
+  if (hobo_status st = hobo_shard(batch, R, P, &lo, &n)) return st;
   const int N = t->host.N, W = t->W;
   int64_t launches = 0;
   if (n > 0) {
@@ -1871,7 +1881,7 @@ hobo_status hobo_search(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t it
   } else if (hobo_status st = check_device(t)) {
     return st;
   }
-  CK(cudaMemsetAsync(t->d_key, 0xFF, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
   if (n > 0) {
     search_best_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, s>>>(t->d_ebest, n, lo,
                                                                                                t->d_key);
@@ -1882,7 +1892,7 @@ hobo_status hobo_search(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t it
   if (hobo_status st = finish_best(t, &b, s)) return st;   // C1 (synchronises the stream)
   const int64_t c = b.idx;
   int owner = 0;
-  while (owner + 1 < P && lo_of(owner + 1) <= c) ++owner;
+  if (hobo_status st = hobo_shard_owner(batch, P, c, &owner)) return st;   // every rank has >= 1 chain overall
   if (hobo_status st = grow(t, t->d_xbc, t->xbc_cap, (size_t)W)) return st;
   if (R == owner)
     CK(cudaMemcpyAsync(t->d_xbc, t->d_xbest + (size_t)(c - lo) * W, (size_t)W * 4, cudaMemcpyDeviceToDevice, s));
@@ -1895,6 +1905,49 @@ hobo_status hobo_search(hobo_tensor* t, uint64_t seed, int64_t batch, int64_t it
     for (int m = 0; m < N; ++m) x_best_host[m] = (uint8_t)((xb[m >> 5] >> (m & 31)) & 1u);
   if (e_best_host) *e_best_host = b.e;
   t->last_launches = launches + 2;
+  return HOBO_OK;
+}
+
+hobo_status hobo_shard(int64_t total, int rank, int world, int64_t* lo, int64_t* n) {
+  if (total < 0 || world < 1 || rank < 0 || rank >= world || !lo || !n)
+    return fail(HOBO_EINVAL, "hobo_shard: total >= 0, 0 <= rank < world, non-null outputs");
+  auto lo_of = [&](int64_t r) { return r * (total / world) + std::min<int64_t>(r, total % world); };
+  *lo = lo_of(rank);
+  *n = lo_of(rank + 1) - *lo;
+  return HOBO_OK;
+}
+
+hobo_status hobo_shard_owner(int64_t total, int world, int64_t index, int* owner) {
+  if (world < 1 || !owner || index < 0 || index >= total)
+    return fail(HOBO_EINVAL, "hobo_shard_owner: index outside [0, total) or world < 1");
+  // the first total % world ranks hold base + 1 items, the rest base
+  const int64_t base = total / world, rem = total % world, big = rem * (base + 1);
+  *owner = (int)(index < big ? index / (base + 1) : rem + (index - big) / base);
+  return HOBO_OK;
+}
+
+hobo_status hobo_best_key(float e, int64_t idx, uint64_t* key) {
+  if (!key || e != e || idx < 0 || idx > (int64_t)0xFFFFFFFF)
+    return fail(HOBO_EINVAL, "hobo_best_key: NaN energy or index outside [0, 2^32)");
+  if (e == 0.0f) e = 0.0f;   // -0 -> +0
+  int32_t i;
+  std::memcpy(&i, &e, 4);
+  if (i < 0) i ^= 0x7FFFFFFF;
+  *key = ((uint64_t)((uint32_t)i ^ 0x80000000u) << 32) | (uint64_t)idx;
+  return HOBO_OK;
+}
+
+hobo_status hobo_best_from_key(uint64_t key, hobo_best* best) {
+  if (!best) return fail(HOBO_EINVAL, "null best");
+  if (key == ~0ull) {
+    best->e = INFINITY;
+    best->idx = -1;
+    return HOBO_OK;
+  }
+  int32_t i = (int32_t)((uint32_t)(key >> 32) ^ 0x80000000u);
+  if (i < 0) i ^= 0x7FFFFFFF;
+  std::memcpy(&best->e, &i, 4);
+  best->idx = (int64_t)(key & 0xFFFFFFFFull);
   return HOBO_OK;
 }
 
@@ -1967,15 +2020,6 @@ hobo_status hobo_last_launch_kind(const hobo_tensor* t, int* i8_planes) {
   return HOBO_OK;
 }
 
-#ifdef HOBO_PIPE_STATS
-// debug builds only: copy (and reset) the per-CTA pipeline counters
-hobo_status hobo_debug_pipe_stats(unsigned long long* out /* 8192 x 16 */) {
-  if (cudaMemcpyFromSymbol(out, g_pipe_stats, sizeof(g_pipe_stats)) != cudaSuccess) return HOBO_ECUDA;
-  static unsigned long long zeros[8192][16];
-  cudaMemcpyToSymbol(g_pipe_stats, zeros, sizeof(zeros));
-  return HOBO_OK;
-}
-#endif
 
 hobo_status hobo_set_profiling(hobo_tensor* t, int enable) {
   if (!t) return fail(HOBO_EINVAL, "null handle");

@@ -51,7 +51,6 @@ struct KrParams {
                             // schedule; split s writes partials G + s*B*N, Q[(s*n_ct + ct)*B + b]
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
   double wp;                // weight of the degree-1 term
-  int dbg;                  // debug builds only (HOBO_PIPE_STATS): pipeline bisection switches
   double qscale;            // int8 digit planes (kr_gemm_kernel<..., I8>): cell = qscale * sum_l 256^l d_l
   const uint4* srec;        // int8: per K-block pair, {runs of 2P, runs of 2P+1, nfix, 0} + the runs
   int srec_u4;              // int8: uint4s per record (the descriptor ring's slot size)
@@ -227,19 +226,6 @@ __device__ __forceinline__ void real_block(const uint16_t* pr, const uint4 d0, c
   if (nruns > 1) apply(d1);
   for (uint32_t i = 2; i < nruns; ++i) apply(__ldg(runs + (d0.w >> 10) + (i - 2)));
 }
-
-#ifdef HOBO_PIPE_STATS
-// debug builds only: per-CTA pipeline accounting (clock64 cycles), accumulated in registers
-//  [0] MMA loop  [1] MMA waiting FULL  [2] stages  [3] K-blocks  [4] issuing MMAs  [5] commits
-//  [6] TMA waiting EMPTY  [7] gen warp waiting EMPTY  [8] gen A bits  [9] gen TMEM store + wait
-//  [10] gen arrive
-__device__ unsigned long long g_pipe_stats[8192][16];
-#define PSTAT_FLUSH(i, v) atomicAdd(&g_pipe_stats[blockIdx.x & 8191][i], (unsigned long long)(v))
-#define PT(...) __VA_ARGS__
-#else
-#define PSTAT_FLUSH(i, v)
-#define PT(...)
-#endif
 
 // int8 digit planes, the common stage (both K-blocks of the box pair) fully unrolled: L planes
 // x 4 MMAs of K = 32, each plane into its own s32 accumulator (top digit signed); only the
@@ -447,7 +433,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     if (lane == 0) {
       int st = 0;                    // ring slot and phase, advanced per stage (no divisions)
       uint32_t ph = 0;
-      PT(unsigned long long w_tma = 0;)
       // I8: the A generator's K-block descriptors, bulk-copied DAHEAD stages ahead of the W
       // boxes into a ring of their own (slot m % MAXD is reused only after the generator is
       // done with stage m - MAXD <= the stage whose W slot was just freed)
@@ -475,9 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
           const int nkb = min(KPS, s.x + s.y - kb0);
-          PT(const long long t0 = clock64();)
           mbar_wait(EMPTY(st), ph ^ 1u);
-          PT(w_tma += clock64() - t0;)
           if constexpr (DEC) dissue();
           if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
             if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)p.L * C::BOX);
@@ -501,7 +484,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           if (++st == NST) { st = 0; ph ^= 1u; }
         }
       }
-      PSTAT_FLUSH(6, w_tma);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: D[tmem] += A[tmem] * B[smem] -------------------------------
@@ -513,7 +495,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       int st = 0, sa = 0;            // W and A ring slots and phases, advanced per stage
       uint32_t ph = 0, pha = 0;
       uint32_t issued = 0;
-      PT(unsigned long long stt[6] = {0, 0, 0, 0, 0, 0}; const long long t_start = clock64(); long long t0;)
       for (int it = 0; it < ntile; ++it) {
       if (it > 0) {   // the previous block's epilogue has read the accumulator
         mbar_wait(acc_empty, (uint32_t)((it - 1) & 1));
@@ -524,10 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
           const int nkb = min(KPS, s.x + s.y - kb0);
-          PT(t0 = clock64();)
           mbar_wait(FULL(st), ph);
           if (DEC) mbar_wait(FULLA(sa), pha);
-          PT(stt[1] += clock64() - t0; stt[2] += 1; stt[3] += nkb; t0 = clock64();)
           tc_fence_after();
           if (elect_one()) {
             if constexpr (I8) {   // KPS K-blocks x L digit planes, each into its own accumulator
@@ -587,14 +566,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
                 }
               }
             }
-            PT(stt[4] += clock64() - t0; t0 = clock64();)
             if constexpr (PAIR) umma_commit_pair(EMPTY(st), 3);
             else umma_commit(EMPTY(st));
             if constexpr (DEC) {
               if constexpr (PAIR) umma_commit_pair(EMPTYA(sa), 3);
               else umma_commit(EMPTYA(sa));
             }
-            PT(stt[5] += clock64() - t0;)
           }
           __syncwarp();
           issued = 1;
@@ -628,7 +605,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       }
       __syncwarp();
       }   // tiles
-      PT(if (lane == 0) { stt[0] = clock64() - t_start; for (int i = 0; i < 6; ++i) PSTAT_FLUSH(i, stt[i]); })
     }
   } else {
     // ---------------- A generator (warps 2..9), then epilogue --------------------------------
@@ -648,7 +624,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     uint32_t wph = 0;
     int gn = 0;                      // I8: stage counter (the teams alternate stages)
     bool any = false;                // has any MMA been issued yet (else F = 0)
-    PT(unsigned long long w_gen = 0, w_bits = 0, w_st = 0, w_arr = 0;)
     const uint16_t* prow_r = prow + (size_t)row * (REAL ? p.pstride : 0);
     // I8: F_m = qscale * sum_l 256^l acc_l[m], exact in int64
     auto load_i8 = [&](int c0, long long (&v)[32]) {
@@ -752,7 +727,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
         for (int kb0 = s.x; kb0 < kend; kb0 += KPS, ++gn) {
           if ((gn & 1) == h) {
-            PT(const long long tb = clock64();)
             mbar_wait(DFULL(wst), wph);
             const uint4* rec = dsm + (size_t)wst * p.srec_u4;
             const uint4 hd = rec[0];
@@ -764,23 +738,16 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             for (int c = 0; c < 16; ++c) w[c] = (((uint32_t)(b0 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
 #pragma unroll
             for (int c = 0; c < 16; ++c) w[16 + c] = (((uint32_t)(b1 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-            PT(w_bits += clock64() - tb;)
-            PT(const long long tg = clock64();)
             mbar_wait(EMPTYA(gst), gph ^ 1u);
-            PT(w_gen += clock64() - tg;)
-            PT(const long long ts = clock64();)
             tc_fence_after();
             tmem_st32(lane_base + (uint32_t)(p.L * NT + gst * KPS * C::A_COLS), w);
             tmem_st_wait();
             tc_fence_before();
-            PT(w_st += clock64() - ts;)
-            PT(const long long ta = clock64();)
             __syncwarp();
             if (lane == 0) {
               if (PAIR && !leader) mbar_arrive_remote(mapa_shared(FULLA(gst), 0));
               else mbar_arrive(FULLA(gst));
             }
-            PT(w_arr += clock64() - ta;)
           }
           if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
           if (++gst == NSTA) { gst = 0; gph ^= 1u; }
@@ -800,25 +767,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const int kb = kb0 + h;                       // this team's K-block of the stage
         const bool mine = h < KPS && kb < kend;
         uint4 n0 = f0, n1 = f1;
-#ifdef HOBO_PIPE_STATS
-        if (!(p.dbg & 1))   // bisection: 1 = reuse the descriptors (wrong A, timing only)
-#endif
         ldk(kb + 3 * KPS, n0, n1);
         const int st = gst;                           // A slot (== the W slot)
         // the A bits depend only on the candidates: computed before the slot frees up
-        PT(const long long tb = clock64();)
-        uint64_t bits = 0ull;
-#ifdef HOBO_PIPE_STATS
-        if (p.dbg & 2) bits = mine ? (uint64_t)d0.x * 0x9E3779B97F4A7C15ull ^ xs[row] : 0ull;   // 2 = no run decoding
-        else
-#endif
-        bits = mine ? block_bits(xs, row, d0, d1, p.runs) : 0ull;
-        PT(w_bits += clock64() - tb;)
-        PT(const long long tg = clock64();)
+        const uint64_t bits = mine ? block_bits(xs, row, d0, d1, p.runs) : 0ull;
         mbar_wait(EMPTY(st), gph ^ 1u);
-        PT(w_gen += clock64() - tg;)
         if (++gst == NSTA) { gst = 0; gph ^= 1u; }
-        PT(const long long ts = clock64();)
         if (mine) {
           tc_fence_after();
           uint32_t w[32];
@@ -828,14 +782,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           tmem_st_wait();
           tc_fence_before();
         }
-        PT(w_st += clock64() - ts;)
-        PT(const long long ta = clock64();)
         __syncwarp();
         if (lane == 0) {
           if (PAIR && !leader) mbar_arrive_remote(mapa_shared(FULL(st), 0));
           else mbar_arrive(FULL(st));
         }
-        PT(w_arr += clock64() - ta;)
         d0 = e0;
         d1 = e1;
         e0 = f0;
@@ -860,7 +811,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     }
 
     // ---------------- epilogue: fields, energy partial (this warp's column half) ---------------
-    PT(if (warp == 2 && lane == 0) { PSTAT_FLUSH(7, w_gen); PSTAT_FLUSH(8, w_bits); PSTAT_FLUSH(9, w_st); PSTAT_FLUSH(10, w_arr); })
     mbar_wait(acc_full, (uint32_t)(it & 1));
     tc_fence_after();
     const long long b = b0t + row;
@@ -1102,25 +1052,40 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
   return v;
 }
 
-// E_b = (sum_ct Q[ct][b]) / lcm; argmin via warp shuffles -> smem block min -> one atomicMin
-__global__ void finalize_kernel(const double* __restrict__ Q, int n_ct, long long B, double lcm, long long row0,
-                                float* __restrict__ E, unsigned long long* __restrict__ best_key) {
+// block min of the keys -> one atomicMin on best_key[0]; a NaN energy clears best_key[1]
+// (NaN is an error, reported by the host after the combine)
+__device__ __forceinline__ void block_argmin(unsigned long long key, bool nan, unsigned long long* best_key) {
   __shared__ unsigned long long red[32];
-  unsigned long long key = ~0ull;
-  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B; b += (long long)gridDim.x * blockDim.x) {
-    const float e = combine_q(Q, n_ct, B, b, lcm);
-    if (E) E[b] = e;
-    const unsigned long long k = argmin_key(e, (unsigned long long)(row0 + b));
-    key = k < key ? k : key;
-  }
+  __shared__ int any_nan;
+  if (threadIdx.x == 0) any_nan = 0;
+  __syncthreads();
+  if (nan) any_nan = 1;
   key = warp_min_u64(key);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
   __syncthreads();
   if (threadIdx.x < 32) {
     key = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : ~0ull;
     key = warp_min_u64(key);
-    if (threadIdx.x == 0 && best_key) atomicMin(best_key, key);
+    if (threadIdx.x == 0) {
+      atomicMin(best_key, key);
+      if (any_nan) atomicAnd(best_key + 1, 0ull);
+    }
   }
+}
+
+// E_b = (sum_ct Q[ct][b]) / lcm; argmin via warp shuffles -> smem block min -> one atomicMin
+__global__ void finalize_kernel(const double* __restrict__ Q, int n_ct, long long B, double lcm, long long row0,
+                                float* __restrict__ E, unsigned long long* __restrict__ best_key) {
+  unsigned long long key = ~0ull;
+  bool nan = false;
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B; b += (long long)gridDim.x * blockDim.x) {
+    const float e = combine_q(Q, n_ct, B, b, lcm);
+    if (E) E[b] = e;
+    nan |= e != e;
+    const unsigned long long k = argmin_key(e, (unsigned long long)(row0 + b));
+    key = k < key ? k : key;
+  }
+  if (best_key) block_argmin(key, nan, best_key);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1286,20 +1251,15 @@ __global__ void search_step_kernel(const double* __restrict__ Q, int n_ct, doubl
 
 __global__ void search_best_kernel(const float* __restrict__ ebest, long long nchains, long long chain0,
                                    unsigned long long* best_key) {
-  __shared__ unsigned long long red[32];
   unsigned long long key = ~0ull;
+  bool nan = false;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nchains; c += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long k = argmin_key(ebest[c], (unsigned long long)(chain0 + c));
+    const float e = ebest[c];
+    nan |= e != e;
+    const unsigned long long k = argmin_key(e, (unsigned long long)(chain0 + c));
     key = k < key ? k : key;
   }
-  key = warp_min_u64(key);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    key = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : ~0ull;
-    key = warp_min_u64(key);
-    if (threadIdx.x == 0) atomicMin(best_key, key);
-  }
+  block_argmin(key, nan, best_key);
 }
 
 }  // namespace hobo

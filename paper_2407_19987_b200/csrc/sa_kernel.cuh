@@ -107,7 +107,6 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
     // ---------------- TMA producer: the sites' W boxes, in visiting order, for every block ---------
     if (lane == 0) {
       uint32_t nw = 0;
-      PT(unsigned long long w_tma = 0;)
       for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x)
         for (long long step = 0; step < p.steps; ++step) {
           const int m = (int)(step % p.N);
@@ -117,15 +116,12 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
             for (int l = 0; l < L; ++l)
               for (int h = 0; h < p.n_ct; ++h, ++nw) {
                 const uint32_t s = nw % C::RW;
-                PT(const long long t0 = clock64();)
                 mbar_wait(EMPTYW(s), ((nw / C::RW) & 1u) ^ 1u);
-                PT(w_tma += clock64() - t0;)
                 mbar_arrive_expect_tx(FULLW(s), C::BOX);
                 tma_load_3d(sW + s * C::BOX, &tmap, FULLW(s), 0, 0, sb + (l * p.n_ct + h) * p.nkb1 + kb);
               }
           }
         }
-      PSTAT_FLUSH(6, w_tma);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: G[:, tile h] += A_q * W_m,q (accumulate, never cleared) ---------
@@ -133,24 +129,19 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
     {
       constexpr uint32_t idesc = idesc_bf16_f32(kBM, NT);
       uint32_t nw = 0, na = 0;
-      PT(unsigned long long wa = 0, ww = 0; const long long tbeg = clock64(); long long t0;)
       for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x)
         for (long long step = 0; step < p.steps; ++step) {
           const int m = (int)(step % p.N);
           const int L = __ldg(p.site_L + m);
           for (int q = 0; q < p.nq; ++q, ++na) {
             const uint32_t a = na % C::RA;
-            PT(t0 = clock64();)
             mbar_wait(FULLA(a), (na / C::RA) & 1u);
-            PT(wa += clock64() - t0;)
             tc_fence_after();
             const uint64_t adesc = sw128_kmajor_desc(sA + a * C::ABOX);
             for (int l = 0; l < L; ++l)
               for (int h = 0; h < p.n_ct; ++h, ++nw) {
                 const uint32_t s = nw % C::RW;
-                PT(t0 = clock64();)
                 mbar_wait(FULLW(s), (nw / C::RW) & 1u);
-                PT(ww += clock64() - t0;)
                 tc_fence_after();
                 const uint64_t bdesc = sw128_kmajor_desc(sW + s * C::BOX);
                 if (elect_one()) {
@@ -167,7 +158,6 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
           if (elect_one()) umma_commit(SITE);   // this site's G update is complete when this arrives
           __syncwarp();
         }
-      PT(if (lane == 0) { PSTAT_FLUSH(0, clock64() - tbeg); PSTAT_FLUSH(1, wa); PSTAT_FLUSH(2, ww); })
     }
   } else {
     // ---------------- decisions (team 0) + A generator (both teams), one row per thread -----------
@@ -177,7 +167,6 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
     const uint32_t lane_base = tmem + ((uint32_t)(qd * 32) << 16);
     const int gtid = threadIdx.x - 64;       // 0..255
     uint32_t na = 0, nsite = 0;
-    PT(unsigned long long g_site = 0, g_dec = 0, g_gen = 0, g_ea = 0; long long tg;)
     for (long long cb = blockIdx.x; cb < n_cb; cb += gridDim.x) {
       const long long b0 = cb * kBM, b = b0 + row;
       const bool live = b < p.B;
@@ -208,13 +197,11 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
           const double u = (double)(d_hash(p.seed, 4, (uint64_t)(p.chain0 + b), (uint64_t)step) >> 11) * 0x1.0p-53;
           thr = -__ldg(p.temps + step / p.N) * log(u);
         }
-        PT(tg = clock64();)
         if (step > 0) {
           mbar_wait(SITE, nsite & 1u);
           ++nsite;
           tc_fence_after();
         }
-        PT(g_site += clock64() - tg; tg = clock64();)
         if (h == 0) {
           const float g = __uint_as_float(tmem_ld1(lane_base + (uint32_t)m));
           tmem_ld_wait();
@@ -233,18 +220,14 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
           sS[row] = sv;
           tc_fence_before();
         }
-        PT(g_dec += clock64() - tg; tg = clock64();)
         named_bar_sync(1, 256);
-        PT(tg = clock64();)
         // A rows of site m: s_b * prod_{u in T} x_bu (x_m itself never occurs with W_m != 0)
         const int sv = sS[row];
         const uint32_t sgn = sv < 0 ? 0x80008000u : 0u;
         for (int q = 0; q < p.nq; ++q, ++na) {
           if ((q & 1) != h) continue;
           const uint32_t a = na % C::RA;
-          PT(const long long te = clock64();)
           mbar_wait(EMPTYA(a), ((na / C::RA) & 1u) ^ 1u);
-          PT(g_ea += clock64() - te;)
           const int kb = sa_site_kb(p, q);
           uint64_t bits = 0;
           if (sv != 0) {
@@ -263,7 +246,6 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
           __syncwarp();
           if (lane == 0) mbar_arrive(FULLA(a));
         }
-        PT(g_gen += clock64() - tg;)
       }
       if (p.steps > 0) {   // the last site's update: then the block's results are final
         mbar_wait(SITE, nsite & 1u);
@@ -277,7 +259,6 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
       tc_fence_before();
       named_bar_sync(1, 256);   // xs and TMEM are reused by the next block
     }
-    PT(if (gtid == 0) { PSTAT_FLUSH(3, g_site); PSTAT_FLUSH(4, g_dec); PSTAT_FLUSH(5, g_gen); PSTAT_FLUSH(7, g_ea); })
   }
 #undef FULLW
 #undef EMPTYW
@@ -293,28 +274,26 @@ __global__ void __launch_bounds__(kThreads, 1) sa_kernel(const __grid_constant__
 // K-block plus its A tile, behind ONE full barrier (TMA bytes + 4 generator-warp arrivals)
 // and ONE empty barrier (a single tcgen05.commit).  The box-ring kernel above pays a wait,
 // a fence and a commit per W box and per A tile; with 128-column tiles (64-cycle MMAs) that
-// bookkeeping is what the lone MMA-issuing thread cannot hide.
-// TS (one column tile, Npad <= 256): the A tiles go to tensor memory next to G (tcgen05.st,
-// A-in-TMEM MMAs), so shared memory carries only the W stream — with A in smem its writes
-// and the MMAs' A reads push shared-memory traffic past the port at 128-column tiles.
-template <int NT, bool TS>
+// bookkeeping is what the lone MMA-issuing thread cannot hide.  (A tiles in TMEM instead of
+// shared memory were measured 4% slower at cfg4 and dropped.)
+template <int NT>
 struct SaStCfg {
   static constexpr int BOX = NT * 128;
-  static constexpr int ABOX = TS ? 0 : kBM * 128;
+  static constexpr int ABOX = kBM * 128;
   static constexpr int MAXST = 8;
   static constexpr int BUDGET = 232448 - 1024 - 1024 - 16 * 1024;   // ring bytes (bits, barriers after it)
   static int stage_bytes(int boxes) { return boxes * BOX + ABOX; }
-  static int nst(int boxes) { return std::min(TS ? MAXST : 4, BUDGET / stage_bytes(boxes)); }
+  static int nst(int boxes) { return std::min(4, BUDGET / stage_bytes(boxes)); }
   static size_t smem_bytes(int boxes, int W) {
     return 1024 + (size_t)nst(boxes) * stage_bytes(boxes) + 8 * (2 * MAXST + 1) + 16 + (size_t)(W + 2) * kBM * 4 +
            kBM * 4 + 128;
   }
 };
 
-template <int NT, bool TS>
+template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_constant__ CUtensorMap tmap, const SaParams p,
                                                                int SB, int NST) {
-  using C = SaStCfg<NT, TS>;
+  using C = SaStCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -333,8 +312,8 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NPAD = NT * p.n_ct;
-  // TMEM: G in [0, NPAD), then (TS) one 32-column A tile per stage
-  const uint32_t TCOLS = TS ? (NPAD + NST * 32 <= 256 ? 256u : 512u) : (uint32_t)NPAD;
+  // TMEM: G in [0, NPAD)
+  const uint32_t TCOLS = (uint32_t)NPAD;
   const long long n_cb = (p.B + kBM - 1) / kBM;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(FULL(s), 5); mbar_init(EMPTY(s), 1); }
@@ -384,16 +363,14 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
             mbar_wait(FULL(s), (n / NST) & 1u);
             tc_fence_after();
             const uint32_t st = sSt + s * SBYTES;
-            const uint64_t adesc = TS ? 0ull : sw128_kmajor_desc(st + (uint32_t)SB * C::BOX);
-            const uint32_t a_t = tmem + (uint32_t)(NPAD + 32 * s);
+            const uint64_t adesc = sw128_kmajor_desc(st + (uint32_t)SB * C::BOX);
             if (elect_one()) {
               for (int l = 0; l < L; ++l)
                 for (int h = 0; h < p.n_ct; ++h) {
                   const uint64_t bdesc = sw128_kmajor_desc(st + (uint32_t)(l * p.n_ct + h) * C::BOX);
 #pragma unroll
                   for (int k = 0; k < kBK / 16; ++k) {
-                    if constexpr (TS) umma_bf16_ts(tmem + (uint32_t)(h * NT), a_t + 8u * k, bdesc + 2u * k, idesc, 1u);
-                    else umma_bf16_ss(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
+                    umma_bf16_ss(tmem + (uint32_t)(h * NT), adesc + 2u * k, bdesc + 2u * k, idesc, 1u);
                   }
                 }
               umma_commit(EMPTY(s));
@@ -478,14 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) sa_stage_kernel(const __grid_cons
           uint32_t w[32];
           expand32((uint32_t)bits, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
           expand32((uint32_t)(bits >> 32), *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
-          if constexpr (TS) {
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) w[c] ^= sgn;
-            tmem_st32(lane_base + (uint32_t)(NPAD + 32 * s), w);
-            tmem_st_wait();
-            tc_fence_before();
-          } else {
+          {
             const uint32_t rowaddr = sSt + s * SBYTES + (uint32_t)SB * C::BOX + (uint32_t)(row >> 3) * 1024u +
                                      (uint32_t)(row & 7) * 128u;
 #pragma unroll

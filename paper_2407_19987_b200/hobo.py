@@ -21,6 +21,7 @@ EXPORTED = [
     "hobo_search", "hobo_search_shard", "hobo_search_samples", "hobo_multilinear_field",
     "hobo_gd_run", "hobo_tt_build", "hobo_tt_energy", "hobo_sa_shard", "hobo_sa_run", "hobo_last_launch_stats", "hobo_last_launch_kind",
     "hobo_set_profiling", "hobo_dist_unique_id", "hobo_dist_init", "hobo_dist_finalize", "hobo_dist_info",
+    "hobo_shard", "hobo_shard_owner", "hobo_best_key", "hobo_best_from_key",
     "hobo_last_error",
 ]
 
@@ -59,12 +60,12 @@ def lib():
         L.hobo_tensor_export_dense.argtypes = [P, P]
         L.hobo_energy.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_local_field.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
-        L.hobo_local_field_host.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
+        L.hobo_local_field_host.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
         L.hobo_energy_host.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_energy_bits.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
         L.hobo_local_field_bits.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
         L.hobo_energy_host_bits.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
-        L.hobo_local_field_host_bits.argtypes = [P, P, I64, I64, P, C.POINTER(HoboBest), P]
+        L.hobo_local_field_host_bits.argtypes = [P, P, I64, I64, P, P, C.POINTER(HoboBest), P]
         L.hobo_search.argtypes = [P, U64, I64, I64, P, C.POINTER(C.c_float), P]
         L.hobo_search_shard.argtypes = [P, U64, I64, I64, I64, D, D, P, C.POINTER(C.c_float),
                                         C.POINTER(I64), P]
@@ -82,6 +83,10 @@ def lib():
         L.hobo_dist_init.argtypes = [I, I, P, I]
         L.hobo_dist_finalize.argtypes = []
         L.hobo_dist_info.argtypes = [C.POINTER(I), C.POINTER(I)]
+        L.hobo_shard.argtypes = [I64, I, I, C.POINTER(I64), C.POINTER(I64)]
+        L.hobo_shard_owner.argtypes = [I64, I, I64, C.POINTER(I)]
+        L.hobo_best_key.argtypes = [C.c_float, I64, C.POINTER(U64)]
+        L.hobo_best_from_key.argtypes = [U64, C.POINTER(HoboBest)]
         L.hobo_last_error.restype = C.c_char_p
         for name in EXPORTED:
             if name != "hobo_last_error":
@@ -245,26 +250,40 @@ class HoboTensor:
                                       C.byref(best) if want_best else None, _stream_handle(stream)))
         return (G, E, (best.e, best.idx)) if want_best else (G, E)
 
-    def local_field_host(self, X, E=None, row0=0, want_best=True, stream=None, fields=True):
+    @staticmethod
+    def _host_ptr(a, dtype, shape):
+        """Host buffer address: a numpy array or a CPU torch tensor (ideally pinned)."""
+        if a is None:
+            return None
+        if hasattr(a, "data_ptr"):
+            if a.is_cuda or tuple(a.shape) != tuple(shape) or not a.is_contiguous() or \
+                    a.element_size() != np.dtype(dtype).itemsize:
+                raise ValueError(f"expected a contiguous CPU tensor of shape {shape} and {np.dtype(dtype)} width")
+            return a.data_ptr()
+        if a.dtype.itemsize != np.dtype(dtype).itemsize or a.dtype.kind != np.dtype(dtype).kind or \
+                a.shape != tuple(shape) or not a.flags.c_contiguous:
+            raise ValueError(f"expected a C-contiguous {np.dtype(dtype)} array of shape {shape}")
+        return a.ctypes.data
+
+    def local_field_host(self, X, E=None, row0=0, want_best=True, stream=None, fields=True, G=None):
         """hobo_local_field_host (fields=True) / hobo_energy_host (fields=False): candidates in
         host memory (numpy u8 B x N, or a CPU torch tensor, ideally pinned); energies into the
-        host array E (f32, allocated if None).  Returns (E, best)."""
-        def host_ptr(a, dtype, shape):
-            if hasattr(a, "data_ptr"):
-                if a.is_cuda or tuple(a.shape) != shape or not a.is_contiguous():
-                    raise ValueError(f"expected a contiguous CPU tensor of shape {shape}")
-                return a.data_ptr()
-            if a.dtype != dtype or a.shape != shape or not a.flags.c_contiguous:
-                raise ValueError(f"expected a C-contiguous {dtype} array of shape {shape}")
-            return a.ctypes.data
+        host array E (f32, allocated if None); with G (host f32 B x N, ideally pinned) the local
+        fields come back too.  Returns (E, best)."""
         B = X.shape[0]
-        xp = host_ptr(X, np.uint8, (B, self.N))
+        xp = self._host_ptr(X, np.uint8, (B, self.N))
         if E is None:
             E = np.empty(B, np.float32)
+        ep = self._host_ptr(E, np.float32, (B,))
         best = HoboBest()
-        fn = lib().hobo_local_field_host if fields else lib().hobo_energy_host
-        _check(fn(self._h, xp, B, row0, host_ptr(E, np.float32, (B,)), C.byref(best) if want_best else None,
-                  _stream_handle(stream)))
+        bp = C.byref(best) if want_best else None
+        if fields:
+            _check(lib().hobo_local_field_host(self._h, xp, B, row0, self._host_ptr(G, np.float32, (B, self.N)), ep, bp,
+                                               _stream_handle(stream)))
+        else:
+            if G is not None:
+                raise ValueError("fields=False computes no fields")
+            _check(lib().hobo_energy_host(self._h, xp, B, row0, ep, bp, _stream_handle(stream)))
         return E, ((best.e, best.idx) if want_best else None)
 
     def energy_host(self, X, E=None, row0=0, want_best=True, stream=None):
@@ -298,9 +317,10 @@ class HoboTensor:
                                            _stream_handle(stream)))
         return (G, E, (best.e, best.idx)) if want_best else (G, E)
 
-    def local_field_host_bits(self, Xb, E=None, row0=0, want_best=True, stream=None, fields=True):
+    def local_field_host_bits(self, Xb, E=None, row0=0, want_best=True, stream=None, fields=True, G=None):
         """hobo_local_field_host_bits (fields=True) / hobo_energy_host_bits: packed rows in host
-        memory (numpy uint32 or a CPU int32 tensor, B x ceil(N/32), ideally pinned)."""
+        memory (numpy uint32 or a CPU int32 tensor, B x ceil(N/32), ideally pinned); G as in
+        local_field_host."""
         W = (self.N + 31) // 32
         B = Xb.shape[0]
         if hasattr(Xb, "data_ptr"):
@@ -313,18 +333,16 @@ class HoboTensor:
             xp = Xb.ctypes.data
         if E is None:
             E = np.empty(B, np.float32)
-        if hasattr(E, "data_ptr"):
-            import torch
-            if E.is_cuda or tuple(E.shape) != (B,) or not E.is_contiguous() or E.dtype != torch.float32:
-                raise ValueError(f"expected a contiguous float32 CPU tensor of shape {(B,)}")
-            ep = E.data_ptr()
-        else:
-            if E.dtype != np.float32 or E.shape != (B,) or not E.flags.c_contiguous:
-                raise ValueError(f"expected a C-contiguous float32 array of shape {(B,)}")
-            ep = E.ctypes.data
+        ep = self._host_ptr(E, np.float32, (B,))
         best = HoboBest()
-        fn = lib().hobo_local_field_host_bits if fields else lib().hobo_energy_host_bits
-        _check(fn(self._h, xp, B, row0, ep, C.byref(best) if want_best else None, _stream_handle(stream)))
+        bp = C.byref(best) if want_best else None
+        if fields:
+            _check(lib().hobo_local_field_host_bits(self._h, xp, B, row0, self._host_ptr(G, np.float32, (B, self.N)), ep,
+                                                    bp, _stream_handle(stream)))
+        else:
+            if G is not None:
+                raise ValueError("fields=False computes no fields")
+            _check(lib().hobo_energy_host_bits(self._h, xp, B, row0, ep, bp, _stream_handle(stream)))
         return E, ((best.e, best.idx) if want_best else None)
 
     def multilinear_field(self, P, G=None, E=None, stream=None):
@@ -462,3 +480,32 @@ def dist_info():
     r, w = C.c_int(), C.c_int()
     _check(lib().hobo_dist_info(C.byref(r), C.byref(w)))
     return r.value, w.value
+
+
+# ---- multi-GPU host logic of the library (hobo_shard*, hobo_best_key; no device needed) -------
+def shard(total: int, rank: int, world: int):
+    """hobo_shard: this rank's contiguous range [lo, hi) of `total` items."""
+    lo, n = C.c_int64(), C.c_int64()
+    _check(lib().hobo_shard(total, rank, world, C.byref(lo), C.byref(n)))
+    return lo.value, lo.value + n.value
+
+
+def shard_owner(total: int, world: int, index: int) -> int:
+    """hobo_shard_owner: the rank whose shard holds global item `index`."""
+    o = C.c_int()
+    _check(lib().hobo_shard_owner(total, world, index, C.byref(o)))
+    return o.value
+
+
+def best_key(e: float, idx: int) -> int:
+    """hobo_best_key: the unsigned 64-bit argmin key of (e, idx) (HoboError on NaN)."""
+    k = C.c_uint64()
+    _check(lib().hobo_best_key(e, idx, C.byref(k)))
+    return k.value
+
+
+def best_from_key(key: int):
+    """hobo_best_from_key: (e, idx); the empty key ~0 gives (inf, -1)."""
+    b = HoboBest()
+    _check(lib().hobo_best_from_key(key, C.byref(b)))
+    return b.e, b.idx

@@ -511,6 +511,21 @@ def test_sa_replays_oracle_exactly(H, torch, name):
         assert np.array_equal(E.cpu().numpy().astype(np.float64), es), (name, chain0)
 
 
+@pytest.mark.parametrize("kind", ["ring", "stage", "pair"])
+@pytest.mark.parametrize("name", ["o4n20", "o3n300"])
+def test_sa_kernel_variants_replay_oracle(H, torch, kind, name):
+    """Every persistent annealing kernel (HOBO_SA_KERNEL override: box ring, staged, CTA pair;
+    a kernel that does not fit the shape falls back to the box ring) replays the oracle."""
+    p = SA_CASES[name]()
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    t0 = t.default_t_start()
+    with env("HOBO_SA_KERNEL", kind):
+        X, E, Et = t.sa_shard(5, 100, 300, 3, t0, 0.05)
+        torch.cuda.synchronize()
+    xs, es = o.sa(5, 100, 300, 3, t0, 0.05)
+    assert np.array_equal(X.cpu().numpy(), xs) and np.array_equal(Et.cpu().numpy(), es)
+
+
 def test_sa_shard_invariance(H, torch):
     p = random_integer_problem(3, 24, 5, 200)
     t = H.HoboTensor.from_problem(p)
@@ -587,6 +602,15 @@ def test_host_entry_points_match_device_path(H, torch):
         assert np.array_equal(Eh, E.cpu().numpy()) and besth == best
         Eh2, besth2 = t.energy_host(src, row0=row0)
         assert np.array_equal(Eh2, Ed.cpu().numpy()) and besth2 == bestd
+        # the fields delivered to host memory (double-buffered copy-out), pinned or pageable
+        Gh = torch.empty(B, t.N, dtype=torch.float32).pin_memory() if pinned else np.empty((B, t.N), np.float32)
+        Gh.fill(np.nan) if not pinned else Gh.fill_(float("nan"))
+        Eh3, besth3 = t.local_field_host(src, row0=row0, G=Gh)
+        Gh = Gh.numpy() if pinned else Gh
+        assert np.array_equal(Gh, G.cpu().numpy()) and np.array_equal(Eh3, Eh) and besth3 == best
+        if B >= 1000:
+            rows = sample_rows(B, 129, 64)
+            assert np.array_equal(Gh[rows].astype(np.float64), Oracle.from_problem(p).field(Xh[rows]))
 
 
 
@@ -626,6 +650,9 @@ def test_packed_entry_points_match_byte_path(H, torch, case):
     for src in (Xp, pinned):
         Eh, besth = t.local_field_host_bits(src, row0=row0)
         assert np.array_equal(Eh, E.cpu().numpy()) and besth == best
+        Gh = np.full((len(Eh), t.N), np.nan, np.float32)
+        Eh1, besth1 = t.local_field_host_bits(src, row0=row0, G=Gh)
+        assert np.array_equal(Gh, G.cpu().numpy()) and np.array_equal(Eh1, Eh) and besth1 == best
         Eh2, besth2 = t.local_field_host_bits(src, row0=row0, fields=False)
         assert np.array_equal(Eh2, Ee.cpu().numpy()) and besth2 == beste
     if o is not None:

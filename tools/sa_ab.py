@@ -1,4 +1,4 @@
-"""A/B timing of the persistent annealing kernels (HOBO_SA_KERNEL=ring|stage|ts|pair) on one config."""
+"""A/B timing of the persistent annealing kernels (HOBO_SA_KERNEL=ring|stage|pair) on one config."""
 import os
 import sys
 
@@ -15,7 +15,7 @@ elif cfg == "cfg4":
     t, B = HoboTensor.import_colex(4, 128, uniform_colex(4, 128, 4)), 262144
 t0 = t.default_t_start() if cfg == "cfg3" else 5.0
 t.sa_shard(1, 0, 128, 1, t0, t0)
-kinds = sys.argv[2:] or ["ring", "stage", "ts", "pair"]
+kinds = sys.argv[2:] or ["ring", "stage", "pair"]
 for kind in kinds:
     os.environ["HOBO_SA_KERNEL"] = kind
     t.set_profiling(True)
