@@ -9,7 +9,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -18,6 +20,7 @@
 #include "tt.h"
 #include "kernels.cuh"
 #include "sa_kernel.cuh"
+#include "persist.cuh"
 
 using namespace hobo;
 
@@ -96,9 +99,18 @@ struct hobo_tensor {
   int srec_u4 = 0;          // uint4s per record (1 + the most runs of any pair)
   float* d_p1 = nullptr;   // padded to 256-multiples
   int W = 0;               // 32-bit words per candidate bit row
-  DevLayout lay[4];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
+  DevLayout lay[5];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
                            // tiles for the real-valued path (p rows + a deeper W ring in smem),
-                           // 3 = bf16 field layout for the real-valued path when 1 holds int8 digits
+                           // 3 = bf16 field layout for the real-valued path when 1 holds int8 digits,
+                           // 4 = bf16 energy layout with 128-column tiles (the persistent kernel)
+  int* d_items = nullptr; size_t items_cap = 0;          // persistent kernel: per-pair item ranges
+  // the search loop as one CUDA graph per (chains, iterations, buffers); seed, chain0 and the
+  // P_t table travel in d_sargs, so a replay needs one small copy and one graph launch
+  unsigned long long* d_sargs = nullptr; size_t sargs_cap = 0;
+  cudaGraphExec_t search_exec = nullptr;
+  cudaStream_t gs = nullptr;                            // graph capture stream
+  std::vector<uintptr_t> search_key;
+  long long items_B = -1;                               // ... computed for this batch
   int dig = -1;            // int8 digit planes of slots 0/1 (0 = bf16 limbs; -1 = not decided yet)
   // scratch (grown on demand)
   uint32_t* d_bits = nullptr; size_t bits_cap = 0;
@@ -176,15 +188,20 @@ hobo_status grow(hobo_tensor* t, T*& p, size_t& cap, size_t n) {
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute of a kernel: set it
 // once per (kernel, device), for the largest size requested so far
+std::map<std::pair<const void*, int>, size_t>& smem_configured() {
+  static std::map<std::pair<const void*, int>, size_t> m;
+  return m;
+}
 template <class K>
 cudaError_t set_smem(K* k, size_t smem) {
-  static size_t configured[64] = {0};
+  static std::mutex mu;   // handles may live on different threads
+  std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (configured[dev] >= smem) return cudaSuccess;
+  size_t& have = smem_configured()[{reinterpret_cast<const void*>(k), dev}];
+  if (have >= smem) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) configured[dev] = smem;
+  if (e == cudaSuccess) have = smem;
   return e;
 }
 
@@ -368,11 +385,11 @@ hobo_status init_device(hobo_tensor* t) {
 hobo_status ensure_layout(hobo_tensor* t, int slot) {
   DevLayout& L = t->lay[slot];
   if (L.built) return HOBO_OK;
-  const int field = slot != 0;
+  const int field = (slot == 0 || slot == 4) ? 0 : 1;
   const HostTensor& H = t->host;
   const int N = H.N, k = H.order;
   L.i8 = slot <= 1 ? digit_planes(t) : 0;
-  L.NT = (N <= 128 || slot == 2) ? 128 : 256;   // a 128-column tile when N fits (no padded columns)
+  L.NT = (N <= 128 || slot == 2 || slot == 4) ? 128 : 256;   // a 128-column tile when N fits (no padded columns)
   if (L.i8 >= 2) L.NT = 128;                    // TMEM: i8 accumulators of NT columns + the A stages
   L.qscale = std::ldexp(1.0, H.qexp);
   const int planes = L.i8 ? L.i8 : H.limbs;
@@ -531,7 +548,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.qscale = L.qscale;
   p.srec = t->d_srec;
   p.srec_u4 = L.i8 ? t->srec_u4 : 0;
-  p.field_mode = (&L == &t->lay[0]) ? 0 : 1;
+  p.field_mode = (&L == &t->lay[0] || &L == &t->lay[4]) ? 0 : 1;
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
   return p;
@@ -620,9 +637,76 @@ int real_slot(hobo_tensor* t) {
   return real_geometry(t, 256, ps, ring, la) ? full : 2;
 }
 
+// the persistent energy kernel (persist.cuh) for short K loops: energy mode on bf16 limbs whose
+// tiles have fewer than 64 K-blocks (QUBO-like, BASELINE config 2), with enough (candidate-block
+// pair, column tile) items to keep every SM pair busy.  HOBO_PERSIST=1 / =0 forces it on / off.
+bool use_persist(hobo_tensor* t, long long B) {
+  if (t->host.limbs > PersistCfg::MAXL || t->kl.nseg > 8) return false;
+  if (const char* e = getenv("HOBO_PERSIST")) return e[0] == '1';
+  if (digit_planes(t) || t->kl.Tpad / kBK >= 64) return false;
+  const long long items = (B + 2 * kBM - 1) / (2 * kBM) * ((t->host.N + 127) / 128);
+  return items >= 4 * 74;
+}
+
+// contiguous item ranges of the persistent kernel, balanced by MMA work: item = candidate-block
+// pair x column tile (heaviest tile of a block first), weight = its K-blocks + one for the
+// per-item handoffs; pair p takes the items whose cumulative weight starts in [p W/P, (p+1) W/P)
+hobo_status persist_items(hobo_tensor* t, const DevLayout& L, long long B, int& npairs, cudaStream_t s) {
+  const int n_cbp = (int)((B + 2 * kBM - 1) / (2 * kBM));
+  const long long nitems = (long long)n_cbp * L.n_ct;
+  npairs = (int)std::min<long long>(74, nitems);
+  if (t->items_B == B) return HOBO_OK;
+  std::vector<double> w(L.n_ct);
+  double per_block = 0;
+  for (int k = 0; k < L.n_ct; ++k) {
+    const int ct = L.n_ct - 1 - k;
+    double kb = 0;
+    for (int j = 0; j < t->kl.nseg; ++j) kb += L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1];
+    w[k] = kb + 1.0;
+    per_block += w[k];
+  }
+  const double total = per_block * n_cbp;
+  std::vector<int> items((size_t)npairs + 1, 0);
+  double acc = 0;
+  int p = 1;
+  for (long long i = 0; i < nitems && p < npairs; ++i) {
+    while (p < npairs && acc >= total * p / npairs) items[(size_t)p++] = (int)i;
+    acc += w[(size_t)(i % L.n_ct)];
+  }
+  while (p <= npairs) items[(size_t)p++] = (int)nitems;
+  items[(size_t)npairs] = (int)nitems;
+  if (hobo_status st = grow(t, t->d_items, t->items_cap, items.size())) return st;
+  CK(cudaMemcpy(t->d_items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
+  t->items_B = B;
+  return HOBO_OK;
+}
+
+cudaError_t launch_persist(const DevLayout& L, const PersistParams& p, int npairs, cudaStream_t s) {
+  auto* k = kr_persist_kernel;
+  const size_t smem = PersistCfg::smem_bytes(p.W);
+  if (cudaError_t e = set_smem(k, smem)) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * npairs));
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, L.tmap_half, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
-                     const uint16_t* P = nullptr, bool packed = false) {
-  const int slot = P ? real_slot(t) : field;
+                     const uint16_t* P = nullptr, bool packed = false, int* slot_used = nullptr) {
+  const bool persist = !P && !field && use_persist(t, B);
+  const int slot = P ? real_slot(t) : persist ? 4 : field;
+  if (slot_used) *slot_used = slot;
   if (hobo_status st = ensure_layout(t, slot)) return st;
   const DevLayout& L = t->lay[slot];
   if (hobo_status st = grow(t, t->d_Q, t->Q_cap, (size_t)B * L.n_ct)) return st;
@@ -635,6 +719,36 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     else
       launch_pack_x(X, B, t->host.N, t->W, t->d_bits, s);
     CK(cudaGetLastError());
+  }
+  if (persist) {
+    int npairs = 0;
+    if (hobo_status st = persist_items(t, L, B, npairs, s)) return st;
+    PersistParams q;
+    q.xbits = t->d_bits;
+    q.runs = t->d_runs;
+    q.kdesc = t->d_kdesc;
+    q.sched = L.d_sched;
+    q.p1 = t->d_p1;
+    q.Q = t->d_Q;
+    q.items = t->d_items;
+    q.B = B;
+    q.N = t->host.N;
+    q.W = t->W;
+    q.n_ct = L.n_ct;
+    q.n_cbp = (int)((B + 2 * kBM - 1) / (2 * kBM));
+    q.nseg = t->kl.nseg;
+    q.L = t->host.limbs;
+    q.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, 2 * kBK) / kBK);
+    q.exp = 0;
+    if (const char* e = getenv("HOBO_PERSIST_EXP")) q.exp = atoi(e);
+    if (t->profile) CK(cudaEventRecord(t->ev0, s));
+    CK(launch_persist(L, q, npairs, s));
+    if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+    t->last_launches = 2;
+    t->last_mma_macs = exec_macs(t, L, B);
+    t->last_i8 = 0;
+    t->last_algo_macs = algo_macs(t, false, B);
+    return HOBO_OK;
   }
   KrParams p = make_params(t, L, t->d_bits, B, G, t->d_Q);
   if (P) {
@@ -776,6 +890,10 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (t->d_sa_s) cudaFree(t->d_sa_s);
   if (t->d_sa_E) cudaFree(t->d_sa_E);
   if (t->d_srec) cudaFree(t->d_srec);
+  if (t->d_items) cudaFree(t->d_items);
+  if (t->d_sargs) cudaFree(t->d_sargs);
+  if (t->search_exec) cudaGraphExecDestroy(t->search_exec);
+  if (t->gs) cudaStreamDestroy(t->gs);
   void* ptrs[] = {t->d_tt, t->d_tt_meta, t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -826,8 +944,9 @@ hobo_status energy_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (B == 0) return empty_best(t, best, s);
-  if (hobo_status st = contract(t, 0, X, B, nullptr, s, nullptr, packed)) return st;
-  const DevLayout& L = t->lay[0];
+  int slot = 0;
+  if (hobo_status st = contract(t, 0, X, B, nullptr, s, nullptr, packed, &slot)) return st;
+  const DevLayout& L = t->lay[slot];
   CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
   finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
       t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
@@ -962,10 +1081,12 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
     CK(cudaStreamWaitEvent(s, t->ev_copied[slot], 0));
     float* Gc = field ? t->d_G + (gout ? (size_t)slot * chunk * N : 0) : nullptr;
     if (gout && i >= 2) CK(cudaStreamWaitEvent(s, t->ev_gfree[slot], 0));   // chunk i-2's fields are on the host
-    if (hobo_status st = contract(t, field, t->d_xh[slot], n, Gc, s, nullptr, packed)) return st;
+    int cslot = field;
+    if (hobo_status st = contract(t, field, t->d_xh[slot], n, Gc, s, nullptr, packed, &cslot)) return st;
     CK(cudaEventRecord(t->ev_free[slot], s));
+    const DevLayout& Lc = t->lay[cslot];
     finalize_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 4), 256, 0, s>>>(
-        t->d_Q, L.n_ct, n, L.lcm, row0 + off, t->d_Eh + off, best ? t->d_key : nullptr);
+        t->d_Q, Lc.n_ct, n, Lc.lcm, row0 + off, t->d_Eh + off, best ? t->d_key : nullptr);
     CK(cudaGetLastError());
     launches += t->last_launches + 1;
     if (gout) {
@@ -1042,21 +1163,57 @@ hobo_status run_search(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nc
     const double v = std::floor(4294967296.0 * p0 * std::pow(p1 / p0, (double)it / (double)std::max<int64_t>(1, iters - 1)));
     P[(size_t)it] = (uint32_t)std::min(4294967295.0, std::max(0.0, v));
   }
+  // device-side arguments: seed, chain0, then the P_t table two per word
+  std::vector<unsigned long long> args(2 + ((size_t)std::max<int64_t>(iters, 1) + 1) / 2, 0ull);
+  args[0] = seed;
+  args[1] = (unsigned long long)chain0;
+  std::memcpy(args.data() + 2, P.data(), P.size() * sizeof(uint32_t));
+  if (hobo_status st = grow(t, t->d_sargs, t->sargs_cap, args.size())) return st;
+  CK(cudaMemcpyAsync(t->d_sargs, args.data(), args.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   launches = 0;
   const unsigned g1 = (unsigned)std::min<long long>((B * W + 255) / 256, 148 * 16);
-  search_init_kernel<<<g1, 256, 0, s>>>(seed, chain0, B, N, W, t->d_bits, t->d_ebest);
-  CK(cudaGetLastError());
-  ++launches;
   KrParams p = make_params(t, L, t->d_bits, B, t->d_G, t->d_Q);   // n_split = 1: per-chain results never
   const unsigned gs = (unsigned)((B * 32 + 255) / 256);             // depend on the shard size
-  if (t->profile) CK(cudaEventRecord(t->ev0, s));
-  for (int64_t it = 0; it <= iters; ++it) {
-    CK(launch_kr_any(L, p, s));
-    const int move = it < iters;
-    search_step_kernel<<<gs, 256, 0, s>>>(t->d_Q, L.n_ct, L.lcm, t->d_G, t->d_bits, t->d_xbest, t->d_ebest, chain0, B,
-                                          N, W, seed, it, move ? P[(size_t)it] : 0u, move);
+  auto enqueue = [&](cudaStream_t q) -> hobo_status {
+    search_init_kernel<<<g1, 256, 0, q>>>(0, 0, B, N, W, t->d_bits, t->d_ebest, t->d_sargs);
     CK(cudaGetLastError());
-    launches += 2;
+    for (int64_t it = 0; it <= iters; ++it) {
+      CK(launch_kr_any(L, p, q));
+      const int move = it < iters;
+      search_step_kernel<<<gs, 256, 0, q>>>(t->d_Q, L.n_ct, L.lcm, t->d_G, t->d_bits, t->d_xbest, t->d_ebest, 0, B, N,
+                                            W, 0, it, 0u, move, 0, t->d_sargs);
+      CK(cudaGetLastError());
+    }
+    return HOBO_OK;
+  };
+  launches = 1 + 2 * (iters + 1);
+  if (t->profile) CK(cudaEventRecord(t->ev0, s));
+  const char* ge = getenv("HOBO_GRAPH");
+  if (ge && ge[0] == '0') {
+    if (hobo_status st = enqueue(s)) return st;
+  } else {
+    // one graph per (chains, iterations, buffers, kernel choice); HOBO_GRAPH=0 launches directly
+    const std::vector<uintptr_t> key = {(uintptr_t)B, (uintptr_t)iters, (uintptr_t)t->d_bits, (uintptr_t)t->d_G,
+                                        (uintptr_t)t->d_Q, (uintptr_t)t->d_xbest, (uintptr_t)t->d_ebest,
+                                        (uintptr_t)t->d_sargs, (uintptr_t)use_pairs(L, p), (uintptr_t)L.W};
+    if (!t->search_exec || key != t->search_key) {
+      // captured on a private stream (the caller's may be the legacy default stream, which
+      // cannot capture); nothing executes during capture, the launch below orders it on s
+      if (!t->gs) CK(cudaStreamCreateWithFlags(&t->gs, cudaStreamNonBlocking));
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(t->gs, cudaStreamCaptureModeRelaxed));
+      hobo_status st = enqueue(t->gs);
+      cudaError_t ce = cudaStreamEndCapture(t->gs, &g);
+      if (st) { if (g) cudaGraphDestroy(g); return st; }
+      CK(ce);
+      if (t->search_exec) cudaGraphExecDestroy(t->search_exec);
+      t->search_exec = nullptr;
+      cudaError_t ie = cudaGraphInstantiate(&t->search_exec, g, 0);
+      cudaGraphDestroy(g);
+      CK(ie);
+      t->search_key = key;
+    }
+    CK(cudaGraphLaunch(t->search_exec, s));
   }
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
   t->last_mma_macs = exec_macs(t, L, B) * (double)(iters + 1);

@@ -1191,8 +1191,11 @@ __global__ void unpack_bits_kernel(const uint32_t* __restrict__ bits, long long 
 }
 
 // chain c's initial x: bit m = bit (m & 63) of h(seed, 1, c, m >> 6)
+// dargs (nullable, a graph-replayable launch): {seed, chain0, P_0 | P_1 << 32, ...} in device
+// memory override the scalar seed / chain0 / P_t
 __global__ void search_init_kernel(uint64_t seed, long long chain0, long long nchains, int N, int W, uint32_t* bits,
-                                   float* ebest) {
+                                   float* ebest, const unsigned long long* __restrict__ dargs = nullptr) {
+  if (dargs) { seed = dargs[0]; chain0 = (long long)dargs[1]; }
   const long long total = nchains * W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long c = i / W;
@@ -1209,10 +1212,16 @@ __global__ void search_init_kernel(uint64_t seed, long long chain0, long long nc
 // one warp per chain: best tracking, flip gain, move rule, flip
 __global__ void search_step_kernel(const double* __restrict__ Q, int n_ct, double lcm, const float* __restrict__ G,
                                    uint32_t* bits, uint32_t* xbest, float* ebest, long long chain0, long long nchains,
-                                   int N, int W, uint64_t seed, long long t, uint32_t P_t, int do_move, int greedy = 0) {
+                                   int N, int W, uint64_t seed, long long t, uint32_t P_t, int do_move, int greedy = 0,
+                                   const unsigned long long* __restrict__ dargs = nullptr) {
   const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (c >= nchains) return;
+  if (dargs) {
+    seed = dargs[0];
+    chain0 = (long long)dargs[1];
+    if (do_move) P_t = reinterpret_cast<const uint32_t*>(dargs + 2)[t];
+  }
   const float e = combine_q(Q, n_ct, nchains, c, lcm);
   uint32_t* xb = bits + c * W;
   if (e < ebest[c]) {  // strict: on equal E the earliest iteration is kept

@@ -257,6 +257,23 @@ def test_search_replays_oracle_exactly(H, torch):
         assert np.array_equal(x, r["chain_xbest"][c - chain0])
 
 
+def test_search_graph_replay(H, torch):
+    """The search loop runs as one CUDA graph per (chains, iterations, buffers) with seed, chain0
+    and the P_t table in device memory: replays with other seeds / shards / schedules equal the
+    directly launched loop (HOBO_GRAPH=0) and the oracle."""
+    p = random_integer_problem(3, 40, 78, nterms=500)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    runs = [(9, 0, 200, 12, 0.5, 0.005), (10, 0, 200, 12, 0.5, 0.005), (11, 300, 200, 12, 0.3, 0.01),
+            (9, 0, 200, 12, 0.5, 0.005), (12, 7, 64, 3, 0.5, 0.005), (12, 7, 64, 3, 0.5, 0.005)]
+    for seed, c0, n, it, p0, p1 in runs:
+        x, e, c = t.search(seed, None, it, chain0=c0, nchains=n, p0=p0, p1=p1)
+        with env("HOBO_GRAPH", "0"):
+            x0, e0, c0_ = t.search(seed, None, it, chain0=c0, nchains=n, p0=p0, p1=p1)
+        r = o.search(seed, c0, n, it, p0, p1)
+        assert (e, c) == (e0, c0_) == (r["e_best"], r["best_chain"]) and np.array_equal(x, x0)
+        assert np.array_equal(x, r["chain_xbest"][c - c0])
+
+
 def test_search_shard_invariance(H, torch):
     p = seating(4)
     t = H.HoboTensor.from_problem(p)
@@ -339,6 +356,38 @@ def test_cfg3_fp32_companion_sampled(H, torch):
     assert np.array_equal(E[rows], f32(colex_energy(3, N, v, X[rows])))
     assert np.array_equal(G[rows], f32(colex_field(3, N, v, X[rows])))
     assert best == (E.min(), int(np.argmin(E)))
+
+
+# ---- the persistent energy kernel (persist.cuh): short K loops, double-buffered accumulators ----
+@pytest.mark.parametrize("case", ["int_qubo", "int_o3", "fp32_qubo"])
+def test_persistent_energy_kernel(H, torch, case):
+    """kr_persist_kernel (HOBO_PERSIST=1; the default for cfg2-like tiles) against the oracle and
+    against the per-tile kernel (HOBO_PERSIST=0), at batches giving odd candidate-block counts,
+    ragged blocks, fewer items than CTA pairs and several candidate blocks per pair."""
+    if case == "int_qubo":
+        idx, val = int_twin_cells(2, 300, 51)
+        t, o = H.HoboTensor.import_cells(2, 300, idx, val), Oracle.from_cells(2, 300, idx, val)
+    elif case == "int_o3":
+        p = random_integer_problem(3, 70, 52, nterms=900)
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    else:
+        idx, val = uniform_cells(2, 520, 53)
+        t, o = H.HoboTensor.import_cells(2, 520, idx, val), Oracle.from_cells(2, 520, idx, val)
+    for B in (1, 129, 300, 5000, 40000):
+        X = x_bits(54, B, t.N)
+        with env("HOBO_PERSIST", "1"):
+            E1, b1 = energies(H, torch, t, X, row0=3)
+        with env("HOBO_PERSIST", "0"):
+            E0, b0 = energies(H, torch, t, X, row0=3)
+        rows = np.arange(B) if B <= 5000 else sample_rows(B, 129)
+        Eo = o.energy(X[rows])
+        if t.is_integer:
+            assert np.array_equal(E1, E0) and b1 == b0, B
+            assert np.array_equal(E1[rows], Eo), B
+        else:
+            assert np.max(np.abs(E1[rows] - Eo)) <= o.tau, B
+            assert np.max(np.abs(E1 - E0)) <= 2 * o.tau, B
+        check_argmin(b1, E1, 0.0, row0=3)
 
 
 # ---- split-K (small batches) -----------------------------------------------------------------
