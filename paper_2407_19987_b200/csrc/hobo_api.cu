@@ -99,10 +99,12 @@ struct hobo_tensor {
   int srec_u4 = 0;          // uint4s per record (1 + the most runs of any pair)
   float* d_p1 = nullptr;   // padded to 256-multiples
   int W = 0;               // 32-bit words per candidate bit row
-  DevLayout lay[5];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
+  DevLayout lay[6];        // 0 = energy (strict), 1 = field (open index), 2 = field with 128-column
                            // tiles for the real-valued path (p rows + a deeper W ring in smem),
                            // 3 = bf16 field layout for the real-valued path when 1 holds int8 digits,
-                           // 4 = bf16 energy layout with 128-column tiles (the persistent kernel)
+                           // 4 = bf16 energy layout with 128-column tiles (the persistent kernel),
+                           // 5 = int8 energy layout with 64-column tiles (the int8 persistent kernel)
+  int* d_p1q = nullptr; int p1_int = -1;                // degree-1 cells on the digit grid (int8 persistent)
   int* d_items = nullptr; size_t items_cap = 0;          // persistent kernel: per-pair item ranges
   // the search loop as one CUDA graph per (chains, iterations, buffers); seed, chain0 and the
   // P_t table travel in d_sargs, so a replay needs one small copy and one graph launch
@@ -110,7 +112,7 @@ struct hobo_tensor {
   cudaGraphExec_t search_exec = nullptr;
   cudaStream_t gs = nullptr;                            // graph capture stream
   std::vector<uintptr_t> search_key;
-  long long items_B = -1;                               // ... computed for this batch
+  long long items_B = -1; int items_nct = 0;            // ... computed for this batch and tiling
   int dig = -1;            // int8 digit planes of slots 0/1 (0 = bf16 limbs; -1 = not decided yet)
   // scratch (grown on demand)
   uint32_t* d_bits = nullptr; size_t bits_cap = 0;
@@ -385,12 +387,13 @@ hobo_status init_device(hobo_tensor* t) {
 hobo_status ensure_layout(hobo_tensor* t, int slot) {
   DevLayout& L = t->lay[slot];
   if (L.built) return HOBO_OK;
-  const int field = (slot == 0 || slot == 4) ? 0 : 1;
+  const int field = (slot == 0 || slot == 4 || slot == 5) ? 0 : 1;
   const HostTensor& H = t->host;
   const int N = H.N, k = H.order;
-  L.i8 = slot <= 1 ? digit_planes(t) : 0;
+  L.i8 = slot <= 1 ? digit_planes(t) : slot == 5 ? H.digits : 0;
   L.NT = (N <= 128 || slot == 2 || slot == 4) ? 128 : 256;   // a 128-column tile when N fits (no padded columns)
   if (L.i8 >= 2) L.NT = 128;                    // TMEM: i8 accumulators of NT columns + the A stages
+  if (slot == 5) L.NT = PersistI8Cfg::NT;       // two accumulator sets of d x 64 columns
   L.qscale = std::ldexp(1.0, H.qexp);
   const int planes = L.i8 ? L.i8 : H.limbs;
   if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
@@ -398,7 +401,7 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   L.Npad = L.n_ct * L.NT;
   const int64_t Tpad = std::max<int64_t>(t->kl.Tpad, 2 * kBK);   // (a multiple of 2 K-blocks)
   const double bytes = (double)planes * L.Npad * Tpad * (L.i8 ? 1.0 : 2.0);
-  if (L.i8 && !t->d_srec) {
+  if (L.i8 && slot <= 1 && !t->d_srec) {
     // stage records: for K-block pair P, uint4 {runs of 2P, runs of 2P+1, nfix, 0} followed by
     // the pair's runs (contiguous in kl.runs), padded to the most runs of any pair; one TMA
     // bulk copy brings a stage's whole generator input (no dependent global loads)
@@ -548,7 +551,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.qscale = L.qscale;
   p.srec = t->d_srec;
   p.srec_u4 = L.i8 ? t->srec_u4 : 0;
-  p.field_mode = (&L == &t->lay[0] || &L == &t->lay[4]) ? 0 : 1;
+  p.field_mode = (&L == &t->lay[0] || &L == &t->lay[4] || &L == &t->lay[5]) ? 0 : 1;
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
   return p;
@@ -640,12 +643,21 @@ int real_slot(hobo_tensor* t) {
 // the persistent energy kernel (persist.cuh) for short K loops: energy mode on bf16 limbs whose
 // tiles have fewer than 64 K-blocks (QUBO-like, BASELINE config 2), with enough (candidate-block
 // pair, column tile) items to keep every SM pair busy.  HOBO_PERSIST=1 / =0 forces it on / off.
-bool use_persist(hobo_tensor* t, long long B) {
-  if (t->host.limbs > PersistCfg::MAXL || t->kl.nseg > 8) return false;
-  if (const char* e = getenv("HOBO_PERSIST")) return e[0] == '1';
-  if (digit_planes(t) || t->kl.Tpad / kBK >= 64) return false;
-  const long long items = (B + 2 * kBM - 1) / (2 * kBM) * ((t->host.N + 127) / 128);
-  return items >= 4 * 74;
+// Returns 0 (per-tile kr_gemm_kernel), 1 (bf16 limbs, kr_persist_kernel) or 2 (int8 digit
+// planes, kr_persist_i8_kernel: exact, half the MMA work and W bytes of 3 bf16 limbs, but its
+// 64-column tiles leave only 128 TMEM columns of A, whose refill loop then paces the MMAs:
+// measured slower at cfg2, 0.185 vs 0.163 ms, so opt-in).  HOBO_PERSIST=1 / =0 forces a
+// persistent kernel on / off, HOBO_PERSIST_I8=1 selects the int8 one when the cells allow.
+int use_persist(hobo_tensor* t, long long B) {
+  const HostTensor& H = t->host;
+  const bool i8_ok = H.digits >= 1 && H.digits <= PersistI8Cfg::MAXP && 255.0 * 32.0 * (double)t->kl.Tpad < 2147483648.0;
+  const char* ei = getenv("HOBO_PERSIST_I8");
+  const int kind = (i8_ok && ei && ei[0] == '1') ? 2 : (H.limbs <= PersistCfg::MAXL ? 1 : 0);
+  if (kind == 0 || t->kl.nseg > 8) return 0;
+  if (const char* e = getenv("HOBO_PERSIST")) return e[0] == '1' ? kind : 0;
+  if (digit_planes(t) || t->kl.Tpad / kBK >= 64) return 0;
+  const long long items = (B + 2 * kBM - 1) / (2 * kBM) * ((H.N + 127) / 128);
+  return items >= 4 * 74 ? kind : 0;
 }
 
 // contiguous item ranges of the persistent kernel, balanced by MMA work: item = candidate-block
@@ -655,7 +667,7 @@ hobo_status persist_items(hobo_tensor* t, const DevLayout& L, long long B, int& 
   const int n_cbp = (int)((B + 2 * kBM - 1) / (2 * kBM));
   const long long nitems = (long long)n_cbp * L.n_ct;
   npairs = (int)std::min<long long>(74, nitems);
-  if (t->items_B == B) return HOBO_OK;
+  if (t->items_B == B && t->items_nct == L.n_ct) return HOBO_OK;
   std::vector<double> w(L.n_ct);
   double per_block = 0;
   for (int k = 0; k < L.n_ct; ++k) {
@@ -678,12 +690,12 @@ hobo_status persist_items(hobo_tensor* t, const DevLayout& L, long long B, int& 
   if (hobo_status st = grow(t, t->d_items, t->items_cap, items.size())) return st;
   CK(cudaMemcpy(t->d_items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
   t->items_B = B;
+  t->items_nct = L.n_ct;
   return HOBO_OK;
 }
 
-cudaError_t launch_persist(const DevLayout& L, const PersistParams& p, int npairs, cudaStream_t s) {
-  auto* k = kr_persist_kernel;
-  const size_t smem = PersistCfg::smem_bytes(p.W);
+template <class K, class Params>
+cudaError_t launch_persist(K* k, size_t smem, const DevLayout& L, const Params& p, int npairs, cudaStream_t s) {
   if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * npairs));
@@ -704,8 +716,9 @@ cudaError_t launch_persist(const DevLayout& L, const PersistParams& p, int npair
 
 hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
                      const uint16_t* P = nullptr, bool packed = false, int* slot_used = nullptr) {
-  const bool persist = !P && !field && use_persist(t, B);
-  const int slot = P ? real_slot(t) : persist ? 4 : field;
+  const int pk = (!P && !field) ? use_persist(t, B) : 0;
+  const bool persist = pk != 0;
+  const int slot = P ? real_slot(t) : pk == 2 ? 5 : pk == 1 ? 4 : field;
   if (slot_used) *slot_used = slot;
   if (hobo_status st = ensure_layout(t, slot)) return st;
   const DevLayout& L = t->lay[slot];
@@ -719,6 +732,53 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     else
       launch_pack_x(X, B, t->host.N, t->W, t->d_bits, s);
     CK(cudaGetLastError());
+  }
+  if (pk == 2) {
+    int npairs = 0;
+    if (hobo_status st = persist_items(t, L, B, npairs, s)) return st;
+    if (t->p1_int < 0) {   // the degree-1 cells as integers on the digit grid, when they all are
+      const int Npad = (t->host.N + 255) / 256 * 256;
+      std::vector<int> q1(Npad, 0);
+      int ok = 1;
+      for (int m = 0; m < t->host.N && ok; ++m) {
+        const double v = std::ldexp((double)t->host.strict[1][m], -t->host.qexp);
+        if (v != std::floor(v) || std::fabs(v) >= 16777216.0) ok = 0;
+        else q1[m] = (int)v;
+      }
+      if (ok) {
+        CK(cudaMalloc(&t->d_p1q, Npad * sizeof(int)));
+        CK(cudaMemcpy(t->d_p1q, q1.data(), Npad * sizeof(int), cudaMemcpyHostToDevice));
+      }
+      t->p1_int = ok;
+    }
+    PersistI8Params q;
+    q.xbits = t->d_bits;
+    q.runs = t->d_runs;
+    q.kdesc = t->d_kdesc;
+    q.sched = L.d_sched;
+    q.p1 = t->d_p1;
+    q.p1q = t->d_p1q;
+    q.p1_int = t->p1_int;
+    q.qscale = L.qscale;
+    q.Q = t->d_Q;
+    q.items = t->d_items;
+    q.B = B;
+    q.N = t->host.N;
+    q.W = t->W;
+    q.n_ct = L.n_ct;
+    q.nseg = t->kl.nseg;
+    q.P = L.i8;
+    q.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, 2 * kBK) / kBK);
+    q.exp = 0;
+    if (const char* e = getenv("HOBO_PERSIST_EXP")) q.exp = atoi(e);
+    if (t->profile) CK(cudaEventRecord(t->ev0, s));
+    CK(launch_persist(kr_persist_i8_kernel, PersistI8Cfg::smem_bytes(q.W), L, q, npairs, s));
+    if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+    t->last_launches = 2;
+    t->last_mma_macs = exec_macs(t, L, B);
+    t->last_i8 = L.i8;
+    t->last_algo_macs = algo_macs(t, false, B);
+    return HOBO_OK;
   }
   if (persist) {
     int npairs = 0;
@@ -742,7 +802,9 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     q.exp = 0;
     if (const char* e = getenv("HOBO_PERSIST_EXP")) q.exp = atoi(e);
     if (t->profile) CK(cudaEventRecord(t->ev0, s));
-    CK(launch_persist(L, q, npairs, s));
+    const char* ek = getenv("HOBO_PERSIST_KPS");   // A/B of the stage size
+    if (ek && ek[0] == '2') CK(launch_persist(kr_persist_kernel<2>, PersistCfgT<2>::smem_bytes(q.W), L, q, npairs, s));
+    else CK(launch_persist(kr_persist_kernel<1>, PersistCfgT<1>::smem_bytes(q.W), L, q, npairs, s));
     if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
     t->last_launches = 2;
     t->last_mma_macs = exec_macs(t, L, B);
@@ -891,6 +953,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (t->d_sa_E) cudaFree(t->d_sa_E);
   if (t->d_srec) cudaFree(t->d_srec);
   if (t->d_items) cudaFree(t->d_items);
+  if (t->d_p1q) cudaFree(t->d_p1q);
   if (t->d_sargs) cudaFree(t->d_sargs);
   if (t->search_exec) cudaGraphExecDestroy(t->search_exec);
   if (t->gs) cudaStreamDestroy(t->gs);

@@ -3,6 +3,7 @@ into profiles/: a markdown table plus a JSON with the numbers bench.py's rooflin
 
   python tools/ncu_summary.py gpurun_out/launches_r1.csv gpurun_out/prof_r1.ncu-rep profiles/r01
   python tools/ncu_summary.py --capture gpurun_out/sa.ncu-rep profiles/r01_sa "what was captured"
+  python tools/ncu_summary.py --bench gpurun_out/launches_cfg3.csv gpurun_out/cfg3.ncu-rep cfg3 65536
 """
 import csv
 import io
@@ -78,7 +79,38 @@ def capture_only(rep, prefix, what):
     print(json.dumps(F, indent=1))
 
 
+def bench_capture(launches, rep, name, batch):
+    """profiles/r02/<name>_ncu_full.{json,md}: the capture bench.py cites for roofline.traffic
+    (its batch, capture date and the commit it was taken at)."""
+    import datetime
+    import os
+    F = full_capture(rep)
+    traffic = F.get("dram_read", 0.0) + F.get("dram_write", 0.0)
+    commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True).stdout.strip()
+    date = datetime.datetime.fromtimestamp(os.path.getmtime(rep)).strftime("%Y-%m-%d %H:%M")
+    L = launch_shares(launches) if launches != "-" else []
+    out = {"config": name, "batch": int(batch), "captured": date, "commit": commit, "traffic_bytes_per_launch": traffic,
+           "top_kernel_full": F, "launch_list": L, "source": {"launches": launches, "capture": rep}}
+    prefix = os.path.join("profiles", "r02", f"{name}_ncu_full")
+    json.dump(out, open(prefix + ".json", "w"), indent=1)
+    with open(prefix + ".md", "w") as f:
+        f.write(f"# ncu: {name} (B = {batch}), captured {date} at commit {commit}\n\n")
+        if L:
+            f.write("## Launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)\n\n")
+            f.write("| kernel | launches | avg us | share |\n|---|---|---|---|\n")
+            for r in L:
+                f.write(f"| `{r['kernel']}` | {r['launches']} | {r['avg_us']:.1f} | {r['share']*100:.2f}% |\n")
+        f.write("\n## Contraction kernel, --set full\n\n| metric | value |\n|---|---|\n")
+        for k, v in F.items():
+            f.write(f"| {k} | {v:.6g} |\n" if isinstance(v, float) else f"| {k} | {v} |\n")
+        f.write(f"| traffic = dram read + write (bytes/launch) | {traffic:.6g} |\n")
+    print(prefix, "traffic", traffic)
+
+
 def main():
+    if sys.argv[1] == "--bench":
+        bench_capture(*sys.argv[2:6])
+        return
     if sys.argv[1] == "--capture":
         capture_only(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "")
         return
