@@ -295,9 +295,10 @@ hobo_status hobo_best_key(float e, int64_t idx, uint64_t* key);
 hobo_status hobo_best_from_key(uint64_t key, hobo_best* best);
 
 /* Launch statistics of the last call on this handle: number of kernel launches issued,
- * the executed tensor-core MACs of its contraction kernel(s), the algorithmic MACs
- * (DESIGN.md "Roofline"), and — when profiling is on — the CUDA-event time in ms of its
- * contraction kernel(s), recorded on the launch stream (this call synchronises on it).  */
+ * the executed tensor-core MACs of its contraction kernel(s), the algorithmic MACs (SURVEY
+ * 8(d): nnz per candidate for energies, 2 nnz for energy + field, nnz = sum_{r<=k} C(N, r)),
+ * and — when profiling is on — the CUDA-event time in ms of its contraction kernel(s),
+ * recorded on the launch stream (this call synchronises on it).  */
 hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mma_macs,
                                    double* algo_macs, double* kernel_ms);
 /* The MMA kind of the last call's contraction: *i8_planes = the number of int8 digit planes

@@ -111,6 +111,10 @@ struct hobo_tensor {
   unsigned long long* d_sargs = nullptr; size_t sargs_cap = 0;
   cudaGraphExec_t search_exec = nullptr;
   cudaStream_t gs = nullptr;                            // graph capture stream
+  // energy / field calls: one CUDA graph (stage X, contraction, split-K reduce, argmin) per
+  // (mode, input format, batch, buffers, kernel choice); replayed when the same call repeats
+  cudaGraphExec_t call_exec[2] = {nullptr, nullptr};
+  std::vector<uintptr_t> call_key[2];
   std::vector<uintptr_t> search_key;
   long long items_B = -1; int items_nct = 0;            // ... computed for this batch and tiling
   int dig = -1;            // int8 digit planes of slots 0/1 (0 = bf16 limbs; -1 = not decided yet)
@@ -118,6 +122,7 @@ struct hobo_tensor {
   uint32_t* d_bits = nullptr; size_t bits_cap = 0;
   double* d_Q = nullptr; size_t Q_cap = 0;
   unsigned long long* d_key = nullptr;
+  unsigned long long* h_key = nullptr;                  // page-locked readback of the key
   float* d_G = nullptr; size_t G_cap = 0;
   uint32_t* d_xbest = nullptr; size_t xbest_cap = 0;
   float* d_ebest = nullptr; size_t ebest_cap = 0;
@@ -205,6 +210,15 @@ cudaError_t set_smem(K* k, size_t smem) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) have = smem;
   return e;
+}
+
+// profiling event around a contraction kernel; inside a stream capture it becomes an
+// external event-record node of the graph, so the replayed graph still times the kernel
+cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaError_t e = cudaStreamIsCapturing(s, &cs)) return e;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(ev, s);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -580,10 +594,13 @@ double exec_macs(hobo_tensor* t, const DevLayout& L, long long B) {
   return kb * kBK * (double)L.NT * kBM * (double)((B + kBM - 1) / kBM) * (L.i8 ? L.i8 : t->host.limbs);
 }
 
+// SURVEY 8(d)'s algorithmic work: nnz MACs (2 nnz flops) per candidate for the energy, 2 nnz
+// MACs (4 nnz flops) for energy + field, nnz = sum_{r<=k} C(N, r) canonical cells.  (The
+// open-index GEMM executes sum_r r C(N, r) MACs per candidate in field mode: exec_macs.)
 double algo_macs(hobo_tensor* t, bool field, long long B) {
   double s = 0;
-  for (int r = 1; r <= t->host.order; ++r) s += (field ? r : 1) * (double)binom(t->host.N, r);
-  return s * (double)B;
+  for (int r = 1; r <= t->host.order; ++r) s += (double)binom(t->host.N, r);
+  return (field ? 2.0 : 1.0) * s * (double)B;
 }
 
 // C1: the global lexicographic (E, idx) minimum over ranks, on the compute stream
@@ -594,12 +611,24 @@ hobo_status key_allreduce(hobo_tensor* t, cudaStream_t s) {
   return HOBO_OK;
 }
 
+// the 16-byte key to the host through a page-locked buffer (a pageable destination makes the
+// driver stage the copy synchronously), then wait for the stream
+cudaError_t read_key(hobo_tensor* t, unsigned long long (&key)[2], cudaStream_t s) {
+  if (!t->h_key)
+    if (cudaError_t e = cudaMallocHost(&t->h_key, 2 * sizeof(unsigned long long))) return e;
+  if (cudaError_t e = cudaMemcpyAsync(t->h_key, t->d_key, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s))
+    return e;
+  if (cudaError_t e = cudaStreamSynchronize(s)) return e;
+  key[0] = t->h_key[0];
+  key[1] = t->h_key[1];
+  return cudaSuccess;
+}
+
 // the argmin key (device) -> host best, after the multi-GPU combine when one is active
 hobo_status finish_best(hobo_tensor* t, hobo_best* best, cudaStream_t s) {
   if (hobo_status st = key_allreduce(t, s)) return st;
   unsigned long long key[2] = {0, 0};
-  CK(cudaMemcpyAsync(key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(read_key(t, key, s));
   if (key[1] != ~0ull) return fail(HOBO_ERANGE, "a candidate's energy is NaN (the argmin rejects NaN)");
   return hobo_best_from_key(key[0], best);
 }
@@ -771,9 +800,9 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     q.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, 2 * kBK) / kBK);
     q.exp = 0;
     if (const char* e = getenv("HOBO_PERSIST_EXP")) q.exp = atoi(e);
-    if (t->profile) CK(cudaEventRecord(t->ev0, s));
+    if (t->profile) CK(record_event(t->ev0, s));
     CK(launch_persist(kr_persist_i8_kernel, PersistI8Cfg::smem_bytes(q.W), L, q, npairs, s));
-    if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+    if (t->profile) { CK(record_event(t->ev1, s)); t->ev_valid = true; }
     t->last_launches = 2;
     t->last_mma_macs = exec_macs(t, L, B);
     t->last_i8 = L.i8;
@@ -801,11 +830,11 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     q.n_kb = (int)(std::max<int64_t>(t->kl.Tpad, 2 * kBK) / kBK);
     q.exp = 0;
     if (const char* e = getenv("HOBO_PERSIST_EXP")) q.exp = atoi(e);
-    if (t->profile) CK(cudaEventRecord(t->ev0, s));
+    if (t->profile) CK(record_event(t->ev0, s));
     const char* ek = getenv("HOBO_PERSIST_KPS");   // A/B of the stage size
     if (ek && ek[0] == '2') CK(launch_persist(kr_persist_kernel<2>, PersistCfgT<2>::smem_bytes(q.W), L, q, npairs, s));
     else CK(launch_persist(kr_persist_kernel<1>, PersistCfgT<1>::smem_bytes(q.W), L, q, npairs, s));
-    if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+    if (t->profile) { CK(record_event(t->ev1, s)); t->ev_valid = true; }
     t->last_launches = 2;
     t->last_mma_macs = exec_macs(t, L, B);
     t->last_i8 = 0;
@@ -836,9 +865,9 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     if (hobo_status st = grow(t, t->d_Qpart, t->Qpart_cap, (size_t)p.n_split * L.n_ct * B)) return st;
     p.Q = t->d_Qpart;
   }
-  if (t->profile) CK(cudaEventRecord(t->ev0, s));
+  if (t->profile) CK(record_event(t->ev0, s));
   CK(launch_kr_any(L, p, s));
-  if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
+  if (t->profile) { CK(record_event(t->ev1, s)); t->ev_valid = true; }
   t->last_launches = P ? 1 : 2;
   if (p.n_split > 1) {
     const long long nG = field ? B * t->host.N : 0, nQ = (long long)L.n_ct * B;
@@ -955,7 +984,10 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (t->d_items) cudaFree(t->d_items);
   if (t->d_p1q) cudaFree(t->d_p1q);
   if (t->d_sargs) cudaFree(t->d_sargs);
+  if (t->h_key) cudaFreeHost(t->h_key);
   if (t->search_exec) cudaGraphExecDestroy(t->search_exec);
+  for (auto& e : t->call_exec)
+    if (e) cudaGraphExecDestroy(e);
   if (t->gs) cudaStreamDestroy(t->gs);
   void* ptrs[] = {t->d_tt, t->d_tt_meta, t->d_theta, t->d_P, t->d_k1, t->d_k2, t->d_flag, t->d_starts, t->d_Gpart, t->d_Qpart, t->d_runs, t->d_kdesc, t->d_runoff, t->d_p1, t->d_bits, t->d_Q, t->d_key, t->d_G, t->d_xbest, t->d_ebest};
   for (void* p : ptrs)
@@ -999,6 +1031,76 @@ hobo_status hobo_tensor_export_dense(const hobo_tensor* t, float* host_out) {
 }  // extern "C"
 
 namespace {
+// the device part of an energy (field = 0) or field (field = 1) call: stage X, contraction,
+// split-K reduce, argmin; the multi-GPU combine and the readback follow in finish_best
+hobo_status enqueue_call(hobo_tensor* t, int field, const uint8_t* X, bool packed, int64_t B, int64_t row0, float* G,
+                         float* E, bool best, cudaStream_t s) {
+  int slot = field;
+  if (hobo_status st = contract(t, field, X, B, G, s, nullptr, packed, &slot)) return st;
+  if (E || best) {
+    const DevLayout& L = t->lay[slot];
+    if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
+    finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
+        t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
+    CK(cudaGetLastError());
+    t->last_launches += 1;
+  }
+  return HOBO_OK;
+}
+
+// what a captured call depends on besides its arguments: the scratch buffers it wrote and the
+// kernel choices read from the environment (a change re-captures)
+std::vector<uintptr_t> call_key(hobo_tensor* t, int field, const uint8_t* X, bool packed, int64_t B, int64_t row0,
+                                const float* G, const float* E, bool best) {
+  std::vector<uintptr_t> k = {(uintptr_t)field, (uintptr_t)packed, (uintptr_t)B, (uintptr_t)row0, (uintptr_t)X,
+                              (uintptr_t)G, (uintptr_t)E, (uintptr_t)best, (uintptr_t)t->profile,
+                              (uintptr_t)t->d_bits, (uintptr_t)t->d_Q, (uintptr_t)t->d_Gpart, (uintptr_t)t->d_Qpart,
+                              (uintptr_t)t->d_items, (uintptr_t)t->d_key, (uintptr_t)t->items_B};
+  for (const char* v : {"HOBO_PAIR", "HOBO_I8", "HOBO_CT_DESC", "HOBO_CB_ITERS", "HOBO_PERSIST", "HOBO_PERSIST_I8",
+                        "HOBO_PERSIST_KPS", "HOBO_PERSIST_EXP"}) {
+    const char* e = getenv(v);
+    k.push_back(e ? (uintptr_t)(unsigned char)e[0] + 1 : 0);
+  }
+  for (auto& L : t->lay) k.push_back((uintptr_t)L.W);
+  return k;
+}
+
+// energy / field call: replay the captured graph when the same call repeats (HOBO_GRAPH=0:
+// launch directly every time); a new call runs directly, then is captured for the next time
+hobo_status run_call(hobo_tensor* t, int field, const uint8_t* X, bool packed, int64_t B, int64_t row0, float* G,
+                     float* E, hobo_best* best, cudaStream_t s) {
+  const char* ge = getenv("HOBO_GRAPH");
+  const bool graphs = !(ge && ge[0] == '0');
+  std::vector<uintptr_t> key = call_key(t, field, X, packed, B, row0, G, E, best != nullptr);
+  if (graphs && t->call_exec[field] && key == t->call_key[field]) {
+    CK(cudaGraphLaunch(t->call_exec[field], s));
+    if (t->profile) t->ev_valid = true;
+  } else {
+    if (hobo_status st = enqueue_call(t, field, X, packed, B, row0, G, E, best != nullptr, s)) return st;
+    key = call_key(t, field, X, packed, B, row0, G, E, best != nullptr);   // the buffers it grew
+    if (graphs) {
+      if (!t->gs) CK(cudaStreamCreateWithFlags(&t->gs, cudaStreamNonBlocking));
+      const int64_t launches = t->last_launches;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(t->gs, cudaStreamCaptureModeRelaxed));
+      hobo_status st = enqueue_call(t, field, X, packed, B, row0, G, E, best != nullptr, t->gs);
+      cudaError_t ce = cudaStreamEndCapture(t->gs, &g);
+      if (st) { if (g) cudaGraphDestroy(g); return st; }
+      CK(ce);
+      if (t->call_exec[field]) cudaGraphExecDestroy(t->call_exec[field]);
+      t->call_exec[field] = nullptr;
+      cudaError_t ie = cudaGraphInstantiate(&t->call_exec[field], g, 0);
+      cudaGraphDestroy(g);
+      CK(ie);
+      t->call_key[field] = key;
+      t->last_launches = launches;
+    }
+  }
+  if (best)
+    if (hobo_status st = finish_best(t, best, s)) return st;
+  return HOBO_OK;
+}
+
 hobo_status energy_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B, int64_t row0, float* E,
                         hobo_best* best, void* stream) {
   if (!t) return fail(HOBO_EINVAL, "null handle");
@@ -1007,17 +1109,7 @@ hobo_status energy_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (B == 0) return empty_best(t, best, s);
-  int slot = 0;
-  if (hobo_status st = contract(t, 0, X, B, nullptr, s, nullptr, packed, &slot)) return st;
-  const DevLayout& L = t->lay[slot];
-  CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
-  finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
-      t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
-  CK(cudaGetLastError());
-  t->last_launches += 1;
-  if (best)
-    if (hobo_status st = finish_best(t, best, s)) return st;
-  return HOBO_OK;
+  return run_call(t, 0, X, packed, B, row0, nullptr, E, best, s);
 }
 
 hobo_status field_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B, int64_t row0, float* G, float* E,
@@ -1028,18 +1120,7 @@ hobo_status field_impl(hobo_tensor* t, const uint8_t* X, bool packed, int64_t B,
   if (hobo_status st = check_device(t)) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (B == 0) return empty_best(t, best, s);
-  if (hobo_status st = contract(t, 1, X, B, G, s, nullptr, packed)) return st;
-  if (E || best) {
-    const DevLayout& L = t->lay[1];
-    if (best) CK(cudaMemsetAsync(t->d_key, 0xFF, 2 * sizeof(unsigned long long), s));
-    finalize_kernel<<<(unsigned)std::min<long long>((B + 255) / 256, 148 * 4), 256, 0, s>>>(
-        t->d_Q, L.n_ct, B, L.lcm, row0, E, best ? t->d_key : nullptr);
-    CK(cudaGetLastError());
-    t->last_launches += 1;
-  }
-  if (best)
-    if (hobo_status st = finish_best(t, best, s)) return st;
-  return HOBO_OK;
+  return run_call(t, 1, X, packed, B, row0, G, E, best, s);
 }
 }  // namespace
 
@@ -1320,8 +1401,7 @@ hobo_status hobo_search_shard(hobo_tensor* t, uint64_t seed, int64_t chain0, int
   CK(cudaGetLastError());
   ++launches;
   unsigned long long key[2] = {0, 0};
-  CK(cudaMemcpyAsync(key, t->d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(read_key(t, key, s));
   if (key[1] != ~0ull) return fail(HOBO_ERANGE, "a chain's energy is NaN (the argmin rejects NaN)");
   hobo_best b;
   hobo_best_from_key(key[0], &b);

@@ -274,6 +274,44 @@ def test_search_graph_replay(H, torch):
         assert np.array_equal(x, r["chain_xbest"][c - c0])
 
 
+@pytest.mark.parametrize("case", ["cfg3_small", "qubo_persist", "splitk"])
+def test_call_graph_replay(H, torch, case):
+    """Energy / field calls replay a captured CUDA graph when the same call repeats (same
+    buffers and batch): new candidate contents in the same buffers, profiling on and off, the
+    per-tile, persistent and split-K paths -- all equal to direct launches (HOBO_GRAPH=0) and
+    to the oracle."""
+    if case == "cfg3_small":
+        p = cfg3_problem()
+        t, o, B = H.HoboTensor.from_problem(p), Oracle.from_problem(p), 3000
+    elif case == "qubo_persist":
+        idx, val = int_twin_cells(2, 1024, 61)
+        t, o, B = H.HoboTensor.import_cells(2, 1024, idx, val), Oracle.from_cells(2, 1024, idx, val), 20000
+    else:
+        p = random_integer_problem(3, 200, 62, nterms=800)
+        t, o, B = H.HoboTensor.from_problem(p), Oracle.from_problem(p), 40
+    Xd = torch.empty(B, t.N, dtype=torch.uint8, device="cuda")
+    G = torch.empty(B, t.N, dtype=torch.float32, device="cuda")
+    E = torch.empty(B, dtype=torch.float32, device="cuda")
+    for rep, seed in enumerate((71, 72, 73, 71)):
+        X = x_bits(seed, B, t.N)
+        Xd.copy_(torch.from_numpy(X))
+        t.set_profiling(rep == 2)
+        _, be = t.energy(Xd, E, row0=5)
+        Ee = E.cpu().numpy().astype(np.float64)
+        t.local_field(Xd, G, E, row0=5)
+        Gf, Ef = G.cpu().numpy().astype(np.float64), E.cpu().numpy().astype(np.float64)
+        if rep == 2:
+            assert t.launch_stats()["kernel_ms"] > 0
+        with env("HOBO_GRAPH", "0"):
+            E0, b0 = t.energy(Xd, row0=5)
+            G0, E1 = t.local_field(Xd, row0=5)
+        assert np.array_equal(Ee, E0.cpu().numpy()) and be == b0
+        assert np.array_equal(Gf, G0.cpu().numpy()) and np.array_equal(Ef, E1.cpu().numpy())
+        rows = sample_rows(B, 37, 40)
+        assert np.array_equal(Ee[rows], o.energy(X[rows])) and np.array_equal(Gf[rows], o.field(X[rows]))
+    t.set_profiling(False)
+
+
 def test_search_shard_invariance(H, torch):
     p = seating(4)
     t = H.HoboTensor.from_problem(p)
