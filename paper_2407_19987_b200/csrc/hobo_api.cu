@@ -432,8 +432,21 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
       r[0] = b - a;
       r[1] = c - b;
       r[2] = kl.kdesc[(size_t)(2 * P) * 8 + 3] & 7u;   // nfix (a pair never spans two segments)
-      for (uint32_t i = a; i < c; ++i)
-        for (int f = 0; f < 4; ++f) r[4 * (1 + i - a) + f] = kl.runs[(size_t)i * 4 + f];
+      for (uint32_t i = a; i < c; ++i) {
+        // run (start, cnt, lo, fixed ids) -> the precomputed form run_bits8 reads (kernels.cuh):
+        // output bits [start, start + cnt) of the K-block = x bits lo .. lo + cnt, i.e. the
+        // 64-bit window at s = lo - start + 64 counted from two zero words in front of the row
+        const uint32_t* q = &kl.runs[(size_t)i * 4];
+        const uint32_t start = q[0] & 0xFFu, cnt = (q[0] >> 8) & 0xFFu, lo = q[0] >> 16;
+        const uint64_t mask = (cnt >= 64 ? ~0ull : ((1ull << cnt) - 1ull)) << start;
+        const uint32_t sw = lo + 64u - start;
+        const uint32_t f0 = q[1] & 1023u, f1 = (q[1] >> 16) & 1023u, f2 = q[2] & 1023u, f3 = (q[2] >> 16) & 1023u;
+        uint32_t* o = &r[4 * (1 + i - a)];
+        o[0] = (uint32_t)mask;
+        o[1] = (uint32_t)(mask >> 32);
+        o[2] = (sw >> 5) | ((sw & 31u) << 6) | (f0 << 11) | (f1 << 21);
+        o[3] = f2 | (f3 << 10);
+      }
     }
     CK(cudaMalloc(&t->d_srec, rec.size() * 4));
     CK(cudaMemcpy(t->d_srec, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice));

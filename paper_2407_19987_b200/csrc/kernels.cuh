@@ -88,7 +88,8 @@ struct KrCfg {
   // I8: the descriptor ring holds the stages' run records (srec_u4 uint4s per slot)
   __host__ __device__ static size_t desc_bytes(int srec_u4) { return I8 ? (size_t)MAXD * srec_u4 * 16 : DESC_BYTES; }
   static size_t smem_bytes(int W, int srec_u4 = 0) {
-    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + desc_bytes(srec_u4) + (size_t)(W + 2) * kBM * 4 + 128;
+    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + desc_bytes(srec_u4) +
+           (size_t)(W + (I8 ? 4 : 2)) * kBM * 4 + 128;   // I8: two zero words in front (run_bits8)
   }
   // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages.  Two
   // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
@@ -163,6 +164,38 @@ __device__ __forceinline__ void expand32(uint32_t half, uint32_t (&w)[16]) {
       w[4 * k + sh] = prmt_b32(ev, od, sel) & 0x3F803F80u;
     }
   }
+}
+
+// int8 A bytes {0, 1} of a 64-tuple K-block from its 64 bits, 16 words.  The int8 planes store
+// the K positions of each 32-tuple group permuted (layout_kernel: tuple 8i + k of the group at
+// byte 4k + i), so word k of a group is bit k of each byte of the group's 32 bits: one shift
+// and one AND per word (a natural order needs the 4-op nibble spread)
+__device__ __forceinline__ void expand_bytes64(uint64_t bits, uint32_t (&w)[16]) {
+  const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    w[k] = (lo >> k) & 0x01010101u;
+    w[8 + k] = (hi >> k) & 0x01010101u;
+  }
+}
+
+// the int8 path's generator runs, precomputed on the host (hobo_api.cu, the stage records):
+// x, y = the 64-bit output mask ((1 << cnt) - 1) << start; z = window word | shift << 6 |
+// fixed0 << 11 | fixed1 << 21; w = fixed2 | fixed3 << 10 (10-bit variable ids).  The 64 output
+// bits are x bits [s, s + 64) of the row, s = 32 word + shift, counted from two zero words in
+// front of the row (xs2 = xs - 2 kBM), so no per-run mask or 64-bit shift is computed here.
+__device__ __forceinline__ void run_bits8(const uint32_t* xs, const uint32_t* xs2, int row, const uint4 rr,
+                                          uint32_t nfix, uint32_t& lo, uint32_t& hi) {
+  uint32_t on = 1;
+  const uint32_t f[4] = {(rr.z >> 11) & 1023u, (rr.z >> 21) & 1023u, rr.w & 1023u, (rr.w >> 10) & 1023u};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if ((uint32_t)q < nfix) on &= xs[(f[q] >> 5) * kBM + row] >> (f[q] & 31);
+  const uint32_t wi = rr.z & 63u, sh = (rr.z >> 6) & 31u;
+  const uint32_t w0 = xs2[wi * kBM + row], w1 = xs2[(wi + 1) * kBM + row], w2 = xs2[(wi + 2) * kBM + row];
+  const uint32_t m = 0u - (on & 1u);
+  lo |= __funnelshift_r(w0, w1, sh) & rr.x & m;
+  hi |= __funnelshift_r(w1, w2, sh) & rr.y & m;
 }
 
 // counter-based RNG of SURVEY 8(d): h(s,a,b,c) = sm(sm(sm(s^a)^b)^c)
@@ -272,8 +305,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t tslot = acc_full + 32;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
   const uint32_t sD = sQ + kBM * 8;                               // I8: descriptor ring (one slot per W stage)
-  const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4);
+  const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4) + (I8 ? 2u * kBM * 4u : 0u);
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
+  if constexpr (I8) {   // the two zero words in front of every row (run_bits8's window)
+    for (int i = threadIdx.x; i < 2 * kBM; i += kThreads) xs[i - 2 * kBM] = 0u;
+  }
   uint16_t* prow = reinterpret_cast<uint16_t*>(gbase + (sX - base));   // REAL: p rows [128][pstride]
   double* qpart = reinterpret_cast<double*>(gbase + (sQ - base));
   volatile uint32_t* tslot_g = reinterpret_cast<volatile uint32_t*>(gbase + (tslot - base));
@@ -730,14 +766,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             mbar_wait(DFULL(wst), wph);
             const uint4* rec = dsm + (size_t)wst * p.srec_u4;
             const uint4 hd = rec[0];
-            uint64_t b0 = 0ull, b1 = 0ull;
-            for (uint32_t i = 0; i < hd.x; ++i) b0 |= run_bits(xs, row, rec[1 + i], hd.z);
-            for (uint32_t i = 0; i < hd.y; ++i) b1 |= run_bits(xs, row, rec[1 + hd.x + i], hd.z);
-            uint32_t w[32];   // byte t of the K-block = bit t (nibble * 0x204081 spreads 4 bits)
-#pragma unroll
-            for (int c = 0; c < 16; ++c) w[c] = (((uint32_t)(b0 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) w[16 + c] = (((uint32_t)(b1 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+            uint32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+            for (uint32_t i = 0; i < hd.x; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + i], hd.z, l0, h0);
+            for (uint32_t i = 0; i < hd.y; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], hd.z, l1, h1);
+            uint32_t w[32];   // the K-block pair's bytes in the planes' permuted K order
+            expand_bytes64(((uint64_t)h0 << 32) | l0, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+            expand_bytes64(((uint64_t)h1 << 32) | l1, *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
             mbar_wait(EMPTYA(gst), gph ^ 1u);
             tc_fence_after();
             tmem_st32(lane_base + (uint32_t)(p.L * NT + gst * KPS * C::A_COLS), w);
@@ -1137,7 +1171,10 @@ __global__ void layout_kernel(const LayoutParams lp) {
       const long long q = __double2ll_rn((double)c * lp.inv_qscale);
       const size_t plane = (size_t)lp.Npad * lp.Tpad;
       const long long n_kbp = lp.Tpad / 128;   // boxes of 128-byte rows: K-block pairs
-      const size_t off = ((size_t)((m / lp.NT) * n_kbp + t / 128) * lp.NT + (m % lp.NT)) * 128 + (t % 128);
+      // K position of tuple t in its 128-byte row: within each 32-tuple group, tuple 8i + k at
+      // byte 4k + i (the generator's one-shift expansion, expand_bytes64)
+      const int tg = (int)(t % 128), j = tg % 32;
+      const size_t off = ((size_t)((m / lp.NT) * n_kbp + t / 128) * lp.NT + (m % lp.NT)) * 128 + (tg - j) + 4 * (j % 8) + j / 8;
       for (int l = 0; l < lp.L; ++l) lp.Wout8[(size_t)l * plane + off] = (uint8_t)((q >> (8 * l)) & 0xFF);
       continue;
     }

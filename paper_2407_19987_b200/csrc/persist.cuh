@@ -514,11 +514,9 @@ __global__ void __launch_bounds__(kPThreads, 1) kr_persist_i8_kernel(const __gri
             const uint64_t b1 = (kb0 + 1 < kend && !(p.exp & 2))
                                     ? block_bits(xs, row, __ldg(p.kdesc + 2 * kb0 + 2), __ldg(p.kdesc + 2 * kb0 + 3), p.runs)
                                     : 0ull;
-            uint32_t w[32];   // byte t of the K-block = bit t (a nibble * 0x204081 spreads 4 bits)
-#pragma unroll
-            for (int c = 0; c < 16; ++c) w[c] = (((uint32_t)(b0 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) w[16 + c] = (((uint32_t)(b1 >> (4 * c)) & 15u) * 0x204081u) & 0x01010101u;
+            uint32_t w[32];   // the K-block pair's bytes in the planes' permuted K order
+            expand_bytes64(b0, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+            expand_bytes64(b1, *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
             mbar_wait(EMPTYA(gst), gph ^ 1u);
             tc_fence_after();
             tmem_st32(lane_base + A0 + (uint32_t)(gst * C::ACOLS), w);
