@@ -656,8 +656,6 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     int n = 0;                       // stage counter (same sequence as the MMA issuer)
     int gst = 0;                     // binary path: A slot and phase, advanced per stage
     uint32_t gph = 0;
-    int wst = 0;                     // I8: the descriptor slot and phase
-    uint32_t wph = 0;
     int gn = 0;                      // I8: stage counter (the teams alternate stages)
     bool any = false;                // has any MMA been issued yet (else F = 0)
     const uint16_t* prow_r = prow + (size_t)row * (REAL ? p.pstride : 0);
@@ -759,10 +757,18 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         // DAHEAD stages ahead, DFULL ring) and writes them with ONE tcgen05.st (32 columns),
         // so one store round trip (~400 cycles) covers two K-blocks and each team has two
         // stage times per stage.  FULLA counts the one team's 4 warps (pairs: 8).
-        const int kend = s.x + s.y;
+        // The team visits only its own stages: the absolute stage counter n gives the ring
+        // slots and phases directly (MAXD and NSTA are powers of two), so the other team's
+        // stages cost no loop iterations.
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
-        for (int kb0 = s.x; kb0 < kend; kb0 += KPS, ++gn) {
-          if ((gn & 1) == h) {
+        const int nstages = (s.y + KPS - 1) / KPS;
+        const int lg_a = NSTA == 8 ? 3 : NSTA == 4 ? 2 : NSTA == 2 ? 1 : 0;
+        static_assert((C::MAXD & (C::MAXD - 1)) == 0 && C::MAXD == 16, "descriptor ring: a power of two");
+        for (int i = (gn ^ h) & 1; i < nstages; i += 2) {
+          {
+            const int n = gn + i;
+            const int wst = n & (C::MAXD - 1), gst = n & (NSTA - 1);
+            const uint32_t wph = (uint32_t)(n >> 4) & 1u, gph = (uint32_t)(n >> lg_a) & 1u;
             mbar_wait(DFULL(wst), wph);
             const uint4* rec = dsm + (size_t)wst * p.srec_u4;
             const uint4 hd = rec[0];
@@ -783,9 +789,8 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
               else mbar_arrive(FULLA(gst));
             }
           }
-          if (++wst == C::MAXD) { wst = 0; wph ^= 1u; }
-          if (++gst == NSTA) { gst = 0; gph ^= 1u; }
         }
+        gn += nstages;
       } else {
       // this team's K-block descriptors, prefetched three stages ahead (d: this stage, e, f:
       // the next two)
