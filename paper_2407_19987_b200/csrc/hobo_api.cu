@@ -407,7 +407,10 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   L.i8 = slot <= 1 ? digit_planes(t) : slot == 5 ? H.digits : 0;
   L.NT = (N <= 128 || slot == 2 || slot == 4) ? 128 : 256;   // a 128-column tile when N fits (no padded columns)
   if (L.i8 >= 2) L.NT = 128;                    // TMEM: i8 accumulators of NT columns + the A stages
-  if (slot == 5) L.NT = PersistI8Cfg::NT;       // two accumulator sets of d x 64 columns
+  if (slot == 5) {                              // the int8 persistent kernel's tiles: 64 columns, two
+    const char* e = getenv("HOBO_PERSIST_I8_NT");   // accumulator sets (128: one set, measured slower)
+    L.NT = (e && atoi(e) == 128) ? 128 : 64;
+  }
   L.qscale = std::ldexp(1.0, H.qexp);
   const int planes = L.i8 ? L.i8 : H.limbs;
   if (N > 1024) return fail(HOBO_EINVAL, "the device path supports N <= 1024 (candidate bits are staged in shared memory)");
@@ -686,13 +689,15 @@ int real_slot(hobo_tensor* t) {
 // tiles have fewer than 64 K-blocks (QUBO-like, BASELINE config 2), with enough (candidate-block
 // pair, column tile) items to keep every SM pair busy.  HOBO_PERSIST=1 / =0 forces it on / off.
 // Returns 0 (per-tile kr_gemm_kernel), 1 (bf16 limbs, kr_persist_kernel) or 2 (int8 digit
-// planes, kr_persist_i8_kernel: exact, half the MMA work and W bytes of 3 bf16 limbs, but its
-// 64-column tiles leave only 128 TMEM columns of A, whose refill loop then paces the MMAs:
-// measured slower at cfg2, 0.185 vs 0.163 ms, so opt-in).  HOBO_PERSIST=1 / =0 forces a
+// planes, kr_persist_i8_kernel: exact, half the MMA work and W bytes of 3 bf16 limbs -- but
+// each plane has its own s32 accumulator, and reading 3 accumulators per tile through TMEM's
+// 64 B/clk read port costs about as much as a short tile's MMAs: 0.176 ms (64-column tiles,
+// two accumulator sets) / 0.197 ms (128-column tiles, one set) against 0.161 ms on bf16
+// limbs at cfg2, so opt-in).  HOBO_PERSIST=1 / =0 forces a
 // persistent kernel on / off, HOBO_PERSIST_I8=1 selects the int8 one when the cells allow.
 int use_persist(hobo_tensor* t, long long B) {
   const HostTensor& H = t->host;
-  const bool i8_ok = H.digits >= 1 && H.digits <= PersistI8Cfg::MAXP && 255.0 * 32.0 * (double)t->kl.Tpad < 2147483648.0;
+  const bool i8_ok = H.digits >= 1 && H.digits <= PersistI8Cfg<128>::MAXP && 255.0 * 32.0 * (double)t->kl.Tpad < 2147483648.0;
   const char* ei = getenv("HOBO_PERSIST_I8");
   const int kind = (i8_ok && ei && ei[0] == '1') ? 2 : (H.limbs <= PersistCfg::MAXL ? 1 : 0);
   if (kind == 0 || t->kl.nseg > 8) return 0;
@@ -814,7 +819,8 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     q.exp = 0;
     if (const char* e = getenv("HOBO_PERSIST_EXP")) q.exp = atoi(e);
     if (t->profile) CK(record_event(t->ev0, s));
-    CK(launch_persist(kr_persist_i8_kernel, PersistI8Cfg::smem_bytes(q.W), L, q, npairs, s));
+    if (L.NT == 64) CK(launch_persist(kr_persist_i8_kernel<64>, PersistI8Cfg<64>::smem_bytes(q.W), L, q, npairs, s));
+    else CK(launch_persist(kr_persist_i8_kernel<128>, PersistI8Cfg<128>::smem_bytes(q.W), L, q, npairs, s));
     if (t->profile) { CK(record_event(t->ev1, s)); t->ev_valid = true; }
     t->last_launches = 2;
     t->last_mma_macs = exec_macs(t, L, B);

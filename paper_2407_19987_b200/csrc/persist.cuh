@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(kPThreads, 1) kr_persist_kernel(const __grid_c
   const uint32_t prank = cluster_ctarank();
   const bool leader = prank == 0;
   const int pair = (int)(blockIdx.x >> 1);
-  const int it0 = __ldg(p.items + pair), it1 = __ldg(p.items + pair + 1);
+  const int pr = (p.exp & 16) ? 0 : pair;   // exp 16: every pair walks pair 0's items (lockstep W stream)
+  const int it0 = __ldg(p.items + pr), it1 = __ldg(p.items + pr + 1);
   auto item_ct = [&](int it) { return p.n_ct - 1 - it % p.n_ct; };   // heaviest tile of a block first
   auto item_cb = [&](int it) { return 2 * (it / p.n_ct) + (int)prank; };
   const uint32_t stage_bytes = (uint32_t)(C::KPS * p.L) * C::HBOX;
@@ -314,15 +315,21 @@ __global__ void __launch_bounds__(kPThreads, 1) kr_persist_kernel(const __grid_c
 // MMA time and the W stream from L2 halve.  TMEM: two accumulator sets of d x 64 columns
 // (64-column tiles: 2 x 3 x 64 = 384) and the A stages (32 columns per K-block pair) in the
 // rest; the W ring (smem) runs deeper than the A ring (TMEM), each with its own barriers.
+template <int NT_>
 struct PersistI8Cfg {
-  static constexpr int NT = 64;                      // column tile (UMMA N)
-  static constexpr int HBOX = (NT / 2) * 128;        // this CTA's half of one plane box (32 rows x 128 bytes)
+  static constexpr int NT = NT_;                     // column tile (UMMA N): 64 or 128
+  static constexpr int HBOX = (NT / 2) * 128;        // this CTA's half of one plane box (NT/2 rows x 128 bytes)
   static constexpr int MAXP = 3;                     // digit planes
-  static constexpr int WST = 12;                     // W ring stages (one K-block pair each)
+  static constexpr int WST = NT == 64 ? 12 : 6;      // W ring stages (one K-block pair each)
   static constexpr int MAXA = 8;                     // A ring stages (TMEM)
   static constexpr int ACOLS = 32;                   // TMEM columns of one K-block pair of A (128 bytes)
   static constexpr int NBAR = 2 * WST + 2 * MAXA + 4;
-  __host__ __device__ static int nsta(int P) { return (512 - 2 * P * NT) / ACOLS < MAXA ? (512 - 2 * P * NT) / ACOLS : MAXA; }
+  // accumulator sets: two when 2 x d x NT columns leave room for A (64-column tiles), else one
+  // (128-column tiles: the next item's MMAs wait for the epilogue's accumulator read)
+  __host__ __device__ static int nbuf(int P) { return 2 * P * NT <= 384 ? 2 : 1; }
+  __host__ __device__ static int nsta(int P) {
+    return (512 - nbuf(P) * P * NT) / ACOLS < MAXA ? (512 - nbuf(P) * P * NT) / ACOLS : MAXA;
+  }
   static size_t smem_bytes(int W) {
     return 1024 + (size_t)WST * MAXP * HBOX + 8 * NBAR + 16 + 128 + (size_t)(W + 2) * kBM * 4;
   }
@@ -344,9 +351,10 @@ struct PersistI8Params {
   int exp;                  // measurement switch, as PersistParams::exp
 };
 
+template <int NT_>
 __global__ void __launch_bounds__(kPThreads, 1) kr_persist_i8_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                       const PersistI8Params p) {
-  using C = PersistI8Cfg;
+  using C = PersistI8Cfg<NT_>;
   constexpr int NT = C::NT;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -374,7 +382,8 @@ __global__ void __launch_bounds__(kPThreads, 1) kr_persist_i8_kernel(const __gri
   auto item_ct = [&](int it) { return p.n_ct - 1 - it % p.n_ct; };
   auto item_cb = [&](int it) { return 2 * (it / p.n_ct) + (int)prank; };
   const int NSTA = C::nsta(p.P);
-  const uint32_t A0 = (uint32_t)(2 * p.P * NT);
+  const int NBUF = C::nbuf(p.P);
+  const uint32_t A0 = (uint32_t)(NBUF * p.P * NT);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::WST; ++s) { mbar_init(FULL(s), 1); mbar_init(EMPTY(s), 1); }
@@ -436,9 +445,9 @@ __global__ void __launch_bounds__(kPThreads, 1) kr_persist_i8_kernel(const __gri
       int st = 0, sa = 0;
       uint32_t ph = 0, pha = 0;
       for (int it = it0, n = 0; it < it1; ++it, ++n) {
-        const int buf = n & 1;
+        const int buf = NBUF == 2 ? (n & 1) : 0, use = NBUF == 2 ? (n >> 1) : n;
         const uint32_t acc = tmem + (uint32_t)(buf * p.P * NT);
-        mbar_wait(ACC_EMPTY0 + 8u * buf, (uint32_t)(((n >> 1) & 1) ^ 1));
+        mbar_wait(ACC_EMPTY0 + 8u * buf, (uint32_t)((use & 1) ^ 1));   // the buffer's previous item is drained
         tc_fence_after();
         const int ct = item_ct(it);
         uint32_t issued = 0;
@@ -541,7 +550,7 @@ __global__ void __launch_bounds__(kPThreads, 1) kr_persist_i8_kernel(const __gri
     const int row = q * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     for (int it = it0, n = 0; it < it1; ++it, ++n) {
-      const int buf = n & 1;
+      const int buf = NBUF == 2 ? (n & 1) : 0, use = NBUF == 2 ? (n >> 1) : n;
       const int ct = item_ct(it);
       const long long b = (long long)item_cb(it) * kBM + row;
       const bool live = b < p.B;
@@ -551,7 +560,7 @@ __global__ void __launch_bounds__(kPThreads, 1) kr_persist_i8_kernel(const __gri
         const int w = ct * (NT / 32) + c;
         xw[c] = (live && w < p.W) ? __ldg(p.xbits + (size_t)b * p.W + w) : 0u;
       }
-      mbar_wait(ACC_FULL0 + 8u * buf, (uint32_t)((n >> 1) & 1));
+      mbar_wait(ACC_FULL0 + 8u * buf, (uint32_t)(use & 1));
       tc_fence_after();
       long long tot = 0;
       double d1 = 0.0;
