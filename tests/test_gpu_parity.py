@@ -851,6 +851,33 @@ def test_empty_batches_and_argument_errors(H, torch):
 
 
 
+def test_nan_energy_is_an_error(H, torch):
+    """a NaN energy is an error, not a candidate.  Cells of +-3e38 at the
+    all-ones candidate overflow the persistent kernel's fp32 chunk sums to +inf in one column
+    tile and -inf in the other; their sum is NaN, and the argmin returns ERANGE (also through
+    the library communicator at world 1).  Without the argmin the energies are still written."""
+    N = 256
+    idx = np.array([[0, 1], [0, 2], [0, 129], [0, 130]], np.int32)
+    val = np.array([3e38, 3e38, -3e38, -3e38], np.float32)
+    t = H.HoboTensor.import_cells(2, N, idx, val)
+    X = torch.ones(64, N, dtype=torch.uint8, device="cuda")
+    with env("HOBO_PERSIST", "1"):
+        E, _ = t.energy(X, want_best=False)
+        torch.cuda.synchronize()
+        assert torch.isnan(E).all()
+        with pytest.raises(H.HoboError) as e:
+            t.energy(X)
+        assert e.value.status == H.HOBO_ERANGE
+        uid = H.dist_unique_id()
+        H.dist_init(0, 1, uid, torch.cuda.current_device())
+        try:
+            with pytest.raises(H.HoboError) as e:
+                t.energy(X)
+            assert e.value.status == H.HOBO_ERANGE
+        finally:
+            H.dist_finalize()
+
+
 # ---- CTA pairs (cta_group::2) and the single-CTA kernel, each forced on both limb regimes ----
 @pytest.mark.parametrize("force", ["1", "0"])
 def test_cta_pair_and_single_paths(H, torch, force):
