@@ -24,9 +24,17 @@
  *       HOBO_I8=1|0          int8 digit planes (kind::i8) whenever exact / never
  *       HOBO_CT_DESC=1|0     column tiles longest-first (default when the last tile is the
  *                            heaviest) / in index order
- *     Pairs and annealing kernels give identical results.  The int8 path computes the
- *     contraction exactly (integer accumulation), the bf16 path within the fp32
- *     tolerance; both are exact on integer instances with sum|H| < 2^24.
+ *       HOBO_PERSIST=1|0     the persistent energy kernel (short K loops, e.g. QUBO) on / off
+ *       HOBO_PERSIST_I8=1    ... on int8 digit planes when the cells allow (exact; opt-in)
+ *       HOBO_PERSIST_I8_NT=64|128, HOBO_PERSIST_KPS=1|2   its tile width / stage size
+ *       HOBO_GRAPH=0         launch energy / field calls and the search loop directly instead
+ *                            of replaying their captured CUDA graphs
+ *       HOBO_PERSIST_EXP=<bits>  MEASUREMENT ONLY: switches parts of the persistent kernels off
+ *                            (tools/persist_exp.sh); results are wrong whenever it is set
+ *     Pairs, persistent kernels, graphs and annealing kernels give the same results (bit for
+ *     bit on integer instances).  The int8 path computes the contraction exactly (integer
+ *     accumulation), the bf16 path within the fp32 tolerance; both are exact on integer
+ *     instances with sum|H| < 2^24.
  */
 #ifndef HOBO_H_
 #define HOBO_H_
