@@ -735,7 +735,8 @@ hobo_status persist_items(hobo_tensor* t, const DevLayout& L, long long B, int& 
   while (p <= npairs) items[(size_t)p++] = (int)nitems;
   items[(size_t)npairs] = (int)nitems;
   if (hobo_status st = grow(t, t->d_items, t->items_cap, items.size())) return st;
-  CK(cudaMemcpy(t->d_items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
+  // ordered on the call's stream: an earlier launch on it may still read the old ranges
+  CK(cudaMemcpyAsync(t->d_items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   t->items_B = B;
   t->items_nct = L.n_ct;
   return HOBO_OK;
