@@ -106,6 +106,12 @@ struct hobo_tensor {
                            // 5 = int8 energy layout with 64-column tiles (the int8 persistent kernel)
   int* d_p1q = nullptr; int p1_int = -1;                // degree-1 cells on the digit grid (int8 persistent)
   int* d_items = nullptr; size_t items_cap = 0;          // persistent kernel: per-pair item ranges
+  // stream-K schedule of CTA-pair field launches (sk_plan): units, split tiles, partials
+  int4* d_units = nullptr; size_t units_cap = 0;
+  int4* d_sktiles = nullptr; size_t sktiles_cap = 0;
+  float* d_skG = nullptr; size_t skG_cap = 0;
+  double* d_skQ = nullptr; size_t skQ_cap = 0;
+  long long sk_B = -1; int sk_nunits = 0, sk_ntiles = 0, sk_ctdesc = -1;
   // the search loop as one CUDA graph per (chains, iterations, buffers); seed, chain0 and the
   // P_t table travel in d_sargs, so a replay needs one small copy and one graph launch
   unsigned long long* d_sargs = nullptr; size_t sargs_cap = 0;
@@ -263,7 +269,7 @@ cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s
   const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
   if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
+  cfg.gridDim = dim3((unsigned)(p.units ? 2 * p.n_units : 2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -573,6 +579,10 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
     if (const char* e = getenv("HOBO_CT_DESC")) p.ct_desc = e[0] == '1';
   }
   p.preal = nullptr;
+  p.units = nullptr;
+  p.n_units = 0;
+  p.skG = nullptr;
+  p.skQ = nullptr;
   p.LA = 1;
   p.ring_boxes = L.NT == 128 ? ring_boxes_for<128>() : ring_boxes_for<256>();
   p.pstride = 0;
@@ -762,6 +772,89 @@ cudaError_t launch_persist(K* k, size_t smem, const DevLayout& L, const Params& 
   return cudaGetLastError();
 }
 
+// Stream-K schedule for CTA-pair field launches (bf16 limbs).  A field-mode tile (candidate-
+// block pair x column tile) is the same K loop for every tile, and one CTA pair per two SMs runs
+// at a time (74 slots), so T tiles take ceil(T / 74) tile-times: cfg3's 512 tiles 6.92 -> 7, a
+// GPU's 64 tiles at 8-GPU strong scaling 0.86 -> 1.  Whole waves stay data-parallel (each tile
+// one CTA pair, written in place); the R < 74 tiles left over are cut into 74 equal K ranges of
+// R/74 tile, each range one or two units (its pieces in one or two tiles).  Every unit of a
+// split tile writes partial fields + energies to its own slot; sk_reduce_kernel sums them in K
+// order.  Units are ordered whole tiles, then the ranges' first pieces, then their second pieces
+// longest first: a slot whose first piece ends early takes a long second piece, so every slot
+// does about R/74 of a tile after the data-parallel waves.  HOBO_SK=0 disables it.
+hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long long B, bool& use, cudaStream_t s) {
+  use = false;
+  if (const char* e = getenv("HOBO_SK"))
+    if (e[0] == '0') return HOBO_OK;
+  const int KPS = L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
+  std::vector<int> tot(L.n_ct, 0);
+  for (int ct = 0; ct < L.n_ct; ++ct)
+    for (int j = 0; j < t->kl.nseg; ++j) tot[ct] += (L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1] + KPS - 1) / KPS;
+  for (int ct = 1; ct < L.n_ct; ++ct)
+    if (tot[ct] != tot[0]) return HOBO_OK;   // (field mode: every tile has the same K loop)
+  const int total = tot[0];
+  const int slots = 74;
+  const long long ncbp = (B + 2 * kBM - 1) / (2 * kBM);
+  const long long tiles = ncbp * L.n_ct;
+  const long long D = tiles / slots * slots, R = tiles - D;
+  if (R == 0 || tiles < slots / 2 || total < 4 * slots || total >= (1 << 20)) return HOBO_OK;
+  use = true;
+  if (t->sk_B == B && t->sk_ctdesc == p.ct_desc) return HOBO_OK;
+  auto tile = [&](long long tau, int& cbp, int& ct) {
+    const int ct_i = (int)(tau / ncbp);
+    ct = p.ct_desc ? L.n_ct - 1 - ct_i : ct_i;
+    cbp = (int)(tau % ncbp);
+  };
+  std::vector<int4> units, firsts, seconds, sktiles;
+  for (long long tau = 0; tau < D; ++tau) {
+    int cbp, ct;
+    tile(tau, cbp, ct);
+    units.push_back(make_int4(cbp, ct, 0, total));
+  }
+  const long long flat = R * total;
+  const long long Lr = (flat + slots - 1) / slots;
+  int part = 0;
+  std::vector<int> first_part(R, -1), nparts(R, 0);
+  for (long long i = 0; i < slots; ++i) {
+    long long a = i * Lr, b = std::min(flat, a + Lr);
+    for (int piece = 0; a < b; ++piece) {
+      const long long r = a / total;
+      const long long e = std::min(b, (r + 1) * total);
+      int cbp, ct;
+      tile(D + r, cbp, ct);
+      if (first_part[r] < 0) first_part[r] = part;
+      ++nparts[r];
+      const int4 u = make_int4(cbp, ct, (int)(a - r * total), (int)(e - r * total) | ((part + 1) << 20));
+      (piece == 0 ? firsts : seconds).push_back(u);
+      ++part;
+      a = e;
+    }
+  }
+  if (part >= (1 << 11)) { use = false; return HOBO_OK; }
+  std::stable_sort(seconds.begin(), seconds.end(), [](const int4& x, const int4& y) {
+    return ((x.w & 0xFFFFF) - x.z) > ((y.w & 0xFFFFF) - y.z);
+  });
+  units.insert(units.end(), firsts.begin(), firsts.end());
+  units.insert(units.end(), seconds.begin(), seconds.end());
+  for (long long r = 0; r < R; ++r) {
+    int cbp, ct;
+    tile(D + r, cbp, ct);
+    sktiles.push_back(make_int4(cbp, ct, first_part[r], nparts[r]));
+  }
+  if (hobo_status st = grow(t, t->d_units, t->units_cap, units.size())) return st;
+  if (hobo_status st = grow(t, t->d_sktiles, t->sktiles_cap, sktiles.size())) return st;
+  if (hobo_status st = grow(t, t->d_skG, t->skG_cap, (size_t)part * 2 * kBM * L.NT)) return st;
+  if (hobo_status st = grow(t, t->d_skQ, t->skQ_cap, (size_t)part * 2 * kBM)) return st;
+  // ordered on the call's stream: an earlier launch on it may still read the old plan
+  CK(cudaMemcpyAsync(t->d_units, units.data(), units.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(t->d_sktiles, sktiles.data(), sktiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  t->sk_B = B;
+  t->sk_ctdesc = p.ct_desc;
+  t->sk_nunits = (int)units.size();
+  t->sk_ntiles = (int)sktiles.size();
+  return HOBO_OK;
+}
+
 hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, float* G, cudaStream_t s,
                      const uint16_t* P = nullptr, bool packed = false, int* slot_used = nullptr) {
   const int pk = (!P && !field) ? use_persist(t, B) : 0;
@@ -877,6 +970,16 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     p.cb_iters = (long long)L.n_ct * ((p.n_cb + 1) / 2) >= 4 * 148 ? 2 : 1;
     if (const char* e = getenv("HOBO_CB_ITERS")) p.cb_iters = std::max(1, atoi(e));
   }
+  bool sk = false;
+  if (field && !P && !L.i8 && use_pairs(L, p) && slot == 1)
+    if (hobo_status st = sk_plan(t, L, p, B, sk, s)) return st;
+  if (sk) {
+    p.n_split = 1;
+    p.units = t->d_units;
+    p.n_units = t->sk_nunits;
+    p.skG = t->d_skG;
+    p.skQ = t->d_skQ;
+  }
   if (p.n_split > 1) {
     if (field) {
       if (hobo_status st = grow(t, t->d_Gpart, t->Gpart_cap, (size_t)p.n_split * B * t->host.N * (L.i8 ? 2 : 1))) return st;
@@ -888,7 +991,13 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   if (t->profile) CK(record_event(t->ev0, s));
   CK(launch_kr_any(L, p, s));
   if (t->profile) { CK(record_event(t->ev1, s)); t->ev_valid = true; }
-  t->last_launches = P ? 1 : 2;
+  if (sk) {
+    const long long n = (long long)t->sk_ntiles * 2 * kBM * (L.NT / 4);
+    sk_reduce_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, s>>>(
+        t->d_sktiles, t->sk_ntiles, t->d_skG, t->d_skQ, G, t->d_Q, B, t->host.N, L.NT, 1);
+    CK(cudaGetLastError());
+  }
+  t->last_launches = (P ? 1 : 2) + (sk ? 1 : 0);
   if (p.n_split > 1) {
     const long long nG = field ? B * t->host.N : 0, nQ = (long long)L.n_ct * B;
     splitk_reduce_kernel<<<(unsigned)std::min<long long>((std::max(nG, nQ) + 255) / 256, 148 * 8), 256, 0, s>>>(
@@ -1002,6 +1111,8 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (t->d_sa_E) cudaFree(t->d_sa_E);
   if (t->d_srec) cudaFree(t->d_srec);
   if (t->d_items) cudaFree(t->d_items);
+  for (void* q : {(void*)t->d_units, (void*)t->d_sktiles, (void*)t->d_skG, (void*)t->d_skQ})
+    if (q) cudaFree(q);
   if (t->d_p1q) cudaFree(t->d_p1q);
   if (t->d_sargs) cudaFree(t->d_sargs);
   if (t->h_key) cudaFreeHost(t->h_key);
@@ -1075,9 +1186,10 @@ std::vector<uintptr_t> call_key(hobo_tensor* t, int field, const uint8_t* X, boo
   std::vector<uintptr_t> k = {(uintptr_t)field, (uintptr_t)packed, (uintptr_t)B, (uintptr_t)row0, (uintptr_t)X,
                               (uintptr_t)G, (uintptr_t)E, (uintptr_t)best, (uintptr_t)t->profile,
                               (uintptr_t)t->d_bits, (uintptr_t)t->d_Q, (uintptr_t)t->d_Gpart, (uintptr_t)t->d_Qpart,
-                              (uintptr_t)t->d_items, (uintptr_t)t->d_key, (uintptr_t)t->items_B};
+                              (uintptr_t)t->d_items, (uintptr_t)t->d_key, (uintptr_t)t->items_B, (uintptr_t)t->d_units,
+                              (uintptr_t)t->d_skG, (uintptr_t)t->d_skQ, (uintptr_t)t->sk_B};
   for (const char* v : {"HOBO_PAIR", "HOBO_I8", "HOBO_CT_DESC", "HOBO_CB_ITERS", "HOBO_PERSIST", "HOBO_PERSIST_I8",
-                        "HOBO_PERSIST_KPS", "HOBO_PERSIST_EXP"}) {
+                        "HOBO_PERSIST_KPS", "HOBO_PERSIST_EXP", "HOBO_SK"}) {
     const char* e = getenv(v);
     k.push_back(e ? (uintptr_t)(unsigned char)e[0] + 1 : 0);
   }

@@ -66,6 +66,14 @@ struct KrParams {
   long long sa_chain0;      // global id of chain 0 of this shard
   long long sa_step;        // s * N + m: counter of the acceptance uniform
   int sa_m, sa_prev;        // visited site, previous site (-1: none)
+  // stream-K schedule (CTA-pair field launches; nullable): unit u of CTA pair u = {candidate-
+  // block pair, column tile, first stage, last stage | (part + 1) << 20}; part -1 = the whole
+  // tile, written in place; part >= 0 = a K range of a split tile, written to the partial
+  // buffers skG [part][256 rows][NT] and skQ [part][256], summed by sk_reduce_kernel
+  const int4* units;
+  int n_units;              // CTA pairs of a stream-K launch
+  float* skG;
+  double* skQ;
 };
 
 // I8: W as int8 digit planes (one byte per tuple; a box row = 128 bytes = the K-block pair
@@ -327,10 +335,14 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const int MB = (PAIR || SA || REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
   const int ncb_eff = PAIR ? (p.n_cb + 1) / 2 : (p.n_cb + MB - 1) / MB;
   const int bid = PAIR ? (int)(blockIdx.x / 2) : (int)blockIdx.x;
-  const int cb = PAIR ? 2 * (bid % ncb_eff) + (int)prank : bid % ncb_eff;
+  const bool sk = PAIR && !I8 && p.units != nullptr;   // stream-K unit (see KrParams::units)
+  const int4 unit = sk ? __ldg(p.units + bid) : make_int4(0, 0, 0, 0);
+  const int sk_part = sk ? (unit.w >> 20) - 1 : -1;
   const int ct_i = (bid / ncb_eff) % p.n_ct;
-  const int ct = (!SA && p.ct_desc) ? p.n_ct - 1 - ct_i : ct_i;
-  const int split = bid / (ncb_eff * p.n_ct);
+  const int cb = sk ? 2 * unit.x + (int)prank : PAIR ? 2 * (bid % ncb_eff) + (int)prank : bid % ncb_eff;
+  const int ct = sk ? unit.y : (!SA && p.ct_desc) ? p.n_ct - 1 - ct_i : ct_i;
+  const int split = sk ? 0 : bid / (ncb_eff * p.n_ct);
+  const bool first_range = sk ? unit.z == 0 : split == 0;   // adds the degree-1 cells (counted once)
   const long long b0 = (long long)cb * kBM;
   // MB > 1: this CTA's candidate blocks are cb, cb + ncb_eff, ... (< n_cb)
   const int ntile = MB == 1 ? 1 : (p.n_cb - 1 - cb) / ncb_eff + 1;
@@ -353,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     int total = 0;
     for (int j = 0; j < p.nseg; ++j) total += (gs[j].y + KPS - 1) / KPS;
     const int per = (total + p.n_split - 1) / p.n_split;
-    const int c0 = split * per, c1 = min(total, c0 + per);
+    const int c0 = sk ? unit.z : split * per, c1 = sk ? (unit.w & 0xFFFFF) : min(total, c0 + per);
     int s0 = 0;
     for (int j = p.nseg - 1; j >= 0; --j) {
       const int ns = (gs[j].y + KPS - 1) / KPS;
@@ -863,7 +875,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       float pmv[32];
 #pragma unroll
       for (int c = 0; c < 32; c += 4) {
-        const float4 v4 = split == 0 ? __ldg(reinterpret_cast<const float4*>(p.p1 + mbase + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 v4 = first_range ? __ldg(reinterpret_cast<const float4*>(p.p1 + mbase + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
         pmv[c] = v4.x; pmv[c + 1] = v4.y; pmv[c + 2] = v4.z; pmv[c + 3] = v4.w;
       }
       float g[32];
@@ -937,7 +949,11 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         }
       } else if (p.field_mode && live && !(I8 && p.n_split > 1)) {
         float* gout = p.G + ((size_t)split * p.B + b) * p.N + mbase;
-        const int nvalid = min(32, p.N - mbase);
+        int nvalid = min(32, p.N - mbase);
+        if (sk_part >= 0) {   // a K range of a split tile: its partial fields, every column of the tile
+          gout = p.skG + ((size_t)sk_part * 2 * kBM + prank * kBM + row) * NT + (mbase - ct * NT);
+          nvalid = 32;
+        }
         if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(gout) & 15) == 0)) {
 #pragma unroll
           for (int c = 0; c < 32; c += 4) *reinterpret_cast<float4*>(gout + c) = make_float4(g[c], g[c + 1], g[c + 2], g[c + 3]);
@@ -970,7 +986,10 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     // combine the two column halves in a fixed order (deterministic, no atomics)
     if (h == 1) qpart[row] = qsum;
     named_bar_sync(1, 256);
-    if (h == 0 && live) p.Q[((size_t)split * p.n_ct + ct) * p.B + b] = qsum + qpart[row];
+    if (h == 0 && live) {
+      if (sk_part >= 0) p.skQ[(size_t)sk_part * 2 * kBM + prank * kBM + row] = qsum + qpart[row];
+      else p.Q[((size_t)split * p.n_ct + ct) * p.B + b] = qsum + qpart[row];
+    }
     }
     }   // tiles
   }
@@ -1063,6 +1082,41 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ Gp, float* __rest
     double q = 0.0;
     for (int s = 0; s < n_split; ++s) q += Qp[(size_t)s * nQ + i];
     Q[i] = q;
+  }
+}
+
+// stream-K: the split tiles' fields and energy partials, their K ranges summed in K order
+// (deterministic).  tiles[s] = {candidate-block pair, column tile, first part, #parts}.
+__global__ void sk_reduce_kernel(const int4* __restrict__ tiles, int ntiles, const float* __restrict__ skG,
+                                 const double* __restrict__ skQ, float* __restrict__ G, double* __restrict__ Q,
+                                 long long B, int N, int NT, int field) {
+  const long long per_tile = 2LL * kBM * (NT / 4);   // float4 groups of one tile
+  const long long total = (long long)ntiles * per_tile;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int4 t = __ldg(tiles + i / per_tile);
+    const long long e = i % per_tile;
+    const int r = (int)(e / (NT / 4)), c4 = (int)(e % (NT / 4)) * 4;
+    const long long b = 2LL * kBM * t.x + r;
+    if (b >= B) continue;
+    const int m = t.y * NT + c4;
+    if (field && m < N) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < t.w; ++q) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(skG + ((size_t)(t.z + q) * 2 * kBM + r) * NT + c4));
+        a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+      }
+      float* g = G + b * N + m;
+      if (m + 3 < N && (reinterpret_cast<uintptr_t>(g) & 15) == 0) *reinterpret_cast<float4*>(g) = a;
+      else {
+        const float av[4] = {a.x, a.y, a.z, a.w};
+        for (int c = 0; c < 4 && m + c < N; ++c) g[c] = av[c];
+      }
+    }
+    if (c4 == 0) {
+      double qs = 0.0;
+      for (int q = 0; q < t.w; ++q) qs += skQ[(size_t)(t.z + q) * 2 * kBM + r];
+      Q[(size_t)t.y * B + b] = qs;
+    }
   }
 }
 

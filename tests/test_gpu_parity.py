@@ -435,6 +435,41 @@ def test_persistent_energy_kernel(H, torch, case, i8):
         check_argmin(b1, E1, 0.0, row0=3)
 
 
+# ---- stream-K (CTA-pair field launches: whole waves in place, the leftover tiles split) ------
+@pytest.mark.parametrize("case", ["int_cfg3", "fp32_bf16"])
+def test_stream_k_matches_data_parallel(H, torch, case):
+    """The stream-K schedule (leftover tiles cut into 74 equal K ranges, partials summed in K
+    order) against the plain one-tile-per-pair launch (HOBO_SK=0) and the oracle: 8,192
+    candidates (one GPU's share at 8 GPUs: every tile split), 20,000 (two whole waves + 10
+    split tiles) and 65,536 (cfg3's launch: 6 waves + 68 split tiles)."""
+    if case == "int_cfg3":
+        p = cfg3_problem()
+        t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+        sizes = (8192, 20000, 65536)
+    else:
+        idx, val = uniform_cells(3, 300, 81)
+        t = H.HoboTensor.import_cells(3, 300, idx, val)     # HOBO_I8=0 below: the bf16 limbs (L = 3)
+        o = Oracle.from_cells(3, 300, idx, val)
+        sizes = (8192, 20000)
+    for B in sizes:
+        X = x_bits(82, B, t.N)
+        Xd = dev(torch, X)
+        with env("HOBO_I8", "0"):
+            G1, E1, b1 = t.local_field(Xd, row0=9, want_best=True)
+            with env("HOBO_SK", "0"):
+                G0, E0, b0 = t.local_field(Xd, row0=9, want_best=True)
+        torch.cuda.synchronize()
+        G1, E1, G0, E0 = (a.cpu().numpy().astype(np.float64) for a in (G1, E1, G0, E0))
+        rows = sample_rows(B, 257, 64)
+        Go, Eo = o.field(X[rows]), o.energy(X[rows])
+        if t.is_integer:
+            assert np.array_equal(G1, G0) and np.array_equal(E1, E0) and b1 == b0, B
+            assert np.array_equal(G1[rows], Go) and np.array_equal(E1[rows], Eo), B
+        else:
+            assert np.max(np.abs(G1[rows] - Go)) <= o.tau and np.max(np.abs(E1[rows] - Eo)) <= o.tau, B
+            assert np.max(np.abs(G1 - G0)) <= 2 * o.tau and np.max(np.abs(E1 - E0)) <= 2 * o.tau, B
+
+
 # ---- split-K (small batches) -----------------------------------------------------------------
 @pytest.mark.parametrize("B", [1, 16, 200])
 def test_small_batch_split_k_matches(H, torch, B):
