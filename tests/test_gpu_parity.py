@@ -398,7 +398,7 @@ def test_cfg3_fp32_companion_sampled(H, torch):
 
 # ---- the persistent energy kernel (persist.cuh): short K loops, double-buffered accumulators ----
 @pytest.mark.parametrize("i8", ["1", "0"])
-@pytest.mark.parametrize("case", ["int_qubo", "int_o3", "fp32_qubo"])
+@pytest.mark.parametrize("case", ["int_qubo", "int_o3", "fp32_qubo", "int_qubo_words"])
 def test_persistent_energy_kernel(H, torch, case, i8):
     """The persistent energy kernels (HOBO_PERSIST=1; the default for cfg2-like tiles): int8 digit
     planes (kr_persist_i8_kernel, exact: energies equal fp32(oracle)) and bf16 limbs
@@ -411,9 +411,12 @@ def test_persistent_energy_kernel(H, torch, case, i8):
     elif case == "int_o3":
         p = random_integer_problem(3, 70, 52, nterms=900)
         t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
-    else:
+    elif case == "fp32_qubo":
         idx, val = uniform_cells(2, 520, 53)
         t, o = H.HoboTensor.import_cells(2, 520, idx, val), Oracle.from_cells(2, 520, idx, val)
+    else:   # whole 32-bit rows (the vectorised pack kernel feeds the persistent one)
+        idx, val = int_twin_cells(2, 256, 55)
+        t, o = H.HoboTensor.import_cells(2, 256, idx, val), Oracle.from_cells(2, 256, idx, val)
     for B in (1, 129, 300, 5000, 40000):
         X = x_bits(54, B, t.N)
         with env("HOBO_PERSIST", "1"), env("HOBO_PERSIST_I8", i8):
