@@ -343,8 +343,15 @@ void run_pipe(const char* name, int iters, int ctas = 148) {
   cudaFree(d); cudaFree(buf);
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int it = 20000;
+  if (argc > 1 && argv[1][0] == 'n') {   // the N sweep only (bf16, A in TMEM, no waits)
+    run<256, true, 0>("TS M128 N256 no-wait", it);
+    run<128, true, 0>("TS M128 N128 no-wait", it);
+    run<64, true, 0>("TS M128 N64 no-wait", it);
+    run<64, false, 0>("SS M128 N64 no-wait", it);
+    return 0;
+  }
   run<256, false, 0>("SS M128 N256 no-wait", it);
   run<256, true, 0>("TS M128 N256 no-wait", it);
   run<128, false, 0>("SS M128 N128 no-wait", it);
