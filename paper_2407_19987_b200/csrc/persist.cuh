@@ -48,7 +48,7 @@ struct PersistParams {
   long long B;
   int N, W, n_ct, n_cbp, nseg, L, n_kb;
   int exp;                  // measurement switch (HOBO_PERSIST_EXP, wrong results): 1 no epilogue math, 2 no A
-                            // decoding, 4 no bit restaging, 8 no MMAs
+                            // decoding, 4 no bit restaging, 8 no MMAs, 16 every pair walks pair 0's items
 };
 
 using PersistCfg = PersistCfgT<1>;
