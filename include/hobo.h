@@ -29,6 +29,10 @@
  *       HOBO_PERSIST_I8_NT=64|128, HOBO_PERSIST_KPS=1|2   its tile width / stage size
  *       HOBO_GRAPH=0         launch energy / field calls and the search loop directly instead
  *                            of replaying their captured CUDA graphs
+ *       HOBO_SK=0            no stream-K schedule for CTA-pair field launches
+ *       HOBO_E2E_TAIL=<n>, HOBO_E2E_HEAD=<q>   host-buffer field calls returning G: n
+ *                            halvings after the last whole wave (default 1), first chunk q
+ *                            quarter waves (default 2)
  *       HOBO_PERSIST_EXP=<bits>  MEASUREMENT ONLY: switches parts of the persistent kernels off
  *                            (tools/persist_exp.sh); results are wrong whenever it is set
  *     Pairs, persistent kernels, graphs and annealing kernels give the same results (bit for

@@ -107,11 +107,19 @@ struct hobo_tensor {
   int* d_p1q = nullptr; int p1_int = -1;                // degree-1 cells on the digit grid (int8 persistent)
   int* d_items = nullptr; size_t items_cap = 0;          // persistent kernel: per-pair item ranges
   // stream-K schedule of CTA-pair field launches (sk_plan): units, split tiles, partials
-  int4* d_units = nullptr; size_t units_cap = 0;
-  int4* d_sktiles = nullptr; size_t sktiles_cap = 0;
+  // stream-K plans, one per (batch, layout, column order), uploaded once and kept for the
+  // handle's lifetime (captured graphs point at them); the partial buffers are shared
+  struct SkPlan {
+    long long B;
+    const void* L;
+    int ctdesc;
+    int4* d_units;
+    int4* d_sktiles;
+    int nunits, ntiles;
+  };
+  std::vector<SkPlan> sk_plans;
   float* d_skG = nullptr; size_t skG_cap = 0;
   double* d_skQ = nullptr; size_t skQ_cap = 0;
-  long long sk_B = -1; int sk_nunits = 0, sk_ntiles = 0, sk_ctdesc = -1;
   // the search loop as one CUDA graph per (chains, iterations, buffers); seed, chain0 and the
   // P_t table travel in d_sargs, so a replay needs one small copy and one graph launch
   unsigned long long* d_sargs = nullptr; size_t sargs_cap = 0;
@@ -782,8 +790,9 @@ cudaError_t launch_persist(K* k, size_t smem, const DevLayout& L, const Params& 
 // order.  Units are ordered whole tiles, then the ranges' first pieces, then their second pieces
 // longest first: a slot whose first piece ends early takes a long second piece, so every slot
 // does about R/74 of a tile after the data-parallel waves.  HOBO_SK=0 disables it.
-hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long long B, bool& use, cudaStream_t s) {
-  use = false;
+hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long long B,
+                    const hobo_tensor::SkPlan*& use, cudaStream_t s) {
+  use = nullptr;
   if (const char* e = getenv("HOBO_SK"))
     if (e[0] == '0') return HOBO_OK;
   const int KPS = L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
@@ -798,8 +807,12 @@ hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long 
   const long long tiles = ncbp * L.n_ct;
   const long long D = tiles / slots * slots, R = tiles - D;
   if (R == 0 || tiles < slots / 2 || total < 4 * slots || total >= (1 << 20)) return HOBO_OK;
-  use = true;
-  if (t->sk_B == B && t->sk_ctdesc == p.ct_desc) return HOBO_OK;
+  for (const auto& q : t->sk_plans)
+    if (q.B == B && q.L == &L && q.ctdesc == p.ct_desc) {
+      use = &q;
+      return HOBO_OK;
+    }
+  if (t->sk_plans.size() >= 16) return HOBO_OK;   // a new batch size beyond the cache: data-parallel
   auto tile = [&](long long tau, int& cbp, int& ct) {
     const int ct_i = (int)(tau / ncbp);
     ct = p.ct_desc ? L.n_ct - 1 - ct_i : ct_i;
@@ -830,7 +843,7 @@ hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long 
       a = e;
     }
   }
-  if (part >= (1 << 11)) { use = false; return HOBO_OK; }
+  if (part >= (1 << 11)) return HOBO_OK;
   std::stable_sort(seconds.begin(), seconds.end(), [](const int4& x, const int4& y) {
     return ((x.w & 0xFFFFF) - x.z) > ((y.w & 0xFFFFF) - y.z);
   });
@@ -841,17 +854,18 @@ hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long 
     tile(D + r, cbp, ct);
     sktiles.push_back(make_int4(cbp, ct, first_part[r], nparts[r]));
   }
-  if (hobo_status st = grow(t, t->d_units, t->units_cap, units.size())) return st;
-  if (hobo_status st = grow(t, t->d_sktiles, t->sktiles_cap, sktiles.size())) return st;
   if (hobo_status st = grow(t, t->d_skG, t->skG_cap, (size_t)part * 2 * kBM * L.NT)) return st;
   if (hobo_status st = grow(t, t->d_skQ, t->skQ_cap, (size_t)part * 2 * kBM)) return st;
-  // ordered on the call's stream: an earlier launch on it may still read the old plan
-  CK(cudaMemcpyAsync(t->d_units, units.data(), units.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(t->d_sktiles, sktiles.data(), sktiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-  t->sk_B = B;
-  t->sk_ctdesc = p.ct_desc;
-  t->sk_nunits = (int)units.size();
-  t->sk_ntiles = (int)sktiles.size();
+  hobo_tensor::SkPlan q{B, &L, p.ct_desc, nullptr, nullptr, (int)units.size(), (int)sktiles.size()};
+  CK(cudaMalloc(&q.d_units, units.size() * sizeof(int4)));
+  if (cudaMalloc(&q.d_sktiles, sktiles.size() * sizeof(int4)) != cudaSuccess) {
+    cudaFree(q.d_units);
+    return fail(HOBO_ECUDA, "stream-K plan allocation");
+  }
+  t->sk_plans.push_back(q);   // freed with the handle
+  CK(cudaMemcpyAsync(q.d_units, units.data(), units.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(q.d_sktiles, sktiles.data(), sktiles.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  use = &t->sk_plans.back();
   return HOBO_OK;
 }
 
@@ -970,13 +984,13 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     p.cb_iters = (long long)L.n_ct * ((p.n_cb + 1) / 2) >= 4 * 148 ? 2 : 1;
     if (const char* e = getenv("HOBO_CB_ITERS")) p.cb_iters = std::max(1, atoi(e));
   }
-  bool sk = false;
+  const hobo_tensor::SkPlan* sk = nullptr;
   if (field && !P && !L.i8 && use_pairs(L, p) && slot == 1)
     if (hobo_status st = sk_plan(t, L, p, B, sk, s)) return st;
   if (sk) {
     p.n_split = 1;
-    p.units = t->d_units;
-    p.n_units = t->sk_nunits;
+    p.units = sk->d_units;
+    p.n_units = sk->nunits;
     p.skG = t->d_skG;
     p.skQ = t->d_skQ;
   }
@@ -992,9 +1006,9 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   CK(launch_kr_any(L, p, s));
   if (t->profile) { CK(record_event(t->ev1, s)); t->ev_valid = true; }
   if (sk) {
-    const long long n = (long long)t->sk_ntiles * 2 * kBM * (L.NT / 4);
+    const long long n = (long long)sk->ntiles * 2 * kBM * (L.NT / 4);
     sk_reduce_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, s>>>(
-        t->d_sktiles, t->sk_ntiles, t->d_skG, t->d_skQ, G, t->d_Q, B, t->host.N, L.NT, 1);
+        sk->d_sktiles, sk->ntiles, t->d_skG, t->d_skQ, G, t->d_Q, B, t->host.N, L.NT, 1);
     CK(cudaGetLastError());
   }
   t->last_launches = (P ? 1 : 2) + (sk ? 1 : 0);
@@ -1111,7 +1125,11 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   if (t->d_sa_E) cudaFree(t->d_sa_E);
   if (t->d_srec) cudaFree(t->d_srec);
   if (t->d_items) cudaFree(t->d_items);
-  for (void* q : {(void*)t->d_units, (void*)t->d_sktiles, (void*)t->d_skG, (void*)t->d_skQ})
+  for (const auto& q : t->sk_plans) {
+    cudaFree(q.d_units);
+    cudaFree(q.d_sktiles);
+  }
+  for (void* q : {(void*)t->d_skG, (void*)t->d_skQ})
     if (q) cudaFree(q);
   if (t->d_p1q) cudaFree(t->d_p1q);
   if (t->d_sargs) cudaFree(t->d_sargs);
@@ -1186,8 +1204,8 @@ std::vector<uintptr_t> call_key(hobo_tensor* t, int field, const uint8_t* X, boo
   std::vector<uintptr_t> k = {(uintptr_t)field, (uintptr_t)packed, (uintptr_t)B, (uintptr_t)row0, (uintptr_t)X,
                               (uintptr_t)G, (uintptr_t)E, (uintptr_t)best, (uintptr_t)t->profile,
                               (uintptr_t)t->d_bits, (uintptr_t)t->d_Q, (uintptr_t)t->d_Gpart, (uintptr_t)t->d_Qpart,
-                              (uintptr_t)t->d_items, (uintptr_t)t->d_key, (uintptr_t)t->items_B, (uintptr_t)t->d_units,
-                              (uintptr_t)t->d_skG, (uintptr_t)t->d_skQ, (uintptr_t)t->sk_B};
+                              (uintptr_t)t->d_items, (uintptr_t)t->d_key, (uintptr_t)t->items_B, (uintptr_t)t->d_skG,
+                              (uintptr_t)t->d_skQ};
   for (const char* v : {"HOBO_PAIR", "HOBO_I8", "HOBO_CT_DESC", "HOBO_CB_ITERS", "HOBO_PERSIST", "HOBO_PERSIST_I8",
                         "HOBO_PERSIST_KPS", "HOBO_PERSIST_EXP", "HOBO_SK"}) {
     const char* e = getenv(v);
@@ -1301,20 +1319,36 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   // previous chunk's contraction (>= 60 ns per candidate).  With the fields coming back
   // (4N bytes per candidate, about as long as the contraction at N = 512), chunk i's
   // device->host copy overlaps chunk i+1's contraction, so the chunks stay two waves long and
-  // the last one is a single wave (its copy is the exposed one at the end).
+  // the ends are short (below).
   const long long per_wave = std::max<long long>(2, 148 / L.n_ct / 2 * 2) * kBM;
   std::vector<long long> sizes;
   if (!gout) {
     for (long long off = 0, n = per_wave; off < B; off += sizes.back(), n *= 6) sizes.push_back(std::min(n, B - off));
   } else {
-    sizes.push_back(std::min<long long>(per_wave, B));
-    for (long long off = sizes[0]; off < B;) {
-      const long long left = B - off;
-      if (left <= per_wave) { sizes.push_back(left); break; }
-      if (left <= 3 * per_wave) { sizes.push_back(left - per_wave); sizes.push_back(per_wave); break; }
-      sizes.push_back(2 * per_wave);
-      off += 2 * per_wave;
+    // a half-wave first chunk (its input copy is the exposed one) and a half-wave last chunk
+    // (its copy-out is): a partial wave runs split across every SM, 0.33 ms for half a wave
+    // at cfg3 against 0.61 ms for a whole one, so it still hides the previous chunk's copy-out.
+    // cfg3 e2e: 4.89 -> 4.75 ms; two halvings (1/2, 1/4) measured 4.87-4.97 ms (the quarter
+    // wave takes 0.235 ms, little less than the half).  HOBO_E2E_TAIL = halvings,
+    // HOBO_E2E_HEAD = first chunk in quarter waves (A/B knobs, tools/e2e_zc.sh).
+    int tail = 1;
+    if (const char* e = getenv("HOBO_E2E_TAIL")) tail = atoi(e);
+    long long head = std::max<long long>(kBM, per_wave / 2 / kBM * kBM);
+    if (const char* e = getenv("HOBO_E2E_HEAD")) head = std::max<long long>(kBM, per_wave * atoi(e) / 4 / kBM * kBM);
+    std::vector<long long> ends;   // the tail, smallest last
+    long long rest = B - std::min<long long>(head, B);
+    for (long long w = per_wave / 2, i = 0; i < tail && rest > 2 * w && w >= kBM; ++i, w /= 2) {
+      ends.push_back(w / kBM * kBM);
+      rest -= ends.back();
     }
+    sizes.push_back(std::min<long long>(head, B));
+    while (rest > 0) {
+      if (rest <= per_wave) { sizes.push_back(rest); break; }
+      if (rest <= 3 * per_wave) { sizes.push_back(rest - per_wave); sizes.push_back(per_wave); break; }
+      sizes.push_back(2 * per_wave);
+      rest -= 2 * per_wave;
+    }
+    sizes.insert(sizes.end(), ends.begin(), ends.end());
   }
   const long long chunk = *std::max_element(sizes.begin(), sizes.end());
   if (!t->cs) {
