@@ -511,12 +511,15 @@ def main():
     # launching stream, against SURVEY 8(d)'s algorithmic work
     st = t.launch_stats()
     i8 = st.get("i8_planes", 0)
+    f8 = i8 < 0                                  # e4m3 limbs (kind::f8f6f4): -planes
+    i8 = abs(i8)
     kms = statistics.mean(kern_ms)
     algo_flops, algo_bytes, nnz = algorithmic(order, N, B, mode)
     exec_flops = 2.0 * st["mma_macs"]
     burst, sustained, src = measured_peaks()
-    # int8 digit planes (kind::i8): the peak for that dtype is the measured bf16 peak x the
-    # nominal ratio 4.5 / 2.25 PFLOP/s = 2 (also measured: tools/mma_i8.cu, 8192 vs 4096 MAC/clk/SM)
+    # int8 digit planes (kind::i8) and e4m3 limbs (kind::f8f6f4): the peak for that dtype is the
+    # measured bf16 peak x the nominal ratio 4.5 / 2.25 PFLOP/s = 2 (also measured:
+    # tools/mma_i8.cu and tools/fp8_probe.cu, 8192 vs 4096 MAC/clk/SM)
     kind_ratio = 2.0 if i8 else 1.0
     burst, sustained = burst * kind_ratio, sustained * kind_ratio
     # the timed region is back-to-back steps with clocks at max (see "clocks"): judged against
@@ -540,17 +543,18 @@ def main():
                            "contraction kernel's CUDA-event time"),
             "nnz": nnz, "algorithmic_flops_per_launch": algo_flops, "algorithmic_bytes_per_launch": algo_bytes,
             "achieved_gbs": achieved_b, "frac_of_hbm": achieved_b / hbm_peak,
-            "kernel": f"kr_gemm_kernel<{'I8' if i8 else 'bf16'}> (open-index contraction, {mode} mode)",
+            "kernel": f"kr_gemm_kernel<{'F8' if f8 else 'I8' if i8 else 'bf16'}> (open-index contraction, {mode} mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms, "launches_per_step": launches / max(1, a.steps),
             "frac_of_sustained": achieved / sustained,
             "executed_mma_flops_per_launch": exec_flops, "executed_tflops": exec_flops / (kms / 1e3) / 1e12,
             "frac_executed_of_peak": exec_flops / (kms / 1e3) / 1e12 / peak,
             "hw_nominal_tflops": hw, "frac_executed_of_hw_nominal": exec_flops / (kms / 1e3) / 1e12 / hw,
-            "mma_kind": f"i8 ({i8} digit planes, s32 accumulate)" if i8 else f"bf16 ({t.limbs} limbs, fp32 accumulate)",
-            "peak_source": (f"{src} bf16 dense (MEASURED_PEAKS.json) x 2 (nominal i8/bf16 ratio): burst {burst}, "
-                            f"sustained {sustained} TOP/s" if i8 else
+            "mma_kind": (f"e4m3 ({i8} limb planes, the stages' own limb counts; fp32 accumulate, exact)" if f8 else
+                         f"i8 ({i8} digit planes, s32 accumulate)" if i8 else f"bf16 ({t.limbs} limbs, fp32 accumulate)"),
+            "peak_source": (f"{src} bf16 dense (MEASURED_PEAKS.json) x 2 (nominal {'fp8' if f8 else 'i8'}/bf16 ratio): "
+                            f"burst {burst}, sustained {sustained} TFLOP/s" if i8 else
                             f"{src} bf16 dense (MEASURED_PEAKS.json): burst {burst}, sustained {sustained} TFLOP/s"),
-            "hw_nominal_source": "4096 bf16 MAC/clk/SM (x2 for i8) x 148 SMs x the run's median SM clock"}
+            "hw_nominal_source": "4096 bf16 MAC/clk/SM (x2 for i8 / e4m3) x 148 SMs x the run's median SM clock"}
 
     extras = {}
     if world > 1 and a.config == "cfg3" and scaling == "strong":
@@ -666,7 +670,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
-                "vs_baseline": None, "dtype": "i8" if i8 else "bf16", "data": "synthetic",
+                "vs_baseline": None, "dtype": "e4m3 (exact limbs)" if f8 else "i8" if i8 else "bf16", "data": "synthetic",
                 "config": {"workload": wl_text, "name": a.config, "order": order, "N": N,
                            "global_batch": units, "batch_per_gpu": B, "limbs": t.limbs,
                            "parallelism": f"dp{world} (H replicated, batch sharded{' by hobo_shard' if scaling == 'strong' else ''})",

@@ -22,6 +22,9 @@
  *       HOBO_PAIR=1|0        CTA-pair (cta_group::2) contraction on / off
  *       HOBO_SA_KERNEL=ring|stage|pair   the persistent annealing kernel
  *       HOBO_I8=1|0          int8 digit planes (kind::i8) whenever exact / never
+ *       HOBO_F8=1|0          e4m3 limbs (kind::f8f6f4) also on non-integer instances when
+ *                            the split is exact / never (default: integer instances whose
+ *                            limbs save >= 20% of the tensor-core cycles)
  *       HOBO_CT_DESC=1|0     column tiles longest-first (default when the last tile is the
  *                            heaviest) / in index order
  *       HOBO_PERSIST=1|0     the persistent energy kernel (short K loops, e.g. QUBO) on / off
@@ -314,8 +317,10 @@ hobo_status hobo_best_from_key(uint64_t key, hobo_best* best);
 hobo_status hobo_last_launch_stats(hobo_tensor* t, int64_t* launches, double* mma_macs,
                                    double* algo_macs, double* kernel_ms);
 /* The MMA kind of the last call's contraction: *i8_planes = the number of int8 digit planes
- * (tcgen05.mma kind::i8), or 0 for bf16 limbs (kind::f16).
- * mma_macs above counts 8-bit MACs in the first case, bf16 MACs in the second.            */
+ * (tcgen05.mma kind::i8), MINUS the number of e4m3 limb
+ * planes (kind::f8f6f4; the stages multiply only the limbs they
+ * need), or 0 for bf16 limbs (kind::f16).  mma_macs above counts 8-bit MACs in the first two
+ * cases, bf16 MACs in the third.                                                           */
 hobo_status hobo_last_launch_kind(const hobo_tensor* t, int* i8_planes);
 /* profiling on/off: record CUDA events around every contraction-kernel launch.         */
 hobo_status hobo_set_profiling(hobo_tensor* t, int enable);

@@ -75,6 +75,9 @@ struct DevLayout {
   __nv_bfloat16* W = nullptr;          // bf16 limb planes, or (i8 > 0) int8 digit planes
   int i8 = 0;                          // int8 digit planes: their count; 0 = bf16 limbs
   double qscale = 1.0;                 // int8: cell = qscale * (digit integer)
+  bool f8 = false;                     // the i8 1-byte planes hold e4m3 limbs (kind::f8f6f4)
+  float fscale = 1.0f;                 // e4m3: F = fscale * accumulator (2^(s + 9))
+  double f8_density = 0.0;             // e4m3: mean limb boxes per stage (MMA work vs one plane)
   int2* d_sched = nullptr;
   std::vector<int32_t> sched;
   alignas(64) CUtensorMap tmap;
@@ -132,6 +135,10 @@ struct hobo_tensor {
   std::vector<uintptr_t> search_key;
   long long items_B = -1; int items_nct = 0;            // ... computed for this batch and tiling
   int dig = -1;            // int8 digit planes of slots 0/1 (0 = bf16 limbs; -1 = not decided yet)
+  int f8 = -1;             // e4m3 limbs of slots 0/1 (0 = none; -1 = not decided yet)
+  int f8_s = 0;            // their scale exponent: limbs of cell * 2^-f8_s
+  bool f8_off[2] = {false, false};   // slot measured not worth it (too many second limbs)
+  std::vector<uint32_t> srec_host;   // the stage records (their headers carry the e4m3 limb counts)
   // scratch (grown on demand)
   uint32_t* d_bits = nullptr; size_t bits_cap = 0;
   double* d_Q = nullptr; size_t Q_cap = 0;
@@ -251,9 +258,9 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-template <int NT, bool REAL, bool I8 = false>
+template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  auto* k = kr_gemm_kernel<NT, REAL, false, false, I8>;
+  auto* k = kr_gemm_kernel<NT, REAL, false, false, I8, F8>;
   const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
   if (cudaError_t e = set_smem(k, smem)) return e;
   const int mb = (REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
@@ -271,9 +278,9 @@ cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) 
 }
 
 // CTA pairs: clusters of 2 (adjacent candidate blocks of one column tile), cta_group::2 MMAs
-template <int NT, bool REAL, bool I8 = false>
+template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
-  auto* k = kr_gemm_kernel<NT, REAL, false, true, I8>;
+  auto* k = kr_gemm_kernel<NT, REAL, false, true, I8, F8>;
   const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
   if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
@@ -305,6 +312,11 @@ bool use_pairs(const DevLayout& L, const KrParams& p) {
 }
 
 cudaError_t launch_kr_any(const DevLayout& L, const KrParams& p, cudaStream_t s) {
+  if (L.f8) {
+    if (use_pairs(L, p))
+      return L.NT == 128 ? launch_kr_pair<128, false, true, true>(L, p, s) : launch_kr_pair<256, false, true, true>(L, p, s);
+    return L.NT == 128 ? launch_kr<128, false, true, true>(L, p, s) : launch_kr<256, false, true, true>(L, p, s);
+  }
   if (L.i8) {
     if (use_pairs(L, p)) return L.NT == 128 ? launch_kr_pair<128, false, true>(L, p, s) : launch_kr_pair<256, false, true>(L, p, s);
     return L.NT == 128 ? launch_kr<128, false, true>(L, p, s) : launch_kr<256, false, true>(L, p, s);
@@ -372,6 +384,68 @@ int digit_planes(hobo_tensor* t) {
   return d;
 }
 
+// e4m3 limbs (kind::f8f6f4 at the int8 rate, one fp32 accumulator) for the binary energy /
+// field layouts of INTEGER instances: every degree >= 2
+// cell c, scaled by 2^-s so that max |c| 2^-s <= 448, must split exactly into <= 3 e4m3 limbs
+// (greedy round-to-nearest, the layout kernel's split).  Binary-integer-encoded instances
+// (cells = small integers x powers of two) need one limb for almost every cell, so a stage
+// multiplies one limb box at the int8 rate, twice the bf16 rate; the limbs are exact and the
+// accumulation is exact in fp32 under the bf16 path's own condition (integer cells,
+// sum |H| < 2^24).  HOBO_F8=0 / =1: never / also for non-integer instances when the split is
+// exact.  Returns the limb planes needed (0: not used).
+double e4m3_rn(double v) {   // round to nearest even on the e4m3 grid (|v| <= 448 assumed)
+  const double a = std::fabs(v);
+  if (a == 0.0) return 0.0;
+  int e = std::ilogb(a);
+  const double q = std::ldexp(1.0, std::max(e, -6) - 3);   // the grid step (subnormals below 2^-6)
+  const double r = std::nearbyint(a / q) * q;
+  return v < 0 ? -r : r;
+}
+
+int e4m3_limbs(hobo_tensor* t) {
+  if (t->f8 >= 0) return t->f8;
+  t->f8 = 0;
+  const HostTensor& H = t->host;
+  const char* e = getenv("HOBO_F8");
+  if (e && e[0] == '0') return 0;
+  const char* ei = getenv("HOBO_I8");
+  if (ei && ei[0] == '1') return 0;   // int8 digit planes forced
+  if (H.order < 2 || t->kl.Tpad / kBK < 64) return 0;   // short K loops: the persistent / bf16 kernels
+  if (!H.is_integer && !(e && e[0] == '1')) return 0;
+  if (H.is_integer && !(H.sum_abs < 16777216.0)) return 0;
+  if (KrCfg<256, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl)) > kMaxSmem) return 0;
+  double amax = 0.0;
+  for (int r = 2; r <= H.order; ++r)
+    for (float c : H.strict[r]) amax = std::max(amax, (double)std::fabs(c));
+  if (amax == 0.0) return 0;
+  // s >= 0 on integer instances: every limb is then an integer in cell units (a cell >= 16 has
+  // a grid step >= 1, a smaller one is a single exact limb), so each partial sum is an integer
+  // multiple of 2^-(s+9) bounded by sum |H| < 2^24 of them: exact in fp32.  Otherwise the largest
+  // cell is scaled into [224, 448] (the most headroom above the subnormal floor).
+  int sexp = 0;
+  while (std::ldexp(amax, -sexp) > 448.0) ++sexp;
+  if (!H.is_integer)
+    while (sexp > -60 && std::ldexp(amax, -(sexp - 1)) <= 448.0) --sexp;
+  int need = 1;
+  for (int r = 2; r <= H.order && need <= 3; ++r)
+    for (float c : H.strict[r]) {
+      double v = std::ldexp((double)c, -sexp);
+      int l = 0;
+      while (v != 0.0 && l < 4) {
+        const double h = e4m3_rn(v);
+        if (h == 0.0) { l = 4; break; }   // below the e4m3 grid: not representable
+        v -= h;                            // exact (h is v rounded to 4 significant bits)
+        ++l;
+      }
+      if (l > need) need = l;
+      if (need > 3) break;
+    }
+  if (need > 3) return 0;
+  t->f8_s = sexp;
+  t->f8 = need;
+  return need;
+}
+
 hobo_status check_device(hobo_tensor* t) {
   if (t->poisoned) return fail(HOBO_ESTATE, "handle poisoned by an earlier CUDA error");
   if (!t->dev_init) return init_device(t);
@@ -419,8 +493,16 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   const HostTensor& H = t->host;
   const int N = H.N, k = H.order;
   L.i8 = slot <= 1 ? digit_planes(t) : slot == 5 ? H.digits : 0;
+  L.f8 = false;
+  if (slot <= 1 && !t->f8_off[slot] && e4m3_limbs(t) > 0) {   // tried first; kept if the scan says it pays
+    L.i8 = e4m3_limbs(t);
+    L.f8 = true;
+    if (const char* ex = getenv("HOBO_KR_EXP"))   // MEASUREMENT ONLY: 4 = one limb plane (results wrong)
+      if (atoi(ex) & 4) L.i8 = 1;
+    L.fscale = (float)std::ldexp(1.0, t->f8_s + 9);   // A = e4m3 0x01 = 2^-9
+  }
   L.NT = (N <= 128 || slot == 2 || slot == 4) ? 128 : 256;   // a 128-column tile when N fits (no padded columns)
-  if (L.i8 >= 2) L.NT = 128;                    // TMEM: i8 accumulators of NT columns + the A stages
+  if (L.i8 >= 2 && !L.f8) L.NT = 128;           // TMEM: i8 accumulators of NT columns + the A stages
   if (slot == 5) {                              // the int8 persistent kernel's tiles: 64 columns, two
     const char* e = getenv("HOBO_PERSIST_I8_NT");   // accumulator sets (128: one set, measured slower)
     L.NT = (e && atoi(e) == 128) ? 128 : 64;
@@ -467,6 +549,7 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
     }
     CK(cudaMalloc(&t->d_srec, rec.size() * 4));
     CK(cudaMemcpy(t->d_srec, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice));
+    t->srec_host = std::move(rec);
   }
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
@@ -504,13 +587,64 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
     lp.L = planes;
     lp.field_mode = field;
     lp.NT = L.NT;
+    int* d_err = nullptr;
     if (L.i8) {
       lp.Wout8 = reinterpret_cast<uint8_t*>(L.W);
       lp.inv_qscale = std::ldexp(1.0, -H.qexp);
     }
+    if (L.f8) {
+      lp.f8_scale = std::ldexp(1.0, -t->f8_s);
+      CK(cudaMalloc(&d_err, sizeof(int)));
+      CK(cudaMemset(d_err, 0, sizeof(int)));
+      lp.err = d_err;
+    }
     layout_kernel<<<148 * 8, 256>>>(lp);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
+    if (L.f8) {
+      // each stage's limb count per column tile (the most limb planes a cell of its box needs),
+      // into bits [shift + 2 ct, shift + 2 ct + 2) of the stage record's header word w
+      int err = 0;
+      CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+      cudaFree(d_err);
+      const char* ex = getenv("HOBO_KR_EXP");
+      if (err && !(ex && (atoi(ex) & 4)))
+        return fail(HOBO_ECUDA, "e4m3 limb split inexact on the device (host and device grids disagree)");
+      const int64_t n_kbp = Tpad / (2 * kBK);
+      std::vector<uint32_t> nl((size_t)L.n_ct * n_kbp, 1u);
+      uint32_t* d_nl = nullptr;
+      CK(cudaMalloc(&d_nl, nl.size() * 4));
+      CK(cudaMemcpy(d_nl, nl.data(), nl.size() * 4, cudaMemcpyHostToDevice));
+      f8_limbs_kernel<<<148 * 8, 256>>>(reinterpret_cast<const uint8_t*>(L.W), L.i8, L.n_ct, n_kbp, L.NT, d_nl);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(nl.data(), d_nl, nl.size() * 4, cudaMemcpyDeviceToHost));
+      cudaFree(d_nl);
+      double sum = 0;
+      for (uint32_t v : nl) sum += v;
+      L.f8_density = sum / (double)nl.size();
+      const int shift = field ? 0 : 16;
+      for (int64_t P = 0; P < n_kbp; ++P) {
+        uint32_t& w = t->srec_host[(size_t)P * t->srec_u4 * 4 + 3];
+        w &= ~(0xFFFFu << shift);
+        for (int ct = 0; ct < L.n_ct; ++ct) w |= (uint32_t)nl[(size_t)ct * n_kbp + P] << (shift + 2 * ct);
+      }
+      CK(cudaMemcpy(t->d_srec, t->srec_host.data(), t->srec_host.size() * 4, cudaMemcpyHostToDevice));
+      // a limb box costs half a bf16 limb box (as an int8 digit plane does): keep e4m3 only
+      // when it saves >= 20% of the tensor-core cycles of the path chosen otherwise, else
+      // rebuild this slot's layout with int8 digits / bf16 limbs
+      const int dp = digit_planes(t);
+      const double other = dp ? 0.5 * dp : (double)H.limbs;
+      if (0.5 * L.f8_density > 0.8 * other) {
+        for (int r = 2; r <= k; ++r) cudaFree(dstrict[r]);
+        cudaFree(d_strict_ptrs);
+        cudaFree(d_bt);
+        cudaFree(d_tup);
+        cudaFree(L.W);
+        L = DevLayout();
+        t->f8_off[slot] = true;
+        return ensure_layout(t, slot);
+      }
+    }
     for (int r = 2; r <= k; ++r) cudaFree(dstrict[r]);
     cudaFree(d_strict_ptrs);
     cudaFree(d_bt);
@@ -524,7 +658,7 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
   // 3-D view of the tile-blocked planes: (64 tuples, NT rows, box index), box = one block
   // (int8 digit planes: 128-byte rows = K-block pairs, boxes (128 tuples, NT rows, pair index))
   const int64_t n_kb = Tpad / kBK;
-  const int inner = L.i8 ? 2 * kBK : kBK;          // elements per 128-byte box row
+  const int inner = L.i8 ? 2 * kBK : kBK;          // elements per 128-byte box row (e4m3 limbs: UINT8 too)
   const int64_t nbox = L.i8 ? n_kb / 2 : n_kb;
   const CUtensorMapDataType dt = L.i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B;
@@ -597,9 +731,13 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.nseg = t->kl.nseg;
   p.L = L.i8 ? L.i8 : t->host.limbs;
   p.qscale = L.qscale;
+  p.fscale = L.fscale;
   p.srec = t->d_srec;
   p.srec_u4 = L.i8 ? t->srec_u4 : 0;
   p.field_mode = (&L == &t->lay[0] || &L == &t->lay[4] || &L == &t->lay[5]) ? 0 : 1;
+  p.nl_shift = p.field_mode ? 0 : 16;
+  p.exp = 0;
+  if (const char* e = getenv("HOBO_KR_EXP")) p.exp = atoi(e);
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
   p.wp = L.wp;
   return p;
@@ -625,7 +763,8 @@ double exec_macs(hobo_tensor* t, const DevLayout& L, long long B) {
   double kb = 0;
   for (int ct = 0; ct < L.n_ct; ++ct)
     for (int j = 0; j < t->kl.nseg; ++j) kb += L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1];
-  return kb * kBK * (double)L.NT * kBM * (double)((B + kBM - 1) / kBM) * (L.i8 ? L.i8 : t->host.limbs);
+  return kb * kBK * (double)L.NT * kBM * (double)((B + kBM - 1) / kBM) *
+         (L.f8 ? L.f8_density : L.i8 ? L.i8 : t->host.limbs);
 }
 
 // SURVEY 8(d)'s algorithmic work: nnz MACs (2 nnz flops) per candidate for the energy, 2 nnz
@@ -795,7 +934,7 @@ hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long 
   use = nullptr;
   if (const char* e = getenv("HOBO_SK"))
     if (e[0] == '0') return HOBO_OK;
-  const int KPS = L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
+  const int KPS = L.i8 ? 2 : L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
   std::vector<int> tot(L.n_ct, 0);
   for (int ct = 0; ct < L.n_ct; ++ct)
     for (int j = 0; j < t->kl.nseg; ++j) tot[ct] += (L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1] + KPS - 1) / KPS;
@@ -932,7 +1071,7 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     if (t->profile) { CK(record_event(t->ev1, s)); t->ev_valid = true; }
     t->last_launches = 2;
     t->last_mma_macs = exec_macs(t, L, B);
-    t->last_i8 = L.i8;
+    t->last_i8 = L.f8 ? -L.i8 : L.i8;
     t->last_algo_macs = algo_macs(t, false, B);
     return HOBO_OK;
   }
@@ -985,7 +1124,7 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
     if (const char* e = getenv("HOBO_CB_ITERS")) p.cb_iters = std::max(1, atoi(e));
   }
   const hobo_tensor::SkPlan* sk = nullptr;
-  if (field && !P && !L.i8 && use_pairs(L, p) && slot == 1)
+  if (field && !P && (!L.i8 || L.f8) && use_pairs(L, p) && slot == 1)
     if (hobo_status st = sk_plan(t, L, p, B, sk, s)) return st;
   if (sk) {
     p.n_split = 1;
@@ -996,7 +1135,8 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   }
   if (p.n_split > 1) {
     if (field) {
-      if (hobo_status st = grow(t, t->d_Gpart, t->Gpart_cap, (size_t)p.n_split * B * t->host.N * (L.i8 ? 2 : 1))) return st;
+      if (hobo_status st = grow(t, t->d_Gpart, t->Gpart_cap, (size_t)p.n_split * B * t->host.N * (L.i8 && !L.f8 ? 2 : 1)))
+        return st;
       p.G = t->d_Gpart;
     }
     if (hobo_status st = grow(t, t->d_Qpart, t->Qpart_cap, (size_t)p.n_split * L.n_ct * B)) return st;
@@ -1015,12 +1155,12 @@ hobo_status contract(hobo_tensor* t, int field, const uint8_t* X, long long B, f
   if (p.n_split > 1) {
     const long long nG = field ? B * t->host.N : 0, nQ = (long long)L.n_ct * B;
     splitk_reduce_kernel<<<(unsigned)std::min<long long>((std::max(nG, nQ) + 255) / 256, 148 * 8), 256, 0, s>>>(
-        t->d_Gpart, G, nG, t->d_Qpart, t->d_Q, nQ, p.n_split, L.i8 ? 1 : 0);
+        t->d_Gpart, G, nG, t->d_Qpart, t->d_Q, nQ, p.n_split, L.i8 && !L.f8 ? 1 : 0);
     CK(cudaGetLastError());
     t->last_launches += 1;
   }
   t->last_mma_macs = exec_macs(t, L, B) * p.LA;
-  t->last_i8 = L.i8;
+  t->last_i8 = L.f8 ? -L.i8 : L.i8;
   t->last_algo_macs = algo_macs(t, field != 0, B);
   return HOBO_OK;
 }
@@ -1420,7 +1560,7 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   }
   t->last_launches = launches;
   t->last_mma_macs = exec_macs(t, L, B);
-  t->last_i8 = L.i8;
+  t->last_i8 = L.f8 ? -L.i8 : L.i8;
   t->last_algo_macs = algo_macs(t, field != 0, B);
   return HOBO_OK;
 }
@@ -1527,7 +1667,7 @@ hobo_status run_search(hobo_tensor* t, uint64_t seed, int64_t chain0, int64_t nc
   }
   if (t->profile) { CK(cudaEventRecord(t->ev1, s)); t->ev_valid = true; }
   t->last_mma_macs = exec_macs(t, L, B) * (double)(iters + 1);
-  t->last_i8 = L.i8;
+  t->last_i8 = L.f8 ? -L.i8 : L.i8;
   t->last_algo_macs = algo_macs(t, true, B) * (double)(iters + 1);
   return HOBO_OK;
 }

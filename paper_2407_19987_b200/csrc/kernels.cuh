@@ -52,6 +52,11 @@ struct KrParams {
   double wdeg[8];           // field mode: weight lcm/r of the degree-r part of the energy
   double wp;                // weight of the degree-1 term
   double qscale;            // int8 digit planes (kr_gemm_kernel<..., I8>): cell = qscale * sum_l 256^l d_l
+  float fscale;             // e4m3 limbs (kr_gemm_kernel<..., I8, F8>): F = fscale * accumulator
+  int exp;                  // MEASUREMENT ONLY (HOBO_KR_EXP, 1-byte plane launches): 1 = the generator
+                            // skips the run decode, 2 = skips the TMEM store; results are wrong
+  int nl_shift;             // e4m3 limbs: the stage record's limb counts for this layout start at bit
+                            // nl_shift of its header's w (2 bits per column tile)
   const uint4* srec;        // int8: per K-block pair, {runs of 2P, runs of 2P+1, nfix, 0} + the runs
   int srec_u4;              // int8: uint4s per record (the descriptor ring's slot size)
   // simulated annealing (kr_gemm_kernel<NT, false, true>): one launch per visited site m with
@@ -287,6 +292,32 @@ __device__ __forceinline__ void issue_i8_stage(uint32_t tmem, uint32_t a_t, uint
   }
 }
 
+// e4m3 limbs: nl limb boxes of the stage (a K-block pair, or nkb = 1 K-block), all into the ONE
+// fp32 accumulator (the limbs of a cell sum exactly: their products with A = 2^-9 are exact in
+// fp32); only the stage's first MMA may start the accumulator
+template <int NT, bool PAIR>
+__device__ __forceinline__ void issue_f8_stage(uint32_t tmem, uint32_t a_t, uint32_t sbase, uint32_t boxb, uint32_t issued,
+                                               int nl, int nkb) {
+  constexpr uint32_t id = idesc_e4m3_f32(PAIR ? 2 * kBM : kBM, NT);
+  if (nkb == 2 && nl == 1) {   // the common stage
+    const uint64_t bd = sw128_kmajor_desc(sbase);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      if constexpr (PAIR) umma_f8_ts_pair(tmem, a_t + 8u * kk, bd + 2u * kk, id, kk ? 1u : issued);
+      else umma_f8_ts(tmem, a_t + 8u * kk, bd + 2u * kk, id, kk ? 1u : issued);
+    }
+    return;
+  }
+  for (int l = 0; l < nl; ++l) {
+    const uint64_t bd = sw128_kmajor_desc(sbase + (uint32_t)l * boxb);
+    for (int kk = 0; kk < 2 * nkb; ++kk) {
+      const uint32_t acc = (l | kk) ? 1u : issued;
+      if constexpr (PAIR) umma_f8_ts_pair(tmem, a_t + 8u * kk, bd + 2u * kk, id, acc);
+      else umma_f8_ts(tmem, a_t + 8u * kk, bd + 2u * kk, id, acc);
+    }
+  }
+}
+
 // One pipeline stage = KPS consecutive K-blocks of one segment (x L limb boxes of W).
 // Ring slot s holds the stage's W boxes in shared memory and its A K-blocks in TMEM;
 // FULL(s) completes when the 8 generator warps arrived and the TMA bytes landed, EMPTY(s)
@@ -295,9 +326,15 @@ __device__ __forceinline__ void issue_i8_stage(uint32_t tmem, uint32_t a_t, uint
 // blocks of one column tile and share every W box: each loads half of its NT rows, the
 // leader issues cta_group::2 MMAs (M = 256: 128 rows of A in each CTA's TMEM), so one MMA
 // instruction covers both SMs and each SM's shared memory carries half the W stream.
-template <int NT, bool REAL, bool SA = false, bool PAIR = false, bool I8 = false>
+// F8 (with I8): the 1-byte planes hold e4m3 limbs of the cells scaled by 2^-s instead of int8
+// digits; the generator's A bytes 0x01 are e4m3 2^-9, the MMAs are kind::f8f6f4 into one fp32
+// accumulator, F = 2^(s+9) * accumulator; a stage loads and multiplies only the limb boxes its
+// column tile needs (the stage record's limb count, 1 almost everywhere on integer-encoded
+// instances)
+template <int NT, bool REAL, bool SA = false, bool PAIR = false, bool I8 = false, bool F8 = false>
 __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
   static_assert(!(PAIR && SA), "CTA pairs: not for the per-site annealing launch");
+  static_assert(!F8 || I8, "e4m3 limbs run on the 1-byte plane path");
   static_assert(!(I8 && (REAL || SA)), "int8 digit planes: binary candidates, energy / field launches");
   using C = KrCfg<NT, I8>;
   extern __shared__ uint8_t smem_raw[];
@@ -335,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const int MB = (PAIR || SA || REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
   const int ncb_eff = PAIR ? (p.n_cb + 1) / 2 : (p.n_cb + MB - 1) / MB;
   const int bid = PAIR ? (int)(blockIdx.x / 2) : (int)blockIdx.x;
-  const bool sk = PAIR && !I8 && p.units != nullptr;   // stream-K unit (see KrParams::units)
+  const bool sk = PAIR && (!I8 || F8) && p.units != nullptr;   // stream-K unit (see KrParams::units)
   const int4 unit = sk ? __ldg(p.units + bid) : make_int4(0, 0, 0, 0);
   const int sk_part = sk ? (unit.w >> 20) - 1 : -1;
   const int ct_i = (bid / ncb_eff) % p.n_ct;
@@ -356,7 +393,15 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
                  : DEC ? C::nstw(p.L, PAIR ? 2 * ring : ring)
                        : C::nst_c(p.L, PAIR ? 2 * ring : ring);
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
-  const int NSTA = DEC ? C::nsta(p.L) : NST;                       // A stages (DEC: own ring)
+  const int NSTA = DEC ? C::nsta(F8 ? 1 : p.L) : NST;              // A stages (DEC: own ring)
+  const int NACC = F8 ? 1 : I8 ? p.L : 1;                          // accumulators in TMEM [0, NACC * NT)
+  // F8: the limb count of stage n of this CTA (its record, in the descriptor ring)
+  const uint4* dsm_rec = reinterpret_cast<const uint4*>(gbase + (sD - base));
+  auto stage_nl = [&](int n) -> int {
+    mbar_wait(DFULL(n & (C::MAXD - 1)), (uint32_t)(n >> 4) & 1u);
+    const int v = (int)((dsm_rec[(size_t)(n & (C::MAXD - 1)) * p.srec_u4].w >> (p.nl_shift + 2 * ct)) & 3u);
+    return v ? v : 1;
+  };
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
   __shared__ int ssa[SA ? kBM : 1];   // annealing: this CTA's decisions for site sa_m
   if (threadIdx.x == 0) {
@@ -481,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
     if (lane == 0) {
       int st = 0;                    // ring slot and phase, advanced per stage (no divisions)
       uint32_t ph = 0;
+      int pn = 0;                    // stage counter (F8: the record holding its limb count)
       // I8: the A generator's K-block descriptors, bulk-copied DAHEAD stages ahead of the W
       // boxes into a ring of their own (slot m % MAXD is reused only after the generator is
       // done with stage m - MAXD <= the stage whose W slot was just freed)
@@ -511,8 +557,9 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
           mbar_wait(EMPTY(st), ph ^ 1u);
           if constexpr (DEC) dissue();
           if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
-            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)p.L * C::BOX);
-            for (int l = 0; l < p.L; ++l) {
+            const int nl = F8 ? stage_nl(pn) : p.L;
+            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)nl * C::BOX);
+            for (int l = 0; l < nl; ++l) {
               const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1);
               const uint32_t dst = sB + st * stage_bytes + (uint32_t)l * BOXB;
               if constexpr (PAIR) tma_load_3d_pair(dst, &tmap, mapa_shared(FULL(st), 0), 0, (int)prank * (NT / 2), box);
@@ -530,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
               }
           }
           if (++st == NST) { st = 0; ph ^= 1u; }
+          ++pn;
         }
       }
     }
@@ -543,6 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       int st = 0, sa = 0;            // W and A ring slots and phases, advanced per stage
       uint32_t ph = 0, pha = 0;
       uint32_t issued = 0;
+      int mn = 0;                    // stage counter (F8: limb counts)
       for (int it = 0; it < ntile; ++it) {
       if (it > 0) {   // the previous block's epilogue has read the accumulator
         mbar_wait(acc_empty, (uint32_t)((it - 1) & 1));
@@ -553,11 +602,16 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
           const int nkb = min(KPS, s.x + s.y - kb0);
+          const int nl = F8 ? stage_nl(mn) : 0;
+          ++mn;
           mbar_wait(FULL(st), ph);
           if (DEC) mbar_wait(FULLA(sa), pha);
           tc_fence_after();
           if (elect_one()) {
-            if constexpr (I8) {   // KPS K-blocks x L digit planes, each into its own accumulator
+            if constexpr (F8) {
+              issue_f8_stage<NT, PAIR>(tmem, tmem + (uint32_t)(NT + sa * KPS * C::A_COLS), sB + st * stage_bytes, BOXB,
+                                       issued, nl, nkb);
+            } else if constexpr (I8) {   // KPS K-blocks x L digit planes, each into its own accumulator
               const uint32_t a_t = tmem + (uint32_t)(p.L * NT + sa * KPS * C::A_COLS);
               const uint32_t sbase = sB + st * stage_bytes;
               if (nkb == 2 && p.L == 3) issue_i8_stage<3, NT, PAIR>(tmem, a_t, sbase, BOXB, issued);
@@ -686,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       }
     };
     auto xsum = [&](void) -> double {  // sum over this warp's columns of x_m * F_m (p_m * F_m)
-      if constexpr (I8) {
+      if constexpr (I8 && !F8) {
         long long acc = 0;
         for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
           const int mbase = ct * NT + c0;
@@ -716,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             if ((xw >> c) & 1u) acc += (double)__uint_as_float(r[c]);
         }
       }
+      if constexpr (F8) acc *= (double)p.fscale;
       return acc;
     };
     for (int it = 0; it < ntile; ++it) {
@@ -785,14 +840,23 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
             const uint4* rec = dsm + (size_t)wst * p.srec_u4;
             const uint4 hd = rec[0];
             uint32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+            if (p.exp & 1) { l0 = hd.x * (uint32_t)row; h0 = l0 ^ hd.y; l1 = h0 + 1; h1 = l1 * 3u; }
+            else {
             for (uint32_t i = 0; i < hd.x; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + i], hd.z, l0, h0);
             for (uint32_t i = 0; i < hd.y; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], hd.z, l1, h1);
+            }
             uint32_t w[32];   // the K-block pair's bytes in the planes' permuted K order
             expand_bytes64(((uint64_t)h0 << 32) | l0, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
             expand_bytes64(((uint64_t)h1 << 32) | l1, *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
             mbar_wait(EMPTYA(gst), gph ^ 1u);
             tc_fence_after();
-            tmem_st32(lane_base + (uint32_t)(p.L * NT + gst * KPS * C::A_COLS), w);
+            if (!(p.exp & 2)) tmem_st32(lane_base + (uint32_t)(NACC * NT + gst * KPS * C::A_COLS), w);
+            else {   // keep w live
+              uint32_t x = 0;
+#pragma unroll
+              for (int c = 0; c < 32; ++c) x ^= w[c];
+              if (x == 0x9E3779B9u) xs[0] = 0u;
+            }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -879,7 +943,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         pmv[c] = v4.x; pmv[c + 1] = v4.y; pmv[c + 2] = v4.z; pmv[c + 3] = v4.w;
       }
       float g[32];
-      if constexpr (I8) {   // exact integer field; one rounding to fp32 after adding the degree-1 cell
+      if constexpr (I8 && !F8) {   // exact integer field; one rounding to fp32 after adding the degree-1 cell
         long long v[32];
         if (any) load_i8(c0, v);
         else {
@@ -912,7 +976,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       }
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
-        const float v = __uint_as_float(r[c]);
+        const float v = F8 ? __uint_as_float(r[c]) * p.fscale : __uint_as_float(r[c]);
         const float pm = pmv[c];   // degree 1 counted once
         g[c] = v + pm;
         if constexpr (REAL) {
@@ -947,7 +1011,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
               if (c < nvalid) gout[c] += sf * g[c];
           }
         }
-      } else if (p.field_mode && live && !(I8 && p.n_split > 1)) {
+      } else if (p.field_mode && live && !(I8 && !F8 && p.n_split > 1)) {
         float* gout = p.G + ((size_t)split * p.B + b) * p.N + mbase;
         int nvalid = min(32, p.N - mbase);
         if (sk_part >= 0) {   // a K range of a split tile: its partial fields, every column of the tile
@@ -1191,11 +1255,50 @@ struct LayoutParams {
   __nv_bfloat16* Wout;           // [L][Npad][Tpad]
   uint8_t* Wout8 = nullptr;      // int8 digit planes instead (non-null): [L][n_ct][n_kb/2][NT][128] bytes
   double inv_qscale = 1.0;       // cell / qscale = the integer the digits encode
+  double f8_scale = 0.0;         // > 0: the 1-byte planes hold e4m3 limbs of cell * f8_scale instead
+  int* err = nullptr;            // e4m3: set when a cell does not split exactly into L limbs
   long long Tpad;
   int N, Npad, L, field_mode, NT;
 };
 
 __device__ __forceinline__ long long dbinom(const long long* t, int n, int i) { return (n < i || i < 0) ? 0 : t[n * 7 + i]; }
+
+// the e4m3 grid: round to nearest even (|v| <= 448), and the byte of an exact e4m3 value
+__device__ __forceinline__ double e4m3_rn_d(double v) {
+  const double a = fabs(v);
+  if (a == 0.0) return 0.0;
+  const int e = ilogb(a);
+  const double q = ldexp(1.0, max(e, -6) - 3);
+  const double r = rint(a / q) * q;
+  return v < 0 ? -r : r;
+}
+__device__ __forceinline__ uint8_t e4m3_byte(double h) {
+  if (h == 0.0) return 0;
+  const uint32_t sgn = h < 0 ? 0x80u : 0u;
+  const double a = fabs(h);
+  const int e = ilogb(a);
+  if (e < -6) return (uint8_t)(sgn | (uint32_t)(a * 512.0));                      // subnormal: m 2^-9
+  return (uint8_t)(sgn | ((uint32_t)(e + 7) << 3) | (uint32_t)((a * ldexp(1.0, -e) - 1.0) * 8.0));
+}
+
+// e4m3 limbs: nl[ct][P] = 1 + the highest limb plane with a nonzero byte in box (ct, P)
+// (nl preset to 1 by the caller); one warp per (limb >= 1, ct, P) box of NT x 128 bytes
+__global__ void f8_limbs_kernel(const uint8_t* __restrict__ W8, int L, int n_ct, long long n_kbp, int NT,
+                                unsigned int* __restrict__ nl) {
+  const long long nbox = (long long)(L - 1) * n_ct * n_kbp;
+  const int lane = threadIdx.x & 31;
+  for (long long wb = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; wb < nbox;
+       wb += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long l = 1 + wb / (n_ct * n_kbp), rest = wb % (n_ct * n_kbp);
+    const uint4* box = reinterpret_cast<const uint4*>(W8 + ((size_t)l * n_ct * n_kbp + rest) * NT * 128);
+    uint32_t any = 0;
+    for (int i = lane; i < NT * 8; i += 32) {
+      const uint4 v = box[i];
+      any |= v.x | v.y | v.z | v.w;
+    }
+    if (__any_sync(0xFFFFFFFFu, any != 0) && lane == 0) atomicMax(nl + rest, (unsigned int)(l + 1));
+  }
+}
 
 __global__ void layout_kernel(const LayoutParams lp) {
   const long long total = (long long)lp.Npad * lp.Tpad;
@@ -1227,13 +1330,23 @@ __global__ void layout_kernel(const LayoutParams lp) {
     }
     if (lp.Wout8) {
       // two's-complement base-256 digits of q = c / qscale: unsigned low digits, signed top digit
-      const long long q = __double2ll_rn((double)c * lp.inv_qscale);
+      const long long q = lp.f8_scale > 0.0 ? 0 : __double2ll_rn((double)c * lp.inv_qscale);
       const size_t plane = (size_t)lp.Npad * lp.Tpad;
       const long long n_kbp = lp.Tpad / 128;   // boxes of 128-byte rows: K-block pairs
       // K position of tuple t in its 128-byte row: within each 32-tuple group, tuple 8i + k at
       // byte 4k + i (the generator's one-shift expansion, expand_bytes64)
       const int tg = (int)(t % 128), j = tg % 32;
       const size_t off = ((size_t)((m / lp.NT) * n_kbp + t / 128) * lp.NT + (m % lp.NT)) * 128 + (tg - j) + 4 * (j % 8) + j / 8;
+      if (lp.f8_scale > 0.0) {   // e4m3 limbs: greedy round-to-nearest-even (hobo_api.cu e4m3_rn)
+        double v = (double)c * lp.f8_scale;
+        for (int l = 0; l < lp.L; ++l) {
+          const double h = e4m3_rn_d(v);
+          lp.Wout8[(size_t)l * plane + off] = e4m3_byte(h);
+          v -= h;
+        }
+        if (v != 0.0) atomicOr(lp.err, 1);
+        continue;
+      }
       for (int l = 0; l < lp.L; ++l) lp.Wout8[(size_t)l * plane + off] = (uint8_t)((q >> (8 * l)) & 0xFF);
       continue;
     }

@@ -453,7 +453,8 @@ class HoboTensor:
 
     def launch_stats(self):
         """Launches, executed MMA MACs, algorithmic MACs, (profiling on) kernel ms of the last call, and
-        its MMA kind: i8_planes = int8 digit planes (kind::i8, MACs are 8-bit) or 0 (bf16 limbs)."""
+        its MMA kind: i8_planes = int8 digit planes (kind::i8, MACs are 8-bit), minus the e4m3 limb
+        planes (kind::f8f6f4, MACs are 8-bit), or 0 (bf16 limbs)."""
         n, mm, am, ms, i8 = C.c_int64(), C.c_double(), C.c_double(), C.c_double(), C.c_int()
         _check(lib().hobo_last_launch_stats(self._h, C.byref(n), C.byref(mm), C.byref(am), C.byref(ms)))
         _check(lib().hobo_last_launch_kind(self._h, C.byref(i8)))

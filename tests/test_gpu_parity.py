@@ -11,6 +11,7 @@ import pytest
 from oracle import Oracle
 from workloads import (cfg3_problem, exhaustive_X, h, int_twin_cells, paper_grids, pythagoras,
                        random_integer_problem, seating, tsp, uniform_cells, x_bits)
+from workloads.gen import canonical_cells_all
 
 pytestmark = pytest.mark.gpu
 
@@ -1053,11 +1054,15 @@ def test_int8_digit_planes_choice(H, torch):
         t = make()
         t.energy(dev(torch, X))
         got = t.launch_stats()["i8_planes"]
-        assert (got == want) if want is not None else got in (0, 1)
+        assert (got == want) if want is not None else got in (0, 1, -1, -2, -3)
     p = cfg3_problem()
     t = H.HoboTensor.from_problem(p)
     t.local_field(dev(torch, x_bits(3, 128, 512)))
-    assert t.launch_stats()["i8_planes"] == 0
+    assert t.launch_stats()["i8_planes"] == -2             # e4m3 limbs (two planes, the second sparse)
+    with env("HOBO_F8", "0"):
+        t = H.HoboTensor.from_problem(p)
+        t.local_field(dev(torch, x_bits(3, 128, 512)))
+        assert t.launch_stats()["i8_planes"] == 0
     t = H.HoboTensor.import_cells(3, 64, *uniform_cells(3, 64, 1))
     t.energy(dev(torch, x_bits(1, 256, 64)))
     assert t.launch_stats()["i8_planes"] == 0              # 33 K-blocks: bf16
@@ -1098,4 +1103,110 @@ def test_int8_host_entry_points_and_search(H, torch):
         x, e, c = t.search(9, None, 20, chain0=0, nchains=300)
         assert t.launch_stats()["i8_planes"] >= 1
     r = o.search(9, 0, 300, 20)
+    assert (e, c) == (r["e_best"], r["best_chain"]) and np.array_equal(x, r["chain_xbest"][c])
+
+
+# ---- e4m3 limbs (tcgen05.mma kind::f8f6f4): exact on integer-encoded instances --------------
+def pow2_int_cells(order, N, seed, density=0.02, wide=0.0):
+    """Sparse integer cells shaped like binary-integer encodings: s * m * 2^e with m in
+    {1, 3, 5, 7} and e in [0, 8] (one e4m3 limb each); a fraction `wide` of them get a 9-12
+    significant-bit m instead (second and third limbs).  Exact in fp32; sum |H| < 2^24."""
+    idx = canonical_cells_all(order, N)
+    cid = h(seed, 1, np.arange(len(idx), dtype=np.uint64), 0)
+    keep = (cid % np.uint64(10000)) < np.uint64(int(density * 10000))
+    idx = idx[keep]
+    r = h(seed, 2, np.arange(len(idx), dtype=np.uint64), 0)
+    m = np.array([1, 3, 5, 7], np.int64)[(r % np.uint64(4)).astype(np.int64)]
+    e = ((r >> np.uint64(8)) % np.uint64(9)).astype(np.int64)
+    wm = ((r >> np.uint64(16)) % np.uint64(3840)).astype(np.int64) + 257   # 9-12 significant bits
+    is_wide = ((r >> np.uint64(32)) % np.uint64(10000)).astype(np.int64) < int(wide * 10000)
+    mag = np.where(is_wide, wm, m << e)
+    sgn = np.where((r >> np.uint64(48)) & np.uint64(1), -1, 1)
+    return idx, (sgn * mag).astype(np.float32)
+
+
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_e4m3_limbs_integer_instances(H, torch, pair):
+    """Integer instances on the e4m3-limb path (cfg3: 2 limb planes, the second needed by a
+    few degree-2 cells only; wide cells: 3 planes): fields, energies (field and energy modes)
+    and the argmin bit-exact against the oracle and equal to the bf16 path (HOBO_F8=0)."""
+    cases = [("cfg3", None, None, cfg3_problem(), 1000, -2),
+             ("pow2", 3, 200, pow2_int_cells(3, 200, 5), 700, -1),
+             ("wide", 3, 200, pow2_int_cells(3, 200, 6, wide=0.0003), 383, -3),
+             ("order4", 4, 60, pow2_int_cells(4, 60, 7, density=0.05), 300, None)]
+
+    def build(order, N, src):
+        if order is None:
+            return H.HoboTensor.from_problem(src), Oracle.from_problem(src)
+        return H.HoboTensor.import_cells(order, N, *src), Oracle.from_cells(order, N, *src)
+
+    with env("HOBO_PAIR", pair):
+        for name, order, N, src, B, want in cases:
+            t, o = build(order, N, src)
+            X = x_bits(17, B, t.N)
+            G, E = fields(H, torch, t, X)
+            kind = t.launch_stats()["i8_planes"]
+            assert kind < 0 and (want is None or kind == want), (name, kind)
+            Ee, best = energies(H, torch, t, X, row0=3)
+            assert t.launch_stats()["i8_planes"] < 0, name
+            Eo, Go = o.energy(X), o.field(X)
+            assert np.array_equal(G, Go) and np.array_equal(E, Eo) and np.array_equal(Ee, Eo), name
+            check_argmin(best, Eo, 0.0, row0=3)
+            with env("HOBO_F8", "0"):
+                tb, _ = build(order, N, src)
+                Gb, Eb = fields(H, torch, tb, X)
+                assert tb.launch_stats()["i8_planes"] >= 0
+                assert np.array_equal(Gb, G) and np.array_equal(Eb, E), name
+
+
+def test_e4m3_limbs_choice(H, torch):
+    """e4m3 limbs only where they pay: cells needing two limbs almost everywhere (5-8
+    significant bits: one bf16 limb) fall back to bf16 after the limb scan; cells beyond three
+    limbs (13+ bits) or non-integer cells never take them; HOBO_F8=1 forces an exact split of
+    scaled fractions."""
+    X = x_bits(2, 300, 200)
+    idx = canonical_cells_all(3, 200)
+    r = h(9, 3, np.arange(len(idx), dtype=np.uint64), 0)
+    keep = (r % np.uint64(100)) < np.uint64(2)
+    idx = idx[keep]
+    mag = ((r[keep] >> np.uint64(8)) % np.uint64(120)).astype(np.int64) * 2 + 17   # odd, 5-8 bits
+    t = H.HoboTensor.import_cells(3, 200, idx, mag.astype(np.float32))
+    o = Oracle.from_cells(3, 200, idx, mag.astype(np.float32))
+    E, _ = energies(H, torch, t, X)
+    assert t.launch_stats()["i8_planes"] == 0 and np.array_equal(E, o.energy(X))
+    big = ((r[keep] >> np.uint64(8)) % np.uint64(4096)).astype(np.int64) * 2 + 8193  # 14 bits
+    t = H.HoboTensor.import_cells(3, 200, idx, big.astype(np.float32))
+    energies(H, torch, t, X)
+    assert t.launch_stats()["i8_planes"] >= 0
+    # 1, 3, 5, 7 x 2^-e, e in [0, 12]: one e4m3 limb each (scaled by 2^5: 2^-7 .. 224), but a
+    # 15-bit fixed-point grid (two int8 digits against one bf16 limb), so e4m3 pays
+    fr = (((mag % 8) | 1).astype(np.float64) * 2.0 ** -(mag % 13).astype(np.float64)).astype(np.float32)
+    with env("HOBO_F8", "1"):
+        t = H.HoboTensor.import_cells(3, 200, idx, fr)
+        o = Oracle.from_cells(3, 200, idx, fr)
+        E, best = energies(H, torch, t, X)
+        assert t.launch_stats()["i8_planes"] < 0
+        assert np.max(np.abs(E - o.energy(X))) <= o.tau
+    t = H.HoboTensor.import_cells(3, 200, idx, fr)
+    energies(H, torch, t, X)
+    assert t.launch_stats()["i8_planes"] >= 0                               # not integer: default off
+
+
+def test_e4m3_limbs_split_schedules(H, torch):
+    """The e4m3-limb contraction under the stream-K schedule (partial wave: leftover tiles cut
+    into K ranges), under split-K (tiny batches) and in the search loop: bit-exact against the
+    oracle and against the data-parallel schedule."""
+    p = cfg3_problem()
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    for B in (5000, 64, 1):
+        X = x_bits(23, B, 512)
+        G, E = fields(H, torch, t, X)
+        assert t.launch_stats()["i8_planes"] == -2
+        with env("HOBO_SK", "0"):
+            G0, E0 = fields(H, torch, t, X)
+        assert np.array_equal(G, G0) and np.array_equal(E, E0)
+        rows = sample_rows(B, 129, 64) if B >= 64 else np.arange(B)
+        assert np.array_equal(G[rows], o.field(X[rows])) and np.array_equal(E[rows], o.energy(X[rows]))
+    x, e, c = t.search(9, None, 2, chain0=0, nchains=64)
+    r = o.search(9, 0, 64, 2)
     assert (e, c) == (r["e_best"], r["best_chain"]) and np.array_equal(x, r["chain_xbest"][c])
