@@ -836,8 +836,11 @@ void launch_pack_x(const uint8_t* X, long long B, int N, int W, uint32_t* bits, 
 // with 128-column tiles (half-size boxes).  (128-column tiles everywhere measured 1.8x slower
 // at cfg3: twice the CTAs generate A.)
 int real_slot(hobo_tensor* t) {
-  const int full = digit_planes(t) ? 3 : 1;   // the real-valued path needs bf16 limb planes
-  if (t->host.N <= 128) return digit_planes(t) ? 2 : 1;
+  // the real-valued path needs bf16 limb planes: slot 1 holds 1-byte planes (int8 digits, or
+  // e4m3 limbs unless its build measured them not worth it) -> a bf16 copy in slot 3 (or 2)
+  const bool bytes = t->lay[1].built ? t->lay[1].i8 != 0 : (digit_planes(t) || (e4m3_limbs(t) > 0 && !t->f8_off[1]));
+  const int full = bytes ? 3 : 1;
+  if (t->host.N <= 128) return bytes ? 2 : 1;
   int ps = 0, ring = 0, la = 0;
   return real_geometry(t, 256, ps, ring, la) ? full : 2;
 }
