@@ -264,7 +264,7 @@ cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
   if (cudaError_t e = set_smem(k, smem)) return e;
   const int mb = (REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
-  k<<<dim3((unsigned)(p.n_split * p.n_ct * ((p.n_cb + mb - 1) / mb))), dim3(kThreads), smem, s>>>(L.tmap, p);
+  k<<<dim3((unsigned)(p.n_split * p.n_ct * ((p.n_cb + mb - 1) / mb))), dim3(kr_threads<F8>()), smem, s>>>(L.tmap, p);
   return cudaGetLastError();
 }
 
@@ -285,7 +285,7 @@ cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s
   if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.units ? 2 * p.n_units : 2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kr_threads<F8>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

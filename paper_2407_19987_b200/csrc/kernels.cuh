@@ -54,7 +54,8 @@ struct KrParams {
   double qscale;            // int8 digit planes (kr_gemm_kernel<..., I8>): cell = qscale * sum_l 256^l d_l
   float fscale;             // e4m3 limbs (kr_gemm_kernel<..., I8, F8>): F = fscale * accumulator
   int exp;                  // MEASUREMENT ONLY (HOBO_KR_EXP, 1-byte plane launches): 1 = the generator
-                            // skips the run decode, 2 = skips the TMEM store; results are wrong
+                            // skips the run decode, 2 = skips the TMEM store (4: host side, one e4m3
+                            // limb plane); results are wrong
   int nl_shift;             // e4m3 limbs: the stage record's limb counts for this layout start at bit
                             // nl_shift of its header's w (2 bits per column tile)
   const uint4* srec;        // int8: per K-block pair, {runs of 2P, runs of 2P+1, nfix, 0} + the runs
@@ -94,8 +95,9 @@ struct KrCfg {
   static constexpr int A_COLS = I8 ? kBK / 4 : kBK / 2;  // TMEM columns of one K-block of A (64 bf16 / 64 bytes per lane)
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator (I8: L of them), then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
-  static constexpr int MAXD = 16;                        // descriptor ring slots (>= DAHEAD + MAXST)
-  static constexpr int DAHEAD = 8;                       // descriptors run this many stages ahead of W
+  static constexpr int MAXD = 32;                        // descriptor ring slots (>= DAHEAD + MAXST)
+  static constexpr int LG_MAXD = 5;
+  static constexpr int DAHEAD = 16;                      // descriptors run this many stages ahead of W
   static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 4;
   static constexpr int DESC_BYTES = 0;                   // (bf16 launches read their descriptors with __ldg)
   // I8: the descriptor ring holds the stages' run records (srec_u4 uint4s per slot)
@@ -331,8 +333,15 @@ __device__ __forceinline__ void issue_f8_stage(uint32_t tmem, uint32_t a_t, uint
 // accumulator, F = 2^(s+9) * accumulator; a stage loads and multiplies only the limb boxes its
 // column tile needs (the stage record's limb count, 1 almost everywhere on integer-encoded
 // instances)
+// threads of a kr_gemm launch (a third generator team for F8, warps 10-13, measured no faster:
+// cfg3 2.90 -> 2.92 ms)
+template <bool F8>
+__host__ __device__ constexpr int kr_threads() { return kThreads; }
+
 template <int NT, bool REAL, bool SA = false, bool PAIR = false, bool I8 = false, bool F8 = false>
-__global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
+__global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
+  constexpr int THREADS = kr_threads<F8>();
+  constexpr int NTEAM = 2;            // generator teams (both also run the epilogue)
   static_assert(!(PAIR && SA), "CTA pairs: not for the per-site annealing launch");
   static_assert(!F8 || I8, "e4m3 limbs run on the 1-byte plane path");
   static_assert(!(I8 && (REAL || SA)), "int8 digit planes: binary candidates, energy / field launches");
@@ -353,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4) + (I8 ? 2u * kBM * 4u : 0u);
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
   if constexpr (I8) {   // the two zero words in front of every row (run_bits8's window)
-    for (int i = threadIdx.x; i < 2 * kBM; i += kThreads) xs[i - 2 * kBM] = 0u;
+    for (int i = threadIdx.x; i < 2 * kBM; i += THREADS) xs[i - 2 * kBM] = 0u;
   }
   uint16_t* prow = reinterpret_cast<uint16_t*>(gbase + (sX - base));   // REAL: p rows [128][pstride]
   double* qpart = reinterpret_cast<double*>(gbase + (sQ - base));
@@ -398,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
   // F8: the limb count of stage n of this CTA (its record, in the descriptor ring)
   const uint4* dsm_rec = reinterpret_cast<const uint4*>(gbase + (sD - base));
   auto stage_nl = [&](int n) -> int {
-    mbar_wait(DFULL(n & (C::MAXD - 1)), (uint32_t)(n >> 4) & 1u);
+    mbar_wait(DFULL(n & (C::MAXD - 1)), (uint32_t)(n >> C::LG_MAXD) & 1u);
     const int v = (int)((dsm_rec[(size_t)(n & (C::MAXD - 1)) * p.srec_u4].w >> (p.nl_shift + 2 * ct)) & 3u);
     return v ? v : 1;
   };
@@ -471,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
       prow[i] = v;
     }
   } else {
-    stage_x(b0, (int)threadIdx.x, kThreads);
+    stage_x(b0, (int)threadIdx.x, THREADS);
   }
   tc_fence_before();
   if constexpr (PAIR) cluster_sync_all();   // both CTAs' barriers initialised, TMEM allocated
@@ -830,12 +839,12 @@ __global__ void __launch_bounds__(kThreads, 1) kr_gemm_kernel(const __grid_const
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
         const int nstages = (s.y + KPS - 1) / KPS;
         const int lg_a = NSTA == 8 ? 3 : NSTA == 4 ? 2 : NSTA == 2 ? 1 : 0;
-        static_assert((C::MAXD & (C::MAXD - 1)) == 0 && C::MAXD == 16, "descriptor ring: a power of two");
-        for (int i = (gn ^ h) & 1; i < nstages; i += 2) {
+        static_assert(C::MAXD == (1 << C::LG_MAXD) && C::MAXD >= C::DAHEAD + C::MAXST, "descriptor ring: a power of two");
+        for (int i = ((h - gn) % NTEAM + NTEAM) % NTEAM; i < nstages; i += NTEAM) {
           {
             const int n = gn + i;
             const int wst = n & (C::MAXD - 1), gst = n & (NSTA - 1);
-            const uint32_t wph = (uint32_t)(n >> 4) & 1u, gph = (uint32_t)(n >> lg_a) & 1u;
+            const uint32_t wph = (uint32_t)(n >> C::LG_MAXD) & 1u, gph = (uint32_t)(n >> lg_a) & 1u;
             mbar_wait(DFULL(wst), wph);
             const uint4* rec = dsm + (size_t)wst * p.srec_u4;
             const uint4 hd = rec[0];
