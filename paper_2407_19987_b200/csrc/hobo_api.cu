@@ -78,6 +78,8 @@ struct DevLayout {
   bool f8 = false;                     // the i8 1-byte planes hold e4m3 limbs (kind::f8f6f4)
   float fscale = 1.0f;                 // e4m3: F = fscale * accumulator (2^(s + 9))
   double f8_density = 0.0;             // e4m3: mean limb boxes per stage (MMA work vs one plane)
+  uint32_t* d_nltab = nullptr;         // e4m3: [n_ct][nl_words] limb counts per K-block pair, 2 bits
+  int nl_words = 0;
   int2* d_sched = nullptr;
   std::vector<int32_t> sched;
   alignas(64) CUtensorMap tmap;
@@ -138,7 +140,6 @@ struct hobo_tensor {
   int f8 = -1;             // e4m3 limbs of slots 0/1 (0 = none; -1 = not decided yet)
   int f8_s = 0;            // their scale exponent: limbs of cell * 2^-f8_s
   bool f8_off[2] = {false, false};   // slot measured not worth it (too many second limbs)
-  std::vector<uint32_t> srec_host;   // the stage records (their headers carry the e4m3 limb counts)
   // scratch (grown on demand)
   uint32_t* d_bits = nullptr; size_t bits_cap = 0;
   double* d_Q = nullptr; size_t Q_cap = 0;
@@ -261,7 +262,8 @@ EncodeTiledFn encode_fn() {
 template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, false, I8, F8>;
-  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
+  const size_t smem =
+      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0);
   if (cudaError_t e = set_smem(k, smem)) return e;
   const int mb = (REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
   k<<<dim3((unsigned)(p.n_split * p.n_ct * ((p.n_cb + mb - 1) / mb))), dim3(kr_threads<F8>()), smem, s>>>(L.tmap, p);
@@ -281,7 +283,8 @@ cudaError_t launch_kr_sa(const DevLayout& L, const KrParams& p, cudaStream_t s) 
 template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, true, I8, F8>;
-  const size_t smem = REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4);
+  const size_t smem =
+      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0);
   if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.units ? 2 * p.n_units : 2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
@@ -413,7 +416,9 @@ int e4m3_limbs(hobo_tensor* t) {
   if (H.order < 2 || t->kl.Tpad / kBK < 64) return 0;   // short K loops: the persistent / bf16 kernels
   if (!H.is_integer && !(e && e[0] == '1')) return 0;
   if (H.is_integer && !(H.sum_abs < 16777216.0)) return 0;
-  if (KrCfg<256, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl)) > kMaxSmem) return 0;
+  if (KrCfg<256, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl), (int)((t->kl.Tpad / (2 * kBK) + 15) / 16)) >
+      kMaxSmem)
+    return 0;
   double amax = 0.0;
   for (int r = 2; r <= H.order; ++r)
     for (float c : H.strict[r]) amax = std::max(amax, (double)std::fabs(c));
@@ -549,7 +554,6 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
     }
     CK(cudaMalloc(&t->d_srec, rec.size() * 4));
     CK(cudaMemcpy(t->d_srec, rec.data(), rec.size() * 4, cudaMemcpyHostToDevice));
-    t->srec_host = std::move(rec);
   }
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
@@ -622,13 +626,13 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
       double sum = 0;
       for (uint32_t v : nl) sum += v;
       L.f8_density = sum / (double)nl.size();
-      const int shift = field ? 0 : 16;
-      for (int64_t P = 0; P < n_kbp; ++P) {
-        uint32_t& w = t->srec_host[(size_t)P * t->srec_u4 * 4 + 3];
-        w &= ~(0xFFFFu << shift);
-        for (int ct = 0; ct < L.n_ct; ++ct) w |= (uint32_t)nl[(size_t)ct * n_kbp + P] << (shift + 2 * ct);
-      }
-      CK(cudaMemcpy(t->d_srec, t->srec_host.data(), t->srec_host.size() * 4, cudaMemcpyHostToDevice));
+      L.nl_words = (int)((n_kbp + 15) / 16);
+      std::vector<uint32_t> tab((size_t)L.n_ct * L.nl_words, 0u);
+      for (int ct = 0; ct < L.n_ct; ++ct)
+        for (int64_t P = 0; P < n_kbp; ++P)
+          tab[(size_t)ct * L.nl_words + P / 16] |= nl[(size_t)ct * n_kbp + P] << (2 * (P % 16));
+      CK(cudaMalloc(&L.d_nltab, tab.size() * 4));
+      CK(cudaMemcpy(L.d_nltab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
       // a limb box costs half a bf16 limb box (as an int8 digit plane does): keep e4m3 only
       // when it saves >= 20% of the tensor-core cycles of the path chosen otherwise, else
       // rebuild this slot's layout with int8 digits / bf16 limbs
@@ -640,6 +644,7 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
         cudaFree(d_bt);
         cudaFree(d_tup);
         cudaFree(L.W);
+        cudaFree(L.d_nltab);
         L = DevLayout();
         t->f8_off[slot] = true;
         return ensure_layout(t, slot);
@@ -735,7 +740,8 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.srec = t->d_srec;
   p.srec_u4 = L.i8 ? t->srec_u4 : 0;
   p.field_mode = (&L == &t->lay[0] || &L == &t->lay[4] || &L == &t->lay[5]) ? 0 : 1;
-  p.nl_shift = p.field_mode ? 0 : 16;
+  p.nltab = L.d_nltab;
+  p.nl_words = L.nl_words;
   p.exp = 0;
   if (const char* e = getenv("HOBO_KR_EXP")) p.exp = atoi(e);
   for (int r = 0; r < 8; ++r) p.wdeg[r] = L.wdeg[r];
@@ -1246,6 +1252,7 @@ hobo_status hobo_tensor_free(hobo_tensor* t) {
   for (auto& L : t->lay) {
     if (L.W) cudaFree(L.W);
     if (L.d_sched) cudaFree(L.d_sched);
+    if (L.d_nltab) cudaFree(L.d_nltab);
   }
   if (t->ev0) { cudaEventDestroy(t->ev0); cudaEventDestroy(t->ev1); }
   for (hobo_tensor* c : t->sa_child) hobo_tensor_free(c);

@@ -56,8 +56,8 @@ struct KrParams {
   int exp;                  // MEASUREMENT ONLY (HOBO_KR_EXP, 1-byte plane launches): 1 = the generator
                             // skips the run decode, 2 = skips the TMEM store (4: host side, one e4m3
                             // limb plane); results are wrong
-  int nl_shift;             // e4m3 limbs: the stage record's limb counts for this layout start at bit
-                            // nl_shift of its header's w (2 bits per column tile)
+  const uint32_t* nltab;    // e4m3 limbs: [n_ct][nl_words] limb counts of the K-block pairs, 2 bits each
+  int nl_words;             // (16 pairs per word); copied to shared memory by every CTA
   const uint4* srec;        // int8: per K-block pair, {runs of 2P, runs of 2P+1, nfix, 0} + the runs
   int srec_u4;              // int8: uint4s per record (the descriptor ring's slot size)
   // simulated annealing (kr_gemm_kernel<NT, false, true>): one launch per visited site m with
@@ -102,9 +102,10 @@ struct KrCfg {
   static constexpr int DESC_BYTES = 0;                   // (bf16 launches read their descriptors with __ldg)
   // I8: the descriptor ring holds the stages' run records (srec_u4 uint4s per slot)
   __host__ __device__ static size_t desc_bytes(int srec_u4) { return I8 ? (size_t)MAXD * srec_u4 * 16 : DESC_BYTES; }
-  static size_t smem_bytes(int W, int srec_u4 = 0) {
+  static size_t smem_bytes(int W, int srec_u4 = 0, int nl_words = 0) {
     return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + desc_bytes(srec_u4) +
-           (size_t)(W + (I8 ? 4 : 2)) * kBM * 4 + 128;   // I8: two zero words in front (run_bits8)
+           (size_t)(W + (I8 ? 4 : 2)) * kBM * 4 + 128 +   // I8: two zero words in front (run_bits8)
+           (size_t)nl_words * 4;                          // e4m3: the column tile's limb counts
   }
   // stage geometry for L limbs: KPS K-blocks x L limb boxes per stage, NST stages.  Two
   // K-blocks per stage halve the MMA thread's waits and commits per MMA; with 256-column
@@ -404,13 +405,15 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
   const int NSTA = DEC ? C::nsta(F8 ? 1 : p.L) : NST;              // A stages (DEC: own ring)
   const int NACC = F8 ? 1 : I8 ? p.L : 1;                          // accumulators in TMEM [0, NACC * NT)
-  // F8: the limb count of stage n of this CTA (its record, in the descriptor ring)
-  const uint4* dsm_rec = reinterpret_cast<const uint4*>(gbase + (sD - base));
-  auto stage_nl = [&](int n) -> int {
-    mbar_wait(DFULL(n & (C::MAXD - 1)), (uint32_t)(n >> C::LG_MAXD) & 1u);
-    const int v = (int)((dsm_rec[(size_t)(n & (C::MAXD - 1)) * p.srec_u4].w >> (p.nl_shift + 2 * ct)) & 3u);
+  // F8: the limb count of the stage at K-block kb0 (this column tile's table, in shared memory:
+  // a dependent wait on the stage's record here cost 12% at cfg3)
+  uint32_t* snl = reinterpret_cast<uint32_t*>(gbase + (sX - base) + (size_t)(p.W + 2) * kBM * 4);
+  auto stage_nl = [&](int kb0) -> int {
+    const int v = (int)((snl[kb0 >> 5] >> ((kb0 >> 1) & 15) * 2) & 3u);
     return v ? v : 1;
   };
+  if constexpr (F8)
+    for (int i = threadIdx.x; i < p.nl_words; i += THREADS) snl[i] = __ldg(p.nltab + (size_t)ct * p.nl_words + i);
   __shared__ int2 sched[8];          // this CTA's (first K-block, #K-blocks) per segment
   __shared__ int ssa[SA ? kBM : 1];   // annealing: this CTA's decisions for site sa_m
   if (threadIdx.x == 0) {
@@ -535,7 +538,6 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
     if (lane == 0) {
       int st = 0;                    // ring slot and phase, advanced per stage (no divisions)
       uint32_t ph = 0;
-      int pn = 0;                    // stage counter (F8: the record holding its limb count)
       // I8: the A generator's K-block descriptors, bulk-copied DAHEAD stages ahead of the W
       // boxes into a ring of their own (slot m % MAXD is reused only after the generator is
       // done with stage m - MAXD <= the stage whose W slot was just freed)
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
           mbar_wait(EMPTY(st), ph ^ 1u);
           if constexpr (DEC) dissue();
           if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
-            const int nl = F8 ? stage_nl(pn) : p.L;
+            const int nl = F8 ? stage_nl(kb0) : p.L;
             if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)nl * C::BOX);
             for (int l = 0; l < nl; ++l) {
               const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1);
@@ -586,7 +588,6 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
               }
           }
           if (++st == NST) { st = 0; ph ^= 1u; }
-          ++pn;
         }
       }
     }
@@ -600,7 +601,6 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
       int st = 0, sa = 0;            // W and A ring slots and phases, advanced per stage
       uint32_t ph = 0, pha = 0;
       uint32_t issued = 0;
-      int mn = 0;                    // stage counter (F8: limb counts)
       for (int it = 0; it < ntile; ++it) {
       if (it > 0) {   // the previous block's epilogue has read the accumulator
         mbar_wait(acc_empty, (uint32_t)((it - 1) & 1));
@@ -611,8 +611,7 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
           const int nkb = min(KPS, s.x + s.y - kb0);
-          const int nl = F8 ? stage_nl(mn) : 0;
-          ++mn;
+          const int nl = F8 ? stage_nl(kb0) : 0;
           mbar_wait(FULL(st), ph);
           if (DEC) mbar_wait(FULLA(sa), pha);
           tc_fence_after();

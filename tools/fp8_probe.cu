@@ -71,15 +71,16 @@ __global__ void __launch_bounds__(128, 1) exact_kernel(const uint8_t* __restrict
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
-template <int KIND>   // 0 f16 (bf16), 1 f8f6f4, 2 i8
+template <int KIND>   // 0 f16 (bf16), 1 f8f6f4, 2 i8; 3/4: f8f6f4 with 1/2 commits per 4 MMAs (the
+                      // e4m3 kernel's per-stage EMPTY + EMPTYA); 5: bf16 with 1 commit per 8 MMAs
 __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long long* cycles) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* g = smem_raw + (base - raw);
-  const uint32_t sB = base, bar = base + 32768, tslot = bar + 8;
+  const uint32_t sB = base, bar = base + 32768, tslot = bar + 8, bar2 = bar + 16, bar3 = bar + 24;
   for (int i = threadIdx.x; i < 32768 / 4; i += 128) reinterpret_cast<uint32_t*>(g)[i] = 0x38383838u & (i * 2654435761u);
-  if (threadIdx.x == 0) { mbar_init(bar, 1); fence_mbar_init(); }
+  if (threadIdx.x == 0) { mbar_init(bar, 1); mbar_init(bar2, 1); mbar_init(bar3, 1); fence_mbar_init(); }
   fence_async_smem();
   if (threadIdx.x < 32) tmem_alloc(tslot, 512);
   tc_fence_before();
@@ -92,10 +93,13 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long l
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (KIND == 0) umma_bf16_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc_bf16_f32(128, 256), (it | k) != 0);
-        else if (KIND == 1) umma_f8_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc_e4m3_f32(128, 256), (it | k) != 0);
-        else umma_i8_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc_i8_s32(128, 256, 1), (it | k) != 0);
+        if (KIND == 0 || KIND == 5) umma_bf16_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc_bf16_f32(128, 256), (it | k) != 0);
+        else if (KIND == 2) umma_i8_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc_i8_s32(128, 256, 1), (it | k) != 0);
+        else umma_f8_ts(tmem, tmem + 256 + 8 * k, bd + 2 * k, idesc_e4m3_f32(128, 256), (it | k) != 0);
       }
+      if (KIND == 3 || KIND == 4) umma_commit(bar2);
+      if (KIND == 4) umma_commit(bar3);
+      if (KIND == 5 && (it & 1)) umma_commit(bar2);
     }
     umma_commit(bar);
     mbar_wait(bar, 0);
@@ -175,5 +179,8 @@ int main() {
   rate(rate_kernel<0>, "bf16", 128.0 * 256 * 16);
   rate(rate_kernel<1>, "e4m3", 128.0 * 256 * 32);
   rate(rate_kernel<2>, "i8", 128.0 * 256 * 32);
+  rate(rate_kernel<3>, "e4m3+1c", 128.0 * 256 * 32);
+  rate(rate_kernel<4>, "e4m3+2c", 128.0 * 256 * 32);
+  rate(rate_kernel<5>, "bf16+c/8", 128.0 * 256 * 16);
   return 0;
 }
