@@ -337,12 +337,12 @@ __device__ __forceinline__ void issue_f8_stage(uint32_t tmem, uint32_t a_t, uint
 // threads of a kr_gemm launch (a third generator team for F8, warps 10-13, measured no faster:
 // cfg3 2.90 -> 2.92 ms)
 template <bool F8>
-__host__ __device__ constexpr int kr_threads() { return kThreads; }
+__host__ __device__ constexpr int kr_threads() { return F8 ? kThreads + 128 : kThreads; }
 
 template <int NT, bool REAL, bool SA = false, bool PAIR = false, bool I8 = false, bool F8 = false>
 __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
   constexpr int THREADS = kr_threads<F8>();
-  constexpr int NTEAM = 2;            // generator teams (both also run the epilogue)
+  constexpr int NTEAM = F8 ? 3 : 2;   // generator teams (the first two also run the epilogue)
   static_assert(!(PAIR && SA), "CTA pairs: not for the per-site annealing launch");
   static_assert(!F8 || I8, "e4m3 limbs run on the 1-byte plane path");
   static_assert(!(I8 && (REAL || SA)), "int8 digit planes: binary candidates, energy / field launches");
@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
       }
       }
       any = any || s.y > 0;
-      if (snaps && j > 0) {
+      if (snaps && j > 0 && h < 2) {
         mbar_wait(snap_full, (uint32_t)(nsnap & 1));
         tc_fence_after();
         S[nsnap] = any ? xsum() : 0.0;
@@ -933,6 +933,7 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
       }
     }
 
+    if (h >= 2) continue;   // generation-only team (F8)
     // ---------------- epilogue: fields, energy partial (this warp's column half) ---------------
     mbar_wait(acc_full, (uint32_t)(it & 1));
     tc_fence_after();
