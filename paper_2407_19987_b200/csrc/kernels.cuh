@@ -334,15 +334,16 @@ __device__ __forceinline__ void issue_f8_stage(uint32_t tmem, uint32_t a_t, uint
 // accumulator, F = 2^(s+9) * accumulator; a stage loads and multiplies only the limb boxes its
 // column tile needs (the stage record's limb count, 1 almost everywhere on integer-encoded
 // instances)
-// threads of a kr_gemm launch (a third generator team for F8, warps 10-13, measured no faster:
-// cfg3 2.90 -> 2.92 ms)
+// threads of a kr_gemm launch: F8 runs two more generator teams (warps 10-17, generation only,
+// no epilogue): an e4m3 stage is half an int8 3-plane stage's MMA time (cfg3 kernel: 2 teams
+// 2.80 ms, 3 teams 2.64 ms, 4 teams 2.60 ms)
 template <bool F8>
-__host__ __device__ constexpr int kr_threads() { return F8 ? kThreads + 128 : kThreads; }
+__host__ __device__ constexpr int kr_threads() { return F8 ? kThreads + 256 : kThreads; }
 
 template <int NT, bool REAL, bool SA = false, bool PAIR = false, bool I8 = false, bool F8 = false>
 __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __grid_constant__ CUtensorMap tmap, const KrParams p) {
   constexpr int THREADS = kr_threads<F8>();
-  constexpr int NTEAM = F8 ? 3 : 2;   // generator teams (the first two also run the epilogue)
+  constexpr int NTEAM = F8 ? 4 : 2;   // generator teams (the first two also run the epilogue)
   static_assert(!(PAIR && SA), "CTA pairs: not for the per-site annealing launch");
   static_assert(!F8 || I8, "e4m3 limbs run on the 1-byte plane path");
   static_assert(!(I8 && (REAL || SA)), "int8 digit planes: binary candidates, energy / field launches");
