@@ -263,7 +263,7 @@ template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, false, I8, F8>;
   const size_t smem =
-      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0);
+      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0, p.desc_lg);
   if (cudaError_t e = set_smem(k, smem)) return e;
   const int mb = (REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
   k<<<dim3((unsigned)(p.n_split * p.n_ct * ((p.n_cb + mb - 1) / mb))), dim3(kr_threads<F8>()), smem, s>>>(L.tmap, p);
@@ -284,7 +284,7 @@ template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, true, I8, F8>;
   const size_t smem =
-      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0);
+      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0, p.desc_lg);
   if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.units ? 2 * p.n_units : 2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
@@ -375,7 +375,7 @@ int digit_planes(hobo_tensor* t) {
   int d = H.digits;
   if (d > 0 && 255.0 * (double)std::max<int64_t>(t->kl.Tpad, kBK) >= 2147483648.0) d = 0;
   // shared memory: W ring + 16 run-record slots + the candidates' bits must fit one CTA
-  if (d > 0 && KrCfg<128, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl)) > kMaxSmem) d = 0;
+  if (d > 0 && KrCfg<128, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl), 0, 4) > kMaxSmem) d = 0;
   if (d > 0) {
     const char* e = getenv("HOBO_I8");
     if (e && e[0] == '0') d = 0;
@@ -416,7 +416,7 @@ int e4m3_limbs(hobo_tensor* t) {
   if (H.order < 2 || t->kl.Tpad / kBK < 64) return 0;   // short K loops: the persistent / bf16 kernels
   if (!H.is_integer && !(e && e[0] == '1')) return 0;
   if (H.is_integer && !(H.sum_abs < 16777216.0)) return 0;
-  if (KrCfg<256, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl), (int)((t->kl.Tpad / (2 * kBK) + 15) / 16)) >
+  if (KrCfg<256, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl), (int)((t->kl.Tpad / (2 * kBK) + 15) / 16), 4) >
       kMaxSmem)
     return 0;
   double amax = 0.0;
@@ -739,6 +739,10 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.fscale = L.fscale;
   p.srec = t->d_srec;
   p.srec_u4 = L.i8 ? t->srec_u4 : 0;
+  // 32 descriptor-ring slots when they fit next to the rest of the CTA's shared memory, else 16
+  const size_t sm32 = L.NT == 128 ? KrCfg<128, true>::smem_bytes(t->W, p.srec_u4, L.nl_words, 5)
+                                  : KrCfg<256, true>::smem_bytes(t->W, p.srec_u4, L.nl_words, 5);
+  p.desc_lg = (L.i8 && sm32 > kMaxSmem) ? 4 : 5;
   p.field_mode = (&L == &t->lay[0] || &L == &t->lay[4] || &L == &t->lay[5]) ? 0 : 1;
   p.nltab = L.d_nltab;
   p.nl_words = L.nl_words;

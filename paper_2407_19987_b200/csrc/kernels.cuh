@@ -60,6 +60,7 @@ struct KrParams {
   int nl_words;             // (16 pairs per word); copied to shared memory by every CTA
   const uint4* srec;        // int8: per K-block pair, {runs of 2P, runs of 2P+1, nfix, 0} + the runs
   int srec_u4;              // int8: uint4s per record (the descriptor ring's slot size)
+  int desc_lg;              // int8: log2 of the descriptor ring's slots in use (4 or 5)
   // simulated annealing (kr_gemm_kernel<NT, false, true>): one launch per visited site m with
   // the layout of P_m = dE/dx_m; every CTA decides site m for its chains, column tile 0
   // commits the decisions, and the epilogue adds s_b * (field of P_m) to G
@@ -95,15 +96,17 @@ struct KrCfg {
   static constexpr int A_COLS = I8 ? kBK / 4 : kBK / 2;  // TMEM columns of one K-block of A (64 bf16 / 64 bytes per lane)
   static constexpr int TMEM_COLS = 512;                  // [0, NT): accumulator (I8: L of them), then the A stages
   static_assert(NT % 32 == 0 && NT >= 32 && NT <= 256, "UMMA N for M=128");
-  static constexpr int MAXD = 32;                        // descriptor ring slots (>= DAHEAD + MAXST)
-  static constexpr int LG_MAXD = 5;
-  static constexpr int DAHEAD = 16;                      // descriptors run this many stages ahead of W
+  static constexpr int MAXD = 32;                        // descriptor ring slots: 32 (records 16 stages ahead of
+                                                         // W: e4m3 cfg3 2.94 -> 2.90 ms), or 16 (8 ahead) when
+                                                         // 32 records do not fit shared memory (KrParams::desc_lg)
   static constexpr int NBAR = 2 * MAXST + 2 * MAXA + MAXD + 4;
   static constexpr int DESC_BYTES = 0;                   // (bf16 launches read their descriptors with __ldg)
   // I8: the descriptor ring holds the stages' run records (srec_u4 uint4s per slot)
-  __host__ __device__ static size_t desc_bytes(int srec_u4) { return I8 ? (size_t)MAXD * srec_u4 * 16 : DESC_BYTES; }
-  static size_t smem_bytes(int W, int srec_u4 = 0, int nl_words = 0) {
-    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + desc_bytes(srec_u4) +
+  __host__ __device__ static size_t desc_bytes(int srec_u4, int desc_lg = 5) {
+    return I8 ? ((size_t)1 << desc_lg) * srec_u4 * 16 : DESC_BYTES;
+  }
+  static size_t smem_bytes(int W, int srec_u4 = 0, int nl_words = 0, int desc_lg = 5) {
+    return 1024 + (size_t)RING_BOXES * BOX + 8 * NBAR + 16 + 128 + kBM * 8 + desc_bytes(srec_u4, desc_lg) +
            (size_t)(W + (I8 ? 4 : 2)) * kBM * 4 + 128 +   // I8: two zero words in front (run_bits8)
            (size_t)nl_words * 4;                          // e4m3: the column tile's limb counts
   }
@@ -361,7 +364,8 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
   const uint32_t tslot = acc_full + 32;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
   const uint32_t sD = sQ + kBM * 8;                               // I8: descriptor ring (one slot per W stage)
-  const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4) + (I8 ? 2u * kBM * 4u : 0u);
+  const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4, p.desc_lg) + (I8 ? 2u * kBM * 4u : 0u);
+  const int MD = 1 << p.desc_lg;   // descriptor ring slots in use (16 or 32), records MD/2 stages ahead
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
   if constexpr (I8) {   // the two zero words in front of every row (run_bits8's window)
     for (int i = threadIdx.x; i < 2 * kBM; i += THREADS) xs[i - 2 * kBM] = 0u;
@@ -552,14 +556,14 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
         const uint32_t rbytes = (uint32_t)p.srec_u4 * 16u;
         mbar_arrive_expect_tx(DFULL(dslot), rbytes);
         bulk_g2s(sD + (uint32_t)dslot * rbytes, p.srec + (size_t)(dkb >> 1) * p.srec_u4, rbytes, DFULL(dslot));
-        if (++dslot == C::MAXD) dslot = 0;
+        if (++dslot == MD) dslot = 0;
         dkb += KPS;
         dskip();
       };
       if constexpr (DEC) {
         if (dj >= 0) dkb = sched[dj].x;
         dskip();
-        for (int i = 0; i < C::DAHEAD; ++i) dissue();
+        for (int i = 0; i < MD / 2; ++i) dissue();
       }
       for (int it = 0; it < ntile; ++it)   // MB > 1: the same W sequence for every block
       for (int j = p.nseg - 1; j >= 0; --j) {
@@ -839,12 +843,12 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
         const int nstages = (s.y + KPS - 1) / KPS;
         const int lg_a = NSTA == 8 ? 3 : NSTA == 4 ? 2 : NSTA == 2 ? 1 : 0;
-        static_assert(C::MAXD == (1 << C::LG_MAXD) && C::MAXD >= C::DAHEAD + C::MAXST, "descriptor ring: a power of two");
+        static_assert(C::MAXD == 32 && C::MAXST <= 8, "descriptor ring: 16 or 32 slots, >= MD / 2 + MAXST");
         for (int i = ((h - gn) % NTEAM + NTEAM) % NTEAM; i < nstages; i += NTEAM) {
           {
             const int n = gn + i;
-            const int wst = n & (C::MAXD - 1), gst = n & (NSTA - 1);
-            const uint32_t wph = (uint32_t)(n >> C::LG_MAXD) & 1u, gph = (uint32_t)(n >> lg_a) & 1u;
+            const int wst = n & (MD - 1), gst = n & (NSTA - 1);
+            const uint32_t wph = (uint32_t)(n >> p.desc_lg) & 1u, gph = (uint32_t)(n >> lg_a) & 1u;
             mbar_wait(DFULL(wst), wph);
             const uint4* rec = dsm + (size_t)wst * p.srec_u4;
             const uint4 hd = rec[0];
