@@ -35,7 +35,7 @@
  *       HOBO_SK=0            no stream-K schedule for CTA-pair field launches
  *       HOBO_E2E_TAIL=<n>, HOBO_E2E_HEAD=<q>   host-buffer field calls returning G: n
  *                            halvings after the last whole wave (default 1), first chunk q
- *                            quarter waves (default 2)
+ *                            quarter waves (default 1)
  *       HOBO_PERSIST_EXP=<bits>  MEASUREMENT ONLY: switches parts of the persistent kernels off
  *                            (tools/persist_exp.sh); results are wrong whenever it is set
  *     Pairs, persistent kernels, graphs and annealing kernels give the same results (bit for

@@ -1479,15 +1479,16 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   if (!gout) {
     for (long long off = 0, n = per_wave; off < B; off += sizes.back(), n *= 6) sizes.push_back(std::min(n, B - off));
   } else {
-    // a half-wave first chunk (its input copy is the exposed one) and a half-wave last chunk
-    // (its copy-out is): a partial wave runs split across every SM, 0.33 ms for half a wave
-    // at cfg3 against 0.61 ms for a whole one, so it still hides the previous chunk's copy-out.
-    // cfg3 e2e: 4.89 -> 4.75 ms; two halvings (1/2, 1/4) measured 4.87-4.97 ms (the quarter
-    // wave takes 0.235 ms, little less than the half).  HOBO_E2E_TAIL = halvings,
-    // HOBO_E2E_HEAD = first chunk in quarter waves (A/B knobs, tools/e2e_zc.sh).
+    // a quarter-wave first chunk (nothing overlaps its input copy and its contraction) and a
+    // half-wave last chunk (its copy-out is the exposed one): a partial wave runs split across
+    // every SM, so it still hides the previous chunk's copy-out.  bf16 cfg3 e2e: 4.89 -> 4.75
+    // ms (half-wave ends); e4m3 cfg3, whose contraction now takes about as long as the 128 MiB
+    // copy-out: 3.67 (half-wave head) -> 3.57 ms; two halvings (1/2, 1/4) measured slower in
+    // both.  HOBO_E2E_TAIL = halvings, HOBO_E2E_HEAD = first chunk in quarter waves (A/B
+    // knobs, tools/e2e_zc.sh).
     int tail = 1;
     if (const char* e = getenv("HOBO_E2E_TAIL")) tail = atoi(e);
-    long long head = std::max<long long>(kBM, per_wave / 2 / kBM * kBM);
+    long long head = std::max<long long>(kBM, per_wave / 4 / kBM * kBM);
     if (const char* e = getenv("HOBO_E2E_HEAD")) head = std::max<long long>(kBM, per_wave * atoi(e) / 4 / kBM * kBM);
     std::vector<long long> ends;   // the tail, smallest last
     long long rest = B - std::min<long long>(head, B);
