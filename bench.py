@@ -546,6 +546,7 @@ def main():
             "kernel": f"kr_gemm_kernel<{'F8' if f8 else 'I8' if i8 else 'bf16'}> (open-index contraction, {mode} mode)",
             "kernel_ms": kms, "kernel_share_of_step": kms / my_ms, "launches_per_step": launches / max(1, a.steps),
             "frac_of_sustained": achieved / sustained,
+            "achieved_vs_bf16_burst": achieved / (burst / kind_ratio),   # context: the same work against bf16's peak
             "executed_mma_flops_per_launch": exec_flops, "executed_tflops": exec_flops / (kms / 1e3) / 1e12,
             "frac_executed_of_peak": exec_flops / (kms / 1e3) / 1e12 / peak,
             "hw_nominal_tflops": hw, "frac_executed_of_hw_nominal": exec_flops / (kms / 1e3) / 1e12 / hw,
