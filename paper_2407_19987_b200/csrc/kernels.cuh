@@ -203,13 +203,16 @@ __device__ __forceinline__ void expand_bytes64(uint64_t bits, uint32_t (&w)[16])
 // fixed0 << 11 | fixed1 << 21; w = fixed2 | fixed3 << 10 (10-bit variable ids).  The 64 output
 // bits are x bits [s, s + 64) of the row, s = 32 word + shift, counted from two zero words in
 // front of the row (xs2 = xs - 2 kBM), so no per-run mask or 64-bit shift is computed here.
+// NF >= 0: exactly NF fixed elements (no predicated loads for the absent ones: the stage's
+// nfix is warp-uniform, so the caller dispatches on it); NF = -1: up to 4, nfix at run time
+template <int NF = -1>
 __device__ __forceinline__ void run_bits8(const uint32_t* xs, const uint32_t* xs2, int row, const uint4 rr,
                                           uint32_t nfix, uint32_t& lo, uint32_t& hi) {
   uint32_t on = 1;
   const uint32_t f[4] = {(rr.z >> 11) & 1023u, (rr.z >> 21) & 1023u, rr.w & 1023u, (rr.w >> 10) & 1023u};
 #pragma unroll
   for (int q = 0; q < 4; ++q)
-    if ((uint32_t)q < nfix) on &= xs[(f[q] >> 5) * kBM + row] >> (f[q] & 31);
+    if (NF >= 0 ? q < NF : (uint32_t)q < nfix) on &= xs[(f[q] >> 5) * kBM + row] >> (f[q] & 31);
   const uint32_t wi = rr.z & 63u, sh = (rr.z >> 6) & 31u;
   const uint32_t w0 = xs2[wi * kBM + row], w1 = xs2[(wi + 1) * kBM + row], w2 = xs2[(wi + 2) * kBM + row];
   const uint32_t m = 0u - (on & 1u);
@@ -855,8 +858,16 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
             uint32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
             if (p.exp & 1) { l0 = hd.x * (uint32_t)row; h0 = l0 ^ hd.y; l1 = h0 + 1; h1 = l1 * 3u; }
             else {
+            if (F8 && hd.z == 1) {   // e.g. order 3's degree-3 part: one fixed element per run
+              for (uint32_t i = 0; i < hd.x; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + i], 1, l0, h0);
+              for (uint32_t i = 0; i < hd.y; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 1, l1, h1);
+            } else if (F8 && hd.z == 0) {
+              for (uint32_t i = 0; i < hd.x; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + i], 0, l0, h0);
+              for (uint32_t i = 0; i < hd.y; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 0, l1, h1);
+            } else {
             for (uint32_t i = 0; i < hd.x; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + i], hd.z, l0, h0);
             for (uint32_t i = 0; i < hd.y; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], hd.z, l1, h1);
+            }
             }
             uint32_t w[32];   // the K-block pair's bytes in the planes' permuted K order
             expand_bytes64(((uint64_t)h0 << 32) | l0, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
