@@ -859,16 +859,24 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
             if (p.exp & 1) { l0 = hd.x * (uint32_t)row; h0 = l0 ^ hd.y; l1 = h0 + 1; h1 = l1 * 3u; }
             else {
             if (hd.z == 1) {   // e.g. order 3's degree-3 part: one fixed element per run
+#pragma unroll 1
               for (uint32_t i = 0; i < hd.x; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + i], 1, l0, h0);
+#pragma unroll 1
               for (uint32_t i = 0; i < hd.y; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 1, l1, h1);
             } else if (hd.z == 2) {   // order 4's degree-4 part
+#pragma unroll 1
               for (uint32_t i = 0; i < hd.x; ++i) run_bits8<2>(xs, xs - 2 * kBM, row, rec[1 + i], 2, l0, h0);
+#pragma unroll 1
               for (uint32_t i = 0; i < hd.y; ++i) run_bits8<2>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 2, l1, h1);
             } else if (hd.z == 0) {
+#pragma unroll 1
               for (uint32_t i = 0; i < hd.x; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + i], 0, l0, h0);
+#pragma unroll 1
               for (uint32_t i = 0; i < hd.y; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 0, l1, h1);
             } else {
+#pragma unroll 1
             for (uint32_t i = 0; i < hd.x; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + i], hd.z, l0, h0);
+#pragma unroll 1
             for (uint32_t i = 0; i < hd.y; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], hd.z, l1, h1);
             }
             }
