@@ -317,8 +317,10 @@ __device__ __forceinline__ void issue_f8_stage(uint32_t tmem, uint32_t a_t, uint
     }
     return;
   }
+#pragma unroll 1
   for (int l = 0; l < nl; ++l) {
     const uint64_t bd = sw128_kmajor_desc(sbase + (uint32_t)l * boxb);
+#pragma unroll 1
     for (int kk = 0; kk < 2 * nkb; ++kk) {
       const uint32_t acc = (l | kk) ? 1u : issued;
       if constexpr (PAIR) umma_f8_ts_pair(tmem, a_t + 8u * kk, bd + 2u * kk, id, acc);
