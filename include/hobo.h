@@ -36,6 +36,9 @@
  *       HOBO_E2E_TAIL=<n>, HOBO_E2E_HEAD=<q>   host-buffer field calls returning G: n
  *                            halvings after the last whole wave (default 1), first chunk q
  *                            quarter waves (default 1)
+ *       HOBO_KR_EXP=<bits>   MEASUREMENT ONLY: switches parts of the 1-byte-plane contraction
+ *                            off (1 run decode, 2 A store, 4 second e4m3 limb; tools/f8_check.sh);
+ *                            results are wrong whenever it is set
  *       HOBO_PERSIST_EXP=<bits>  MEASUREMENT ONLY: switches parts of the persistent kernels off
  *                            (tools/persist_exp.sh); results are wrong whenever it is set
  *     Pairs, persistent kernels, graphs and annealing kernels give the same results (bit for

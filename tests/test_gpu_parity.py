@@ -1133,7 +1133,8 @@ def test_e4m3_limbs_integer_instances(H, torch, pair):
     cases = [("cfg3", None, None, cfg3_problem(), 1000, -2),
              ("pow2", 3, 200, pow2_int_cells(3, 200, 5), 700, -1),
              ("wide", 3, 200, pow2_int_cells(3, 200, 6, wide=0.0003), 383, -3),
-             ("order4", 4, 60, pow2_int_cells(4, 60, 7, density=0.05), 300, None)]
+             ("order4", 4, 60, pow2_int_cells(4, 60, 7, density=0.05), 300, None),
+             ("ragged", 3, 300, pow2_int_cells(3, 300, 8, density=0.01), 1000, None)]   # N=300: padded tile
 
     def build(order, N, src):
         if order is None:
