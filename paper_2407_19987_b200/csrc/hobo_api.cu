@@ -263,7 +263,7 @@ template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, false, I8, F8>;
   const size_t smem =
-      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0, p.desc_lg);
+      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4 * (F8 ? 2 : 1), F8 ? p.nl_words : 0, p.desc_lg);
   if (cudaError_t e = set_smem(k, smem)) return e;
   const int mb = (REAL || I8 || p.field_mode || p.n_split > 1 || p.cb_iters < 1) ? 1 : p.cb_iters;
   k<<<dim3((unsigned)(p.n_split * p.n_ct * ((p.n_cb + mb - 1) / mb))), dim3(kr_threads<F8>()), smem, s>>>(L.tmap, p);
@@ -284,7 +284,7 @@ template <int NT, bool REAL, bool I8 = false, bool F8 = false>
 cudaError_t launch_kr_pair(const DevLayout& L, const KrParams& p, cudaStream_t s) {
   auto* k = kr_gemm_kernel<NT, REAL, false, true, I8, F8>;
   const size_t smem =
-      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4, F8 ? p.nl_words : 0, p.desc_lg);
+      REAL ? KrCfg<NT>::smem_bytes_real(p.ring_boxes, p.pstride) : KrCfg<NT, I8>::smem_bytes(p.W, p.srec_u4 * (F8 ? 2 : 1), F8 ? p.nl_words : 0, p.desc_lg);
   if (cudaError_t e = set_smem(k, smem)) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.units ? 2 * p.n_units : 2 * ((p.n_cb + 1) / 2) * p.n_ct * p.n_split));
@@ -416,7 +416,7 @@ int e4m3_limbs(hobo_tensor* t) {
   if (H.order < 2 || t->kl.Tpad / kBK < 64) return 0;   // short K loops: the persistent / bf16 kernels
   if (!H.is_integer && !(e && e[0] == '1')) return 0;
   if (H.is_integer && !(H.sum_abs < 16777216.0)) return 0;
-  if (KrCfg<256, true>::smem_bytes(t->W, 1 + (int)pair_runs_max(t->kl), (int)((t->kl.Tpad / (2 * kBK) + 15) / 16), 4) >
+  if (KrCfg<256, true>::smem_bytes(t->W, 2 * (1 + (int)pair_runs_max(t->kl)), (int)((t->kl.Tpad / (2 * kBK) + 15) / 16), 4) >
       kMaxSmem)
     return 0;
   double amax = 0.0;
@@ -526,7 +526,7 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
     const KLayout& kl = t->kl;
     const int64_t npair = Tpad / (2 * kBK);
     t->srec_u4 = 1 + (int)pair_runs_max(kl);
-    std::vector<uint32_t> rec((size_t)npair * t->srec_u4 * 4, 0);
+    std::vector<uint32_t> rec((size_t)(npair + 1) * t->srec_u4 * 4, 0);   // + a zero record (e4m3 stages copy 2)
     for (int64_t P = 0; P < npair; ++P) {
       uint32_t* r = &rec[(size_t)P * t->srec_u4 * 4];
       const size_t nkb = kl.run_off.size() - 1;
@@ -740,8 +740,9 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
   p.srec = t->d_srec;
   p.srec_u4 = L.i8 ? t->srec_u4 : 0;
   // 32 descriptor-ring slots when they fit next to the rest of the CTA's shared memory, else 16
-  const size_t sm32 = L.NT == 128 ? KrCfg<128, true>::smem_bytes(t->W, p.srec_u4, L.nl_words, 5)
-                                  : KrCfg<256, true>::smem_bytes(t->W, p.srec_u4, L.nl_words, 5);
+  const int rslot = p.srec_u4 * (L.f8 ? 2 : 1);   // e4m3 stages carry two pairs' records
+  const size_t sm32 = L.NT == 128 ? KrCfg<128, true>::smem_bytes(t->W, rslot, L.nl_words, 5)
+                                  : KrCfg<256, true>::smem_bytes(t->W, rslot, L.nl_words, 5);
   p.desc_lg = (L.i8 && sm32 > kMaxSmem) ? 4 : 5;
   p.field_mode = (&L == &t->lay[0] || &L == &t->lay[4] || &L == &t->lay[5]) ? 0 : 1;
   p.nltab = L.d_nltab;
@@ -758,7 +759,7 @@ KrParams make_params(hobo_tensor* t, const DevLayout& L, const uint32_t* bits, l
 int choose_split(hobo_tensor* t, const DevLayout& L, long long B) {
   const long long tiles = ((B + kBM - 1) / kBM) * L.n_ct;
   if (tiles >= 148) return 1;
-  const int KPS = L.i8 ? 2 : L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
+  const int KPS = L.f8 ? 4 : L.i8 ? 2 : L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
   int stages = 0;
   for (int ct = 0; ct < L.n_ct; ++ct) {
     int s = 0;
@@ -947,7 +948,7 @@ hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long 
   use = nullptr;
   if (const char* e = getenv("HOBO_SK"))
     if (e[0] == '0') return HOBO_OK;
-  const int KPS = L.i8 ? 2 : L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
+  const int KPS = L.f8 ? 4 : L.i8 ? 2 : L.NT == 128 ? KrCfg<128>::kps(t->host.limbs) : KrCfg<256>::kps(t->host.limbs);
   std::vector<int> tot(L.n_ct, 0);
   for (int ct = 0; ct < L.n_ct; ++ct)
     for (int j = 0; j < t->kl.nseg; ++j) tot[ct] += (L.sched[((size_t)ct * t->kl.nseg + j) * 2 + 1] + KPS - 1) / KPS;

@@ -301,32 +301,39 @@ __device__ __forceinline__ void issue_i8_stage(uint32_t tmem, uint32_t a_t, uint
   }
 }
 
-// e4m3 limbs: nl limb boxes of the stage (a K-block pair, or nkb = 1 K-block), all into the ONE
-// fp32 accumulator (the limbs of a cell sum exactly: their products with A = 2^-9 are exact in
-// fp32); only the stage's first MMA may start the accumulator
+// e4m3 limbs: np K-block pairs (1 or 2) x nl limb boxes of the stage, all into the ONE fp32
+// accumulator (the limbs of a cell sum exactly: their products with A = 2^-9 are exact in
+// fp32); only the stage's first MMA may start the accumulator.  Pair q's A is 32 TMEM columns
+// at a_t + 32 q; box (limb l, pair q) sits at slot offset (2 l + q) boxes.
 template <int NT, bool PAIR>
 __device__ __forceinline__ void issue_f8_stage(uint32_t tmem, uint32_t a_t, uint32_t sbase, uint32_t boxb, uint32_t issued,
-                                               int nl, int nkb) {
+                                               int nl, int np) {
   constexpr uint32_t id = idesc_e4m3_f32(PAIR ? 2 * kBM : kBM, NT);
-  if (nkb == 2 && nl == 1) {   // the common stage
-    const uint64_t bd = sw128_kmajor_desc(sbase);
+  if (np == 2 && nl == 1) {   // the common stage: 2 pairs x 4 MMAs of K = 32
+    const uint64_t bd0 = sw128_kmajor_desc(sbase), bd1 = sw128_kmajor_desc(sbase + boxb);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      if constexpr (PAIR) umma_f8_ts_pair(tmem, a_t + 8u * kk, bd + 2u * kk, id, kk ? 1u : issued);
-      else umma_f8_ts(tmem, a_t + 8u * kk, bd + 2u * kk, id, kk ? 1u : issued);
-    }
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t at = a_t + 32u * q + 8u * kk;
+        const uint64_t bd = (q ? bd1 : bd0) + 2u * kk;
+        if constexpr (PAIR) umma_f8_ts_pair(tmem, at, bd, id, (q | kk) ? 1u : issued);
+        else umma_f8_ts(tmem, at, bd, id, (q | kk) ? 1u : issued);
+      }
     return;
   }
 #pragma unroll 1
-  for (int l = 0; l < nl; ++l) {
-    const uint64_t bd = sw128_kmajor_desc(sbase + (uint32_t)l * boxb);
+  for (int l = 0; l < nl; ++l)
 #pragma unroll 1
-    for (int kk = 0; kk < 2 * nkb; ++kk) {
-      const uint32_t acc = (l | kk) ? 1u : issued;
-      if constexpr (PAIR) umma_f8_ts_pair(tmem, a_t + 8u * kk, bd + 2u * kk, id, acc);
-      else umma_f8_ts(tmem, a_t + 8u * kk, bd + 2u * kk, id, acc);
+    for (int q = 0; q < np; ++q) {
+      const uint64_t bd = sw128_kmajor_desc(sbase + (uint32_t)(2 * l + q) * boxb);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t acc = (l | q | kk) ? 1u : issued;
+        if constexpr (PAIR) umma_f8_ts_pair(tmem, a_t + 32u * q + 8u * kk, bd + 2u * kk, id, acc);
+        else umma_f8_ts(tmem, a_t + 32u * q + 8u * kk, bd + 2u * kk, id, acc);
+      }
     }
-  }
 }
 
 // One pipeline stage = KPS consecutive K-blocks of one segment (x L limb boxes of W).
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
   const uint32_t tslot = acc_full + 32;
   const uint32_t sQ = (tslot + 16 + 127u) & ~127u;              // 128 doubles: half-sum exchange
   const uint32_t sD = sQ + kBM * 8;                               // I8: descriptor ring (one slot per W stage)
-  const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4, p.desc_lg) + (I8 ? 2u * kBM * 4u : 0u);
+  const uint32_t sX = sD + (uint32_t)C::desc_bytes(p.srec_u4 * (F8 ? 2 : 1), p.desc_lg) + (I8 ? 2u * kBM * 4u : 0u);
   const int MD = 1 << p.desc_lg;   // descriptor ring slots in use (16 or 32), records MD/2 stages ahead
   uint32_t* xs = reinterpret_cast<uint32_t*>(gbase + (sX - base));
   if constexpr (I8) {   // the two zero words in front of every row (run_bits8's window)
@@ -404,22 +411,30 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
   // MB > 1: this CTA's candidate blocks are cb, cb + ncb_eff, ... (< n_cb)
   const int ntile = MB == 1 ? 1 : (p.n_cb - 1 - cb) / ncb_eff + 1;
   constexpr uint32_t BOXB = PAIR ? C::BOX / 2 : C::BOX;   // shared-memory bytes of one W box per CTA
-  const int KPS = REAL ? 1 : C::kps(p.L);
+  // F8: a stage is two K-block pairs (4 K-blocks): 1024 MMA cycles per stage like the bf16
+  // kernel's, half the per-stage handshakes of one pair
+  const int KPS = REAL ? 1 : F8 ? 4 : C::kps(p.L);
+  constexpr int RPS = F8 ? 2 : 1;   // K-block pairs (run records, W boxes per limb) per stage
   // CTA pairs hold half boxes, so the same ring fits twice the stages (TMEM: 256 + 4 x 64 columns)
   // DEC: the int8 launches run decoupled W / A / descriptor rings (for bf16 limbs the single
   // ring measured faster: cfg3 15.2 vs 14.2 M cand/s)
   constexpr bool DEC = I8;
   const int NST = REAL ? C::nst_real(p.L, p.LA, PAIR ? 2 * ring : ring)
+                 : F8 ? min(C::MAXST, (PAIR ? 2 * ring : ring) / (RPS * p.L))
                  : DEC ? C::nstw(p.L, PAIR ? 2 * ring : ring)
                        : C::nst_c(p.L, PAIR ? 2 * ring : ring);
   const int ACOLS = REAL ? p.LA * C::A_COLS : KPS * C::A_COLS;   // TMEM columns of A per stage
-  const int NSTA = DEC ? C::nsta(F8 ? 1 : p.L) : NST;              // A stages (DEC: own ring)
+  const int NSTA = F8 ? ((C::TMEM_COLS - NT) / (KPS * C::A_COLS) >= 8   ? 8   // a power of two
+                         : (C::TMEM_COLS - NT) / (KPS * C::A_COLS) >= 4 ? 4
+                                                                          : 2)
+                 : DEC ? C::nsta(p.L) : NST;                      // A stages (DEC: own ring)
   const int NACC = F8 ? 1 : I8 ? p.L : 1;                          // accumulators in TMEM [0, NACC * NT)
   // F8: the limb count of the stage at K-block kb0 (this column tile's table, in shared memory:
   // a dependent wait on the stage's record here cost 12% at cfg3)
   uint32_t* snl = reinterpret_cast<uint32_t*>(gbase + (sX - base) + (size_t)(p.W + 2) * kBM * 4);
-  auto stage_nl = [&](int kb0) -> int {
-    const int v = (int)((snl[kb0 >> 5] >> ((kb0 >> 1) & 15) * 2) & 3u);
+  auto pair_nl = [&](int P) -> int { return (int)((snl[P >> 4] >> (P & 15) * 2) & 3u); };
+  auto stage_nl = [&](int kb0, int np) -> int {   // the most limbs of the stage's np pairs
+    const int v = np > 1 ? max(pair_nl(kb0 >> 1), pair_nl((kb0 >> 1) + 1)) : pair_nl(kb0 >> 1);
     return v ? v : 1;
   };
   if constexpr (F8)
@@ -442,7 +457,7 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
       s0 += ns;
     }
   }
-  const uint32_t stage_bytes = (uint32_t)((I8 ? 1 : KPS) * p.L) * BOXB;
+  const uint32_t stage_bytes = (uint32_t)((I8 ? RPS : KPS) * p.L) * BOXB;
   // segments run in ascending degree order (j = nseg-1 .. 0); in field mode the single
   // accumulator is snapshot after each degree so the energy can weight degree r by 1/r
   const bool snaps = p.field_mode != 0 && !SA;
@@ -557,8 +572,9 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
       };
       auto dissue = [&]() {
         if (dj < 0) return;
-        // the K-block pair's run record (dkb even)
-        const uint32_t rbytes = (uint32_t)p.srec_u4 * 16u;
+        // the stage's run records (dkb even; RPS consecutive pairs, one bulk copy; the record
+        // array carries a zero record past its end for a stage of one pair)
+        const uint32_t rbytes = (uint32_t)p.srec_u4 * 16u * RPS;
         mbar_arrive_expect_tx(DFULL(dslot), rbytes);
         bulk_g2s(sD + (uint32_t)dslot * rbytes, p.srec + (size_t)(dkb >> 1) * p.srec_u4, rbytes, DFULL(dslot));
         if (++dslot == MD) dslot = 0;
@@ -578,14 +594,18 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
           mbar_wait(EMPTY(st), ph ^ 1u);
           if constexpr (DEC) dissue();
           if constexpr (I8) {   // one box per digit plane: the K-block pair (kb0, kb0 + 1), kb0 even
-            const int nl = F8 ? stage_nl(kb0) : p.L;
-            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)nl * C::BOX);
-            for (int l = 0; l < nl; ++l) {
-              const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1);
-              const uint32_t dst = sB + st * stage_bytes + (uint32_t)l * BOXB;
-              if constexpr (PAIR) tma_load_3d_pair(dst, &tmap, mapa_shared(FULL(st), 0), 0, (int)prank * (NT / 2), box);
-              else tma_load_3d(dst, &tmap, FULL(st), 0, 0, box);
-            }
+            // pairs in this stage (a segment's K-block count may be odd: its last pair then holds
+            // one K-block of tuples and one of zero padding, multiplied whole)
+            const int np = F8 ? ((nkb + 1) >> 1) : 1;
+            const int nl = F8 ? stage_nl(kb0, np) : p.L;
+            if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)(nl * np) * C::BOX);
+            for (int l = 0; l < nl; ++l)
+              for (int q = 0; q < np; ++q) {   // box (limb l, pair q) at slot offset (l RPS + q)
+                const int box = (l * p.n_ct + ct) * (p.n_kb >> 1) + (kb0 >> 1) + q;
+                const uint32_t dst = sB + st * stage_bytes + (uint32_t)(l * RPS + q) * BOXB;
+                if constexpr (PAIR) tma_load_3d_pair(dst, &tmap, mapa_shared(FULL(st), 0), 0, (int)prank * (NT / 2), box);
+                else tma_load_3d(dst, &tmap, FULL(st), 0, 0, box);
+              }
           } else {
             if (leader) mbar_arrive_expect_tx(FULL(st), (uint32_t)(nkb * p.L) * C::BOX);   // pairs: both halves
             for (int q = 0; q < nkb; ++q)
@@ -621,14 +641,14 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
         const int2 s = sched[j];
         for (int kb0 = s.x; kb0 < s.x + s.y; kb0 += KPS) {
           const int nkb = min(KPS, s.x + s.y - kb0);
-          const int nl = F8 ? stage_nl(kb0) : 0;
+          const int nl = F8 ? stage_nl(kb0, (nkb + 1) >> 1) : 0;
           mbar_wait(FULL(st), ph);
           if (DEC) mbar_wait(FULLA(sa), pha);
           tc_fence_after();
           if (elect_one()) {
             if constexpr (F8) {
               issue_f8_stage<NT, PAIR>(tmem, tmem + (uint32_t)(NT + sa * KPS * C::A_COLS), sB + st * stage_bytes, BOXB,
-                                       issued, nl, nkb);
+                                       issued, nl, (nkb + 1) >> 1);
             } else if constexpr (I8) {   // KPS K-blocks x L digit planes, each into its own accumulator
               const uint32_t a_t = tmem + (uint32_t)(p.L * NT + sa * KPS * C::A_COLS);
               const uint32_t sbase = sB + st * stage_bytes;
@@ -855,44 +875,56 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
             const int wst = n & (MD - 1), gst = n & (NSTA - 1);
             const uint32_t wph = (uint32_t)(n >> p.desc_lg) & 1u, gph = (uint32_t)(n >> lg_a) & 1u;
             mbar_wait(DFULL(wst), wph);
-            const uint4* rec = dsm + (size_t)wst * p.srec_u4;
-            const uint4 hd = rec[0];
+            // the K-block pair's A bits from its run record (two K-blocks: l0 h0 | l1 h1)
+            auto decode = [&](const uint4* rec, uint32_t& l0, uint32_t& h0, uint32_t& l1, uint32_t& h1) {
+              const uint4 hd = rec[0];
+              if (p.exp & 1) { l0 = hd.x * (uint32_t)row; h0 = l0 ^ hd.y; l1 = h0 + 1; h1 = l1 * 3u; return; }
+              if (hd.z == 1) {   // e.g. order 3's degree-3 part: one fixed element per run
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.x; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + i], 1, l0, h0);
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.y; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 1, l1, h1);
+              } else if (hd.z == 2) {   // order 4's degree-4 part
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.x; ++i) run_bits8<2>(xs, xs - 2 * kBM, row, rec[1 + i], 2, l0, h0);
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.y; ++i) run_bits8<2>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 2, l1, h1);
+              } else if (hd.z == 0) {
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.x; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + i], 0, l0, h0);
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.y; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 0, l1, h1);
+              } else {
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.x; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + i], hd.z, l0, h0);
+#pragma unroll 1
+                for (uint32_t i = 0; i < hd.y; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], hd.z, l1, h1);
+              }
+            };
+            const uint4* rec = dsm + (size_t)wst * p.srec_u4 * RPS;
+            const int np = F8 ? ((min(KPS, s.y - i * KPS) + 1) >> 1) : 1;   // pairs in this stage
             uint32_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
-            if (p.exp & 1) { l0 = hd.x * (uint32_t)row; h0 = l0 ^ hd.y; l1 = h0 + 1; h1 = l1 * 3u; }
-            else {
-            if (hd.z == 1) {   // e.g. order 3's degree-3 part: one fixed element per run
-#pragma unroll 1
-              for (uint32_t i = 0; i < hd.x; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + i], 1, l0, h0);
-#pragma unroll 1
-              for (uint32_t i = 0; i < hd.y; ++i) run_bits8<1>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 1, l1, h1);
-            } else if (hd.z == 2) {   // order 4's degree-4 part
-#pragma unroll 1
-              for (uint32_t i = 0; i < hd.x; ++i) run_bits8<2>(xs, xs - 2 * kBM, row, rec[1 + i], 2, l0, h0);
-#pragma unroll 1
-              for (uint32_t i = 0; i < hd.y; ++i) run_bits8<2>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 2, l1, h1);
-            } else if (hd.z == 0) {
-#pragma unroll 1
-              for (uint32_t i = 0; i < hd.x; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + i], 0, l0, h0);
-#pragma unroll 1
-              for (uint32_t i = 0; i < hd.y; ++i) run_bits8<0>(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], 0, l1, h1);
-            } else {
-#pragma unroll 1
-            for (uint32_t i = 0; i < hd.x; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + i], hd.z, l0, h0);
-#pragma unroll 1
-            for (uint32_t i = 0; i < hd.y; ++i) run_bits8(xs, xs - 2 * kBM, row, rec[1 + hd.x + i], hd.z, l1, h1);
-            }
-            }
+            decode(rec, l0, h0, l1, h1);
             uint32_t w[32];   // the K-block pair's bytes in the planes' permuted K order
             expand_bytes64(((uint64_t)h0 << 32) | l0, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
             expand_bytes64(((uint64_t)h1 << 32) | l1, *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
             mbar_wait(EMPTYA(gst), gph ^ 1u);
             tc_fence_after();
-            if (!(p.exp & 2)) tmem_st32(lane_base + (uint32_t)(NACC * NT + gst * KPS * C::A_COLS), w);
+            const uint32_t a_col = lane_base + (uint32_t)(NACC * NT + gst * KPS * C::A_COLS);
+            if (!(p.exp & 2)) tmem_st32(a_col, w);
             else {   // keep w live
               uint32_t x = 0;
 #pragma unroll
               for (int c = 0; c < 32; ++c) x ^= w[c];
               if (x == 0x9E3779B9u) xs[0] = 0u;
+            }
+            if (F8 && np > 1) {   // the stage's second pair: 32 TMEM columns further
+              tmem_st_wait();    // (w's registers are the source of the store above)
+              l0 = h0 = l1 = h1 = 0;
+              decode(rec + p.srec_u4, l0, h0, l1, h1);
+              expand_bytes64(((uint64_t)h0 << 32) | l0, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+              expand_bytes64(((uint64_t)h1 << 32) | l1, *reinterpret_cast<uint32_t(*)[16]>(&w[16]));
+              if (!(p.exp & 2)) tmem_st32(a_col + 32u, w);
             }
             tmem_st_wait();
             tc_fence_before();

@@ -1211,3 +1211,22 @@ def test_e4m3_limbs_split_schedules(H, torch):
     x, e, c = t.search(9, None, 2, chain0=0, nchains=64)
     r = o.search(9, 0, 64, 2)
     assert (e, c) == (r["e_best"], r["best_chain"]) and np.array_equal(x, r["chain_xbest"][c])
+
+
+@pytest.mark.parametrize("N", [128, 193, 200, 255])
+def test_e4m3_segment_tails(H, torch, N):
+    """Segments whose K-block count is odd end in a pair holding one K-block of tuples and one of
+    zero padding; e4m3 stages take two pairs, so such a pair can be a stage's second.  Two-bit
+    candidates x_a = x_b = 1 select single tuples {a, b} (plus degree-2 ones) across the whole
+    last stretch of the order-3 segment: fields bit-exact against the oracle."""
+    idx, val = pow2_int_cells(3, N, 5)
+    t, o = H.HoboTensor.import_cells(3, N, idx, val), Oracle.from_cells(3, N, idx, val)
+    prs = [(a, b) for b in range(max(1, N - 12), N) for a in range(b)]
+    X = np.zeros((len(prs) + 2, N), np.uint8)
+    for r, (a, b) in enumerate(prs):
+        X[r, a] = X[r, b] = 1
+    X[-2, :] = 1
+    X[-1, 1::2] = 1
+    G, E = fields(H, torch, t, X)
+    assert t.launch_stats()["i8_planes"] < 0
+    assert np.array_equal(G, o.field(X)) and np.array_equal(E, o.energy(X))
