@@ -960,6 +960,9 @@ hobo_status sk_plan(hobo_tensor* t, const DevLayout& L, const KrParams& p, long 
   const long long tiles = ncbp * L.n_ct;
   const long long D = tiles / slots * slots, R = tiles - D;
   if (R == 0 || tiles < slots / 2 || total < 4 * slots || total >= (1 << 20)) return HOBO_OK;
+  // a leftover wave this full behind whole waves gains less than the partial sums cost
+  // (e4m3 cfg3, 68 of 74 slots: step 2.242 ms without, 2.257 ms with)
+  if (D > 0 && 10 * R >= 9 * slots) return HOBO_OK;
   for (const auto& q : t->sk_plans)
     if (q.B == B && q.L == &L && q.ctdesc == p.ct_desc) {
       use = &q;

@@ -445,7 +445,8 @@ def test_stream_k_matches_data_parallel(H, torch, case):
     """The stream-K schedule (leftover tiles cut into 74 equal K ranges, partials summed in K
     order) against the plain one-tile-per-pair launch (HOBO_SK=0) and the oracle: 8,192
     candidates (one GPU's share at 8 GPUs: every tile split), 20,000 (two whole waves + 10
-    split tiles) and 65,536 (cfg3's launch: 6 waves + 68 split tiles)."""
+    split tiles) and 65,536 (cfg3's launch: 6 waves + 68 leftover tiles, which the schedule now
+    leaves data-parallel: a 92%-full leftover wave gains less than its partial sums cost)."""
     if case == "int_cfg3":
         p = cfg3_problem()
         t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
