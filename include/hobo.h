@@ -34,8 +34,8 @@
  *                            of replaying their captured CUDA graphs
  *       HOBO_SK=0            no stream-K schedule for CTA-pair field launches
  *       HOBO_E2E_TAIL=<n>, HOBO_E2E_HEAD=<q>   host-buffer field calls returning G: n
- *                            halvings after the last whole wave (default 1), first chunk q
- *                            quarter waves (default 1)
+ *                            halvings after the last whole wave (default 0), first chunk q
+ *                            quarter waves (default 4)
  *       HOBO_KR_EXP=<bits>   MEASUREMENT ONLY: switches parts of the 1-byte-plane contraction
  *                            off (1 run decode, 2 A store, 4 second e4m3 limb; tools/f8_check.sh);
  *                            results are wrong whenever it is set

@@ -1483,16 +1483,16 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
   if (!gout) {
     for (long long off = 0, n = per_wave; off < B; off += sizes.back(), n *= 6) sizes.push_back(std::min(n, B - off));
   } else {
-    // a quarter-wave first chunk (nothing overlaps its input copy and its contraction) and a
-    // half-wave last chunk (its copy-out is the exposed one): a partial wave runs split across
-    // every SM, so it still hides the previous chunk's copy-out.  bf16 cfg3 e2e: 4.89 -> 4.75
-    // ms (half-wave ends); e4m3 cfg3, whose contraction now takes about as long as the 128 MiB
-    // copy-out: 3.67 (half-wave head) -> 3.57 ms; two halvings (1/2, 1/4) measured slower in
-    // both.  HOBO_E2E_TAIL = halvings, HOBO_E2E_HEAD = first chunk in quarter waves (A/B
-    // knobs, tools/e2e_zc.sh).
-    int tail = 1;
+    // one-wave first chunk, two-wave chunks, one-wave last chunk.  The e4m3 contraction
+    // (2.2 ms at cfg3) is now faster than the 128 MiB copy-out (2.35 ms at 57 GB/s, less while
+    // X streams the other way), so the call is copy-bound and fewer chunks mean fewer gaps:
+    // cfg3 3.25 ms; a quarter-wave head 3.34, plus a half-wave tail 3.52, plus a quarter-wave
+    // tail 3.65 ms.  (While the bf16 kernel, 4.2 ms, was the longer side, half-wave ends had
+    // won: 4.89 -> 4.75 ms.)  HOBO_E2E_TAIL = halvings after the last whole wave,
+    // HOBO_E2E_HEAD = first chunk in quarter waves (A/B knobs, tools/e2e_zc.sh).
+    int tail = 0;
     if (const char* e = getenv("HOBO_E2E_TAIL")) tail = atoi(e);
-    long long head = std::max<long long>(kBM, per_wave / 4 / kBM * kBM);
+    long long head = per_wave;
     if (const char* e = getenv("HOBO_E2E_HEAD")) head = std::max<long long>(kBM, per_wave * atoi(e) / 4 / kBM * kBM);
     std::vector<long long> ends;   // the tail, smallest last
     long long rest = B - std::min<long long>(head, B);
