@@ -1489,7 +1489,7 @@ hobo_status run_host(hobo_tensor* t, int field, const uint8_t* X_host, int64_t B
     // cfg3 3.25 ms; a quarter-wave head 3.34, plus a half-wave tail 3.52, plus a quarter-wave
     // tail 3.65 ms.  (While the bf16 kernel, 4.2 ms, was the longer side, half-wave ends had
     // won: 4.89 -> 4.75 ms.)  HOBO_E2E_TAIL = halvings after the last whole wave,
-    // HOBO_E2E_HEAD = first chunk in quarter waves (A/B knobs, tools/e2e_zc.sh).
+    // HOBO_E2E_HEAD = first chunk in quarter waves (A/B knobs, tools/e2e_chunks.sh).
     int tail = 0;
     if (const char* e = getenv("HOBO_E2E_TAIL")) tail = atoi(e);
     long long head = per_wave;
