@@ -672,6 +672,9 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "e4m3 (exact limbs)" if f8 else "i8" if i8 else "bf16", "data": "synthetic",
+                "exactness": ("operands are exact splits of the fp32 cells (e4m3 limbs / int8 digits / bf16 limbs summing "
+                              "to the cell); on integer instances every energy, field and the argmin are bit-identical to the "
+                              "fp64 oracle (tests/test_gpu_parity.py: test_cfg3_full_batch, test_e4m3_*)"),
                 "config": {"workload": wl_text, "name": a.config, "order": order, "N": N,
                            "global_batch": units, "batch_per_gpu": B, "limbs": t.limbs,
                            "parallelism": f"dp{world} (H replicated, batch sharded{' by hobo_shard' if scaling == 'strong' else ''})",
