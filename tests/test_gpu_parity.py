@@ -11,7 +11,7 @@ import pytest
 from oracle import Oracle
 from workloads import (cfg3_problem, exhaustive_X, h, int_twin_cells, paper_grids, pythagoras,
                        random_integer_problem, seating, tsp, uniform_cells, x_bits)
-from workloads.gen import canonical_cells_all
+from workloads.gen import canonical_cells_all, int_encoded_problem
 
 pytestmark = pytest.mark.gpu
 
@@ -1231,3 +1231,19 @@ def test_e4m3_segment_tails(H, torch, N):
     G, E = fields(H, torch, t, X)
     assert t.launch_stats()["i8_planes"] < 0
     assert np.array_equal(G, o.field(X)) and np.array_equal(E, o.energy(X))
+
+
+def test_e4m3_n1024_integer_encoded(H, torch):
+    """cfg3's recipe at N = 1024 (256 four-bit variables, the device path's largest N): the
+    e4m3-limb path in field and energy mode, strided rows and the argmin bit-exact against
+    the oracle (sum |H| < 2^24, so the exactness guard admits it)."""
+    p = int_encoded_problem(256, 4, 2048, 4096, 7)
+    t, o = H.HoboTensor.from_problem(p), Oracle.from_problem(p)
+    X = x_bits(5, 4096, p.N)
+    G, E = fields(H, torch, t, X)
+    assert t.launch_stats()["i8_planes"] < 0
+    rows = sample_rows(4096, 97)
+    assert np.array_equal(G[rows], o.field(X[rows])) and np.array_equal(E[rows], o.energy(X[rows]))
+    Ee, best = energies(H, torch, t, X)
+    assert np.array_equal(Ee, E)
+    assert best == (E.min(), int(np.argmin(E)))

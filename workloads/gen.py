@@ -199,6 +199,30 @@ def cfg3_problem() -> Problem:
     return tb.problem(3, 512, "cfg3")
 
 
+def int_encoded_problem(nvars: int, bits: int, ncubic: int, nquad: int, seed: int) -> Problem:
+    """cfg3's recipe at other sizes: nvars integer variables of `bits` bits (bit t weighs 2^t),
+    ncubic +-1 cubic and nquad {+-1..+-4} quadratic terms over distinct variables (tests only)."""
+    tb = TermBuilder()
+    y = lambda a: _int_factor([(bits * a + t, 2.0 ** t) for t in range(bits)])  # noqa: E731
+
+    def distinct(tag, t, k):
+        vals, j = [], 0
+        while len(vals) < k:
+            v = int(h(seed, tag, t, j) % np.uint64(nvars))
+            if v not in vals:
+                vals.append(v)
+            j += 1
+        return sorted(vals)
+
+    for t in range(ncubic):
+        a, b, c = distinct(10, t, 3)
+        tb.add(1.0 if (h(seed, 12, t, 0) & 1) else -1.0, [y(a), y(b), y(c)])
+    for t in range(nquad):
+        a, b = distinct(11, t, 2)
+        tb.add(float([-4, -3, -2, -1, 1, 2, 3, 4][int(h(seed, 13, t, 0) % np.uint64(8))]), [y(a), y(b)])
+    return tb.problem(3, nvars * bits, f"intenc{nvars}x{bits}")
+
+
 def subsets(N: int, r: int) -> np.ndarray:
     """All r-subsets of range(N) as sorted rows, lexicographic order, int32 (C(N,r) x r)."""
     if r == 0:
