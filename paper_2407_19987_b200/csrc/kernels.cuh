@@ -24,7 +24,8 @@ namespace hobo {
 
 constexpr int kBM = 128;        // candidates per CTA (UMMA M, TMEM lanes)
 constexpr int kBK = 64;         // tuples per K-block (one 128-byte SW128 row of bf16)
-constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2-9 A-generator + epilogue (2 per lane quarter)
+constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2-9 A-generator + epilogue (2 per lane quarter);
+                                // e4m3 launches add warps 10-17 (generation only, kr_threads)
 
 struct KrParams {
   const uint32_t* xbits;    // [B][W] bit-packed candidates (bit m of word m/32)
@@ -857,14 +858,15 @@ __global__ void __launch_bounds__(kr_threads<F8>(), 1) kr_gemm_kernel(const __gr
           d1 = n1;
         }
       } else if constexpr (DEC) {
-        // int8: the teams take whole stages in turn (team h: stages with gn % 2 == h).  A team
-        // decodes both K-blocks of its stage from the stage's run record (TMA bulk copy,
-        // DAHEAD stages ahead, DFULL ring) and writes them with ONE tcgen05.st (32 columns),
-        // so one store round trip (~400 cycles) covers two K-blocks and each team has two
-        // stage times per stage.  FULLA counts the one team's 4 warps (pairs: 8).
-        // The team visits only its own stages: the absolute stage counter n gives the ring
-        // slots and phases directly (MAXD and NSTA are powers of two), so the other team's
-        // stages cost no loop iterations.
+        // 1-byte planes: the NTEAM teams take whole stages in turn (team h: stages n with
+        // n % NTEAM == h; NTEAM = 2 for int8 digits, 4 for e4m3 limbs).  A team decodes the
+        // K-blocks of its stage from the stage's run records (TMA bulk copy, MD/2 stages ahead,
+        // DFULL ring) and writes each K-block pair with ONE tcgen05.st (32 columns), so one
+        // store round trip (~400 cycles) covers two K-blocks and each team has NTEAM stage
+        // times per stage.  FULLA counts the one team's 4 warps (pairs: 8).  The team visits
+        // only its own stages: the absolute stage counter n gives the ring slots and phases
+        // directly (MD and NSTA are powers of two), so the other teams' stages cost no loop
+        // iterations.
         const uint4* dsm = reinterpret_cast<const uint4*>(gbase + (sD - base));
         const int nstages = (s.y + KPS - 1) / KPS;
         const int lg_a = NSTA == 8 ? 3 : NSTA == 4 ? 2 : NSTA == 2 ? 1 : 0;
