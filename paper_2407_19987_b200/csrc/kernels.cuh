@@ -168,6 +168,7 @@ __device__ __forceinline__ uint64_t block_bits(const uint32_t* xs, int row, cons
   uint64_t bits = 0;
   if (nruns > 0) bits |= run_bits(xs, row, d0, nfix);
   if (nruns > 1) bits |= run_bits(xs, row, d1, nfix);
+#pragma unroll 1   // overflow runs are rare: keep the hot loop's code small
   for (uint32_t i = 2; i < nruns; ++i) bits |= run_bits(xs, row, __ldg(runs + (d0.w >> 10) + (i - 2)), nfix);
   return bits;
 }
