@@ -44,7 +44,8 @@
  *     Pairs, persistent kernels, graphs and annealing kernels give the same results (bit for
  *     bit on integer instances).  The int8 path computes the contraction exactly (integer
  *     accumulation), the bf16 path within the fp32 tolerance; both are exact on integer
- *     instances with sum|H| < 2^24.
+ *     instances with sum|H| < 2^24, as is the e4m3-limb path (taken only for such instances
+ *     unless HOBO_F8=1).
  */
 #ifndef HOBO_H_
 #define HOBO_H_
