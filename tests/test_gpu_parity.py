@@ -1247,3 +1247,32 @@ def test_e4m3_n1024_integer_encoded(H, torch):
     Ee, best = energies(H, torch, t, X)
     assert np.array_equal(Ee, E)
     assert best == (E.min(), int(np.argmin(E)))
+
+
+def test_bench_line_contract(H, torch):
+    """`python bench.py` (the driver's command, few steps) prints one JSON line carrying the
+    contract's keys, consistent with each other: value = units / step time, the roofline
+    fraction = achieved / peak, the e2e byte counts of the host-buffer call, the clocks."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3"], cwd=root,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["higher_is_better"] is True
+    assert abs(d["value"] - d["config"]["global_batch"] / (d["ms_per_step"] / 1e3)) <= 1e-6 * d["value"]
+    r = d["roofline"]
+    assert r["bound"] in ("tensor", "hbm") and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert 0.0 < r["frac"] <= 1.0 and r["kernel_ms"] > 0
+    e = d["e2e"]
+    B, N = d["config"]["global_batch"], d["config"]["N"]
+    assert e["h2d_bytes_per_step"] == B * N and e["d2h_bytes_per_step"] == B * 4 + B * N * 4 + 16
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["gpu_launches"] > 0 and isinstance(d["clocks"], dict)
