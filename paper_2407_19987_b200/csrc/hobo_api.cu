@@ -606,8 +606,8 @@ hobo_status ensure_layout(hobo_tensor* t, int slot) {
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     if (L.f8) {
-      // each stage's limb count per column tile (the most limb planes a cell of its box needs),
-      // into bits [shift + 2 ct, shift + 2 ct + 2) of the stage record's header word w
+      // each K-block pair's limb count per column tile (the most limb planes a cell of its box
+      // needs), packed 2 bits per pair into L.d_nltab [n_ct][nl_words] (KrParams::nltab)
       int err = 0;
       CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
       cudaFree(d_err);
